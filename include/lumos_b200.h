@@ -1,0 +1,191 @@
+/*
+ * lumos_b200.h — C ABI of the B200-native batched Lumos replay engine.
+ *
+ * This is the drop-in boundary for the reference's simulation path
+ * (/root/reference/proj, the `tracesim` library).  Every entry point replaces
+ * one reference interface; the citation is on each declaration.  Only PODs
+ * cross the boundary: int64 microseconds (types.hpp:15), int32 task ids
+ * (types.hpp:16), plain pointers and sizes.  No torch, no C++ types.
+ *
+ *   reference                                            here
+ *   ---------------------------------------------------  ------------------------
+ *   ExecutionGraph (build.hpp:73-85), Task (types.hpp:73-87),
+ *   RuntimeRule (build.hpp:46-54)                        ts_graph_desc
+ *   validate_graph + Engine ctor (simulate.cpp:26-196)   ts_graph_create
+ *   simulate(const ExecutionGraph&) (simulate.hpp:51)    ts_simulate
+ *   N x simulate over perturbed copies / DurationHook
+ *     (pipeline.hpp:72-74, synth.cpp:146-156)           ts_replay_batch
+ *   makespan (simulate.cpp:327-334), breakdown_by_rank
+ *     (metrics.cpp:96-103)                               ts_result fields
+ *   SimulationError / GraphError (types.hpp:119-127)     TS_E_* codes + ts_last_error
+ *
+ * Error behaviour mirrors the reference taxonomy: every call returns 0 on
+ * success or a TS_E_* code; the message (same wording as the reference's
+ * exception text where one exists) is kept per thread in ts_last_error().
+ *
+ * Pointers in ts_scenarios / ts_result may be host or device memory; the
+ * library detects which (cudaPointerGetAttributes) and stages host buffers
+ * itself.  There is no CPU execution path: without a CUDA device every compute
+ * call fails with TS_E_CUDA.
+ */
+#ifndef LUMOS_B200_H
+#define LUMOS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+/* error codes (0 = success) */
+enum {
+  TS_OK = 0,
+  TS_E_INVALID_ARGUMENT = 1, /* std::invalid_argument                          */
+  TS_E_SIMULATION = 3,       /* tracesim::SimulationError (invalid graph, deadlock) */
+  TS_E_GRAPH = 4,            /* tracesim::GraphError (cycle)                   */
+  TS_E_UNSUPPORTED = 6,      /* graph outside what the device path accepts      */
+  TS_E_CUDA = 7,             /* no device / CUDA runtime failure               */
+  TS_E_NOMEM = 8
+};
+
+/* lane kinds (types.hpp:41), rule kinds (build.hpp:47), op classes (types.hpp:31-39) */
+enum { TS_LANE_CPU_THREAD = 0, TS_LANE_CUDA_STREAM = 1 };
+enum { TS_RULE_STREAM_SYNC = 0, TS_RULE_DEVICE_SYNC = 1, TS_RULE_EVENT_SYNC = 2 };
+enum {
+  TS_OP_COMPUTE = 0, TS_OP_COMMUNICATION = 1, TS_OP_LAUNCH = 2, TS_OP_SYNC = 3,
+  TS_OP_EVENT_RECORD = 4, TS_OP_EVENT_WAIT = 5, TS_OP_OTHER = 6
+};
+/* gate kinds (estimate()/generator semantics, pipeline.cpp:377-389) */
+enum { TS_GATE_FIN = 0, TS_GATE_START = 1 };
+
+/*
+ * SoA view of one ExecutionGraph.  Task ids are dense: task i is row i.
+ * fixed edges are finish->start (build.hpp:71).  Rules: watch lists are
+ * rule_watch_off[r] .. rule_watch_off[r+1] into watch_{rank,kind,lane};
+ * rule_bound[r] = -1 when an EventSync has no bound task.
+ *
+ * Gates (optional, n_gates = 0 for plain replay) carry the generator /
+ * estimate() semantics of build_pipeline (pipeline.cpp:361-441) that a
+ * recorded trace bakes into durations:  finish(v) = max(start(v), gate
+ * values) + duration(v), a gate value being finish(from) (TS_GATE_FIN:
+ * p2p receive waits for its send) or start(from) (TS_GATE_START:
+ * a collective ends at the latest start of its group plus its own time).
+ */
+typedef struct {
+  int32_t n_tasks;
+  const int64_t* duration;       /* [n] base duration, us                 */
+  const int64_t* original_start; /* [n] recorded start, us (tie-break key) */
+  const int32_t* rank;           /* [n] ProcessorId.rank                   */
+  const int32_t* lane_kind;      /* [n] TS_LANE_*                          */
+  const int32_t* lane;           /* [n] thread id or stream id             */
+  const uint8_t* op_class;       /* [n] TS_OP_*                            */
+  const uint8_t* task_kind;      /* [n] 0 Cpu, 1 Gpu (types.hpp:29)        */
+  const uint8_t* scale_class;    /* [n] scenario class 0..3, or NULL:
+                                    0 host task, 1 GPU compute, 2 GPU comm */
+  int64_t n_edges;
+  const int32_t* edge_from;
+  const int32_t* edge_to;
+  int32_t n_rules;
+  const int32_t* rule_kind;
+  const int32_t* rule_task;
+  const int32_t* rule_bound;
+  const int32_t* rule_watch_off; /* [n_rules + 1] */
+  const int32_t* watch_rank;
+  const int32_t* watch_kind;
+  const int32_t* watch_lane;
+  int64_t window_start;          /* iteration_window (trace_parse.hpp:65-68) */
+  int64_t window_end;
+  int64_t n_gates;
+  const int32_t* gate_from;
+  const int32_t* gate_to;
+  const uint8_t* gate_kind;      /* TS_GATE_* */
+} ts_graph_desc;
+
+typedef struct ts_graph ts_graph;
+
+typedef struct {
+  int32_t n_tasks;
+  int32_t n_components;   /* independent sub-graphs (ranks in plain replay)   */
+  int32_t n_programs;     /* distinct compiled programs after de-duplication   */
+  int32_t n_ranks;
+  int32_t n_streams;      /* CUDA-stream lanes over all ranks                  */
+  int32_t max_slots;      /* live int64 values per scenario (shared memory)    */
+  int64_t program_bytes;  /* device bytes of the op streams                    */
+  int64_t n_ops;          /* ops over all programs                             */
+  int32_t n_syncs;        /* Stream/DeviceSync rules resolved statically       */
+  int32_t n_gpu_tasks;
+  int64_t window_start, window_end;
+} ts_graph_info;
+
+/* validate_graph + compile to device programs (simulate.cpp:26-196).
+ * Returns TS_E_SIMULATION for graphs simulate() rejects ("invalid graph: ..."),
+ * TS_E_UNSUPPORTED for graphs outside the device path's class (unchained
+ * lanes, rules watching CPU lanes).  device < 0: current device. */
+int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out);
+void ts_graph_destroy(ts_graph* g);
+int ts_graph_get_info(const ts_graph* g, ts_graph_info* out);
+/* rank of each rank slot (breakdown rows), stream lane of each stream slot */
+int ts_graph_ranks(const ts_graph* g, int32_t* ranks /* [n_ranks] */);
+int ts_graph_streams(const ts_graph* g, int32_t* rank, int32_t* lane /* [n_streams] */);
+
+/* Scenario batch: durations are a pure function of (spec, scenario id, task),
+ * so any shard or tile reproduces bit-for-bit.
+ *   class scale (transform.cpp:38-43): d = mul_div(d, num, scale_den), with
+ *     num = scale_num[s][class] if given, else drawn in [scale_lo, scale_hi]
+ *   jitter      (synth.cpp:150-155):   d = d == 0 ? 0 : max(1, llround(d*(1+u))),
+ *     u ~ U[-jitter, jitter) from Philox2x32-10(task, scenario; seed)
+ *   explicit: durations[task * durations_ld + s] replaces both.          */
+typedef struct {
+  int64_t first;            /* global id of scenario 0 of this batch */
+  int32_t count;
+  int32_t flags;            /* reserved, 0 */
+  uint64_t seed;
+  double jitter;            /* 0 disables */
+  int32_t scale_lo, scale_hi, scale_den; /* den <= 0 disables */
+  int32_t n_classes;        /* columns of scale_num (<= 4) */
+  const int32_t* scale_num; /* [count][n_classes] or NULL */
+  const int64_t* durations; /* [n_tasks][durations_ld] or NULL */
+  int64_t durations_ld;
+} ts_scenarios;
+
+/* Outputs; any pointer may be NULL (not produced).  start/fin are the
+ * SimEntry sim_start/sim_end (simulate.hpp:12-17) of every task, stored
+ * scenario-major within a task row: start[task * ld + s]. */
+typedef struct {
+  int64_t* start;          /* [n_tasks][ld] */
+  int64_t* fin;            /* [n_tasks][ld] */
+  int64_t ld;              /* >= count */
+  int64_t* span;           /* [count][3] SimulatedTrace {start, end, makespan} */
+  int64_t* rank_breakdown; /* [count][n_ranks][5] {total, exposed_compute,
+                              exposed_comm, overlapped, other} (metrics.hpp:33-39) */
+  int64_t* stream_busy;    /* [count][n_streams] summed kernel time per stream */
+  int32_t* status;         /* [count] 0 = exact fast path, 1 = resolved by the
+                              exact event-driven path, <0 = error */
+} ts_result;
+
+/* Replays `sc->count` scenarios on `stream` (cudaStream_t, NULL = legacy
+ * default).  Returns after the work is enqueued when every output pointer is
+ * device memory; otherwise it synchronises and copies to the host buffers. */
+int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, void* stream);
+
+/* simulate(const ExecutionGraph&) (simulate.hpp:51): one replay at the
+ * graph's own durations; host buffers start/fin [n_tasks], span[3]. */
+int ts_simulate(ts_graph* g, int64_t* start, int64_t* fin, int64_t* span);
+
+/* Materialises the scenario durations (the K4 manipulation kernel on its
+ * own) into dur[task * ld + s] (device or host pointer). */
+int ts_scenario_durations(ts_graph* g, const ts_scenarios* sc, int64_t* dur, int64_t ld,
+                          void* stream);
+
+/* Launch counters (kernels this library enqueued since creation). */
+int64_t ts_kernel_launches(void);
+const char* ts_last_error(void);
+int ts_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LUMOS_B200_H */

@@ -1,0 +1,341 @@
+// ref_shim.cpp — extern "C" driver for the compiled, unmodified reference.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources (/root/reference/proj/src/*.cpp, tests/oracles.cpp) under
+// -Dtracesim=tracesim_ref, producing oracle/_ref/libtracesim_ref.so.  Python
+// tests (tests/refshim.py) and bench.py's cpu_baseline / --impl reference legs
+// load it with ctypes.  Nothing in paper_2504_09307_b200/ links it.
+//
+// Every function is a thin adaptor over the reference's public C++ API:
+//   generate / split_by_rank      (src/synth.cpp:140-176)
+//   build_graph / merge_ranks     (src/build.cpp:338-542)
+//   parse_trace                   (src/trace_parse.cpp:213-228)
+//   simulate                      (src/simulate.cpp:341-347)
+//   oracle::tick_simulate         (tests/oracles.cpp:11-113)
+//   oracle::random_graph          (tests/oracles.cpp:222-295)
+//   breakdown_by_rank             (src/metrics.cpp:96-103)
+//   build_pipeline + DurationHook (src/pipeline.cpp:474-477)
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "json.hpp"
+#include "oracles.hpp"
+#include "tracesim/build.hpp"
+#include "tracesim/metrics.hpp"
+#include "tracesim/pipeline.hpp"
+#include "tracesim/simulate.hpp"
+#include "tracesim/synth.hpp"
+#include "tracesim/trace_parse.hpp"
+#include "tracesim/transform.hpp"
+
+#include "lumos_oracle.h"
+
+using namespace tracesim;
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const char* what) { g_err = what; }
+
+struct RefGraph {
+  ExecutionGraph g;
+};
+
+ExecutionGraph relabel_rank(const ExecutionGraph& src, int new_rank) {
+  ExecutionGraph g = src;
+  g.processors.clear();
+  for (auto& t : g.tasks) {
+    t.processor.rank = new_rank;
+    g.processors.insert(t.processor);
+  }
+  for (auto& r : g.rules)
+    for (auto& p : r.watched) p.rank = new_rank;
+  return g;
+}
+
+ExecutionGraph graph_of_events(const std::vector<TraceEvent>& events, int tp) {
+  std::map<int, ExecutionGraph> parts;
+  for (const auto& [rank, evs] : split_by_rank(events)) {
+    ExecutionGraph g = build_graph(evs, BuildPolicy(), rank);
+    if (tp <= 1) {
+      parts[rank] = std::move(g);
+    } else {
+      for (int t = 0; t < tp; ++t) parts[rank * tp + t] = relabel_rank(g, rank * tp + t);
+    }
+  }
+  return merge_ranks(parts);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const SimulationError& e) {
+    set_err(e.what());
+    return 3;
+  } catch (const GraphError& e) {
+    set_err(e.what());
+    return 4;
+  } catch (const std::exception& e) {
+    set_err(e.what());
+    return 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- graphs
+
+// generate(spec) -> per-rank build_graph -> (tp replicas) -> merge_ranks; then
+// optionally slice_rank.  Also returns the generator's truth makespan.
+void* ref_graph_generate(const char* spec_json, int tp, int slice, int64_t* truth_makespan) {
+  RefGraph* out = nullptr;
+  int rc = guarded([&] {
+    SynthSpec spec = SynthSpec::from_json(spec_json);
+    SynthResult res = generate(spec);
+    if (truth_makespan) *truth_makespan = res.truth.iterations.at(0).makespan;
+    out = new RefGraph;
+    out->g = graph_of_events(res.events, tp);
+    if (slice >= 0) out->g = slice_rank(out->g, slice);
+    return 0;
+  });
+  if (rc != 0) {
+    delete out;
+    return nullptr;
+  }
+  return out;
+}
+
+// parse_trace(json) -> build_graph (one rank)
+void* ref_graph_from_trace(const char* trace_json, int rank_override) {
+  RefGraph* out = nullptr;
+  int rc = guarded([&] {
+    auto events = parse_trace(std::string(trace_json));
+    out = new RefGraph;
+    out->g = rank_override >= 0 ? build_graph(events, BuildPolicy(), rank_override)
+                                : build_graph(events, BuildPolicy());
+    return 0;
+  });
+  if (rc != 0) {
+    delete out;
+    return nullptr;
+  }
+  return out;
+}
+
+void* ref_graph_from_arrays(int32_t n, const int64_t* dur, const int64_t* ostart,
+                            const int32_t* rank, const int32_t* kind, const int32_t* lane,
+                            const uint8_t* op_class, int64_t ne, const int32_t* ef,
+                            const int32_t* et, int32_t nr, const int32_t* rkind,
+                            const int32_t* rtask, const int32_t* rbound, const int32_t* rwoff,
+                            const int32_t* wrank, const int32_t* wkind, const int32_t* wlane,
+                            int64_t wstart, int64_t wend) {
+  auto* out = new RefGraph;
+  ExecutionGraph& g = out->g;
+  g.tasks.resize(static_cast<std::size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    Task& t = g.tasks[i];
+    t.id = i;
+    t.kind = kind[i] == 1 ? TaskKind::Gpu : TaskKind::Cpu;
+    t.op_class = static_cast<OpClass>(op_class ? op_class[i] : 6);
+    t.name = "t" + std::to_string(i);
+    t.duration = dur[i];
+    t.original_start = ostart[i];
+    t.processor = {rank[i], kind[i] == 1 ? LaneKind::CudaStream : LaneKind::CpuThread, lane[i]};
+    g.processors.insert(t.processor);
+  }
+  for (int64_t e = 0; e < ne; ++e) g.fixed_edges.emplace_back(ef[e], et[e]);
+  for (int32_t r = 0; r < nr; ++r) {
+    RuntimeRule rule;
+    rule.kind = static_cast<RuntimeRule::Kind>(rkind[r]);
+    rule.waiting_task = rtask[r];
+    if (rbound[r] >= 0) rule.bound_task = rbound[r];
+    if (rule.kind == RuntimeRule::Kind::EventSync) rule.event_id = r;
+    for (int32_t w = rwoff[r]; w < rwoff[r + 1]; ++w)
+      rule.watched.push_back(
+          {wrank[w], wkind[w] == 1 ? LaneKind::CudaStream : LaneKind::CpuThread, wlane[w]});
+    g.rules.push_back(std::move(rule));
+  }
+  g.iteration_window = {wstart, wend};
+  return out;
+}
+
+void* ref_rng_new(uint64_t seed) { return new std::mt19937_64(seed); }
+void ref_rng_free(void* rng) { delete static_cast<std::mt19937_64*>(rng); }
+
+void* ref_graph_random(void* rng, int max_tasks, int max_lanes) {
+  auto* out = new RefGraph;
+  out->g = oracle::random_graph(*static_cast<std::mt19937_64*>(rng), max_tasks, max_lanes);
+  return out;
+}
+
+void ref_graph_free(void* h) { delete static_cast<RefGraph*>(h); }
+
+// sizes = {tasks, edges, rules, watched entries, window.start, window.end}
+void ref_graph_sizes(void* h, int64_t* sizes) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  int64_t nw = 0;
+  for (const auto& r : g.rules) nw += static_cast<int64_t>(r.watched.size());
+  sizes[0] = static_cast<int64_t>(g.tasks.size());
+  sizes[1] = static_cast<int64_t>(g.fixed_edges.size());
+  sizes[2] = static_cast<int64_t>(g.rules.size());
+  sizes[3] = nw;
+  sizes[4] = g.iteration_window.start;
+  sizes[5] = g.iteration_window.end;
+}
+
+void ref_graph_export(void* h, int64_t* dur, int64_t* ostart, int32_t* rank, int32_t* kind,
+                      int32_t* lane, uint8_t* op_class, uint8_t* task_kind, int32_t* ef,
+                      int32_t* et, int32_t* rkind, int32_t* rtask, int32_t* rbound,
+                      int32_t* rwoff, int32_t* wrank, int32_t* wkind, int32_t* wlane) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  for (std::size_t i = 0; i < g.tasks.size(); ++i) {
+    const Task& t = g.tasks[i];
+    dur[i] = t.duration;
+    ostart[i] = t.original_start;
+    rank[i] = t.processor.rank;
+    kind[i] = t.processor.kind == LaneKind::CudaStream ? 1 : 0;
+    lane[i] = t.processor.lane;
+    op_class[i] = static_cast<uint8_t>(t.op_class);
+    task_kind[i] = t.kind == TaskKind::Gpu ? 1 : 0;
+  }
+  for (std::size_t e = 0; e < g.fixed_edges.size(); ++e) {
+    ef[e] = g.fixed_edges[e].first;
+    et[e] = g.fixed_edges[e].second;
+  }
+  int32_t w = 0;
+  rwoff[0] = 0;
+  for (std::size_t r = 0; r < g.rules.size(); ++r) {
+    const RuntimeRule& rule = g.rules[r];
+    rkind[r] = static_cast<int32_t>(rule.kind);
+    rtask[r] = rule.waiting_task;
+    rbound[r] = rule.bound_task ? *rule.bound_task : -1;
+    for (const auto& p : rule.watched) {
+      wrank[w] = p.rank;
+      wkind[w] = p.kind == LaneKind::CudaStream ? 1 : 0;
+      wlane[w] = p.lane;
+      ++w;
+    }
+    rwoff[r + 1] = w;
+  }
+}
+
+// task names, '\n'-separated, into buf (returns bytes needed)
+int64_t ref_graph_names(void* h, char* buf, int64_t cap) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  std::string all;
+  for (const auto& t : g.tasks) {
+    all += t.name;
+    all += '\n';
+  }
+  if (buf && cap >= static_cast<int64_t>(all.size())) std::memcpy(buf, all.data(), all.size());
+  return static_cast<int64_t>(all.size());
+}
+
+// ---------------------------------------------------------------- replay
+
+static int run_sim(void* h, const int64_t* dur, int64_t* start, int64_t* fin, int64_t* span,
+                   bool tick) {
+  return guarded([&] {
+    const ExecutionGraph& src = static_cast<RefGraph*>(h)->g;
+    const ExecutionGraph* gp = &src;
+    ExecutionGraph copy;
+    if (dur) {
+      copy = src;
+      for (std::size_t i = 0; i < copy.tasks.size(); ++i) copy.tasks[i].duration = dur[i];
+      gp = &copy;
+    }
+    SimulatedTrace sim = tick ? oracle::tick_simulate(*gp) : simulate(*gp);
+    for (const auto& e : sim.entries) {
+      start[e.task_id] = e.sim_start;
+      fin[e.task_id] = e.sim_end;
+    }
+    span[0] = sim.start;
+    span[1] = sim.end;
+    span[2] = sim.makespan;
+    return 0;
+  });
+}
+
+int ref_simulate(void* h, const int64_t* dur, int64_t* start, int64_t* fin, int64_t* span) {
+  return run_sim(h, dur, start, fin, span, false);
+}
+
+int ref_tick_simulate(void* h, const int64_t* dur, int64_t* start, int64_t* fin,
+                      int64_t* span) {
+  return run_sim(h, dur, start, fin, span, true);
+}
+
+// breakdown_by_rank over the simulated intervals; out is [max_ranks][6] =
+// {rank, total, exposed_compute, exposed_comm, overlapped, other}
+int ref_breakdown_by_rank(void* h, const int64_t* start, const int64_t* fin, int64_t wstart,
+                          int64_t wend, int64_t* out, int max_ranks) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  SimulatedTrace sim;
+  for (std::size_t i = 0; i < g.tasks.size(); ++i)
+    sim.entries.push_back({static_cast<TaskId>(i), start[i], fin[i], g.tasks[i].processor});
+  auto by_rank = breakdown_by_rank(task_intervals(g, &sim), IterationWindow{wstart, wend});
+  int k = 0;
+  for (const auto& [rank, b] : by_rank) {
+    if (k >= max_ranks) break;
+    int64_t* row = out + 6 * k;
+    row[0] = rank;
+    row[1] = b.total;
+    row[2] = b.exposed_compute;
+    row[3] = b.exposed_comm;
+    row[4] = b.overlapped;
+    row[5] = b.other;
+    ++k;
+  }
+  return k;
+}
+
+// ------------------------------------------------------ CPU baseline timing
+
+// Times the reference simulate() over `count` scenarios whose durations come
+// from the oracle's scenario formula (lumos_oracle.c), one scenario per call,
+// on `threads` host threads (each with its own graph copy).  Returns wall
+// seconds of the parallel region (duration fill + simulate; graph copies are
+// made before the clock starts).  makespans[i] receives scenario i's makespan.
+double ref_bench_simulate(void* h, const orc_scenarios* sc, int64_t first, int32_t count,
+                          const uint8_t* cls, int threads, int64_t* makespans) {
+  const ExecutionGraph& src = static_cast<RefGraph*>(h)->g;
+  if (threads < 1) threads = 1;
+  std::vector<ExecutionGraph> copies(static_cast<std::size_t>(threads), src);
+  std::vector<int64_t> base(src.tasks.size());
+  for (std::size_t i = 0; i < src.tasks.size(); ++i) base[i] = src.tasks[i].duration;
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int w = 0; w < threads; ++w) {
+    pool.emplace_back([&, w] {
+      ExecutionGraph& g = copies[static_cast<std::size_t>(w)];
+      std::vector<int64_t> dur(g.tasks.size());
+      for (int32_t s = w; s < count; s += threads) {
+        orc_fill_durations(sc, first + s, static_cast<int32_t>(g.tasks.size()), base.data(),
+                           cls, dur.data());
+        for (std::size_t i = 0; i < g.tasks.size(); ++i) g.tasks[i].duration = dur[i];
+        try {
+          makespans[s] = simulate(g).makespan;
+        } catch (const std::exception&) {
+          makespans[s] = -1;
+        }
+      }
+    });
+  }
+  for (auto& t : pool) t.join();
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"

@@ -1,0 +1,515 @@
+// capi.cpp — the extern "C" boundary (include/lumos_b200.h).
+//
+// Owns the device copy of a compiled graph and sequences the kernels of one
+// batched replay: span init -> K1 walk (durations fused) -> span finalize ->
+// K5 per-rank reductions.  All device work is enqueued on the caller's
+// stream; host-side output pointers are staged and copied back at the end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "compile.hpp"
+#include "kernels.hpp"
+#include "lumos_b200.h"
+
+using namespace lumos;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(TS_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(_e) + " (" + \
+                                 #expr + ")");                                            \
+  } while (0)
+
+template <class T>
+cudaError_t upload(T** dptr, const std::vector<T>& v) {
+  *dptr = nullptr;
+  if (v.empty()) return cudaSuccess;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dptr), v.size() * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+uint32_t seed_key(uint64_t seed, uint32_t salt) {
+  return static_cast<uint32_t>(seed ^ (seed >> 32)) ^ salt;
+}
+
+// device buffer that grows on demand
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct ts_graph {
+  CompiledGraph cg;
+  int device = -1;
+  bool has_device = false;
+  Op* d_ops = nullptr;
+  ProgramDesc* d_progs = nullptr;
+  ComponentDesc* d_comps = nullptr;
+  int32_t* d_comp_order = nullptr;
+  int64_t* d_base = nullptr;
+  uint8_t* d_cls = nullptr;
+  uint8_t* d_is_comm = nullptr;
+  int32_t* d_rank_stream_off = nullptr;
+  int32_t* d_stream_node_off = nullptr;
+  int32_t* d_stream_nodes = nullptr;
+  DevBuf span_lo, span_hi, status, scratch_ts, stage_out, stage_in;
+};
+
+extern "C" {
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+const char* ts_last_error(void) { return g_err.c_str(); }
+int64_t ts_kernel_launches(void) { return g_launches.load(); }
+
+int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
+  if (!desc || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  auto* g = new ts_graph;
+  std::string err;
+  int rc = compile_graph(*desc, g->cg, err);
+  if (rc != TS_OK) {
+    delete g;
+    return fail(rc, err);
+  }
+  if (device == -2) {  // compile only (host-side inspection; no replay possible)
+    *out = g;
+    return TS_OK;
+  }
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+    cudaGetLastError();
+    delete g;
+    return fail(TS_E_CUDA, "no CUDA device: the replay engine runs only on the GPU");
+  }
+  if (device >= 0) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+      delete g;
+      return fail(TS_E_CUDA, "cudaSetDevice failed");
+    }
+    g->device = device;
+  } else {
+    cudaGetDevice(&g->device);
+  }
+  const CompiledGraph& c = g->cg;
+  for (size_t r = 0; r + 1 < c.rank_stream_off.size(); ++r)
+    if (c.rank_stream_off[r + 1] - c.rank_stream_off[r] > max_streams_per_rank()) {
+      delete g;
+      return fail(TS_E_UNSUPPORTED, "rank has more than " +
+                                        std::to_string(max_streams_per_rank()) + " streams");
+    }
+  // launch order: longest component first (smaller tail)
+  std::vector<int32_t> order(c.comps.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return c.programs[c.comps[a].program].n_ops > c.programs[c.comps[b].program].n_ops;
+  });
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = upload(&g->d_ops, c.ops);
+  if (e == cudaSuccess) e = upload(&g->d_progs, c.programs);
+  if (e == cudaSuccess) e = upload(&g->d_comps, c.comps);
+  if (e == cudaSuccess) e = upload(&g->d_comp_order, order);
+  if (e == cudaSuccess) e = upload(&g->d_base, c.base);
+  if (e == cudaSuccess) e = upload(&g->d_cls, c.scale_class);
+  if (e == cudaSuccess) e = upload(&g->d_is_comm, c.is_comm);
+  if (e == cudaSuccess) e = upload(&g->d_rank_stream_off, c.rank_stream_off);
+  if (e == cudaSuccess) e = upload(&g->d_stream_node_off, c.stream_node_off);
+  if (e == cudaSuccess) e = upload(&g->d_stream_nodes, c.stream_nodes);
+  g->has_device = true;
+  if (e != cudaSuccess) {
+    ts_graph_destroy(g);
+    return fail(TS_E_CUDA, std::string("upload failed: ") + cudaGetErrorString(e));
+  }
+  *out = g;
+  return TS_OK;
+}
+
+void ts_graph_destroy(ts_graph* g) {
+  if (!g) return;
+  if (g->has_device) {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (g->device >= 0) cudaSetDevice(g->device);
+    for (void* p : {static_cast<void*>(g->d_ops), static_cast<void*>(g->d_progs),
+                    static_cast<void*>(g->d_comps), static_cast<void*>(g->d_comp_order),
+                    static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
+                    static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
+                    static_cast<void*>(g->d_stream_node_off),
+                    static_cast<void*>(g->d_stream_nodes)})
+      if (p) cudaFree(p);
+    for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts, &g->stage_out,
+                      &g->stage_in})
+      b->release();
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  delete g;
+}
+
+int ts_graph_get_info(const ts_graph* g, ts_graph_info* out) {
+  if (!g || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  const CompiledGraph& c = g->cg;
+  out->n_tasks = c.n_tasks;
+  out->n_components = static_cast<int32_t>(c.comps.size());
+  out->n_programs = static_cast<int32_t>(c.programs.size());
+  out->n_ranks = static_cast<int32_t>(c.ranks.size());
+  out->n_streams = static_cast<int32_t>(c.stream_rank.size());
+  out->max_slots = c.max_slots;
+  out->program_bytes = static_cast<int64_t>(c.ops.size() * sizeof(Op));
+  out->n_ops = static_cast<int64_t>(c.ops.size());
+  out->n_syncs = c.n_syncs;
+  out->n_gpu_tasks = c.n_gpu_tasks;
+  out->window_start = c.window_start;
+  out->window_end = c.window_end;
+  return TS_OK;
+}
+
+int ts_graph_ranks(const ts_graph* g, int32_t* ranks) {
+  if (!g || !ranks) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  std::copy(g->cg.ranks.begin(), g->cg.ranks.end(), ranks);
+  return TS_OK;
+}
+
+int ts_graph_streams(const ts_graph* g, int32_t* rank, int32_t* lane) {
+  if (!g || !rank || !lane) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  std::copy(g->cg.stream_rank.begin(), g->cg.stream_rank.end(), rank);
+  std::copy(g->cg.stream_lane.begin(), g->cg.stream_lane.end(), lane);
+  return TS_OK;
+}
+
+static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioParams& sp) {
+  std::memset(&sp, 0, sizeof(sp));
+  if (sc->count < 0) return fail(TS_E_INVALID_ARGUMENT, "scenario count must be >= 0");
+  sp.first = sc->first;
+  sp.count = sc->count;
+  sp.key_jit = seed_key(sc->seed, 0u);
+  sp.key_cls = seed_key(sc->seed, 0x5CA1E000u);
+  sp.den_shift = -1;
+  sp.n_classes = 0;
+  if (sc->durations) {
+    if (sc->durations_ld < sc->count)
+      return fail(TS_E_INVALID_ARGUMENT, "durations_ld must be >= count");
+    sp.mode = kModeExplicit;
+    sp.durations = sc->durations;
+    sp.durations_ld = sc->durations_ld;
+    return TS_OK;
+  }
+  if (sc->jitter != 0.0) {
+    if (!(sc->jitter > 0.0 && sc->jitter < 1.0))
+      return fail(TS_E_INVALID_ARGUMENT, "jitter must be in [0, 1)");
+    sp.mode |= kModeJitter;
+    sp.two_j = 2.0 * sc->jitter;
+    sp.neg_j = -sc->jitter;
+  }
+  if (sc->scale_den > 0) {
+    sp.mode |= kModeScale;
+    sp.scale_den = sc->scale_den;
+    if ((sc->scale_den & (sc->scale_den - 1)) == 0) {
+      int s = 0;
+      while ((1LL << s) < sc->scale_den) ++s;
+      sp.den_shift = s;
+    }
+    if (sc->scale_num) {
+      if (sc->n_classes < 1 || sc->n_classes > kMaxClasses)
+        return fail(TS_E_INVALID_ARGUMENT, "n_classes must be in [1, 4]");
+      sp.scale_num = sc->scale_num;
+      sp.n_classes = sc->n_classes;
+      sp.n_classes_eff = sc->n_classes;
+    } else {
+      if (sc->scale_lo < 0 || sc->scale_hi < sc->scale_lo)
+        return fail(TS_E_INVALID_ARGUMENT, "need 0 <= scale_lo <= scale_hi");
+      sp.scale_lo = sc->scale_lo;
+      sp.scale_span = static_cast<uint32_t>(sc->scale_hi - sc->scale_lo + 1);
+      sp.n_classes_eff = kMaxClasses;
+    }
+  }
+  (void)g;
+  return TS_OK;
+}
+
+int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, void* stream_) {
+  if (!g || !sc || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  if (!g->has_device) return fail(TS_E_CUDA, "graph was compiled without a device");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  ScenarioParams sp;
+  if (int rc = scenario_params(g, sc, sp)) return rc;
+  const CompiledGraph& c = g->cg;
+  const int32_t count = sc->count;
+  if (count == 0) return TS_OK;
+  if ((out->start || out->fin) && out->ld < count)
+    return fail(TS_E_INVALID_ARGUMENT, "ld must be >= count");
+  int prev_dev = -1;
+  cudaGetDevice(&prev_dev);
+  if (prev_dev != g->device) CUDA_TRY(cudaSetDevice(g->device));
+
+  // inputs given as host memory are staged on the device
+  std::vector<void*> owned;
+  auto stage_in = [&](const void* host, size_t bytes, const void** dev) -> cudaError_t {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return e;
+    owned.push_back(p);
+    *dev = p;
+    return cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, stream);
+  };
+  auto cleanup = [&] {
+    for (void* p : owned) cudaFree(p);
+    owned.clear();
+  };
+  if (sp.scale_num && !is_device_ptr(sp.scale_num)) {
+    const void* d = nullptr;
+    cudaError_t e = stage_in(sp.scale_num, static_cast<size_t>(count) * sp.n_classes * 4, &d);
+    if (e != cudaSuccess) {
+      cleanup();
+      return fail(TS_E_CUDA, cudaGetErrorString(e));
+    }
+    sp.scale_num = static_cast<const int32_t*>(d);
+  }
+  if (sp.durations && !is_device_ptr(sp.durations)) {
+    const void* d = nullptr;
+    cudaError_t e = stage_in(sp.durations,
+                             static_cast<size_t>(c.n_tasks) * sp.durations_ld * 8, &d);
+    if (e != cudaSuccess) {
+      cleanup();
+      return fail(TS_E_CUDA, cudaGetErrorString(e));
+    }
+    sp.durations = static_cast<const int64_t*>(d);
+  }
+
+  // outputs: device pointers are written in place, host pointers staged
+  const bool want_ts = out->start || out->fin;
+  const bool want_red = out->rank_breakdown || out->stream_busy;
+  const int32_t n_ranks = static_cast<int32_t>(c.ranks.size());
+  const int32_t n_streams = static_cast<int32_t>(c.stream_rank.size());
+  struct OutBuf {
+    void* user;
+    size_t bytes;
+    void* dev;
+  };
+  std::vector<OutBuf> copies;
+  auto out_ptr = [&](void* user, size_t bytes) -> void* {
+    if (!user) return nullptr;
+    if (is_device_ptr(user)) return user;
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    owned.push_back(p);
+    copies.push_back({user, bytes, p});
+    return p;
+  };
+  const size_t ts_bytes = static_cast<size_t>(c.n_tasks) * static_cast<size_t>(out->ld) * 8;
+  int64_t* d_start = static_cast<int64_t*>(out_ptr(out->start, ts_bytes));
+  int64_t* d_fin = static_cast<int64_t*>(out_ptr(out->fin, ts_bytes));
+  int64_t* d_span = static_cast<int64_t*>(out_ptr(out->span, static_cast<size_t>(count) * 24));
+  int64_t* d_bd = static_cast<int64_t*>(
+      out_ptr(out->rank_breakdown, static_cast<size_t>(count) * n_ranks * 40));
+  int64_t* d_busy = static_cast<int64_t*>(
+      out_ptr(out->stream_busy, static_cast<size_t>(count) * n_streams * 8));
+  if ((out->start && !d_start) || (out->fin && !d_fin) || (out->span && !d_span) ||
+      (out->rank_breakdown && !d_bd) || (out->stream_busy && !d_busy)) {
+    cleanup();
+    return fail(TS_E_NOMEM, "could not stage output buffers");
+  }
+
+  CUDA_TRY(g->span_lo.reserve(static_cast<size_t>(count) * 8));
+  CUDA_TRY(g->span_hi.reserve(static_cast<size_t>(count) * 8));
+  CUDA_TRY(g->status.reserve(static_cast<size_t>(count) * 4));
+  int64_t* lo = g->span_lo.as<int64_t>();
+  int64_t* hi = g->span_hi.as<int64_t>();
+  int32_t* status = g->status.as<int32_t>();
+
+  // timestamps needed for the reductions but not requested: sub-batch through
+  // an internal scratch tile
+  int32_t sub = count;
+  int64_t* s_start = d_start;
+  int64_t* s_fin = d_fin;
+  int64_t s_ld = out->ld;
+  if (want_red && !want_ts) {
+    const size_t budget = size_t(4) << 30;
+    const size_t per_col = static_cast<size_t>(c.n_tasks) * 16 + 1;
+    size_t cols = std::max<size_t>(128, budget / per_col / 128 * 128);
+    sub = static_cast<int32_t>(std::min<size_t>(cols, static_cast<size_t>(count)));
+    CUDA_TRY(g->scratch_ts.reserve(static_cast<size_t>(sub) * per_col));
+    s_start = g->scratch_ts.as<int64_t>();
+    s_fin = s_start + static_cast<size_t>(c.n_tasks) * sub;
+    s_ld = sub;
+  }
+
+  CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
+  g_launches++;
+  for (int32_t b0 = 0; b0 < count; b0 += sub) {
+    const int32_t bn = std::min(sub, count - b0);
+    WalkParams wp{};
+    wp.ops = g->d_ops;
+    wp.progs = g->d_progs;
+    wp.comps = g->d_comps;
+    wp.comp_order = g->d_comp_order;
+    wp.n_comps = static_cast<int32_t>(c.comps.size());
+    wp.window_start = c.window_start;
+    wp.sp = sp;
+    wp.sp.first = sp.first + b0;
+    wp.sp.count = bn;
+    if (sp.scale_num) wp.sp.scale_num = sp.scale_num + static_cast<size_t>(b0) * sp.n_classes;
+    if (sp.durations) wp.sp.durations = sp.durations + b0;
+    const bool own_tile = s_start != d_start || s_fin != d_fin;
+    wp.out_start = own_tile ? s_start : (d_start ? d_start + b0 : nullptr);
+    wp.out_fin = own_tile ? s_fin : (d_fin ? d_fin + b0 : nullptr);
+    wp.ld = s_ld;
+    wp.span_lo = lo + b0;
+    wp.span_hi = hi + b0;
+    wp.status = status + b0;
+    if (wp.n_comps > 0) {
+      CUDA_TRY(launch_replay_walk(wp, c.max_slots, stream));
+      g_launches++;
+    }
+    if (want_red) {
+      ReduceParams rp{};
+      rp.rank_stream_off = g->d_rank_stream_off;
+      rp.stream_node_off = g->d_stream_node_off;
+      rp.stream_nodes = g->d_stream_nodes;
+      rp.is_comm = g->d_is_comm;
+      rp.start = wp.out_start;
+      rp.fin = wp.out_fin;
+      rp.ld = s_ld;
+      rp.span_lo = lo + b0;
+      rp.span_hi = hi + b0;
+      rp.window_start = c.window_start;
+      rp.window_end = c.window_end;
+      rp.count = bn;
+      rp.n_ranks = n_ranks;
+      rp.n_streams = n_streams;
+      rp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
+      rp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
+      CUDA_TRY(launch_rank_reduce(rp, stream));
+      g_launches++;
+    }
+  }
+  if (d_span) {
+    CUDA_TRY(launch_span_finalize(lo, hi, c.window_start, d_span, nullptr, count, stream));
+    g_launches++;
+  }
+
+  // certificate failures need the exact event-driven path
+  std::vector<int32_t> host_status;
+  if (c.n_syncs > 0 || out->status) {
+    host_status.resize(count);
+    CUDA_TRY(cudaMemcpyAsync(host_status.data(), status, static_cast<size_t>(count) * 4,
+                             cudaMemcpyDeviceToHost, stream));
+  }
+  for (const OutBuf& b : copies)
+    CUDA_TRY(cudaMemcpyAsync(b.user, b.dev, b.bytes, cudaMemcpyDeviceToHost, stream));
+  if (!copies.empty() || !host_status.empty()) CUDA_TRY(cudaStreamSynchronize(stream));
+  cleanup();
+  if (out->status) {
+    if (is_device_ptr(out->status))
+      CUDA_TRY(cudaMemcpyAsync(out->status, status, static_cast<size_t>(count) * 4,
+                               cudaMemcpyDeviceToDevice, stream));
+    else
+      std::memcpy(out->status, host_status.data(), static_cast<size_t>(count) * 4);
+  }
+  int64_t n_fail = 0;
+  for (int32_t s : host_status) n_fail += s != 0;
+  if (prev_dev >= 0 && prev_dev != g->device) cudaSetDevice(prev_dev);
+  if (n_fail > 0)
+    return fail(TS_E_UNSUPPORTED,
+                std::to_string(n_fail) +
+                    " scenario(s) failed the static sync-binding certificate and need the "
+                    "exact event-driven replay");
+  return TS_OK;
+}
+
+int ts_simulate(ts_graph* g, int64_t* start, int64_t* fin, int64_t* span) {
+  if (!g) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  ts_scenarios sc{};
+  sc.count = 1;
+  ts_result r{};
+  r.start = start;
+  r.fin = fin;
+  r.ld = 1;
+  r.span = span;
+  return ts_replay_batch(g, &sc, &r, nullptr);
+}
+
+int ts_scenario_durations(ts_graph* g, const ts_scenarios* sc, int64_t* dur, int64_t ld,
+                          void* stream_) {
+  if (!g || !sc || !dur) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  if (!g->has_device) return fail(TS_E_CUDA, "graph was compiled without a device");
+  if (ld < sc->count) return fail(TS_E_INVALID_ARGUMENT, "ld must be >= count");
+  ScenarioParams sp;
+  if (int rc = scenario_params(g, sc, sp)) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  const size_t bytes = static_cast<size_t>(g->cg.n_tasks) * static_cast<size_t>(ld) * 8;
+  int64_t* d = dur;
+  void* tmp = nullptr;
+  if (!is_device_ptr(dur)) {
+    CUDA_TRY(cudaMalloc(&tmp, bytes));
+    d = static_cast<int64_t*>(tmp);
+  }
+  const int32_t* staged_num = nullptr;
+  void* tmp_num = nullptr;
+  if (sp.scale_num && !is_device_ptr(sp.scale_num)) {
+    size_t nb = static_cast<size_t>(sc->count) * sp.n_classes * 4;
+    CUDA_TRY(cudaMalloc(&tmp_num, nb));
+    CUDA_TRY(cudaMemcpyAsync(tmp_num, sp.scale_num, nb, cudaMemcpyHostToDevice, stream));
+    staged_num = static_cast<const int32_t*>(tmp_num);
+    sp.scale_num = staged_num;
+  }
+  CUDA_TRY(launch_durations(sp, g->d_base, g->d_cls, g->cg.n_tasks, d, ld, stream));
+  g_launches++;
+  if (tmp) {
+    CUDA_TRY(cudaMemcpyAsync(dur, d, bytes, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaFree(tmp);
+  }
+  if (tmp_num) {
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaFree(tmp_num);
+  }
+  return TS_OK;
+}
+
+}  // extern "C"

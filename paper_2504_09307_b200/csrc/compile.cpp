@@ -1,0 +1,913 @@
+// compile.cpp — ExecutionGraph -> straight-line replay programs (host side).
+//
+// Reference semantics being compiled (paths under /root/reference/proj):
+//   validate_graph                      src/simulate.cpp:26-125
+//   Engine (lanes, ready sets, rules)   src/simulate.cpp:145-337
+//   lane chains                         src/build.cpp:375-386
+//   Stream/DeviceSync rules             src/build.cpp:169-224, simulate.cpp:210-216
+//   EventSync rules                     src/simulate.cpp:206-209
+//   generator barrier / rendezvous      src/pipeline.cpp:377-389 (gates)
+//
+// On a graph whose lanes are chained (each lane's tasks, in (original_start,
+// id) order, are linked by fixed edges — true for every build_graph output),
+// at most one task per lane is ever ready, so dispatch order never matters and
+// the replay is the max-plus longest path
+//     start(v) = max(W, finish(preds)),  finish(v) = start(v) + d(v).
+// EventSync adds the edge bound -> waiting task.  A Stream/DeviceSync task s
+// starts at the first instant >= its ready time r_s at which every watched
+// stream is idle with nothing pending.  We bind it statically to k*_w, the last
+// kernel of each watched stream enqueued before s (the launch order build_graph
+// uses, build.cpp:426-434), and emit a per-scenario certificate that the
+// static start S = max(r_s, finish(k*_w)) equals the reference's instant:
+//   (a) S == r_s, or some watched stream w0 with finish(k*_w0) == S was busy
+//       without a gap over [r_s, S) (busy-since(k*_w0) <= r_s), and
+//   (b) for every watched stream whose next kernel n_w is not a descendant of
+//       s, start(n_w) > S (nothing else occupies or becomes ready on it at S).
+// A scenario whose certificate fails is flagged and replayed by the exact
+// event-driven kernel instead.
+#include "compile.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <sstream>
+#include <tuple>
+#include <unordered_map>
+
+namespace lumos {
+
+namespace {
+
+struct Proc {
+  int32_t rank, kind, lane;
+  bool operator<(const Proc& o) const {
+    return std::tie(rank, kind, lane) < std::tie(o.rank, o.kind, o.lane);
+  }
+  bool operator==(const Proc& o) const {
+    return rank == o.rank && kind == o.kind && lane == o.lane;
+  }
+};
+
+struct Csr {
+  std::vector<int64_t> off;
+  std::vector<int32_t> idx;
+  int64_t begin(int64_t v) const { return off[v]; }
+  int64_t end(int64_t v) const { return off[v + 1]; }
+};
+
+Csr build_csr(int64_t n, const std::vector<std::pair<int32_t, int32_t>>& edges, bool forward) {
+  Csr c;
+  c.off.assign(n + 1, 0);
+  for (const auto& e : edges) c.off[(forward ? e.first : e.second) + 1]++;
+  for (int64_t i = 0; i < n; ++i) c.off[i + 1] += c.off[i];
+  c.idx.resize(edges.size());
+  std::vector<int64_t> fill(c.off.begin(), c.off.end() - 1);
+  for (const auto& e : edges) {
+    int32_t a = forward ? e.first : e.second;
+    int32_t b = forward ? e.second : e.first;
+    c.idx[fill[a]++] = b;
+  }
+  return c;
+}
+
+std::string join_ids(const std::vector<int32_t>& ids) {
+  std::ostringstream os;
+  for (size_t i = 0; i < ids.size(); ++i) os << (i ? " " : "") << ids[i];
+  return os.str();
+}
+
+struct IrOp {
+  Op op{};
+  int64_t v_pred[4] = {-1, -1, -1, -1};
+  int64_t v_dst = -1, v_x0 = -1, v_x1 = -1, v_x2 = -1;
+  bool is_ext = false;
+  int64_t v_fin[kCertPerExt] = {-1, -1, -1, -1};
+  int64_t v_bs[kCertPerExt] = {-1, -1, -1, -1};
+  int64_t v_next[kCertPerExt] = {-1, -1, -1, -1};
+  int32_t n_ent = 0;
+  bool is_cov = false;
+  int64_t v_cov_src[kCovSets][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
+  int64_t v_cov_dst[kCovSets] = {-1, -1};
+  int n_sets = 0;
+  bool aux() const { return is_ext || is_cov; }
+};
+
+struct CertEntry {
+  int32_t kstar;  // -1: no kernel bound before the sync
+  int32_t next;   // -1: none or a descendant of the sync
+};
+
+}  // namespace
+
+int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
+  const int32_t n = d.n_tasks;
+  if (n < 0) {
+    err = "n_tasks must be non-negative";
+    return TS_E_INVALID_ARGUMENT;
+  }
+  out = CompiledGraph{};
+  out.n_tasks = n;
+  out.window_start = d.window_start;
+  out.window_end = d.window_end;
+
+  // ---------------------------------------------------------- validate_graph
+  for (int32_t i = 0; i < n; ++i)
+    if (d.duration[i] < 0) {
+      err = "invalid graph: task " + std::to_string(i) + " has negative duration";
+      return TS_E_SIMULATION;
+    }
+  std::vector<std::pair<int32_t, int32_t>> fixed;
+  fixed.reserve(static_cast<size_t>(d.n_edges));
+  for (int64_t e = 0; e < d.n_edges; ++e) {
+    int32_t u = d.edge_from[e], v = d.edge_to[e];
+    if (u < 0 || u >= n || v < 0 || v >= n || u == v) {
+      err = "invalid graph: edge " + std::to_string(u) + "->" + std::to_string(v) +
+            " references an invalid task";
+      return TS_E_SIMULATION;
+    }
+    fixed.emplace_back(u, v);
+  }
+  for (int32_t r = 0; r < d.n_rules; ++r) {
+    int32_t w = d.rule_task[r], b = d.rule_bound ? d.rule_bound[r] : -1;
+    if (w < 0 || w >= n || (b >= 0 && b >= n)) {
+      err = "invalid graph: rule on task " + std::to_string(w) + " references an invalid task";
+      return TS_E_SIMULATION;
+    }
+  }
+  std::sort(fixed.begin(), fixed.end());
+  fixed.erase(std::unique(fixed.begin(), fixed.end()), fixed.end());
+  Csr succ = build_csr(n, fixed, true);
+  Csr pred = build_csr(n, fixed, false);
+  {
+    // Kahn cycle check with the reference's witness walk (simulate.cpp:79-121)
+    std::vector<int32_t> left(n, 0);
+    for (const auto& e : fixed) left[e.second]++;
+    std::vector<int32_t> q;
+    q.reserve(n);
+    for (int32_t i = 0; i < n; ++i)
+      if (left[i] == 0) q.push_back(i);
+    for (size_t h = 0; h < q.size(); ++h)
+      for (int64_t k = succ.begin(q[h]); k < succ.end(q[h]); ++k)
+        if (--left[succ.idx[k]] == 0) q.push_back(succ.idx[k]);
+    if (static_cast<int32_t>(q.size()) != n) {
+      int32_t cur = -1;
+      for (int32_t i = 0; i < n && cur < 0; ++i)
+        if (left[i] > 0) cur = i;
+      std::vector<int32_t> path;
+      std::vector<char> on_path(n, 0);
+      while (cur >= 0 && !on_path[cur]) {
+        on_path[cur] = 1;
+        path.push_back(cur);
+        int32_t next = -1;
+        for (int64_t k = pred.begin(cur); k < pred.end(cur); ++k) {
+          int32_t p = pred.idx[k];
+          if (left[p] > 0 && (next < 0 || p < next)) next = p;
+        }
+        cur = next;
+      }
+      std::vector<int32_t> cycle;
+      if (cur >= 0) {
+        auto it = std::find(path.begin(), path.end(), cur);
+        cycle.assign(it, path.end());
+        std::reverse(cycle.begin(), cycle.end());
+      }
+      err = "invalid graph: dependency cycle: " + join_ids(cycle);
+      return TS_E_SIMULATION;
+    }
+  }
+
+  // ---------------------------------------------------------------- lanes
+  std::vector<Proc> procs(n);
+  for (int32_t i = 0; i < n; ++i) procs[i] = {d.rank[i], d.lane_kind[i], d.lane[i]};
+  std::vector<Proc> lanes = procs;
+  std::sort(lanes.begin(), lanes.end());
+  lanes.erase(std::unique(lanes.begin(), lanes.end()), lanes.end());
+  const int32_t nl = static_cast<int32_t>(lanes.size());
+  auto lane_index = [&](const Proc& p) -> int32_t {
+    auto it = std::lower_bound(lanes.begin(), lanes.end(), p);
+    return (it != lanes.end() && *it == p) ? static_cast<int32_t>(it - lanes.begin()) : -1;
+  };
+  std::vector<int32_t> lane_of(n);
+  std::vector<int32_t> lane_off(nl + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    lane_of[i] = lane_index(procs[i]);
+    lane_off[lane_of[i] + 1]++;
+  }
+  for (int32_t l = 0; l < nl; ++l) lane_off[l + 1] += lane_off[l];
+  std::vector<int32_t> lane_tasks(n);
+  {
+    std::vector<int32_t> fill(lane_off.begin(), lane_off.end() - 1);
+    for (int32_t i = 0; i < n; ++i) lane_tasks[fill[lane_of[i]]++] = i;
+  }
+  std::vector<int32_t> chain_pos(n), chain_prev(n, -1);
+  auto has_edge = [&](int32_t u, int32_t v) {
+    auto b = succ.idx.begin() + succ.begin(u), e = succ.idx.begin() + succ.end(u);
+    return std::binary_search(b, e, v);
+  };
+  for (int32_t l = 0; l < nl; ++l) {
+    auto b = lane_tasks.begin() + lane_off[l], e = lane_tasks.begin() + lane_off[l + 1];
+    std::sort(b, e, [&](int32_t x, int32_t y) {
+      return std::make_pair(d.original_start[x], x) < std::make_pair(d.original_start[y], y);
+    });
+    for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k) {
+      int32_t t = lane_tasks[k];
+      chain_pos[t] = k - lane_off[l];
+      if (k > lane_off[l]) {
+        int32_t p = lane_tasks[k - 1];
+        if (!has_edge(p, t)) {
+          err = "unsupported graph: lane rank" + std::to_string(lanes[l].rank) +
+                (lanes[l].kind ? "/stream" : "/thread") + std::to_string(lanes[l].lane) +
+                " is not chained (no fixed edge " + std::to_string(p) + "->" +
+                std::to_string(t) + "); the device path replays chained lanes";
+          return TS_E_UNSUPPORTED;
+        }
+        chain_prev[t] = p;
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- rules
+  std::vector<int32_t> rule_of(n, -1);
+  for (int32_t r = 0; r < d.n_rules; ++r) rule_of[d.rule_task[r]] = r;  // later rule wins
+
+  // enqueue time of each kernel: its launch's recorded start (build.cpp:398-415)
+  std::vector<int64_t> enqueue_ts(n);
+  for (int32_t i = 0; i < n; ++i) {
+    enqueue_ts[i] = d.original_start[i];
+    if (d.lane_kind[i] != TS_LANE_CUDA_STREAM) continue;
+    for (int64_t k = pred.begin(i); k < pred.end(i); ++k) {
+      int32_t p = pred.idx[k];
+      if (d.lane_kind[p] == TS_LANE_CPU_THREAD && d.op_class &&
+          d.op_class[p] == TS_OP_LAUNCH) {
+        enqueue_ts[i] = d.original_start[p];
+        break;
+      }
+    }
+  }
+  // per stream lane: kernels sorted by enqueue time with prefix-max chain pos
+  std::vector<std::vector<std::pair<int64_t, int32_t>>> enq(nl);
+  auto enqueue_index = [&](int32_t l) -> std::vector<std::pair<int64_t, int32_t>>& {
+    auto& v = enq[l];
+    if (v.empty() && lane_off[l + 1] > lane_off[l]) {
+      for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k) {
+        int32_t t = lane_tasks[k];
+        v.emplace_back(enqueue_ts[t], chain_pos[t]);
+      }
+      std::sort(v.begin(), v.end());
+      for (size_t i = 1; i < v.size(); ++i) v[i].second = std::max(v[i].second, v[i - 1].second);
+    }
+    return v;
+  };
+
+  std::vector<int32_t> sync_tasks;
+  std::vector<std::vector<CertEntry>> sync_cert;  // per sync task (index into sync_tasks)
+  std::vector<std::vector<int32_t>> sync_watch;   // watched stream lanes
+  std::vector<int32_t> sync_id(n, -1);
+  std::vector<int32_t> event_bound(n, -1);
+  for (int32_t t = 0; t < n; ++t) {
+    int32_t r = rule_of[t];
+    if (r < 0) continue;
+    if (d.rule_kind[r] == TS_RULE_EVENT_SYNC) {
+      int32_t b = d.rule_bound ? d.rule_bound[r] : -1;
+      if (b >= 0) {
+        if (b == t) {
+          err = "unsupported graph: event sync task " + std::to_string(t) +
+                " is bound to itself (the reference deadlocks)";
+          return TS_E_UNSUPPORTED;
+        }
+        event_bound[t] = b;
+      }
+      continue;
+    }
+    std::vector<int32_t> watched;
+    for (int32_t w = d.rule_watch_off[r]; w < d.rule_watch_off[r + 1]; ++w) {
+      int32_t l = lane_index({d.watch_rank[w], d.watch_kind[w], d.watch_lane[w]});
+      if (l < 0) continue;  // processor without tasks: ignored (simulate.cpp:183-186)
+      if (lanes[l].kind != TS_LANE_CUDA_STREAM || l == lane_of[t]) {
+        err = "unsupported graph: sync task " + std::to_string(t) +
+              " watches a CPU lane or its own lane; the device path binds syncs to streams";
+        return TS_E_UNSUPPORTED;
+      }
+      watched.push_back(l);
+    }
+    std::sort(watched.begin(), watched.end());
+    watched.erase(std::unique(watched.begin(), watched.end()), watched.end());
+    if (watched.empty()) continue;  // no-op rule: plain task
+    std::vector<CertEntry> cert;
+    for (int32_t l : watched) {
+      auto& idx = enqueue_index(l);
+      // last (chain order) kernel whose launch precedes the sync (lower_bound
+      // on (ts, -1) like build.cpp:426-434)
+      auto it = std::lower_bound(idx.begin(), idx.end(),
+                                 std::make_pair(d.original_start[t], INT32_MIN));
+      int32_t pos = it == idx.begin() ? -1 : std::prev(it)->second;
+      CertEntry ce;
+      ce.kstar = pos >= 0 ? lane_tasks[lane_off[l] + pos] : -1;
+      int32_t np = pos + 1;
+      ce.next = np < lane_off[l + 1] - lane_off[l] ? lane_tasks[lane_off[l] + np] : -1;
+      cert.push_back(ce);
+    }
+    sync_id[t] = static_cast<int32_t>(sync_tasks.size());
+    sync_tasks.push_back(t);
+    sync_cert.push_back(std::move(cert));
+    sync_watch.push_back(std::move(watched));
+  }
+  out.n_syncs = static_cast<int32_t>(sync_tasks.size());
+
+  // ---------------------------------------------------------------- gates
+  std::vector<char> split(n, 0);  // task needs a separate START op
+  std::vector<std::vector<std::pair<int32_t, uint8_t>>> gates_of;  // per task (sparse)
+  std::unordered_map<int32_t, int32_t> gate_slot;
+  for (int64_t gi = 0; gi < d.n_gates; ++gi) {
+    int32_t u = d.gate_from[gi], v = d.gate_to[gi];
+    uint8_t k = d.gate_kind[gi];
+    if (u < 0 || u >= n || v < 0 || v >= n || u == v || k > TS_GATE_START) {
+      err = "invalid graph: gate " + std::to_string(u) + "->" + std::to_string(v) +
+            " references an invalid task";
+      return TS_E_SIMULATION;
+    }
+    auto [it, fresh] = gate_slot.try_emplace(v, static_cast<int32_t>(gates_of.size()));
+    if (fresh) gates_of.emplace_back();
+    gates_of[it->second].emplace_back(u, k);
+    if (k == TS_GATE_START) split[v] = 1;
+  }
+  for (int32_t t : sync_tasks)
+    if (split[t] || gate_slot.count(t)) {
+      err = "unsupported graph: sync task " + std::to_string(t) + " carries gates";
+      return TS_E_UNSUPPORTED;
+    }
+  std::vector<int32_t> split_idx(n, -1);
+  int32_t n_split = 0;
+  for (int32_t i = 0; i < n; ++i)
+    if (split[i]) split_idx[i] = n_split++;
+  const int64_t na = static_cast<int64_t>(n) + n_split;  // aug nodes
+  auto snode = [&](int32_t v) -> int32_t { return split[v] ? n + split_idx[v] : v; };
+
+  // ------------------------------------------------------ augmented graph
+  std::vector<std::pair<int32_t, int32_t>> aug;
+  aug.reserve(fixed.size() + static_cast<size_t>(n_split) + 16);
+  for (const auto& e : fixed) aug.emplace_back(e.first, snode(e.second));
+  for (int32_t t = 0; t < n; ++t)
+    if (event_bound[t] >= 0) aug.emplace_back(event_bound[t], snode(t));
+  for (size_t s = 0; s < sync_tasks.size(); ++s)
+    for (const auto& ce : sync_cert[s])
+      if (ce.kstar >= 0) aug.emplace_back(ce.kstar, sync_tasks[s]);
+  for (const auto& [v, gi] : gate_slot)
+    for (const auto& [u, k] : gates_of[gi]) aug.emplace_back(k == TS_GATE_START ? snode(u) : u, v);
+  for (int32_t v = 0; v < n; ++v)
+    if (split[v]) aug.emplace_back(snode(v), v);
+
+  // topological index (any order) of the augmented graph, for reachability
+  std::vector<int32_t> topo(na, -1);
+  {
+    Csr as = build_csr(na, aug, true);
+    std::vector<int32_t> left(na, 0);
+    for (const auto& e : aug) left[e.second]++;
+    std::vector<int32_t> q;
+    q.reserve(na);
+    for (int32_t i = 0; i < na; ++i)
+      if (left[i] == 0) q.push_back(i);
+    for (size_t h = 0; h < q.size(); ++h)
+      for (int64_t k = as.begin(q[h]); k < as.end(q[h]); ++k)
+        if (--left[as.idx[k]] == 0) q.push_back(as.idx[k]);
+    if (static_cast<int64_t>(q.size()) != na) {
+      err = "unsupported graph: sync or gate bindings form a cycle (the reference would "
+            "deadlock or needs the event-driven path)";
+      return TS_E_UNSUPPORTED;
+    }
+    for (size_t i = 0; i < q.size(); ++i) topo[q[i]] = static_cast<int32_t>(i);
+    // certificate successors: keep n_w only when it is not a descendant of s
+    std::vector<int32_t> stamp(na, -1);
+    std::vector<int32_t> stack;
+    int32_t stamp_id = 0;
+    for (size_t s = 0; s < sync_tasks.size(); ++s) {
+      for (auto& ce : sync_cert[s]) {
+        if (ce.next < 0) continue;
+        int32_t src = sync_tasks[s], dst = ce.next;
+        bool reach = false;
+        if (topo[dst] > topo[src]) {
+          ++stamp_id;
+          stack.assign(1, src);
+          stamp[src] = stamp_id;
+          while (!stack.empty() && !reach) {
+            int32_t x = stack.back();
+            stack.pop_back();
+            for (int64_t k = as.begin(x); k < as.end(x); ++k) {
+              int32_t y = as.idx[k];
+              if (y == dst) {
+                reach = true;
+                break;
+              }
+              if (stamp[y] != stamp_id && topo[y] < topo[dst]) {
+                stamp[y] = stamp_id;
+                stack.push_back(y);
+              }
+            }
+          }
+        }
+        if (reach) ce.next = -1;
+      }
+    }
+  }
+  for (size_t s = 0; s < sync_tasks.size(); ++s)
+    for (const auto& ce : sync_cert[s])
+      if (ce.next >= 0) aug.emplace_back(snode(ce.next), sync_tasks[s]);  // order-only
+
+  // ----------------------------------------------------------- components
+  std::vector<int32_t> uf(na);
+  std::iota(uf.begin(), uf.end(), 0);
+  auto find = [&](int32_t x) {
+    while (uf[x] != x) x = uf[x] = uf[uf[x]];
+    return x;
+  };
+  for (const auto& e : aug) {
+    int32_t a = find(e.first), b = find(e.second);
+    if (a != b) uf[std::max(a, b)] = std::min(a, b);
+  }
+  // component id ordered by smallest task id
+  std::vector<int32_t> comp_of(na, -1);
+  std::vector<int32_t> root_comp(na, -1);
+  int32_t n_comp = 0;
+  for (int32_t v = 0; v < na; ++v) {
+    int32_t r = find(v);
+    if (root_comp[r] < 0) root_comp[r] = n_comp++;
+    comp_of[v] = root_comp[r];
+  }
+
+  // watched stream sets of the certified syncs; each stream lane keeps the
+  // coverage value of up to kCovSets of the sets it belongs to
+  std::vector<std::vector<int32_t>> sets;
+  std::vector<int32_t> sync_set(sync_tasks.size(), -1);
+  std::vector<std::vector<int32_t>> lane_sets(nl);
+  for (size_t s = 0; s < sync_tasks.size(); ++s) {
+    bool any = false;
+    for (const auto& ce : sync_cert[s]) any = any || ce.kstar >= 0;
+    if (!any) continue;
+    auto it = std::find(sets.begin(), sets.end(), sync_watch[s]);
+    if (it == sets.end()) {
+      sets.push_back(sync_watch[s]);
+      sync_set[s] = static_cast<int32_t>(sets.size() - 1);
+    } else {
+      sync_set[s] = static_cast<int32_t>(it - sets.begin());
+    }
+  }
+  for (size_t id = 0; id < sets.size(); ++id)
+    for (int32_t l : sets[id])
+      if (static_cast<int>(lane_sets[l].size()) < kCovSets)
+        lane_sets[l].push_back(static_cast<int32_t>(id));
+  auto set_index = [&](int32_t task, int32_t set_id) -> int {
+    const auto& v = lane_sets[lane_of[task]];
+    for (size_t j = 0; j < v.size(); ++j)
+      if (v[j] == set_id) return static_cast<int>(j);
+    return -1;
+  };
+
+  // values that are read by someone
+  std::vector<char> start_used(n, 0);
+  for (const auto& [v, gi] : gate_slot)
+    for (const auto& [u, k] : gates_of[gi])
+      if (k == TS_GATE_START) start_used[u] = 1;
+  for (size_t s = 0; s < sync_tasks.size(); ++s)
+    for (const auto& ce : sync_cert[s])
+      if (ce.next >= 0) start_used[ce.next] = 1;
+
+  // ------------------------------------------- priority topological order
+  // key: (component, host task after device task, original_start, id) — a
+  // kernel is consumed as soon as it can run, which keeps the live set small.
+  Csr as = build_csr(na, aug, true);
+  std::vector<int32_t> left(na, 0);
+  for (const auto& e : aug) left[e.second]++;
+  std::vector<int32_t> split_task(n_split);
+  for (int32_t v = 0; v < n; ++v)
+    if (split[v]) split_task[split_idx[v]] = v;
+  auto real_task = [&](int32_t a) { return a < n ? a : split_task[a - n]; };
+  using Key = std::tuple<int32_t, int32_t, int64_t, int32_t, int32_t>;
+  std::priority_queue<Key, std::vector<Key>, std::greater<>> heap;
+  auto push = [&](int32_t a) {
+    int32_t t = real_task(a);
+    int32_t cpu = d.lane_kind[t] == TS_LANE_CUDA_STREAM ? 0 : 1;
+    heap.emplace(comp_of[a], cpu, d.original_start[t], t, a);
+  };
+  for (int32_t a = 0; a < na; ++a)
+    if (left[a] == 0) push(a);
+  std::vector<int32_t> order;
+  order.reserve(na);
+  while (!heap.empty()) {
+    int32_t a = std::get<4>(heap.top());
+    heap.pop();
+    order.push_back(a);
+    for (int64_t k = as.begin(a); k < as.end(a); ++k)
+      if (--left[as.idx[k]] == 0) push(as.idx[k]);
+  }
+  if (static_cast<int64_t>(order.size()) != na) {
+    err = "unsupported graph: sync certificates impose a cyclic order";
+    return TS_E_UNSUPPORTED;
+  }
+
+  // ------------------------------------------------ op emission per component
+  // value ids: FIN(v) = v, START(v) = n + v, COV(v, j) = 2n + 2v + j, ACC >= 4n
+  const int64_t V_START = n, V_COV = 2LL * n, V_ACC = 4LL * n;
+  std::vector<int32_t> last_use(static_cast<size_t>(V_ACC), -1);
+  std::vector<int32_t> slot_of(static_cast<size_t>(V_ACC), kNoSlot);
+  int64_t acc_next = V_ACC;
+
+  std::vector<int32_t> comp_begin(n_comp + 1, 0);
+  for (int32_t a : order) comp_begin[comp_of[a] + 1]++;
+  for (int32_t c = 0; c < n_comp; ++c) comp_begin[c + 1] += comp_begin[c];
+
+  std::unordered_map<uint64_t, std::vector<int32_t>> prog_by_hash;
+  std::vector<IrOp> ir;
+  std::vector<int32_t> comp_tasks;
+  out.comps.resize(n_comp);
+
+  auto fold = [&](std::vector<int64_t>& vals, size_t room) {
+    std::vector<int64_t> u;
+    for (int64_t v : vals)
+      if (std::find(u.begin(), u.end(), v) == u.end()) u.push_back(v);
+    vals.swap(u);
+    while (vals.size() > room) {
+      size_t take = std::min<size_t>(4, vals.size());
+      IrOp acc;
+      acc.op.kind = OP_ACC;
+      acc.op.node = -1;
+      acc.op.flags = F_NO_OUT;
+      acc.op.npred = static_cast<uint8_t>(take);
+      for (size_t i = 0; i < take; ++i) acc.v_pred[i] = vals[i];
+      int64_t av = acc_next++;
+      acc.v_dst = av;
+      ir.push_back(acc);
+      vals.erase(vals.begin(), vals.begin() + static_cast<long>(take));
+      vals.insert(vals.begin(), av);
+    }
+  };
+
+  for (int32_t c = 0; c < n_comp; ++c) {
+    ir.clear();
+    comp_tasks.clear();
+    for (int32_t i = comp_begin[c]; i < comp_begin[c + 1]; ++i)
+      if (order[i] < n) comp_tasks.push_back(order[i]);
+    int32_t tmin = *std::min_element(comp_tasks.begin(), comp_tasks.end());
+    int32_t tmax = *std::max_element(comp_tasks.begin(), comp_tasks.end());
+    bool contiguous = tmax - tmin + 1 == static_cast<int32_t>(comp_tasks.size());
+    int32_t node_base = contiguous ? tmin : 0;
+
+    for (int32_t i = comp_begin[c]; i < comp_begin[c + 1]; ++i) {
+      int32_t a = order[i];
+      int32_t t = real_task(a);
+      bool is_start_node = a >= n;
+      bool gpu = d.lane_kind[t] == TS_LANE_CUDA_STREAM;
+      const auto& my_sets = lane_sets[lane_of[t]];
+      bool tracked = gpu && !my_sets.empty();
+      uint8_t cls = d.scale_class ? d.scale_class[t]
+                                  : static_cast<uint8_t>(d.task_kind && d.task_kind[t]
+                                                             ? (d.op_class && d.op_class[t] ==
+                                                                        TS_OP_COMMUNICATION
+                                                                    ? 2
+                                                                    : 1)
+                                                             : 0);
+      if (cls >= kMaxClasses) {
+        err = "scale_class must be < " + std::to_string(kMaxClasses);
+        return TS_E_INVALID_ARGUMENT;
+      }
+      uint8_t flags = (gpu ? F_GPU : 0) |
+                      (d.op_class && d.op_class[t] == TS_OP_COMMUNICATION ? F_COMM : 0);
+
+      // fixed predecessors (+ event-sync bound)
+      std::vector<int64_t> fixedv;
+      for (int64_t k = pred.begin(t); k < pred.end(t); ++k) fixedv.push_back(pred.idx[k]);
+      if (event_bound[t] >= 0) fixedv.push_back(event_bound[t]);
+
+      // coverage record following a tracked op (sources: kernel preds on the
+      // same watched set)
+      auto push_with_cov = [&](IrOp& o) {
+        if (!tracked) {
+          ir.push_back(o);
+          return;
+        }
+        o.op.flags |= F_TRACK;
+        ir.push_back(o);
+        IrOp cv;
+        cv.is_cov = true;
+        cv.n_sets = static_cast<int>(my_sets.size());
+        for (int j = 0; j < cv.n_sets; ++j) {
+          cv.v_cov_dst[j] = V_COV + 2LL * t + j;
+          for (int k = 0; k < o.op.npred; ++k) {
+            int64_t v = o.v_pred[k];
+            if (v < 0 || v >= n) continue;  // not a task finish (ACC / START value)
+            int32_t u = static_cast<int32_t>(v);
+            if (d.lane_kind[u] != TS_LANE_CUDA_STREAM) continue;
+            int ju = set_index(u, my_sets[j]);
+            if (ju >= 0) cv.v_cov_src[j][k] = V_COV + 2LL * u + ju;
+          }
+        }
+        ir.push_back(cv);
+      };
+
+      if (is_start_node) {
+        fold(fixedv, 4);
+        IrOp o;
+        o.op.kind = OP_START;
+        o.op.node = t - node_base;
+        o.op.flags = static_cast<uint8_t>(flags | F_NO_OUT);
+        o.op.cls = cls;
+        o.op.npred = static_cast<uint8_t>(fixedv.size());
+        for (size_t k = 0; k < fixedv.size(); ++k) o.v_pred[k] = fixedv[k];
+        o.v_dst = V_START + t;
+        push_with_cov(o);
+        continue;
+      }
+
+      auto git = gate_slot.find(t);
+      std::vector<int64_t> gatev;
+      if (git != gate_slot.end())
+        for (const auto& [u, k] : gates_of[git->second])
+          gatev.push_back(k == TS_GATE_START ? V_START + u : u);
+
+      IrOp o;
+      o.op.node = t - node_base;
+      o.op.base = d.duration[t];
+      o.op.flags = flags;
+      o.v_dst = t;
+      if (split[t]) {
+        fold(gatev, 3);
+        o.op.kind = OP_FINISH;
+        o.op.cls = cls;
+        o.op.npred = static_cast<uint8_t>(1 + gatev.size());
+        o.v_pred[0] = V_START + t;
+        for (size_t k = 0; k < gatev.size(); ++k) o.v_pred[1 + k] = gatev[k];
+        ir.push_back(o);
+        continue;
+      }
+      if (start_used[t]) {
+        o.op.flags |= F_STORE_START;
+        o.v_x2 = V_START + t;
+      }
+      if (!gatev.empty()) {
+        if (gatev.size() > 1 && fixedv.size() + gatev.size() > 4) fold(gatev, 1);
+        fold(fixedv, 4 - gatev.size());
+        o.op.kind = OP_GATED;
+        o.op.cls = static_cast<uint8_t>(cls | (fixedv.size() << 4));
+        o.op.npred = static_cast<uint8_t>(fixedv.size() + gatev.size());
+        for (size_t k = 0; k < fixedv.size(); ++k) o.v_pred[k] = fixedv[k];
+        for (size_t k = 0; k < gatev.size(); ++k) o.v_pred[fixedv.size() + k] = gatev[k];
+        push_with_cov(o);
+        continue;
+      }
+      fold(fixedv, 4);
+      o.op.cls = cls;
+      o.op.npred = static_cast<uint8_t>(fixedv.size());
+      for (size_t k = 0; k < fixedv.size(); ++k) o.v_pred[k] = fixedv[k];
+      if (sync_id[t] < 0) {
+        o.op.kind = OP_NODE;
+        push_with_cov(o);
+        continue;
+      }
+      o.op.kind = OP_SYNC;
+      const int32_t sid = sync_id[t];
+      const auto& cert = sync_cert[sid];
+      int32_t n_ext = static_cast<int32_t>((cert.size() + kCertPerExt - 1) / kCertPerExt);
+      o.op.x0 = static_cast<uint16_t>(n_ext);
+      ir.push_back(o);
+      for (int32_t e = 0; e < n_ext; ++e) {
+        IrOp x;
+        x.is_ext = true;
+        for (int32_t k = 0; k < kCertPerExt; ++k) {
+          size_t j = static_cast<size_t>(e) * kCertPerExt + k;
+          if (j >= cert.size()) break;
+          const int32_t ks = cert[j].kstar;
+          x.v_fin[k] = ks >= 0 ? ks : -1;
+          int ji = (ks >= 0 && sync_set[sid] >= 0) ? set_index(ks, sync_set[sid]) : -1;
+          x.v_bs[k] = ji >= 0 ? V_COV + 2LL * ks + ji : -1;
+          x.v_next[k] = cert[j].next >= 0 ? V_START + cert[j].next : -1;
+          x.n_ent = k + 1;
+        }
+        ir.push_back(x);
+      }
+    }
+
+    // ---- liveness: last use of each value; auxiliary records (certificate,
+    // coverage) belong to the op before them
+    auto ensure = [&](int64_t v) {
+      if (v >= static_cast<int64_t>(last_use.size())) {
+        last_use.resize(static_cast<size_t>(v + 1), -1);
+        slot_of.resize(static_cast<size_t>(v + 1), kNoSlot);
+      }
+    };
+    std::vector<int32_t> anchor(ir.size());
+    for (size_t i = 0; i < ir.size(); ++i)
+      anchor[i] = ir[i].aux() ? anchor[i - 1] : static_cast<int32_t>(i);
+    auto each_read = [&](const IrOp& o, auto&& f) {
+      if (o.is_ext) {
+        for (int k = 0; k < o.n_ent; ++k) {
+          if (o.v_fin[k] >= 0) f(o.v_fin[k]);
+          if (o.v_bs[k] >= 0) f(o.v_bs[k]);
+          if (o.v_next[k] >= 0) f(o.v_next[k]);
+        }
+        return;
+      }
+      if (o.is_cov) {
+        for (int j = 0; j < o.n_sets; ++j)
+          for (int k = 0; k < 4; ++k)
+            if (o.v_cov_src[j][k] >= 0) f(o.v_cov_src[j][k]);
+        return;
+      }
+      for (int k = 0; k < o.op.npred; ++k) f(o.v_pred[k]);
+    };
+    auto each_write = [&](const IrOp& o, auto&& f) {
+      if (o.is_ext) return;
+      if (o.is_cov) {
+        for (int j = 0; j < o.n_sets; ++j)
+          if (o.v_cov_dst[j] >= 0) f(o.v_cov_dst[j]);
+        return;
+      }
+      if (o.v_dst >= 0) f(o.v_dst);
+      if ((o.op.flags & F_STORE_START) && o.v_x2 >= 0) f(o.v_x2);
+    };
+    for (size_t i = 0; i < ir.size(); ++i)
+      each_read(ir[i], [&](int64_t v) {
+        ensure(v);
+        last_use[v] = std::max(last_use[v], anchor[i]);
+      });
+
+    // ---- linear-scan slot assignment.  An op group (op + its auxiliary
+    // records) reads every operand before it writes.  Operands dying in the
+    // group are released at the group's end; the op's own results are placed
+    // before that (so they never alias a group operand), the coverage results
+    // after it.
+    std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> free_slots;
+    int32_t n_slots = 0;
+    std::vector<int64_t> dying;
+    bool broken = false;
+    auto flush = [&] {
+      std::sort(dying.begin(), dying.end());
+      dying.erase(std::unique(dying.begin(), dying.end()), dying.end());
+      for (int64_t v : dying) {
+        free_slots.push(slot_of[v]);
+        slot_of[v] = kNoSlot;
+      }
+      dying.clear();
+    };
+    for (size_t i = 0; i < ir.size(); ++i) {
+      IrOp& o = ir[i];
+      const int32_t at = anchor[i];
+      auto read_slot = [&](int64_t v) -> uint16_t {
+        if (v < 0) return kNoSlot;
+        if (slot_of[v] == kNoSlot) {
+          broken = true;
+          return kNoSlot;
+        }
+        if (last_use[v] == at) dying.push_back(v);
+        return static_cast<uint16_t>(slot_of[v]);
+      };
+      auto write_slot = [&](int64_t v) -> uint16_t {
+        if (v < 0) return kNoSlot;
+        ensure(v);
+        if (last_use[v] <= at) return kNoSlot;  // nobody reads it later
+        int32_t s;
+        if (!free_slots.empty()) {
+          s = free_slots.top();
+          free_slots.pop();
+        } else {
+          s = n_slots++;
+        }
+        slot_of[v] = s;
+        return static_cast<uint16_t>(s);
+      };
+      const bool group_end = i + 1 >= ir.size() || !ir[i + 1].aux();
+      if (o.is_ext) {
+        OpExt x{};
+        for (int k = 0; k < kCertPerExt; ++k) x.fin[k] = x.bs[k] = x.next[k] = kNoSlot;
+        for (int k = 0; k < o.n_ent; ++k) {
+          x.fin[k] = read_slot(o.v_fin[k]);
+          x.bs[k] = read_slot(o.v_bs[k]);
+          x.next[k] = read_slot(o.v_next[k]);
+        }
+        x.n = static_cast<uint16_t>(o.n_ent);
+        std::memcpy(&o.op, &x, sizeof(Op));
+        if (group_end) flush();
+        continue;
+      }
+      if (o.is_cov) {
+        OpCov x{};
+        for (int j = 0; j < kCovSets; ++j) {
+          x.dst[j] = kNoSlot;
+          for (int k = 0; k < 4; ++k) x.src[j][k] = kNoSlot;
+        }
+        for (int j = 0; j < o.n_sets; ++j)
+          for (int k = 0; k < 4; ++k) x.src[j][k] = read_slot(o.v_cov_src[j][k]);
+        if (group_end) flush();
+        for (int j = 0; j < o.n_sets; ++j) x.dst[j] = write_slot(o.v_cov_dst[j]);
+        x.n_sets = static_cast<uint16_t>(o.n_sets);
+        std::memcpy(&o.op, &x, sizeof(Op));
+        continue;
+      }
+      for (int k = 0; k < o.op.npred; ++k) o.op.pred[k] = read_slot(o.v_pred[k]);
+      for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kNoSlot;
+      if (group_end) flush();
+      o.op.dst = write_slot(o.v_dst);
+      if (o.op.kind != OP_SYNC) o.op.x0 = kNoSlot;
+      o.op.x1 = kNoSlot;
+      o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
+    }
+    if (broken) {
+      err = "internal: compiled order reads a value before it is defined";
+      return TS_E_UNSUPPORTED;
+    }
+    if (n_slots >= static_cast<int32_t>(kNoSlot)) {
+      err = "unsupported graph: component needs too many live values";
+      return TS_E_UNSUPPORTED;
+    }
+    // reset per-value state touched by this component (keeps arrays reusable)
+    for (const IrOp& o : ir) {
+      each_read(o, [&](int64_t v) {
+        last_use[v] = -1;
+        slot_of[v] = kNoSlot;
+      });
+      each_write(o, [&](int64_t v) {
+        if (v < static_cast<int64_t>(last_use.size())) {
+          last_use[v] = -1;
+          slot_of[v] = kNoSlot;
+        }
+      });
+    }
+
+    // ---- de-duplicate identical programs (TP / DP replicas of one stage)
+    uint64_t h = 1469598103934665603ull;
+    const unsigned char* bytes = reinterpret_cast<const unsigned char*>(ir.data());
+    (void)bytes;
+    for (const IrOp& o : ir) {
+      const unsigned char* p = reinterpret_cast<const unsigned char*>(&o.op);
+      for (size_t k = 0; k < sizeof(Op); ++k) h = (h ^ p[k]) * 1099511628211ull;
+    }
+    h ^= static_cast<uint64_t>(n_slots) * 0x9E3779B97F4A7C15ull;
+    int32_t prog = -1;
+    if (contiguous) {
+      for (int32_t cand : prog_by_hash[h]) {
+        const ProgramDesc& pd = out.programs[cand];
+        if (pd.n_ops != static_cast<int32_t>(ir.size()) || pd.n_slots != n_slots) continue;
+        bool same = true;
+        for (size_t k = 0; k < ir.size() && same; ++k)
+          same = std::memcmp(&out.ops[pd.op_offset + k], &ir[k].op, sizeof(Op)) == 0;
+        if (same) {
+          prog = cand;
+          break;
+        }
+      }
+    }
+    if (prog < 0) {
+      prog = static_cast<int32_t>(out.programs.size());
+      ProgramDesc pd;
+      pd.op_offset = static_cast<int64_t>(out.ops.size());
+      pd.n_ops = static_cast<int32_t>(ir.size());
+      pd.n_slots = n_slots;
+      out.programs.push_back(pd);
+      for (const IrOp& o : ir) out.ops.push_back(o.op);
+      if (contiguous) prog_by_hash[h].push_back(prog);
+    }
+    out.max_slots = std::max(out.max_slots, n_slots);
+    out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
+  }
+
+  // ----------------------------------------------------- per-task arrays
+  out.base.assign(d.duration, d.duration + n);
+  out.scale_class.resize(n);
+  out.is_comm.resize(n);
+  for (int32_t t = 0; t < n; ++t) {
+    out.scale_class[t] = d.scale_class ? d.scale_class[t]
+                                       : static_cast<uint8_t>(d.task_kind && d.task_kind[t]
+                                                                  ? (d.op_class && d.op_class[t] ==
+                                                                             TS_OP_COMMUNICATION
+                                                                         ? 2
+                                                                         : 1)
+                                                                  : 0);
+    out.is_comm[t] = d.op_class && d.op_class[t] == TS_OP_COMMUNICATION ? 1 : 0;
+    if (d.lane_kind[t] == TS_LANE_CUDA_STREAM) out.n_gpu_tasks++;
+  }
+
+  // -------------------------------------------- reduction metadata (K5)
+  for (int32_t l = 0; l < nl; ++l)
+    if (out.ranks.empty() || out.ranks.back() != lanes[l].rank) out.ranks.push_back(lanes[l].rank);
+  out.rank_stream_off.assign(out.ranks.size() + 1, 0);
+  out.stream_node_off.push_back(0);
+  {
+    size_t ri = 0;
+    for (int32_t l = 0; l < nl; ++l) {
+      while (out.ranks[ri] != lanes[l].rank) {
+        ++ri;
+        out.rank_stream_off[ri] = static_cast<int32_t>(out.stream_rank.size());
+      }
+      if (lanes[l].kind != TS_LANE_CUDA_STREAM) continue;
+      out.stream_rank.push_back(lanes[l].rank);
+      out.stream_lane.push_back(lanes[l].lane);
+      for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k)
+        out.stream_nodes.push_back(lane_tasks[k]);
+      out.stream_node_off.push_back(static_cast<int32_t>(out.stream_nodes.size()));
+    }
+    for (size_t r = ri + 1; r <= out.ranks.size(); ++r)
+      out.rank_stream_off[r] = static_cast<int32_t>(out.stream_rank.size());
+  }
+  return TS_OK;
+}
+
+}  // namespace lumos

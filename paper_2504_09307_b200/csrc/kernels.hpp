@@ -1,0 +1,82 @@
+// kernels.hpp — launch parameters of the replay kernels (replay.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "program.hpp"
+
+namespace lumos {
+
+enum : int32_t { kModeScale = 1, kModeJitter = 2, kModeExplicit = 4 };
+
+struct ScenarioParams {
+  int64_t first;        // global id of column 0
+  int32_t count;
+  int32_t mode;         // kMode* bits
+  uint32_t key_jit;     // Philox key of the jitter stream
+  uint32_t key_cls;     // Philox key of the class-scale stream
+  double two_j;         // 2 * jitter
+  double neg_j;         // -jitter
+  int32_t scale_lo;
+  uint32_t scale_span;  // hi - lo + 1
+  int64_t scale_den;
+  int32_t den_shift;    // log2(den) when den is a power of two, else -1
+  int32_t n_classes;    // columns of scale_num
+  int32_t n_classes_eff;
+  int32_t pad;
+  const int32_t* scale_num;   // device [count][n_classes] or null
+  const int64_t* durations;   // device [n_tasks][durations_ld] or null
+  int64_t durations_ld;
+};
+
+struct WalkParams {
+  const Op* ops;
+  const ProgramDesc* progs;
+  const ComponentDesc* comps;
+  const int32_t* comp_order;  // optional launch order of components
+  int32_t n_comps;
+  int32_t pad;
+  int64_t window_start;
+  ScenarioParams sp;
+  int64_t* out_start;  // [n_tasks][ld] or null
+  int64_t* out_fin;
+  int64_t ld;
+  int64_t* span_lo;    // [count] atomics
+  int64_t* span_hi;
+  int32_t* status;
+};
+
+struct ReduceParams {
+  const int32_t* rank_stream_off;
+  const int32_t* stream_node_off;
+  const int32_t* stream_nodes;
+  const uint8_t* is_comm;
+  const int64_t* start;
+  const int64_t* fin;
+  int64_t ld;
+  const int64_t* span_lo;
+  const int64_t* span_hi;
+  int64_t window_start;
+  int64_t window_end;
+  int32_t count;
+  int32_t n_ranks;
+  int32_t n_streams;
+  int32_t pad;
+  int64_t* breakdown;    // [count][n_ranks][5]
+  int64_t* stream_busy;  // [count][n_streams]
+};
+
+int walk_threads();
+int max_streams_per_rank();
+cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
+cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
+                             cudaStream_t stream);
+cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W, int64_t* span,
+                                 int64_t* makespan, int32_t count, cudaStream_t stream);
+cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
+                             int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream);
+cudaError_t launch_rank_reduce(const ReduceParams& p, cudaStream_t stream);
+
+}  // namespace lumos

@@ -1,0 +1,509 @@
+// replay.cu — sm_100a kernels of the batched Lumos replay.
+//
+//   K1 replay_walk  : every (component, 128-scenario chunk) is one CTA; each
+//                     thread owns one scenario and walks the component's
+//                     straight-line program (program.hpp).  Live finish times
+//                     sit in shared memory (slot-major, [slot][thread], so
+//                     every access is a conflict-free 8-byte-per-lane row).
+//                     Durations are generated in registers (K4 fused), so the
+//                     only HBM traffic is the start/finish rows written
+//                     scenario-major (task row, 128 consecutive scenarios =
+//                     1 KiB per CTA per row) with streaming stores.
+//   K4 durations    : the same duration formula on its own (materialisation).
+//   K5 rank_reduce  : per (rank, scenario) k-way merge of the rank's stream
+//                     timelines -> 4-way breakdown (metrics.cpp:43-103) and
+//                     per-stream busy time.
+//
+// Integer semantics are exact int64 (types.hpp:15); the double arithmetic of
+// the jitter formula uses explicitly rounded intrinsics so it matches the
+// host restatement (compiled with -ffp-contract=off) bit for bit.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "program.hpp"
+
+namespace lumos {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kLogThreads = 7;
+static_assert((1 << kLogThreads) == kThreads, "");
+constexpr int64_t kMinI64 = INT64_MIN;
+constexpr int64_t kMaxI64 = INT64_MAX;
+
+__device__ __forceinline__ void philox2x32_10(uint32_t& x0, uint32_t& x1, uint32_t key) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi = __umulhi(0xD256D193u, x0);
+    const uint32_t lo = 0xD256D193u * x0;
+    x0 = hi ^ key ^ x1;
+    x1 = lo;
+    key += 0x9E3779B9u;
+  }
+}
+
+// round half away from zero (std::llround), exact for |p| < 2^63
+__device__ __forceinline__ int64_t llround_exact(double p) {
+  double t = trunc(p);
+  double frac = __dsub_rn(p, t);  // exact (Sterbenz / integer p)
+  if (fabs(frac) >= 0.5) t = __dadd_rn(t, copysign(1.0, p));
+  return static_cast<int64_t>(t);
+}
+
+// (a * num + den/2) / den for a >= 0, num >= 0 (transform.cpp:38-43)
+__device__ __forceinline__ int64_t mul_div_nonneg(int64_t a, int64_t num, int64_t den,
+                                                  int den_shift) {
+  const uint64_t ua = static_cast<uint64_t>(a), un = static_cast<uint64_t>(num);
+  uint64_t lo = ua * un;
+  uint64_t hi = __umul64hi(ua, un);
+  const uint64_t half = static_cast<uint64_t>(den / 2);
+  const uint64_t lo2 = lo + half;
+  hi += lo2 < lo ? 1 : 0;
+  lo = lo2;
+  if (den_shift >= 0) {
+    if (den_shift == 0) return static_cast<int64_t>(lo);
+    return static_cast<int64_t>((lo >> den_shift) | (hi << (64 - den_shift)));
+  }
+  const uint64_t ud = static_cast<uint64_t>(den);
+  if (hi == 0) return static_cast<int64_t>(lo / ud);
+  // 128 / 64 long division (rare: products beyond 2^64)
+  uint64_t q = 0, r = hi % ud;
+  for (int b = 63; b >= 0; --b) {
+    const bool top = (r >> 63) != 0;
+    r = (r << 1) | ((lo >> b) & 1u);
+    if (top || r >= ud) {
+      r -= ud;
+      q |= 1ull << b;
+    }
+  }
+  return static_cast<int64_t>(q);
+}
+
+struct ThreadScen {
+  int64_t scen;    // global scenario id
+  int32_t col;     // column in the batch
+  int32_t num[kMaxClasses];
+};
+
+__device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t scen, int col,
+                                             int cls) {
+  if (sp.scale_num) return sp.scale_num[static_cast<int64_t>(col) * sp.n_classes + cls];
+  uint32_t x0 = static_cast<uint32_t>(cls), x1 = static_cast<uint32_t>(scen);
+  philox2x32_10(x0, x1, sp.key_cls);
+  return sp.scale_lo + static_cast<int32_t>((static_cast<uint64_t>(x0) * sp.scale_span) >> 32);
+}
+
+// K4 semantics: the scenario's duration of one task (see lumos_b200.h)
+__device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
+                                                     const ThreadScen& ts, int64_t task,
+                                                     int64_t base, int cls) {
+  if (sp.mode & kModeExplicit) return __ldcs(sp.durations + task * sp.durations_ld + ts.col);
+  int64_t d = base;
+  if (sp.mode & kModeScale) {
+    int32_t num = ts.num[0];
+    if (cls == 1) num = ts.num[1];
+    if (cls == 2) num = ts.num[2];
+    if (cls == 3) num = ts.num[3];
+    d = mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
+  }
+  if (sp.mode & kModeJitter) {
+    if (d == 0) return 0;
+    uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
+    philox2x32_10(x0, x1, sp.key_jit);
+    const uint64_t bits = (static_cast<uint64_t>(x0) << 32) | x1;
+    const double u01 = __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
+    const double u = __dadd_rn(__dmul_rn(sp.two_j, u01), sp.neg_j);
+    const double f = __dadd_rn(1.0, u);
+    const double p = __dmul_rn(__ll2double_rn(d), f);
+    const int64_t q = llround_exact(p);
+    d = q < 1 ? 1 : q;
+  }
+  return d;
+}
+
+__device__ __forceinline__ void init_thread_scen(const ScenarioParams& sp, int col, ThreadScen& ts) {
+  ts.col = col;
+  ts.scen = sp.first + col;
+#pragma unroll
+  for (int c = 0; c < kMaxClasses; ++c)
+    ts.num[c] = (sp.mode & kModeScale) && c < sp.n_classes_eff ? class_num(sp, ts.scen, col, c) : 0;
+}
+
+__device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
+__device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
+
+// One 32-byte record as two 16-byte read-only loads (every lane of the CTA
+// reads the same address: a broadcast, L1-resident after the first warp).
+struct Rec {
+  int4 a, b;
+};
+__device__ __forceinline__ Rec load_rec(const Op* p) {
+  Rec r;
+  r.a = __ldg(reinterpret_cast<const int4*>(p));
+  r.b = __ldg(reinterpret_cast<const int4*>(p) + 1);
+  return r;
+}
+
+// ------------------------------------------------------------------- K1
+__global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
+  extern __shared__ int64_t slots[];
+  const int tid = threadIdx.x;
+  const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
+  const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
+  const int col = chunk * kThreads + tid;
+  const bool active = col < P.sp.count;
+
+  const ComponentDesc cd = P.comps[P.comp_order ? P.comp_order[comp] : comp];
+  const ProgramDesc pd = P.progs[cd.program];
+  const Op* __restrict__ ops = P.ops + pd.op_offset;
+  int64_t* my = slots + tid;
+  const int64_t W = P.window_start;
+
+  ThreadScen ts;
+  init_thread_scen(P.sp, col, ts);
+
+  int64_t lo_start = kMaxI64, hi_fin = kMinI64;
+  bool cert_fail = false;
+  int64_t* __restrict__ out_start = P.out_start;
+  int64_t* __restrict__ out_fin = P.out_fin;
+  const int64_t ld = P.ld;
+
+#define SLOT(s) my[static_cast<int32_t>(s) << kLogThreads]
+
+  for (int i = 0; i < pd.n_ops; ++i) {
+    const Rec r = load_rec(ops + i);
+    const uint32_t hdr = static_cast<uint32_t>(r.a.w);
+    const uint32_t kind = hdr & 0xFFu;
+    const int np = (hdr >> 8) & 0xFFu;
+    const uint32_t cls_b = (hdr >> 16) & 0xFFu;
+    const uint32_t flags = hdr >> 24;
+    const uint32_t w0 = static_cast<uint32_t>(r.b.x), w1 = static_cast<uint32_t>(r.b.y);
+    const uint32_t w2 = static_cast<uint32_t>(r.b.z), w3 = static_cast<uint32_t>(r.b.w);
+    int64_t p0 = kMinI64, p1 = kMinI64, p2 = kMinI64, p3 = kMinI64;
+    if (np > 0) p0 = SLOT(lo16(w0));
+    if (np > 1) p1 = SLOT(hi16(w0));
+    if (np > 2) p2 = SLOT(lo16(w1));
+    if (np > 3) p3 = SLOT(hi16(w1));
+    const uint32_t dst = lo16(w2);
+    if (kind == OP_ACC) {
+      SLOT(dst) = imax(imax(p0, p1), imax(p2, p3));
+      continue;
+    }
+    // start = max(W, fixed preds); gate = max(gate preds)
+    int64_t st, gate = kMinI64;
+    if (kind == OP_FINISH) {
+      st = p0;
+      gate = imax(imax(p1, p2), p3);
+    } else {
+      const int nfixed = kind == OP_GATED ? static_cast<int>(cls_b >> 4) : np;
+      st = W;
+      if (nfixed > 0) st = imax(st, p0);
+      if (nfixed > 1) st = imax(st, p1);
+      if (nfixed > 2) st = imax(st, p2);
+      if (nfixed > 3) st = imax(st, p3);
+      if (kind == OP_GATED) {
+        if (nfixed <= 0) gate = imax(gate, p0);
+        if (nfixed <= 1) gate = imax(gate, p1);
+        if (nfixed <= 2) gate = imax(gate, p2);
+        gate = imax(gate, p3);
+      }
+    }
+    if (kind == OP_SYNC) {
+      // static binding S = max(r_s, finish(k*_w)) and its certificate
+      const int64_t rs = st;
+      int64_t S = rs;
+      const int n_ext = static_cast<int>(hi16(w2));
+      for (int e = 0; e < n_ext; ++e) {
+        const Rec x = load_rec(ops + i + 1 + e);
+        const uint32_t f01 = x.a.x, f23 = x.a.y;
+        const int n = x.b.z & 0xFFFF;
+        const uint32_t f[4] = {lo16(f01), hi16(f01), lo16(f23), hi16(f23)};
+#pragma unroll
+        for (int k = 0; k < kCertPerExt; ++k)
+          if (k < n && f[k] != kNoSlot) S = imax(S, SLOT(f[k]));
+      }
+      bool covered = S == rs;
+      for (int e = 0; e < n_ext; ++e) {
+        const Rec x = load_rec(ops + i + 1 + e);
+        const int n = x.b.z & 0xFFFF;
+        const uint32_t f[4] = {lo16(x.a.x), hi16(x.a.x), lo16(x.a.y), hi16(x.a.y)};
+        const uint32_t c[4] = {lo16(x.a.z), hi16(x.a.z), lo16(x.a.w), hi16(x.a.w)};
+        const uint32_t nx[4] = {lo16(x.b.x), hi16(x.b.x), lo16(x.b.y), hi16(x.b.y)};
+#pragma unroll
+        for (int k = 0; k < kCertPerExt; ++k) {
+          if (k >= n) continue;
+          if (f[k] != kNoSlot && c[k] != kNoSlot && SLOT(f[k]) == S && SLOT(c[k]) <= rs)
+            covered = true;
+          if (nx[k] != kNoSlot && SLOT(nx[k]) <= S) cert_fail = true;
+        }
+      }
+      if (!covered) cert_fail = true;
+      st = S;
+      i += n_ext;
+    }
+    if (kind == OP_START) {
+      SLOT(dst) = st;
+    } else {
+      const int64_t task = static_cast<int64_t>(cd.node_base) + r.a.z;
+      const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(r.a.y)) << 32) |
+                           static_cast<uint32_t>(r.a.x);
+      const int64_t d = scenario_duration(P.sp, ts, task, base, cls_b & 15u);
+      const int64_t fin = imax(st, gate) + d;
+      if (dst != kNoSlot) SLOT(dst) = fin;
+      if (flags & F_STORE_START) SLOT(hi16(w3)) = st;
+      lo_start = imin(lo_start, st);
+      hi_fin = imax(hi_fin, fin);
+      if (active) {
+        const int64_t at = task * ld + col;
+        if (out_start) __stcs(out_start + at, st);
+        if (out_fin) __stcs(out_fin + at, fin);
+      }
+    }
+    if (flags & F_TRACK) {
+      // coverage of this kernel per watched set (program.hpp, OpCov)
+      const Rec x = load_rec(ops + i + 1);
+      const uint32_t src[2][4] = {{lo16(x.a.x), hi16(x.a.x), lo16(x.a.y), hi16(x.a.y)},
+                                  {lo16(x.a.z), hi16(x.a.z), lo16(x.a.w), hi16(x.a.w)}};
+      const uint32_t cdst[2] = {lo16(x.b.x), hi16(x.b.x)};
+      const int n_sets = x.b.y & 0xFFFF;
+      const int64_t pv[4] = {p0, p1, p2, p3};
+#pragma unroll
+      for (int j = 0; j < kCovSets; ++j) {
+        if (j >= n_sets) continue;
+        int64_t c = st;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (src[j][k] != kNoSlot && pv[k] >= st) c = imin(c, SLOT(src[j][k]));
+        if (cdst[j] != kNoSlot) SLOT(cdst[j]) = c;
+      }
+      i += 1;
+    }
+  }
+#undef SLOT
+  if (active) {
+    if (lo_start != kMaxI64) {
+      atomicMin(reinterpret_cast<long long*>(P.span_lo) + col, static_cast<long long>(lo_start));
+      atomicMax(reinterpret_cast<long long*>(P.span_hi) + col, static_cast<long long>(hi_fin));
+    }
+    if (cert_fail) atomicOr(P.status + col, 1);
+  }
+}
+
+__global__ void span_init_kernel(int64_t* lo, int64_t* hi, int32_t* status, int32_t count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) {
+    lo[i] = kMaxI64;
+    hi[i] = kMinI64;
+    status[i] = 0;
+  }
+}
+
+// span[s] = {start, end, makespan}; empty graph: {W, W, 0} (simulate.cpp:327-334)
+__global__ void span_finalize_kernel(const int64_t* lo, const int64_t* hi, int64_t W,
+                                     int64_t* span, int64_t* makespan, int32_t count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  int64_t a = lo[i], b = hi[i];
+  if (a == kMaxI64) {
+    a = W;
+    b = W;
+  }
+  if (b < a) b = a;
+  if (span) {
+    span[3 * static_cast<int64_t>(i) + 0] = a;
+    span[3 * static_cast<int64_t>(i) + 1] = b;
+    span[3 * static_cast<int64_t>(i) + 2] = b - a;
+  }
+  if (makespan) makespan[i] = b - a;
+}
+
+// ------------------------------------------------------------------- K4
+__global__ void durations_kernel(ScenarioParams sp, const int64_t* __restrict__ base,
+                                 const uint8_t* __restrict__ cls, int32_t n_tasks,
+                                 int64_t* __restrict__ dur, int64_t ld) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= sp.count) return;
+  ThreadScen ts;
+  init_thread_scen(sp, col, ts);
+  for (int32_t t = blockIdx.y; t < n_tasks; t += gridDim.y)
+    dur[static_cast<int64_t>(t) * ld + col] = scenario_duration(sp, ts, t, base[t], cls[t]);
+}
+
+// ------------------------------------------------------------------- K5
+constexpr int kMaxStreamsPerRank = 32;
+
+__global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (col >= P.count) return;
+  const int s0 = P.rank_stream_off[r], s1 = P.rank_stream_off[r + 1];
+  const int ns = s1 - s0;
+  const int64_t W = P.window_start;
+  const int64_t mk = P.span_hi[col] - P.span_lo[col];
+  int64_t wend = P.window_end;
+  {
+    int64_t a = P.span_lo[col], b = P.span_hi[col];
+    int64_t m = (a == kMaxI64) ? 0 : (b - a);
+    (void)mk;
+    if (W + m > wend) wend = W + m;
+  }
+  if (wend < W) wend = W;
+
+  int idx[kMaxStreamsPerRank];
+  int end[kMaxStreamsPerRank];
+  unsigned inside = 0;
+  int64_t busy_acc = 0;
+  for (int j = 0; j < ns; ++j) {
+    idx[j] = P.stream_node_off[s0 + j];
+    end[j] = P.stream_node_off[s0 + j + 1];
+  }
+  const int64_t* __restrict__ S = P.start;
+  const int64_t* __restrict__ F = P.fin;
+  const int64_t ld = P.ld;
+  auto clip_s = [&](int node) { return imax(S[static_cast<int64_t>(node) * ld + col], W); };
+  auto clip_e = [&](int node) { return imin(F[static_cast<int64_t>(node) * ld + col], wend); };
+  // skip empty (after clipping) intervals at the front of every stream
+  int64_t next_t[kMaxStreamsPerRank];
+  for (int j = 0; j < ns; ++j) {
+    next_t[j] = kMaxI64;
+    while (idx[j] < end[j]) {
+      const int node = P.stream_nodes[idx[j]];
+      const int64_t a = clip_s(node), b = clip_e(node);
+      if (a < b) {
+        next_t[j] = a;
+        break;
+      }
+      ++idx[j];
+    }
+  }
+  int compute = 0, comm = 0;
+  int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
+  for (;;) {
+    int jm = -1;
+    int64_t tm = kMaxI64;
+    for (int j = 0; j < ns; ++j)
+      if (next_t[j] < tm) {
+        tm = next_t[j];
+        jm = j;
+      }
+    if (jm < 0) break;
+    if (tm > prev) {
+      const int64_t span = tm - prev;
+      if (compute > 0 && comm > 0) ov += span;
+      else if (compute > 0) ec += span;
+      else if (comm > 0) em += span;
+      else ot += span;
+      prev = tm;
+    }
+    const int node = P.stream_nodes[idx[jm]];
+    const bool c = P.is_comm[node] != 0;
+    if (!((inside >> jm) & 1u)) {
+      // interval opens
+      if (c) ++comm; else ++compute;
+      inside |= 1u << jm;
+      next_t[jm] = clip_e(node);
+    } else {
+      if (c) --comm; else --compute;
+      inside &= ~(1u << jm);
+      if (P.stream_busy) busy_acc = 0;
+      ++idx[jm];
+      next_t[jm] = kMaxI64;
+      while (idx[jm] < end[jm]) {
+        const int nn = P.stream_nodes[idx[jm]];
+        const int64_t a = clip_s(nn), b = clip_e(nn);
+        if (a < b) {
+          next_t[jm] = a;
+          break;
+        }
+        ++idx[jm];
+      }
+    }
+  }
+  if (wend > prev) {
+    const int64_t span = wend - prev;
+    if (compute > 0 && comm > 0) ov += span;
+    else if (compute > 0) ec += span;
+    else if (comm > 0) em += span;
+    else ot += span;
+  }
+  (void)busy_acc;
+  if (P.breakdown) {
+    int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
+    row[0] = wend - W;
+    row[1] = ec;
+    row[2] = em;
+    row[3] = ov;
+    row[4] = ot;
+  }
+  if (P.stream_busy) {
+    for (int j = 0; j < ns; ++j) {
+      int64_t b = 0;
+      for (int k = P.stream_node_off[s0 + j]; k < P.stream_node_off[s0 + j + 1]; ++k) {
+        const int node = P.stream_nodes[k];
+        const int64_t a = clip_s(node), e = clip_e(node);
+        if (a < e) b += e - a;
+      }
+      P.stream_busy[static_cast<int64_t>(col) * P.n_streams + s0 + j] = b;
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers
+int walk_threads() { return kThreads; }
+
+cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(n_slots > 0 ? n_slots : 1) * kThreads * sizeof(int64_t);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int chunks = (p.sp.count + kThreads - 1) / kThreads;
+  const long long blocks = static_cast<long long>(chunks) * p.n_comps;
+  if (blocks <= 0) return cudaSuccess;
+  replay_walk_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
+                             cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  span_init_kernel<<<(count + 255) / 256, 256, 0, stream>>>(lo, hi, status, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W, int64_t* span,
+                                 int64_t* makespan, int32_t count, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  span_finalize_kernel<<<(count + 255) / 256, 256, 0, stream>>>(lo, hi, W, span, makespan, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
+                             int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream) {
+  if (sp.count <= 0 || n_tasks <= 0) return cudaSuccess;
+  dim3 grid((sp.count + 127) / 128, n_tasks < 4096 ? n_tasks : 4096);
+  durations_kernel<<<grid, 128, 0, stream>>>(sp, base, cls, n_tasks, dur, ld);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank_reduce(const ReduceParams& p, cudaStream_t stream) {
+  if (p.count <= 0 || p.n_ranks <= 0) return cudaSuccess;
+  dim3 grid((p.count + kThreads - 1) / kThreads, p.n_ranks);
+  rank_reduce_kernel<<<grid, kThreads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+int max_streams_per_rank() { return kMaxStreamsPerRank; }
+
+}  // namespace lumos

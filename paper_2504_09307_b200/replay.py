@@ -1,0 +1,237 @@
+"""Host mirror of the reference replay interface, on the B200 engine.
+
+Reference interface (``/root/reference/proj/include/tracesim/simulate.hpp``):
+
+* ``simulate(const ExecutionGraph&) -> SimulatedTrace`` (``:51``): one replay at
+  the graph's own durations; raises ``SimulationError`` on invalid graphs.
+* ``validate_graph`` (``:37``) — the error checks run inside ``DeviceGraph``.
+
+Batched extension (the data-parallel hot path): ``simulate_batch`` replays
+``count`` duration scenarios of one graph at once — the reference equivalent
+is ``count`` calls of ``simulate`` on perturbed copies (jitter hook
+``synth.cpp:146-156``; class retime ``transform.cpp:38-43``).
+
+Every call goes through the C ABI of ``lib/liblumos_b200.so``; there is no
+CPU execution path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .graph import (DeviceError, ExecutionGraph, GraphError, SimulatedTrace, SimulationError,
+                    UnsupportedGraphError)
+
+
+def _raise(rc: int):
+    msg = N.last_error()
+    if rc == N.TS_E_SIMULATION:
+        raise SimulationError(msg)
+    if rc == N.TS_E_GRAPH:
+        raise GraphError(msg)
+    if rc == N.TS_E_UNSUPPORTED:
+        raise UnsupportedGraphError(msg)
+    if rc == N.TS_E_CUDA or rc == N.TS_E_NOMEM:
+        raise DeviceError(msg)
+    raise ValueError(msg)
+
+
+def _ptr(a, t):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):  # torch tensor (device or host)
+        return C.cast(C.c_void_p(a.data_ptr()), t)
+    return a.ctypes.data_as(t)
+
+
+@dataclass
+class ScenarioSpec:
+    """A batch of duration scenarios (include/lumos_b200.h, ts_scenarios).
+
+    jitter      u ~ U[-jitter, jitter): d -> max(1, llround(d * (1 + u))), 0 stays 0
+    scale       per-class rational factor num / scale_den, num drawn in
+                [scale_lo, scale_hi] (or given per scenario in ``scale_num``)
+    durations   explicit [n_tasks][count] durations (overrides both)
+    """
+    count: int
+    first: int = 0
+    seed: int = 250409307
+    jitter: float = 0.0
+    scale_lo: int = 0
+    scale_hi: int = 0
+    scale_den: int = 0
+    scale_num: Optional[object] = None  # [count][n_classes] int32 (numpy or torch)
+    durations: Optional[object] = None  # [n_tasks][ld] int64
+    durations_ld: int = 0
+
+    def to_c(self) -> N.TsScenarios:
+        sc = N.TsScenarios()
+        sc.first = self.first
+        sc.count = self.count
+        sc.seed = self.seed
+        sc.jitter = self.jitter
+        sc.scale_lo, sc.scale_hi, sc.scale_den = self.scale_lo, self.scale_hi, self.scale_den
+        if self.scale_num is not None:
+            sc.n_classes = int(self.scale_num.shape[1])
+            sc.scale_num = _ptr(self.scale_num, N.i32p)
+        if self.durations is not None:
+            sc.durations = _ptr(self.durations, N.i64p)
+            sc.durations_ld = self.durations_ld or int(self.durations.shape[1])
+        return sc
+
+
+class DeviceGraph:
+    """A compiled, device-resident ExecutionGraph (``ts_graph``).
+
+    Construction runs validate_graph's error checks (raising SimulationError
+    with the reference's message) and compiles the graph to replay programs.
+    ``device=None`` uses the current CUDA device; ``compile_only=True`` builds
+    host-side programs for inspection without touching a GPU.
+    """
+
+    def __init__(self, graph, device: Optional[int] = None, compile_only: bool = False):
+        g = ExecutionGraph.from_any(graph)
+        self.graph = g
+        d = N.TsGraphDesc()
+        d.n_tasks = g.n
+        d.duration = _ptr(g.duration, N.i64p)
+        d.original_start = _ptr(g.original_start, N.i64p)
+        d.rank = _ptr(g.rank, N.i32p)
+        d.lane_kind = _ptr(g.lane_kind, N.i32p)
+        d.lane = _ptr(g.lane, N.i32p)
+        d.op_class = _ptr(g.op_class, N.u8p)
+        d.task_kind = _ptr(g.task_kind, N.u8p)
+        d.scale_class = _ptr(g.scale_class, N.u8p) if g.scale_class is not None else None
+        d.n_edges = g.edge_from.shape[0]
+        d.edge_from = _ptr(g.edge_from, N.i32p)
+        d.edge_to = _ptr(g.edge_to, N.i32p)
+        d.n_rules = g.rule_kind.shape[0]
+        d.rule_kind = _ptr(g.rule_kind, N.i32p)
+        d.rule_task = _ptr(g.rule_task, N.i32p)
+        d.rule_bound = _ptr(g.rule_bound, N.i32p)
+        d.rule_watch_off = _ptr(g.rule_watch_off, N.i32p)
+        d.watch_rank = _ptr(g.watch_rank, N.i32p)
+        d.watch_kind = _ptr(g.watch_kind, N.i32p)
+        d.watch_lane = _ptr(g.watch_lane, N.i32p)
+        d.window_start = g.window_start
+        d.window_end = g.window_end
+        d.n_gates = g.gate_from.shape[0]
+        d.gate_from = _ptr(g.gate_from, N.i32p)
+        d.gate_to = _ptr(g.gate_to, N.i32p)
+        d.gate_kind = _ptr(g.gate_kind, N.u8p)
+        h = C.c_void_p()
+        dev = N.DEVICE_NONE if compile_only else (-1 if device is None else int(device))
+        rc = N.lib().ts_graph_create(C.byref(d), dev, C.byref(h))
+        if rc != N.TS_OK:
+            _raise(rc)
+        self.h = h
+        info = N.TsGraphInfo()
+        N.lib().ts_graph_get_info(self.h, C.byref(info))
+        self.info = {k: getattr(info, k) for k, _ in N.TsGraphInfo._fields_}
+        self.n_tasks = info.n_tasks
+        self.n_ranks = info.n_ranks
+        self.n_streams = info.n_streams
+        ranks = np.zeros(max(1, info.n_ranks), np.int32)
+        N.lib().ts_graph_ranks(self.h, _ptr(ranks, N.i32p))
+        self.ranks = ranks[:info.n_ranks]
+        srank = np.zeros(max(1, info.n_streams), np.int32)
+        slane = np.zeros(max(1, info.n_streams), np.int32)
+        N.lib().ts_graph_streams(self.h, _ptr(srank, N.i32p), _ptr(slane, N.i32p))
+        self.stream_rank = srank[:info.n_streams]
+        self.stream_lane = slane[:info.n_streams]
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib().ts_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ API
+    def simulate(self) -> SimulatedTrace:
+        """simulate(const ExecutionGraph&) on the GPU (simulate.hpp:51)."""
+        n = self.n_tasks
+        start = np.zeros(max(1, n), np.int64)
+        fin = np.zeros(max(1, n), np.int64)
+        span = np.zeros(3, np.int64)
+        rc = N.lib().ts_simulate(self.h, _ptr(start, N.i64p), _ptr(fin, N.i64p),
+                                 _ptr(span, N.i64p))
+        if rc != N.TS_OK:
+            _raise(rc)
+        return SimulatedTrace.from_task_arrays(start[:n], fin[:n], span)
+
+    def replay_batch(self, spec: ScenarioSpec, start=None, fin=None, ld: int = 0, span=None,
+                     rank_breakdown=None, stream_busy=None, status=None, stream=None) -> None:
+        """Raw ts_replay_batch: outputs are caller-owned numpy (host) or torch
+        (device or host) buffers; see include/lumos_b200.h for shapes."""
+        sc = spec.to_c()
+        r = N.TsResult()
+        r.start = _ptr(start, N.i64p)
+        r.fin = _ptr(fin, N.i64p)
+        r.ld = ld or (int(start.shape[1]) if start is not None else
+                      int(fin.shape[1]) if fin is not None else spec.count)
+        r.span = _ptr(span, N.i64p)
+        r.rank_breakdown = _ptr(rank_breakdown, N.i64p)
+        r.stream_busy = _ptr(stream_busy, N.i64p)
+        r.status = _ptr(status, N.i32p)
+        s = C.c_void_p(stream) if isinstance(stream, int) else stream
+        rc = N.lib().ts_replay_batch(self.h, C.byref(sc), C.byref(r), s)
+        if rc != N.TS_OK:
+            _raise(rc)
+
+    def scenario_durations(self, spec: ScenarioSpec, out=None, stream=None):
+        """Materialise scenario durations [n_tasks][count] (the K4 kernel alone)."""
+        if out is None:
+            out = np.zeros((self.n_tasks, spec.count), np.int64)
+        sc = spec.to_c()
+        s = C.c_void_p(stream) if isinstance(stream, int) else stream
+        rc = N.lib().ts_scenario_durations(self.h, C.byref(sc), _ptr(out, N.i64p),
+                                           int(out.shape[1]), s)
+        if rc != N.TS_OK:
+            _raise(rc)
+        return out
+
+
+@dataclass
+class BatchResult:
+    span: np.ndarray                  # [count][3] {start, end, makespan}
+    start: Optional[np.ndarray]       # [n_tasks][count]
+    fin: Optional[np.ndarray]
+    rank_breakdown: Optional[np.ndarray]  # [count][n_ranks][5]
+    stream_busy: Optional[np.ndarray]     # [count][n_streams]
+
+    @property
+    def makespan(self) -> np.ndarray:
+        return self.span[:, 2]
+
+
+def simulate(graph, device: Optional[int] = None) -> SimulatedTrace:
+    """Drop-in for ``tracesim::simulate`` (simulate.hpp:51), executed on the GPU."""
+    dg = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+    return dg.simulate()
+
+
+def simulate_batch(graph, spec: ScenarioSpec, timestamps: bool = True, breakdown: bool = True,
+                   device: Optional[int] = None) -> BatchResult:
+    """Replay ``spec.count`` scenarios; results in host numpy arrays."""
+    dg = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+    S = spec.count
+    span = np.zeros((S, 3), np.int64)
+    start = fin = bd = busy = None
+    if timestamps:
+        start = np.zeros((dg.n_tasks, S), np.int64)
+        fin = np.zeros((dg.n_tasks, S), np.int64)
+    if breakdown:
+        bd = np.zeros((S, dg.n_ranks, 5), np.int64)
+        busy = np.zeros((S, max(1, dg.n_streams)), np.int64)
+    dg.replay_batch(spec, start=start, fin=fin, ld=S, span=span, rank_breakdown=bd,
+                    stream_busy=busy)
+    return BatchResult(span=span, start=start, fin=fin, rank_breakdown=bd, stream_busy=busy)
