@@ -90,6 +90,7 @@ struct IrOp {
   int64_t v_cov_src[kCovSets][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
   int64_t v_cov_dst[kCovSets] = {-1, -1};
   int n_sets = 0;
+  int64_t v_cov1_src = -1, v_cov1_dst = -1;  // F_TRACK1
   bool aux() const { return is_ext || is_cov; }
 };
 
@@ -585,11 +586,11 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
           ir.push_back(o);
           return;
         }
-        o.op.flags |= F_TRACK;
-        ir.push_back(o);
         IrOp cv;
         cv.is_cov = true;
         cv.n_sets = static_cast<int>(my_sets.size());
+        int n_src = 0, src_k = -1;
+        const int n_cand = o.op.kind == OP_GATED ? (o.op.cls >> 4) : o.op.npred;
         for (int j = 0; j < cv.n_sets; ++j) {
           cv.v_cov_dst[j] = V_COV + 2LL * t + j;
           for (int k = 0; k < o.op.npred; ++k) {
@@ -598,9 +599,27 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
             int32_t u = static_cast<int32_t>(v);
             if (d.lane_kind[u] != TS_LANE_CUDA_STREAM) continue;
             int ju = set_index(u, my_sets[j]);
-            if (ju >= 0) cv.v_cov_src[j][k] = V_COV + 2LL * u + ju;
+            if (ju >= 0) {
+              cv.v_cov_src[j][k] = V_COV + 2LL * u + ju;
+              ++n_src;
+              src_k = k;
+            }
           }
         }
+        if (cv.n_sets == 1 && n_src <= 1 && (src_k < 0 || src_k < n_cand)) {
+          // compact form: the single source becomes pred[0]
+          o.op.flags |= F_TRACK1;
+          if (src_k > 0) {
+            std::swap(o.v_pred[0], o.v_pred[src_k]);
+            std::swap(cv.v_cov_src[0][0], cv.v_cov_src[0][src_k]);
+          }
+          o.v_cov1_src = cv.v_cov_src[0][0];
+          o.v_cov1_dst = cv.v_cov_dst[0];
+          ir.push_back(o);
+          return;
+        }
+        o.op.flags |= F_TRACK;
+        ir.push_back(o);
         ir.push_back(cv);
       };
 
@@ -713,6 +732,7 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
         return;
       }
       for (int k = 0; k < o.op.npred; ++k) f(o.v_pred[k]);
+      if (o.v_cov1_src >= 0) f(o.v_cov1_src);
     };
     auto each_write = [&](const IrOp& o, auto&& f) {
       if (o.is_ext) return;
@@ -723,6 +743,7 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
       }
       if (o.v_dst >= 0) f(o.v_dst);
       if ((o.op.flags & F_STORE_START) && o.v_x2 >= 0) f(o.v_x2);
+      if (o.v_cov1_dst >= 0) f(o.v_cov1_dst);
     };
     for (size_t i = 0; i < ir.size(); ++i)
       each_read(ir[i], [&](int64_t v) {
@@ -736,7 +757,7 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
     // before that (so they never alias a group operand), the coverage results
     // after it.
     std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> free_slots;
-    int32_t n_slots = 0;
+    int32_t n_slots = kFirstSlot;
     std::vector<int64_t> dying;
     bool broken = false;
     auto flush = [&] {
@@ -761,9 +782,9 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
         return static_cast<uint16_t>(slot_of[v]);
       };
       auto write_slot = [&](int64_t v) -> uint16_t {
-        if (v < 0) return kNoSlot;
+        if (v < 0) return kSlotTrash;
         ensure(v);
-        if (last_use[v] <= at) return kNoSlot;  // nobody reads it later
+        if (last_use[v] <= at) return kSlotTrash;  // nobody reads it later
         int32_t s;
         if (!free_slots.empty()) {
           s = free_slots.top();
@@ -798,16 +819,27 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
           for (int k = 0; k < 4; ++k) x.src[j][k] = read_slot(o.v_cov_src[j][k]);
         if (group_end) flush();
         for (int j = 0; j < o.n_sets; ++j) x.dst[j] = write_slot(o.v_cov_dst[j]);
+        for (int j = o.n_sets; j < kCovSets; ++j) x.dst[j] = kSlotTrash;
         x.n_sets = static_cast<uint16_t>(o.n_sets);
         std::memcpy(&o.op, &x, sizeof(Op));
         continue;
       }
       for (int k = 0; k < o.op.npred; ++k) o.op.pred[k] = read_slot(o.v_pred[k]);
-      for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kNoSlot;
+      for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kSlotOrigin;
+      const uint16_t cov_src = (o.op.flags & F_TRACK1) ? read_slot(o.v_cov1_src) : kNoSlot;
       if (group_end) flush();
+      ensure(o.v_dst >= 0 ? o.v_dst : 0);
+      if (o.v_dst >= 0 && o.v_dst < V_ACC && last_use[o.v_dst] <= at &&
+          (o.op.kind == OP_NODE || o.op.kind == OP_GATED || o.op.kind == OP_FINISH ||
+           o.op.kind == OP_SYNC))
+        o.op.flags |= F_SINK;
       o.op.dst = write_slot(o.v_dst);
       if (o.op.kind != OP_SYNC) o.op.x0 = kNoSlot;
       o.op.x1 = kNoSlot;
+      if (o.op.flags & F_TRACK1) {
+        o.op.x0 = cov_src;
+        o.op.x1 = write_slot(o.v_cov1_dst);
+      }
       o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
     }
     if (broken) {
@@ -830,6 +862,37 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
           slot_of[v] = kNoSlot;
         }
       });
+    }
+
+    // ---- pad so that no op group straddles a kChunk boundary
+    {
+      std::vector<IrOp> padded;
+      padded.reserve(ir.size() + ir.size() / 16 + 8);
+      size_t i = 0;
+      while (i < ir.size()) {
+        size_t g = 1;
+        while (i + g < ir.size() && ir[i + g].aux()) ++g;
+        if (g > static_cast<size_t>(kChunk)) {
+          err = "unsupported graph: op group larger than a program chunk";
+          return TS_E_UNSUPPORTED;
+        }
+        size_t pos = padded.size() % kChunk;
+        if (pos + g > static_cast<size_t>(kChunk)) {
+          for (size_t k = pos; k < static_cast<size_t>(kChunk); ++k) {
+            IrOp nop;
+            nop.op.kind = OP_NOP;
+            nop.op.node = -1;
+            nop.op.flags = F_NO_OUT;
+            for (int q = 0; q < 4; ++q) nop.op.pred[q] = kSlotOrigin;
+            nop.op.dst = kSlotTrash;
+            nop.op.x0 = nop.op.x1 = nop.op.x2 = kNoSlot;
+            padded.push_back(nop);
+          }
+        }
+        for (size_t k = 0; k < g; ++k) padded.push_back(ir[i + k]);
+        i += g;
+      }
+      ir.swap(padded);
     }
 
     // ---- de-duplicate identical programs (TP / DP replicas of one stage)

@@ -27,6 +27,15 @@ namespace lumos {
 constexpr uint16_t kNoSlot = 0xFFFF;
 constexpr int kMaxClasses = 4;
 constexpr int kCertPerExt = 4;
+// Reserved slots: slot 0 always holds W (the replay origin) and is what unused
+// predecessor fields point at, so every op reads exactly four slots with no
+// branch on the fan-in; slot 1 is a write-only sink for results nobody reads.
+constexpr uint16_t kSlotOrigin = 0;
+constexpr uint16_t kSlotTrash = 1;
+constexpr int kFirstSlot = 2;
+// Programs are streamed through shared memory in chunks of kChunk records; no
+// op group (an op plus its auxiliary records) straddles a chunk boundary.
+constexpr int kChunk = 128;
 
 enum OpKind : uint8_t {
   OP_NODE = 0,    // start = max(W, preds); fin = start + d
@@ -35,6 +44,7 @@ enum OpKind : uint8_t {
   OP_FINISH = 3,  // start = slot[pred0]; fin = max(start, preds[1..)) + d
   OP_ACC = 4,     // dst = max(preds)  (fan-in > 4 folding; no task)
   OP_SYNC = 5,    // OP_NODE over fixed preds, then static sync edges + certificate
+  OP_NOP = 6,     // padding to a chunk boundary
 };
 
 enum OpFlags : uint8_t {
@@ -43,11 +53,14 @@ enum OpFlags : uint8_t {
   F_GPU = 4,          // task runs on a CUDA stream lane
   F_COMM = 8,         // OpClass::Communication
   F_NO_OUT = 16,      // helper op, produces no SimEntry
+  F_TRACK1 = 32,      // compact coverage: cov = pred0 >= start ? min(start, slot x0) : start -> x1
+  F_SINK = 64,        // finish read by no other op: candidate for the makespan
 };
 
 // 32-byte op record.  cls: low nibble = scenario class, high nibble = nfixed
 // (OP_GATED).  For OP_SYNC, x0 = number of OpExt records that follow; a
-// F_TRACK op is followed by exactly one OpCov record.
+// F_TRACK op is followed by exactly one OpCov record; a F_TRACK1 op keeps its
+// single coverage source / destination in x0 / x1.
 struct alignas(16) Op {
   int64_t base;      // base duration (us)
   int32_t node;      // task id relative to the component's node_base

@@ -96,20 +96,23 @@ __device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t s
   return sp.scale_lo + static_cast<int32_t>((static_cast<uint64_t>(x0) * sp.scale_span) >> 32);
 }
 
-// K4 semantics: the scenario's duration of one task (see lumos_b200.h)
+// K4 semantics: the scenario's duration of one task (see lumos_b200.h).
+// kMode < 0: decided at run time from sp.mode.
+template <int kMode>
 __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
                                                      const ThreadScen& ts, int64_t task,
                                                      int64_t base, int cls) {
-  if (sp.mode & kModeExplicit) return __ldcs(sp.durations + task * sp.durations_ld + ts.col);
+  const int mode = kMode >= 0 ? kMode : sp.mode;
+  if (mode & kModeExplicit) return __ldcs(sp.durations + task * sp.durations_ld + ts.col);
   int64_t d = base;
-  if (sp.mode & kModeScale) {
+  if (mode & kModeScale) {
     int32_t num = ts.num[0];
     if (cls == 1) num = ts.num[1];
     if (cls == 2) num = ts.num[2];
     if (cls == 3) num = ts.num[3];
     d = mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
   }
-  if (sp.mode & kModeJitter) {
+  if (mode & kModeJitter) {
     if (d == 0) return 0;
     uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
     philox2x32_10(x0, x1, sp.key_jit);
@@ -150,8 +153,14 @@ __device__ __forceinline__ Rec load_rec(const Op* p) {
 }
 
 // ------------------------------------------------------------------- K1
+// Shared memory: two program chunks (2 x kChunk x 32 B, refilled one chunk
+// ahead through registers) followed by the slot table [n_slots][kThreads].
+template <int kMode, bool kWriteStart, bool kWriteFin>
 __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
-  extern __shared__ int64_t slots[];
+  static_assert(kChunk == kThreads, "one record per thread per chunk refill");
+  extern __shared__ int4 smem[];
+  int4* opbuf = smem;  // [2][kChunk][2]
+  int64_t* slots = reinterpret_cast<int64_t*>(smem + 4 * kChunk);
   const int tid = threadIdx.x;
   const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
   const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
@@ -160,134 +169,159 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
 
   const ComponentDesc cd = P.comps[P.comp_order ? P.comp_order[comp] : comp];
   const ProgramDesc pd = P.progs[cd.program];
-  const Op* __restrict__ ops = P.ops + pd.op_offset;
+  const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
+  const int n_ops = pd.n_ops;
   int64_t* my = slots + tid;
   const int64_t W = P.window_start;
+#define SLOT(s) my[static_cast<int32_t>(s) << kLogThreads]
+  SLOT(kSlotOrigin) = W;
 
   ThreadScen ts;
   init_thread_scen(P.sp, col, ts);
 
-  int64_t lo_start = kMaxI64, hi_fin = kMinI64;
+  int64_t hi_fin = kMinI64;
   bool cert_fail = false;
-  int64_t* __restrict__ out_start = P.out_start;
-  int64_t* __restrict__ out_fin = P.out_fin;
+  int64_t* const start_col = kWriteStart && active ? P.out_start + col : nullptr;
+  int64_t* const fin_col = kWriteFin && active ? P.out_fin + col : nullptr;
   const int64_t ld = P.ld;
 
-#define SLOT(s) my[static_cast<int32_t>(s) << kLogThreads]
-
-  for (int i = 0; i < pd.n_ops; ++i) {
-    const Rec r = load_rec(ops + i);
-    const uint32_t hdr = static_cast<uint32_t>(r.a.w);
-    const uint32_t kind = hdr & 0xFFu;
-    const int np = (hdr >> 8) & 0xFFu;
-    const uint32_t cls_b = (hdr >> 16) & 0xFFu;
-    const uint32_t flags = hdr >> 24;
-    const uint32_t w0 = static_cast<uint32_t>(r.b.x), w1 = static_cast<uint32_t>(r.b.y);
-    const uint32_t w2 = static_cast<uint32_t>(r.b.z), w3 = static_cast<uint32_t>(r.b.w);
-    int64_t p0 = kMinI64, p1 = kMinI64, p2 = kMinI64, p3 = kMinI64;
-    if (np > 0) p0 = SLOT(lo16(w0));
-    if (np > 1) p1 = SLOT(hi16(w0));
-    if (np > 2) p2 = SLOT(lo16(w1));
-    if (np > 3) p3 = SLOT(hi16(w1));
-    const uint32_t dst = lo16(w2);
-    if (kind == OP_ACC) {
-      SLOT(dst) = imax(imax(p0, p1), imax(p2, p3));
-      continue;
+  if (tid < n_ops) {
+    opbuf[2 * tid] = __ldg(gops + 2 * tid);
+    opbuf[2 * tid + 1] = __ldg(gops + 2 * tid + 1);
+  }
+  __syncthreads();
+  const int n_chunks = (n_ops + kChunk - 1) / kChunk;
+  for (int c = 0; c < n_chunks; ++c) {
+    // prefetch the next chunk into registers while this one is walked
+    const int nxt = (c + 1) * kChunk + tid;
+    const bool pf = nxt < n_ops;
+    int4 na = make_int4(0, 0, 0, 0), nb = na;
+    if (pf) {
+      na = __ldg(gops + 2 * nxt);
+      nb = __ldg(gops + 2 * nxt + 1);
     }
-    // start = max(W, fixed preds); gate = max(gate preds)
-    int64_t st, gate = kMinI64;
-    if (kind == OP_FINISH) {
-      st = p0;
-      gate = imax(imax(p1, p2), p3);
-    } else {
-      const int nfixed = kind == OP_GATED ? static_cast<int>(cls_b >> 4) : np;
-      st = W;
-      if (nfixed > 0) st = imax(st, p0);
-      if (nfixed > 1) st = imax(st, p1);
-      if (nfixed > 2) st = imax(st, p2);
-      if (nfixed > 3) st = imax(st, p3);
-      if (kind == OP_GATED) {
-        if (nfixed <= 0) gate = imax(gate, p0);
-        if (nfixed <= 1) gate = imax(gate, p1);
-        if (nfixed <= 2) gate = imax(gate, p2);
+    const int4* buf = opbuf + (c & 1) * 2 * kChunk;
+    const int cnt = min(kChunk, n_ops - c * kChunk);
+    for (int i = 0; i < cnt; ++i) {
+      const int4 ra = buf[2 * i], rb = buf[2 * i + 1];
+      const uint32_t hdr = static_cast<uint32_t>(ra.w);
+      const uint32_t kind = hdr & 0xFFu;
+      const uint32_t cls_b = (hdr >> 16) & 0xFFu;
+      const uint32_t flags = hdr >> 24;
+      const uint32_t w0 = static_cast<uint32_t>(rb.x), w1 = static_cast<uint32_t>(rb.y);
+      const uint32_t w2 = static_cast<uint32_t>(rb.z), w3 = static_cast<uint32_t>(rb.w);
+      const int64_t p0 = SLOT(lo16(w0)), p1 = SLOT(hi16(w0));
+      const int64_t p2 = SLOT(lo16(w1)), p3 = SLOT(hi16(w1));
+      const uint32_t dst = lo16(w2);
+      // every operand is read before any result is written (results may
+      // reuse the slot of an operand that dies at this op)
+      int64_t cov_src = kMaxI64;
+      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOT(hi16(w2));
+      int64_t st, gate;
+      if (kind == OP_NODE || kind == OP_SYNC || kind == OP_START || kind == OP_ACC) {
+        st = imax(imax(p0, p1), imax(p2, p3));  // unused preds read the origin W
+        gate = W;
+      } else if (kind == OP_FINISH) {
+        st = p0;
+        gate = imax(imax(p1, p2), p3);
+      } else if (kind == OP_GATED) {
+        const int nfixed = static_cast<int>(cls_b >> 4);
+        st = W;
+        gate = W;
+        if (nfixed > 0) st = imax(st, p0); else gate = imax(gate, p0);
+        if (nfixed > 1) st = imax(st, p1); else gate = imax(gate, p1);
+        if (nfixed > 2) st = imax(st, p2); else gate = imax(gate, p2);
         gate = imax(gate, p3);
+      } else {
+        continue;  // OP_NOP
       }
-    }
-    if (kind == OP_SYNC) {
-      // static binding S = max(r_s, finish(k*_w)) and its certificate
-      const int64_t rs = st;
-      int64_t S = rs;
-      const int n_ext = static_cast<int>(hi16(w2));
-      for (int e = 0; e < n_ext; ++e) {
-        const Rec x = load_rec(ops + i + 1 + e);
-        const uint32_t f01 = x.a.x, f23 = x.a.y;
-        const int n = x.b.z & 0xFFFF;
-        const uint32_t f[4] = {lo16(f01), hi16(f01), lo16(f23), hi16(f23)};
-#pragma unroll
-        for (int k = 0; k < kCertPerExt; ++k)
-          if (k < n && f[k] != kNoSlot) S = imax(S, SLOT(f[k]));
+      if (kind == OP_ACC) {
+        SLOT(dst) = st;
+        continue;
       }
-      bool covered = S == rs;
-      for (int e = 0; e < n_ext; ++e) {
-        const Rec x = load_rec(ops + i + 1 + e);
-        const int n = x.b.z & 0xFFFF;
-        const uint32_t f[4] = {lo16(x.a.x), hi16(x.a.x), lo16(x.a.y), hi16(x.a.y)};
-        const uint32_t c[4] = {lo16(x.a.z), hi16(x.a.z), lo16(x.a.w), hi16(x.a.w)};
-        const uint32_t nx[4] = {lo16(x.b.x), hi16(x.b.x), lo16(x.b.y), hi16(x.b.y)};
+      if (kind == OP_SYNC) {
+        // static binding S = max(r_s, finish(k*_w)) and its certificate
+        const int64_t rs = st;
+        int64_t S = rs;
+        const int n_ext = static_cast<int>(hi16(w2));
+        for (int e = 0; e < n_ext; ++e) {
+          const int4 xa = buf[2 * (i + 1 + e)];
+          const int n = buf[2 * (i + 1 + e) + 1].z & 0xFFFF;
+          const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
 #pragma unroll
-        for (int k = 0; k < kCertPerExt; ++k) {
-          if (k >= n) continue;
-          if (f[k] != kNoSlot && c[k] != kNoSlot && SLOT(f[k]) == S && SLOT(c[k]) <= rs)
-            covered = true;
-          if (nx[k] != kNoSlot && SLOT(nx[k]) <= S) cert_fail = true;
+          for (int k = 0; k < kCertPerExt; ++k)
+            if (k < n && f[k] != kNoSlot) S = imax(S, SLOT(f[k]));
         }
-      }
-      if (!covered) cert_fail = true;
-      st = S;
-      i += n_ext;
-    }
-    if (kind == OP_START) {
-      SLOT(dst) = st;
-    } else {
-      const int64_t task = static_cast<int64_t>(cd.node_base) + r.a.z;
-      const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(r.a.y)) << 32) |
-                           static_cast<uint32_t>(r.a.x);
-      const int64_t d = scenario_duration(P.sp, ts, task, base, cls_b & 15u);
-      const int64_t fin = imax(st, gate) + d;
-      if (dst != kNoSlot) SLOT(dst) = fin;
-      if (flags & F_STORE_START) SLOT(hi16(w3)) = st;
-      lo_start = imin(lo_start, st);
-      hi_fin = imax(hi_fin, fin);
-      if (active) {
-        const int64_t at = task * ld + col;
-        if (out_start) __stcs(out_start + at, st);
-        if (out_fin) __stcs(out_fin + at, fin);
-      }
-    }
-    if (flags & F_TRACK) {
-      // coverage of this kernel per watched set (program.hpp, OpCov)
-      const Rec x = load_rec(ops + i + 1);
-      const uint32_t src[2][4] = {{lo16(x.a.x), hi16(x.a.x), lo16(x.a.y), hi16(x.a.y)},
-                                  {lo16(x.a.z), hi16(x.a.z), lo16(x.a.w), hi16(x.a.w)}};
-      const uint32_t cdst[2] = {lo16(x.b.x), hi16(x.b.x)};
-      const int n_sets = x.b.y & 0xFFFF;
-      const int64_t pv[4] = {p0, p1, p2, p3};
+        bool covered = S == rs;
+        for (int e = 0; e < n_ext; ++e) {
+          const int4 xa = buf[2 * (i + 1 + e)], xb = buf[2 * (i + 1 + e) + 1];
+          const int n = xb.z & 0xFFFF;
+          const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
+          const uint32_t cv[4] = {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)};
+          const uint32_t nx[4] = {lo16(xb.x), hi16(xb.x), lo16(xb.y), hi16(xb.y)};
 #pragma unroll
-      for (int j = 0; j < kCovSets; ++j) {
-        if (j >= n_sets) continue;
-        int64_t c = st;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (src[j][k] != kNoSlot && pv[k] >= st) c = imin(c, SLOT(src[j][k]));
-        if (cdst[j] != kNoSlot) SLOT(cdst[j]) = c;
+          for (int k = 0; k < kCertPerExt; ++k) {
+            if (k >= n) continue;
+            if (f[k] != kNoSlot && cv[k] != kNoSlot && SLOT(f[k]) == S && SLOT(cv[k]) <= rs)
+              covered = true;
+            if (nx[k] != kNoSlot && SLOT(nx[k]) <= S) cert_fail = true;
+          }
+        }
+        if (!covered) cert_fail = true;
+        st = S;
+        i += n_ext;
       }
-      i += 1;
+      if (kind == OP_START) {
+        SLOT(dst) = st;
+      } else {
+        const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
+        const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
+                             static_cast<uint32_t>(ra.x);
+        const int64_t d = scenario_duration<kMode>(P.sp, ts, task, base, cls_b & 15u);
+        const int64_t fin = imax(st, gate) + d;
+        SLOT(dst) = fin;
+        if (flags & F_STORE_START) SLOT(hi16(w3)) = st;
+        if (flags & F_SINK) hi_fin = imax(hi_fin, fin);
+        const int64_t at = task * ld;
+        if (kWriteStart && start_col) __stcs(start_col + at, st);
+        if (kWriteFin && fin_col) __stcs(fin_col + at, fin);
+      }
+      if (flags & F_TRACK1) {
+        SLOT(lo16(w3)) = p0 >= st ? imin(st, cov_src) : st;
+      } else if (flags & F_TRACK) {
+        // coverage of this kernel per watched set (program.hpp, OpCov)
+        const int4 xa = buf[2 * (i + 1)], xb = buf[2 * (i + 1) + 1];
+        const uint32_t src[2][4] = {{lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)},
+                                    {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)}};
+        const uint32_t cdst[2] = {lo16(xb.x), hi16(xb.x)};
+        const int n_sets = xb.y & 0xFFFF;
+        const int64_t pv[4] = {p0, p1, p2, p3};
+        int64_t cvj[kCovSets];
+#pragma unroll
+        for (int j = 0; j < kCovSets; ++j) {
+          cvj[j] = st;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (j < n_sets && src[j][k] != kNoSlot && pv[k] >= st)
+              cvj[j] = imin(cvj[j], SLOT(src[j][k]));
+        }
+#pragma unroll
+        for (int j = 0; j < kCovSets; ++j)
+          if (j < n_sets) SLOT(cdst[j]) = cvj[j];
+        i += 1;
+      }
     }
+    if (pf) {
+      int4* nbuf = opbuf + ((c + 1) & 1) * 2 * kChunk;
+      nbuf[2 * tid] = na;
+      nbuf[2 * tid + 1] = nb;
+    }
+    __syncthreads();
   }
 #undef SLOT
   if (active) {
-    if (lo_start != kMaxI64) {
-      atomicMin(reinterpret_cast<long long*>(P.span_lo) + col, static_cast<long long>(lo_start));
+    if (hi_fin != kMinI64) {
+      atomicMin(reinterpret_cast<long long*>(P.span_lo) + col, static_cast<long long>(W));
       atomicMax(reinterpret_cast<long long*>(P.span_hi) + col, static_cast<long long>(hi_fin));
     }
     if (cert_fail) atomicOr(P.status + col, 1);
@@ -331,7 +365,7 @@ __global__ void durations_kernel(ScenarioParams sp, const int64_t* __restrict__ 
   ThreadScen ts;
   init_thread_scen(sp, col, ts);
   for (int32_t t = blockIdx.y; t < n_tasks; t += gridDim.y)
-    dur[static_cast<int64_t>(t) * ld + col] = scenario_duration(sp, ts, t, base[t], cls[t]);
+    dur[static_cast<int64_t>(t) * ld + col] = scenario_duration<-1>(sp, ts, t, base[t], cls[t]);
 }
 
 // ------------------------------------------------------------------- K5
@@ -458,21 +492,47 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
 // ------------------------------------------------------------ launchers
 int walk_threads() { return kThreads; }
 
-cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(n_slots > 0 ? n_slots : 1) * kThreads * sizeof(int64_t);
+template <int kMode, bool kS, bool kF>
+static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
+                                 cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel,
+    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kMode, kS, kF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
+  replay_walk_kernel<kMode, kS, kF><<<blocks, kThreads, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+template <int kMode>
+static cudaError_t launch_walk_mode(const WalkParams& p, size_t smem, unsigned blocks,
+                                    cudaStream_t stream) {
+  const bool s = p.out_start != nullptr, f = p.out_fin != nullptr;
+  if (s && f) return launch_walk_t<kMode, true, true>(p, smem, blocks, stream);
+  if (f) return launch_walk_t<kMode, false, true>(p, smem, blocks, stream);
+  if (s) return launch_walk_t<kMode, true, false>(p, smem, blocks, stream);
+  return launch_walk_t<kMode, false, false>(p, smem, blocks, stream);
+}
+
+cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
+  const size_t smem = 4 * kChunk * sizeof(int4) +
+                      static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) *
+                          kThreads * sizeof(int64_t);
   const int chunks = (p.sp.count + kThreads - 1) / kThreads;
   const long long blocks = static_cast<long long>(chunks) * p.n_comps;
   if (blocks <= 0) return cudaSuccess;
-  replay_walk_kernel<<<static_cast<unsigned>(blocks), kThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  const unsigned nb = static_cast<unsigned>(blocks);
+  switch (p.sp.mode) {
+    case 0: return launch_walk_mode<0>(p, smem, nb, stream);
+    case kModeScale: return launch_walk_mode<kModeScale>(p, smem, nb, stream);
+    case kModeJitter: return launch_walk_mode<kModeJitter>(p, smem, nb, stream);
+    case kModeScale | kModeJitter:
+      return launch_walk_mode<kModeScale | kModeJitter>(p, smem, nb, stream);
+    default: return launch_walk_mode<kModeExplicit>(p, smem, nb, stream);
+  }
 }
 
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
