@@ -402,6 +402,11 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.span_lo = lo + b0;
     wp.span_hi = hi + b0;
     wp.status = status + b0;
+    {
+      auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+      wp.vec_store = (wp.ld % 2 == 0) && (bn % 2 == 0) &&
+                     (!wp.out_start || al(wp.out_start)) && (!wp.out_fin || al(wp.out_fin));
+    }
     if (wp.n_comps > 0) {
       CUDA_TRY(launch_replay_walk(wp, c.max_slots, stream));
       g_launches++;

@@ -846,9 +846,42 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
       err = "internal: compiled order reads a value before it is defined";
       return TS_E_UNSUPPORTED;
     }
-    if (n_slots >= static_cast<int32_t>(kNoSlot)) {
-      err = "unsupported graph: component needs too many live values";
+    if (n_slots > kMaxSlots) {
+      err = "unsupported graph: a component needs " + std::to_string(n_slots) +
+            " live values per scenario (limit " + std::to_string(kMaxSlots) + ")";
       return TS_E_UNSUPPORTED;
+    }
+    // slot numbers -> byte offsets into the [slot][thread] table
+    {
+      auto off = [](uint16_t& s) {
+        if (s != kNoSlot) s = slot_off(s);
+      };
+      for (IrOp& o : ir) {
+        if (o.is_ext) {
+          OpExt x;
+          std::memcpy(&x, &o.op, sizeof(x));
+          for (int k = 0; k < kCertPerExt; ++k) {
+            off(x.fin[k]);
+            off(x.bs[k]);
+            off(x.next[k]);
+          }
+          std::memcpy(&o.op, &x, sizeof(x));
+        } else if (o.is_cov) {
+          OpCov x;
+          std::memcpy(&x, &o.op, sizeof(x));
+          for (int j = 0; j < kCovSets; ++j) {
+            off(x.dst[j]);
+            for (int k = 0; k < 4; ++k) off(x.src[j][k]);
+          }
+          std::memcpy(&o.op, &x, sizeof(x));
+        } else {
+          for (int k = 0; k < 4; ++k) off(o.op.pred[k]);
+          off(o.op.dst);
+          if (o.op.kind != OP_SYNC) off(o.op.x0);
+          off(o.op.x1);
+          off(o.op.x2);
+        }
+      }
     }
     // reset per-value state touched by this component (keeps arrays reusable)
     for (const IrOp& o : ir) {
@@ -883,8 +916,8 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
             nop.op.kind = OP_NOP;
             nop.op.node = -1;
             nop.op.flags = F_NO_OUT;
-            for (int q = 0; q < 4; ++q) nop.op.pred[q] = kSlotOrigin;
-            nop.op.dst = kSlotTrash;
+            for (int q = 0; q < 4; ++q) nop.op.pred[q] = slot_off(kSlotOrigin);
+            nop.op.dst = slot_off(kSlotTrash);
             nop.op.x0 = nop.op.x1 = nop.op.x2 = kNoSlot;
             padded.push_back(nop);
           }

@@ -46,6 +46,8 @@ struct WalkParams {
   int64_t* span_lo;    // [count] atomics
   int64_t* span_hi;
   int32_t* status;
+  int32_t vec_store;   // 16-byte output stores allowed (ld, count even; aligned)
+  int32_t pad2;
 };
 
 struct ReduceParams {

@@ -22,6 +22,12 @@
 
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define LUMOS_HD __host__ __device__
+#else
+#define LUMOS_HD
+#endif
+
 namespace lumos {
 
 constexpr uint16_t kNoSlot = 0xFFFF;
@@ -36,6 +42,17 @@ constexpr int kFirstSlot = 2;
 // Programs are streamed through shared memory in chunks of kChunk records; no
 // op group (an op plus its auxiliary records) straddles a chunk boundary.
 constexpr int kChunk = 128;
+// Each walk thread replays kScenPerThread adjacent scenarios.  The slot table
+// is [slot][kWalkThreads] of int64 x kScenPerThread (16 bytes), so slot s of a
+// thread lives kSlotStride * s bytes past slot 0.  Records store offsets in
+// 16-byte units (slot * kWalkThreads), so 16 bits address 512 slots.
+constexpr int kWalkThreads = 128;
+constexpr int kScenPerThread = 2;
+constexpr int kSlotStride = kWalkThreads * 8 * kScenPerThread;
+constexpr int kMaxSlots = 65535 / kWalkThreads;
+LUMOS_HD constexpr uint16_t slot_off(int s) {
+  return static_cast<uint16_t>(s * kWalkThreads);
+}
 
 enum OpKind : uint8_t {
   OP_NODE = 0,    // start = max(W, preds); fin = start + d

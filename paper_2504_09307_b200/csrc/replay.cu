@@ -28,7 +28,7 @@ namespace lumos {
 
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = kWalkThreads;
 constexpr int kLogThreads = 7;
 static_assert((1 << kLogThreads) == kThreads, "");
 constexpr int64_t kMinI64 = INT64_MIN;
@@ -43,14 +43,6 @@ __device__ __forceinline__ void philox2x32_10(uint32_t& x0, uint32_t& x1, uint32
     x1 = lo;
     key += 0x9E3779B9u;
   }
-}
-
-// round half away from zero (std::llround), exact for |p| < 2^63
-__device__ __forceinline__ int64_t llround_exact(double p) {
-  double t = trunc(p);
-  double frac = __dsub_rn(p, t);  // exact (Sterbenz / integer p)
-  if (fabs(frac) >= 0.5) t = __dadd_rn(t, copysign(1.0, p));
-  return static_cast<int64_t>(t);
 }
 
 // (a * num + den/2) / den for a >= 0, num >= 0 (transform.cpp:38-43)
@@ -121,8 +113,12 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
     const double u = __dadd_rn(__dmul_rn(sp.two_j, u01), sp.neg_j);
     const double f = __dadd_rn(1.0, u);
     const double p = __dmul_rn(__ll2double_rn(d), f);
-    const int64_t q = llround_exact(p);
-    d = q < 1 ? 1 : q;
+    // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)
+    // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
+    // already an integer
+    if (p < 1.5) return 1;
+    if (p >= 0x1.0p52) return static_cast<int64_t>(p);
+    return __double2ll_rd(__dadd_rn(p, 0.5));
   }
   return d;
 }
@@ -136,6 +132,7 @@ __device__ __forceinline__ void init_thread_scen(const ScenarioParams& sp, int c
 }
 
 __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ uint32_t tid_offset() { return threadIdx.x * 16u; }
 __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
@@ -153,37 +150,54 @@ __device__ __forceinline__ Rec load_rec(const Op* p) {
 }
 
 // ------------------------------------------------------------------- K1
+// One thread replays two adjacent scenarios (columns c, c+1): the op record is
+// decoded once per pair, each operand is one 16-byte shared load, and each
+// output row is written with one 16-byte streaming store per thread (512
+// contiguous bytes per warp).
 // Shared memory: two program chunks (2 x kChunk x 32 B, refilled one chunk
-// ahead through registers) followed by the slot table [n_slots][kThreads].
+// ahead through registers) followed by the slot table [n_slots][kThreads] x 2.
+struct I64x2 {
+  int64_t x, y;
+};
+__device__ __forceinline__ I64x2 max2(I64x2 a, I64x2 b) { return {imax(a.x, b.x), imax(a.y, b.y)}; }
+
 template <int kMode, bool kWriteStart, bool kWriteFin>
 __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
   static_assert(kChunk == kThreads, "one record per thread per chunk refill");
+  static_assert(kScenPerThread == 2, "pair layout");
   extern __shared__ int4 smem[];
   int4* opbuf = smem;  // [2][kChunk][2]
-  int64_t* slots = reinterpret_cast<int64_t*>(smem + 4 * kChunk);
+  char* slot_base = reinterpret_cast<char*>(smem + 4 * kChunk) + tid_offset();
   const int tid = threadIdx.x;
   const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
   const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
-  const int col = chunk * kThreads + tid;
-  const bool active = col < P.sp.count;
+  // lanes past the last scenario replay the last scenario again: identical
+  // values, so their (duplicate) stores and atomics need no predication
+  const int last = P.sp.count - 1;
+  int c0 = chunk * kThreads * 2 + 2 * tid;
+  if (c0 > last - 1)  // keep pairs even-aligned when the count is even
+    c0 = P.sp.count < 2 ? 0 : ((P.sp.count & 1) ? min(c0, last) : last - 1);
+  const int c1 = min(c0 + 1, last);
+  const bool vec_store = P.vec_store;  // ld even, count even, aligned buffers
 
   const ComponentDesc cd = P.comps[P.comp_order ? P.comp_order[comp] : comp];
   const ProgramDesc pd = P.progs[cd.program];
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
-  int64_t* my = slots + tid;
   const int64_t W = P.window_start;
-#define SLOT(s) my[static_cast<int32_t>(s) << kLogThreads]
-  SLOT(kSlotOrigin) = W;
+#define SLOT2(off) (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << 4)))
+  SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
 
-  ThreadScen ts;
-  init_thread_scen(P.sp, col, ts);
+  ThreadScen ts0, ts1;
+  init_thread_scen(P.sp, c0, ts0);
+  init_thread_scen(P.sp, c1, ts1);
 
-  int64_t hi_fin = kMinI64;
-  bool cert_fail = false;
-  int64_t* const start_col = kWriteStart && active ? P.out_start + col : nullptr;
-  int64_t* const fin_col = kWriteFin && active ? P.out_fin + col : nullptr;
-  const int64_t ld = P.ld;
+  int64_t hi0 = kMinI64, hi1 = kMinI64;
+  bool fail0 = false, fail1 = false;
+  int64_t* const start_c0 = P.out_start + c0;
+  int64_t* const fin_c0 = P.out_fin + c0;
+  const uint32_t ld = static_cast<uint32_t>(P.ld);
+  const int64_t dcol = c1 - c0;
 
   if (tid < n_ops) {
     opbuf[2 * tid] = __ldg(gops + 2 * tid);
@@ -210,39 +224,39 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
       const uint32_t flags = hdr >> 24;
       const uint32_t w0 = static_cast<uint32_t>(rb.x), w1 = static_cast<uint32_t>(rb.y);
       const uint32_t w2 = static_cast<uint32_t>(rb.z), w3 = static_cast<uint32_t>(rb.w);
-      const int64_t p0 = SLOT(lo16(w0)), p1 = SLOT(hi16(w0));
-      const int64_t p2 = SLOT(lo16(w1)), p3 = SLOT(hi16(w1));
-      const uint32_t dst = lo16(w2);
       // every operand is read before any result is written (results may
       // reuse the slot of an operand that dies at this op)
-      int64_t cov_src = kMaxI64;
-      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOT(hi16(w2));
-      int64_t st, gate;
+      const I64x2 p0 = SLOT2(lo16(w0)), p1 = SLOT2(hi16(w0));
+      const I64x2 p2 = SLOT2(lo16(w1)), p3 = SLOT2(hi16(w1));
+      const uint32_t dst = lo16(w2);
+      I64x2 cov_src = {kMaxI64, kMaxI64};
+      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOT2(hi16(w2));
+      I64x2 st, gate;
       if (kind == OP_NODE || kind == OP_SYNC || kind == OP_START || kind == OP_ACC) {
-        st = imax(imax(p0, p1), imax(p2, p3));  // unused preds read the origin W
-        gate = W;
+        st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
+        gate = I64x2{W, W};
       } else if (kind == OP_FINISH) {
         st = p0;
-        gate = imax(imax(p1, p2), p3);
+        gate = max2(max2(p1, p2), p3);
       } else if (kind == OP_GATED) {
         const int nfixed = static_cast<int>(cls_b >> 4);
-        st = W;
-        gate = W;
-        if (nfixed > 0) st = imax(st, p0); else gate = imax(gate, p0);
-        if (nfixed > 1) st = imax(st, p1); else gate = imax(gate, p1);
-        if (nfixed > 2) st = imax(st, p2); else gate = imax(gate, p2);
-        gate = imax(gate, p3);
+        st = I64x2{W, W};
+        gate = st;
+        if (nfixed > 0) st = max2(st, p0); else gate = max2(gate, p0);
+        if (nfixed > 1) st = max2(st, p1); else gate = max2(gate, p1);
+        if (nfixed > 2) st = max2(st, p2); else gate = max2(gate, p2);
+        gate = max2(gate, p3);
       } else {
         continue;  // OP_NOP
       }
       if (kind == OP_ACC) {
-        SLOT(dst) = st;
+        SLOT2(dst) = st;
         continue;
       }
       if (kind == OP_SYNC) {
         // static binding S = max(r_s, finish(k*_w)) and its certificate
-        const int64_t rs = st;
-        int64_t S = rs;
+        const I64x2 rs = st;
+        I64x2 S = rs;
         const int n_ext = static_cast<int>(hi16(w2));
         for (int e = 0; e < n_ext; ++e) {
           const int4 xa = buf[2 * (i + 1 + e)];
@@ -250,9 +264,9 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
           const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
 #pragma unroll
           for (int k = 0; k < kCertPerExt; ++k)
-            if (k < n && f[k] != kNoSlot) S = imax(S, SLOT(f[k]));
+            if (k < n && f[k] != kNoSlot) S = max2(S, SLOT2(f[k]));
         }
-        bool covered = S == rs;
+        bool cov0 = S.x == rs.x, cov1 = S.y == rs.y;
         for (int e = 0; e < n_ext; ++e) {
           const int4 xa = buf[2 * (i + 1 + e)], xb = buf[2 * (i + 1 + e) + 1];
           const int n = xb.z & 0xFFFF;
@@ -262,32 +276,59 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
 #pragma unroll
           for (int k = 0; k < kCertPerExt; ++k) {
             if (k >= n) continue;
-            if (f[k] != kNoSlot && cv[k] != kNoSlot && SLOT(f[k]) == S && SLOT(cv[k]) <= rs)
-              covered = true;
-            if (nx[k] != kNoSlot && SLOT(nx[k]) <= S) cert_fail = true;
+            if (f[k] != kNoSlot && cv[k] != kNoSlot) {
+              const I64x2 fk = SLOT2(f[k]), ck = SLOT2(cv[k]);
+              cov0 = cov0 || (fk.x == S.x && ck.x <= rs.x);
+              cov1 = cov1 || (fk.y == S.y && ck.y <= rs.y);
+            }
+            if (nx[k] != kNoSlot) {
+              const I64x2 nk = SLOT2(nx[k]);
+              fail0 = fail0 || nk.x <= S.x;
+              fail1 = fail1 || nk.y <= S.y;
+            }
           }
         }
-        if (!covered) cert_fail = true;
+        fail0 = fail0 || !cov0;
+        fail1 = fail1 || !cov1;
         st = S;
         i += n_ext;
       }
       if (kind == OP_START) {
-        SLOT(dst) = st;
+        SLOT2(dst) = st;
       } else {
         const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
         const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
                              static_cast<uint32_t>(ra.x);
-        const int64_t d = scenario_duration<kMode>(P.sp, ts, task, base, cls_b & 15u);
-        const int64_t fin = imax(st, gate) + d;
-        SLOT(dst) = fin;
-        if (flags & F_STORE_START) SLOT(hi16(w3)) = st;
-        if (flags & F_SINK) hi_fin = imax(hi_fin, fin);
-        const int64_t at = task * ld;
-        if (kWriteStart && start_col) __stcs(start_col + at, st);
-        if (kWriteFin && fin_col) __stcs(fin_col + at, fin);
+        const int cls = cls_b & 15u;
+        const int64_t d0 = scenario_duration<kMode>(P.sp, ts0, task, base, cls);
+        const int64_t d1 = scenario_duration<kMode>(P.sp, ts1, task, base, cls);
+        const I64x2 fin = {imax(st.x, gate.x) + d0, imax(st.y, gate.y) + d1};
+        SLOT2(dst) = fin;
+        if (flags & F_STORE_START) SLOT2(hi16(w3)) = st;
+        if (flags & F_SINK) {
+          hi0 = imax(hi0, fin.x);
+          hi1 = imax(hi1, fin.y);
+        }
+        const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
+        if (vec_store) {
+          if (kWriteStart)
+            __stcs(reinterpret_cast<longlong2*>(start_c0 + at), make_longlong2(st.x, st.y));
+          if (kWriteFin)
+            __stcs(reinterpret_cast<longlong2*>(fin_c0 + at), make_longlong2(fin.x, fin.y));
+        } else {
+          if (kWriteStart) {
+            __stcs(start_c0 + at, st.x);
+            __stcs(start_c0 + at + dcol, st.y);
+          }
+          if (kWriteFin) {
+            __stcs(fin_c0 + at, fin.x);
+            __stcs(fin_c0 + at + dcol, fin.y);
+          }
+        }
       }
       if (flags & F_TRACK1) {
-        SLOT(lo16(w3)) = p0 >= st ? imin(st, cov_src) : st;
+        SLOT2(lo16(w3)) = I64x2{p0.x >= st.x ? imin(st.x, cov_src.x) : st.x,
+                                p0.y >= st.y ? imin(st.y, cov_src.y) : st.y};
       } else if (flags & F_TRACK) {
         // coverage of this kernel per watched set (program.hpp, OpCov)
         const int4 xa = buf[2 * (i + 1)], xb = buf[2 * (i + 1) + 1];
@@ -295,19 +336,22 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
                                     {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)}};
         const uint32_t cdst[2] = {lo16(xb.x), hi16(xb.x)};
         const int n_sets = xb.y & 0xFFFF;
-        const int64_t pv[4] = {p0, p1, p2, p3};
-        int64_t cvj[kCovSets];
+        const I64x2 pv[4] = {p0, p1, p2, p3};
+        I64x2 cvj[kCovSets];
 #pragma unroll
         for (int j = 0; j < kCovSets; ++j) {
           cvj[j] = st;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (j < n_sets && src[j][k] != kNoSlot && pv[k] >= st)
-              cvj[j] = imin(cvj[j], SLOT(src[j][k]));
+            if (j < n_sets && src[j][k] != kNoSlot) {
+              const I64x2 sv = SLOT2(src[j][k]);
+              if (pv[k].x >= st.x) cvj[j].x = imin(cvj[j].x, sv.x);
+              if (pv[k].y >= st.y) cvj[j].y = imin(cvj[j].y, sv.y);
+            }
         }
 #pragma unroll
         for (int j = 0; j < kCovSets; ++j)
-          if (j < n_sets) SLOT(cdst[j]) = cvj[j];
+          if (j < n_sets) SLOT2(cdst[j]) = cvj[j];
         i += 1;
       }
     }
@@ -318,14 +362,15 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
     }
     __syncthreads();
   }
-#undef SLOT
-  if (active) {
-    if (hi_fin != kMinI64) {
-      atomicMin(reinterpret_cast<long long*>(P.span_lo) + col, static_cast<long long>(W));
-      atomicMax(reinterpret_cast<long long*>(P.span_hi) + col, static_cast<long long>(hi_fin));
-    }
-    if (cert_fail) atomicOr(P.status + col, 1);
+#undef SLOT2
+  if (hi0 != kMinI64) {
+    atomicMin(reinterpret_cast<long long*>(P.span_lo) + c0, static_cast<long long>(W));
+    atomicMax(reinterpret_cast<long long*>(P.span_hi) + c0, static_cast<long long>(hi0));
+    atomicMin(reinterpret_cast<long long*>(P.span_lo) + c1, static_cast<long long>(W));
+    atomicMax(reinterpret_cast<long long*>(P.span_hi) + c1, static_cast<long long>(hi1));
   }
+  if (fail0) atomicOr(P.status + c0, 1);
+  if (fail1) atomicOr(P.status + c1, 1);
 }
 
 __global__ void span_init_kernel(int64_t* lo, int64_t* hi, int32_t* status, int32_t count) {
@@ -520,8 +565,9 @@ static cudaError_t launch_walk_mode(const WalkParams& p, size_t smem, unsigned b
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
   const size_t smem = 4 * kChunk * sizeof(int4) +
                       static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) *
-                          kThreads * sizeof(int64_t);
-  const int chunks = (p.sp.count + kThreads - 1) / kThreads;
+                          kSlotStride;
+  const int per_block = kThreads * kScenPerThread;
+  const int chunks = (p.sp.count + per_block - 1) / per_block;
   const long long blocks = static_cast<long long>(chunks) * p.n_comps;
   if (blocks <= 0) return cudaSuccess;
   const unsigned nb = static_cast<unsigned>(blocks);
