@@ -179,6 +179,63 @@ int ts_simulate(ts_graph* g, int64_t* start, int64_t* fin, int64_t* span);
 int ts_scenario_durations(ts_graph* g, const ts_scenarios* sc, int64_t* dur, int64_t ld,
                           void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Host-side graph sources (the input contract of the replay path).
+ *
+ * ts_synth_graph restates the reference generator (synth.cpp:71-170,
+ * pipeline.cpp:9-477): the one-iteration trace of a GPT-like model under
+ * pp x dp 1F1B pipelining, as either
+ *   estimate = 0: the replay graph build_graph + merge_ranks produce from that
+ *                 trace (what `tracesim replay` simulates), or
+ *   estimate = 1: the generator's own dependency graph with intrinsic
+ *                 durations and gates (p2p rendezvous, collective barrier) —
+ *                 the semantics of build_pipeline(spec, DurationHook).
+ * tp > 1 replicates every (stage, dp) rank as TP replicas r * tp + t (the
+ * reference generator itself rejects tp != 1, synth.cpp:18-19).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_layers, d_model, d_ffn, n_heads, d_head;
+  int32_t tp, pp, dp, num_microbatches;
+  int64_t tokens_per_microbatch, vocab;
+  int64_t launch_us, record_us, wait_us, sync_us;  /* SynthCosts, synth.hpp:17-34 */
+  int64_t gemm_ref_us, gemm_ref_mnk;
+  double bwd_gemm_factor;
+  int64_t attn_misc_us, embed_us, head_us, loss_grad_us;
+  int64_t optimizer_ref_us, optimizer_ref_bytes;
+  double alpha_us, bytes_per_us;
+  int64_t p2p_recv_base_us;
+  int64_t origin;
+  int32_t estimate;   /* 0 replay graph, 1 estimate graph */
+  int32_t slice_rank; /* -1 all ranks; else slice_rank (build.cpp:544-580) */
+} ts_synth_spec;
+
+typedef struct ts_host_graph ts_host_graph;
+
+/* fills the reference defaults (SynthSpec::from_json, synth.cpp:195-247) */
+void ts_synth_defaults(ts_synth_spec* spec);
+int ts_synth_graph(const ts_synth_spec* spec, ts_host_graph** out, int64_t* truth_makespan);
+/* SoA view of a host graph; pointers stay valid while the graph lives */
+int ts_host_graph_desc(const ts_host_graph* g, ts_graph_desc* out);
+/* per task: the generator cost index (DurationHook op_index) or -1 */
+int ts_host_graph_op_index(const ts_host_graph* g, int64_t* out);
+int64_t ts_host_graph_n_ops(const ts_host_graph* g);
+/* per task: name id; ts_host_graph_name(g, id) returns the string */
+int ts_host_graph_name_ids(const ts_host_graph* g, int32_t* out);
+const char* ts_host_graph_name(const ts_host_graph* g, int32_t name_id);
+void ts_host_graph_free(ts_host_graph* g);
+
+/* build_graph (build.cpp:338-510) over one rank's events, SoA.  cat is the
+ * EventCategory (types.hpp:20-27); corr = -1, stream = -1 and
+ * arg_event / arg_stream = INT64_MIN mean absent.  names is a '\n'-separated
+ * string table indexed by name[i].  Appends the rank to *inout (merge_ranks,
+ * build.cpp:512-542) when *inout is non-null, else creates it.  Returns
+ * TS_E_GRAPH on a dependency cycle (message = the reference's witness). */
+int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, const uint8_t* cat,
+                        const int64_t* ts, const int64_t* dur, const int32_t* tid,
+                        const int64_t* corr, const int32_t* stream, const int64_t* arg_event,
+                        const int64_t* arg_stream, const char* names, int64_t gap_threshold_us,
+                        ts_host_graph** inout);
+
 /* Launch counters (kernels this library enqueued since creation). */
 int64_t ts_kernel_launches(void);
 const char* ts_last_error(void);

@@ -339,3 +339,40 @@ double ref_bench_simulate(void* h, const orc_scenarios* sc, int64_t first, int32
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ generator / estimate oracle
+extern "C" {
+
+// build_pipeline(pipeline_spec_for(spec), hook) with hook(i, base) =
+// hook_dur[i] (or base when hook_dur is null).  Writes the events in output
+// order (stable-sorted by (pid, ts, tid), pipeline.cpp:75-78): pid, tid, ts,
+// dur.  Returns the event count (or -1); *n_ops receives the number of hook
+// calls.
+int64_t ref_pipeline_events(const char* spec_json, const int64_t* hook_dur, int64_t n_hook,
+                            int32_t* pid, int32_t* tid, int64_t* ts, int64_t* dur, int64_t cap,
+                            int64_t* n_ops) {
+  int64_t count = -1;
+  guarded([&] {
+    SynthSpec spec = SynthSpec::from_json(spec_json);
+    PipelineSpec ps = pipeline_spec_for(spec);
+    int64_t calls = 0;
+    DurationHook hook = [&](std::size_t i, Micros base) -> Micros {
+      calls = std::max<int64_t>(calls, static_cast<int64_t>(i) + 1);
+      if (hook_dur && static_cast<int64_t>(i) < n_hook) return hook_dur[i];
+      return base;
+    };
+    BuiltPipeline b = build_pipeline(ps, hook);
+    if (n_ops) *n_ops = calls;
+    count = static_cast<int64_t>(b.events.size());
+    for (int64_t i = 0; i < count && i < cap; ++i) {
+      pid[i] = b.events[i].process_id;
+      tid[i] = b.events[i].thread_id;
+      ts[i] = b.events[i].timestamp;
+      dur[i] = b.events[i].duration;
+    }
+    return 0;
+  });
+  return count;
+}
+
+}  // extern "C"

@@ -28,6 +28,14 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace lumos {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace lumos
+
+namespace {
+
 #define CUDA_TRY(expr)                                                                    \
   do {                                                                                    \
     cudaError_t _e = (expr);                                                              \
@@ -138,6 +146,12 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     cudaGetDevice(&g->device);
   }
   const CompiledGraph& c = g->cg;
+  if (walk_width(c.max_slots) == 0) {
+    const std::string msg = "a component needs " + std::to_string(c.max_slots) +
+                            " live values per scenario: more than shared memory holds";
+    delete g;
+    return fail(TS_E_UNSUPPORTED, msg);
+  }
   for (size_t r = 0; r + 1 < c.rank_stream_off.size(); ++r)
     if (c.rank_stream_off[r + 1] - c.rank_stream_off[r] > max_streams_per_rank()) {
       delete g;

@@ -1,0 +1,122 @@
+// capi_host.cpp — extern "C" entry points of the host-side graph sources
+// (synthetic generator, trace-event graph builder); see include/lumos_b200.h.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ingest.hpp"
+#include "lumos_b200.h"
+#include "synth.hpp"
+
+using namespace lumos;
+
+struct ts_host_graph {
+  SynthOutput s;
+};
+
+namespace lumos {
+int set_error(int code, const std::string& msg);  // capi.cpp
+}
+
+extern "C" {
+
+void ts_synth_defaults(ts_synth_spec* spec) {
+  if (spec) synth_defaults(spec);
+}
+
+int ts_synth_graph(const ts_synth_spec* spec, ts_host_graph** out, int64_t* truth_makespan) {
+  if (!spec || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  auto* h = new ts_host_graph;
+  std::string err;
+  int rc = synth_graph(*spec, h->s, err);
+  if (rc != TS_OK) {
+    delete h;
+    *out = nullptr;
+    return set_error(rc, err);
+  }
+  if (truth_makespan) *truth_makespan = h->s.truth_makespan;
+  *out = h;
+  return TS_OK;
+}
+
+int ts_host_graph_desc(const ts_host_graph* g, ts_graph_desc* out) {
+  if (!g || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  *out = g->s.graph.desc();
+  return TS_OK;
+}
+
+int ts_host_graph_op_index(const ts_host_graph* g, int64_t* out) {
+  if (!g || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  std::memcpy(out, g->s.graph.op_index.data(), g->s.graph.op_index.size() * sizeof(int64_t));
+  return TS_OK;
+}
+
+int64_t ts_host_graph_n_ops(const ts_host_graph* g) { return g ? g->s.n_ops : 0; }
+
+int ts_host_graph_name_ids(const ts_host_graph* g, int32_t* out) {
+  if (!g || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  std::memcpy(out, g->s.graph.name.data(), g->s.graph.name.size() * sizeof(int32_t));
+  return TS_OK;
+}
+
+const char* ts_host_graph_name(const ts_host_graph* g, int32_t id) {
+  if (!g || id < 0 || id >= static_cast<int32_t>(g->s.names.str.size())) return "";
+  return g->s.names.str[id].c_str();
+}
+
+void ts_host_graph_free(ts_host_graph* g) { delete g; }
+
+int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, const uint8_t* cat,
+                        const int64_t* ts, const int64_t* dur, const int32_t* tid,
+                        const int64_t* corr, const int32_t* stream, const int64_t* arg_event,
+                        const int64_t* arg_stream, const char* names, int64_t gap_threshold_us,
+                        ts_host_graph** inout) {
+  if (!inout || (n_events > 0 && (!name || !cat || !ts || !dur || !tid || !names)))
+    return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  ts_host_graph* h = *inout ? *inout : new ts_host_graph;
+  // the name table of the incoming events
+  std::vector<int32_t> remap;
+  {
+    const char* p = names;
+    while (*p) {
+      const char* q = std::strchr(p, '\n');
+      std::string s = q ? std::string(p, q) : std::string(p);
+      remap.push_back(h->s.names.get(s));
+      if (!q) break;
+      p = q + 1;
+    }
+  }
+  std::vector<Event> evs(static_cast<size_t>(n_events));
+  for (int64_t i = 0; i < n_events; ++i) {
+    Event& e = evs[i];
+    if (name[i] < 0 || name[i] >= static_cast<int32_t>(remap.size())) {
+      if (!*inout) delete h;
+      return set_error(TS_E_INVALID_ARGUMENT, "event name id out of range");
+    }
+    e.name = remap[name[i]];
+    e.cat = cat[i];
+    e.ts = ts[i];
+    e.dur = dur[i];
+    e.pid = rank;
+    e.tid = tid[i];
+    e.corr = corr ? corr[i] : -1;
+    e.stream = stream ? stream[i] : -1;
+    e.arg_event = arg_event ? arg_event[i] : kNoArg;
+    e.arg_stream = arg_stream ? arg_stream[i] : kNoArg;
+  }
+  HostGraph g;
+  std::string err;
+  BuildPolicyLite pol;
+  pol.gap_threshold_us = gap_threshold_us > 0 ? gap_threshold_us : 1000;
+  int rc = build_rank_graph(evs, h->s.names, rank, pol, g, err);
+  if (rc != TS_OK) {
+    if (!*inout) delete h;
+    return set_error(rc, err);
+  }
+  const bool first = h->s.graph.n() == 0 && h->s.graph.rule_kind.empty();
+  h->s.graph.append(g, first);
+  *inout = h;
+  return TS_OK;
+}
+
+}  // extern "C"

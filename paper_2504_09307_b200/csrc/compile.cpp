@@ -28,6 +28,9 @@
 #include "compile.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -483,19 +486,61 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
   for (int32_t v = 0; v < n; ++v)
     if (split[v]) split_task[split_idx[v]] = v;
   auto real_task = [&](int32_t a) { return a < n ? a : split_task[a - n]; };
-  using Key = std::tuple<int32_t, int32_t, int64_t, int32_t, int32_t>;
+  // demand time: a kernel's nominal finish (one longest-path pass at base
+  // durations, gates included); a host op inherits the earliest demand of
+  // anything downstream, so launches are placed just before the kernels that
+  // consume them rather than at their (much earlier) recorded time.  Keying
+  // kernels by finish keeps a p2p receive — which starts early and then waits
+  // inside its duration — from dragging every earlier launch forward.
+  std::vector<int64_t> demand(na, INT64_MAX);
+  {
+    std::vector<int32_t> by_topo(na);
+    for (int32_t a = 0; a < na; ++a) by_topo[topo[a]] = a;
+    std::vector<int64_t> nstart(n, d.window_start), nfin(n, d.window_start);
+    std::vector<std::vector<int32_t>> static_in(n);
+    for (size_t si = 0; si < sync_tasks.size(); ++si)
+      for (const auto& ce : sync_cert[si])
+        if (ce.kstar >= 0) static_in[sync_tasks[si]].push_back(ce.kstar);
+    for (int64_t k = 0; k < na; ++k) {
+      const int32_t a = by_topo[k];
+      const int32_t t = real_task(a);
+      if (a >= n || !split[t]) {
+        int64_t st = d.window_start;
+        for (int64_t e = pred.begin(t); e < pred.end(t); ++e) st = std::max(st, nfin[pred.idx[e]]);
+        if (event_bound[t] >= 0) st = std::max(st, nfin[event_bound[t]]);
+        for (int32_t u : static_in[t]) st = std::max(st, nfin[u]);
+        nstart[t] = st;
+      }
+      if (a < n) {
+        int64_t f = nstart[t];
+        auto git = gate_slot.find(t);
+        if (git != gate_slot.end())
+          for (const auto& [u, kk] : gates_of[git->second])
+            f = std::max(f, kk == TS_GATE_START ? nstart[u] : nfin[u]);
+        nfin[t] = f + d.duration[t];
+      }
+    }
+    for (int64_t k = na - 1; k >= 0; --k) {
+      const int32_t a = by_topo[k];
+      const int32_t t = real_task(a);
+      int64_t dm = d.lane_kind[t] == TS_LANE_CUDA_STREAM ? nfin[t] : INT64_MAX;
+      for (int64_t e = as.begin(a); e < as.end(a); ++e) dm = std::min(dm, demand[as.idx[e]]);
+      demand[a] = dm == INT64_MAX ? nfin[t] : dm;
+    }
+  }
+  using Key = std::tuple<int32_t, int64_t, int32_t, int64_t, int32_t, int32_t>;
   std::priority_queue<Key, std::vector<Key>, std::greater<>> heap;
   auto push = [&](int32_t a) {
     int32_t t = real_task(a);
     int32_t cpu = d.lane_kind[t] == TS_LANE_CUDA_STREAM ? 0 : 1;
-    heap.emplace(comp_of[a], cpu, d.original_start[t], t, a);
+    heap.emplace(comp_of[a], demand[a], cpu, d.original_start[t], t, a);
   };
   for (int32_t a = 0; a < na; ++a)
     if (left[a] == 0) push(a);
   std::vector<int32_t> order;
   order.reserve(na);
   while (!heap.empty()) {
-    int32_t a = std::get<4>(heap.top());
+    int32_t a = std::get<5>(heap.top());
     heap.pop();
     order.push_back(a);
     for (int64_t k = as.begin(a); k < as.end(a); ++k)
@@ -841,6 +886,37 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
         o.op.x1 = write_slot(o.v_cov1_dst);
       }
       o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
+    }
+    if (std::getenv("LUMOS_DEBUG_SLOTS") && c == 0) {
+      // replay the allocation to find the peak live set (debug only)
+      std::vector<int64_t> live;
+      std::vector<int64_t> peak;
+      std::vector<char> alive(last_use.size(), 0);
+      for (size_t i = 0; i < ir.size(); ++i) {
+        each_write(ir[i], [&](int64_t v) {
+          if (last_use[v] > anchor[i]) alive[v] = 1, live.push_back(v);
+        });
+        live.erase(std::remove_if(live.begin(), live.end(),
+                                  [&](int64_t v) { return last_use[v] <= anchor[i]; }),
+                   live.end());
+        if (live.size() > peak.size()) peak = live;
+      }
+      int kinds[5] = {0, 0, 0, 0, 0};
+      std::map<std::string, int> by;
+      for (int64_t v : peak) {
+        int k = v < n ? 0 : v < V_COV ? 1 : v < V_ACC ? 2 : 3;
+        kinds[k]++;
+        if (k <= 1) {
+          int32_t t = static_cast<int32_t>(k == 0 ? v : v - n);
+          std::string key = std::string(k ? "START " : "FIN ") +
+                            (d.lane_kind[t] ? "stream" : "thread") + std::to_string(d.lane[t]) +
+                            " op" + std::to_string(d.op_class ? d.op_class[t] : 9);
+          by[key]++;
+        }
+      }
+      fprintf(stderr, "[slots] comp 0 peak %zu: fin %d start %d cov %d acc %d\n", peak.size(),
+              kinds[0], kinds[1], kinds[2], kinds[3]);
+      for (auto& [k, cnt] : by) fprintf(stderr, "[slots]   %s x%d\n", k.c_str(), cnt);
     }
     if (broken) {
       err = "internal: compiled order reads a value before it is defined";

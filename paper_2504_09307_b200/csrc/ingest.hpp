@@ -1,0 +1,88 @@
+// ingest.hpp — trace events -> ExecutionGraph (host side, structure of arrays).
+//
+// Restates the reference graph builder (src/build.cpp) so that a trace built
+// here yields the identical task numbering, fixed edges and runtime rules as
+// tracesim::build_graph + merge_ranks: that graph is the input contract of
+// the replay path.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "lumos_b200.h"
+
+namespace lumos {
+
+// EventCategory (types.hpp:20-27)
+enum Cat : uint8_t { CAT_CPU_OP = 0, CAT_RUNTIME = 1, CAT_KERNEL = 2, CAT_MEMCPY = 3,
+                     CAT_MEMSET = 4, CAT_METADATA = 5 };
+
+constexpr int64_t kNoArg = INT64_MIN;
+
+// One normalized trace event (TraceEvent, types.hpp:57-67) with the two args
+// the builder interprets ("event", "stream", build.cpp:29-37) pre-parsed.
+struct Event {
+  int32_t name = 0;  // index into Names
+  uint8_t cat = CAT_METADATA;
+  int64_t ts = 0;
+  int64_t dur = 0;
+  int32_t pid = 0;
+  int32_t tid = 0;
+  int64_t corr = -1;           // correlation id, -1 = none
+  int32_t stream = -1;         // stream_id, -1 = none
+  int64_t arg_event = kNoArg;  // args["event"]
+  int64_t arg_stream = kNoArg; // args["stream"]
+  int64_t op_index = -1;       // generator cost index (estimate mode), -1 = none
+};
+
+struct Names {
+  std::vector<std::string> str;
+  std::unordered_map<std::string, int32_t> idx;
+  int32_t get(const std::string& s) {
+    auto it = idx.find(s);
+    if (it != idx.end()) return it->second;
+    int32_t id = static_cast<int32_t>(str.size());
+    str.push_back(s);
+    idx.emplace(s, id);
+    return id;
+  }
+};
+
+// ExecutionGraph as SoA (the layout of ts_graph_desc).
+struct HostGraph {
+  std::vector<int64_t> duration, original_start;
+  std::vector<int32_t> rank, lane_kind, lane;
+  std::vector<uint8_t> op_class, task_kind;
+  std::vector<int32_t> edge_from, edge_to;
+  std::vector<int32_t> rule_kind, rule_task, rule_bound, rule_watch_off{0};
+  std::vector<int32_t> watch_rank, watch_kind, watch_lane;
+  int64_t window_start = 0, window_end = 0;
+  std::vector<int32_t> gate_from, gate_to;
+  std::vector<uint8_t> gate_kind;
+  std::vector<int32_t> name;      // per task: index into the shared Names
+  std::vector<int64_t> op_index;  // per task: generator cost index (-1 = none)
+  int32_t n_diagnostics = 0;
+
+  int32_t n() const { return static_cast<int32_t>(duration.size()); }
+  ts_graph_desc desc() const;
+  // merge_ranks (build.cpp:512-542): append src with re-densified ids
+  void append(const HostGraph& src, bool first);
+  // copy of one rank's graph with every processor relabelled to new_rank
+  void append_relabelled(const HostGraph& src, int32_t new_rank, bool first);
+};
+
+struct BuildPolicyLite {
+  int64_t gap_threshold_us = 1000;  // build.hpp:18
+};
+
+// build_graph (build.cpp:338-510) over one rank's events.  Returns TS_OK or
+// TS_E_GRAPH (cycle / GPU event without stream) with `err` set.
+int build_rank_graph(const std::vector<Event>& events, const Names& names, int32_t rank,
+                     const BuildPolicyLite& policy, HostGraph& out, std::string& err);
+
+// OpClass of an event under the default BuildPolicy (build.cpp:86-98).
+uint8_t classify_event(const Event& e, const Names& names);
+
+}  // namespace lumos

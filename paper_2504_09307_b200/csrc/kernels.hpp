@@ -71,6 +71,7 @@ struct ReduceParams {
 };
 
 int walk_threads();
+int walk_width(int n_slots);  // walk CTA width for a slot count (0: too many)
 int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,

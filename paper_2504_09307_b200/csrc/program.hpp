@@ -43,9 +43,10 @@ constexpr int kFirstSlot = 2;
 // op group (an op plus its auxiliary records) straddles a chunk boundary.
 constexpr int kChunk = 128;
 // Each walk thread replays kScenPerThread adjacent scenarios.  The slot table
-// is [slot][kWalkThreads] of int64 x kScenPerThread (16 bytes), so slot s of a
-// thread lives kSlotStride * s bytes past slot 0.  Records store offsets in
-// 16-byte units (slot * kWalkThreads), so 16 bits address 512 slots.
+// is [slot][T] of int64 x kScenPerThread (16 bytes) for a CTA of T threads
+// (128, 64 or 32, chosen at launch from the slot count), so slot s of a thread
+// lives s * T * 16 bytes past slot 0.  Records store s * kWalkThreads (16-bit,
+// up to 511 slots); the kernel shifts by log2(T) - 3 to get the byte offset.
 constexpr int kWalkThreads = 128;
 constexpr int kScenPerThread = 2;
 constexpr int kSlotStride = kWalkThreads * 8 * kScenPerThread;

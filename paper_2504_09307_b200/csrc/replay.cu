@@ -28,9 +28,7 @@ namespace lumos {
 
 namespace {
 
-constexpr int kThreads = kWalkThreads;
-constexpr int kLogThreads = 7;
-static_assert((1 << kLogThreads) == kThreads, "");
+constexpr int kThreads = kWalkThreads;  // widest walk CTA; K4/K5 block size
 constexpr int64_t kMinI64 = INT64_MIN;
 constexpr int64_t kMaxI64 = INT64_MAX;
 
@@ -161,9 +159,11 @@ struct I64x2 {
 };
 __device__ __forceinline__ I64x2 max2(I64x2 a, I64x2 b) { return {imax(a.x, b.x), imax(a.y, b.y)}; }
 
-template <int kMode, bool kWriteStart, bool kWriteFin>
-__global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
-  static_assert(kChunk == kThreads, "one record per thread per chunk refill");
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin>
+__global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
+  constexpr int kRecPerThread = kChunk / kT;  // chunk refill: records per thread
+  constexpr int kShift = kT == 128 ? 4 : kT == 64 ? 3 : 2;  // s*128 -> s*kT*16 bytes
+  static_assert(kChunk % kT == 0 && kT >= 32, "");
   static_assert(kScenPerThread == 2, "pair layout");
   extern __shared__ int4 smem[];
   int4* opbuf = smem;  // [2][kChunk][2]
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
   // lanes past the last scenario replay the last scenario again: identical
   // values, so their (duplicate) stores and atomics need no predication
   const int last = P.sp.count - 1;
-  int c0 = chunk * kThreads * 2 + 2 * tid;
+  int c0 = chunk * kT * 2 + 2 * tid;
   if (c0 > last - 1)  // keep pairs even-aligned when the count is even
     c0 = P.sp.count < 2 ? 0 : ((P.sp.count & 1) ? min(c0, last) : last - 1);
   const int c1 = min(c0 + 1, last);
@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
   const int64_t W = P.window_start;
-#define SLOT2(off) (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << 4)))
+#define SLOT2(off) \
+  (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
   SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
 
   ThreadScen ts0, ts1;
@@ -199,20 +200,26 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
   const uint32_t ld = static_cast<uint32_t>(P.ld);
   const int64_t dcol = c1 - c0;
 
-  if (tid < n_ops) {
-    opbuf[2 * tid] = __ldg(gops + 2 * tid);
-    opbuf[2 * tid + 1] = __ldg(gops + 2 * tid + 1);
+#pragma unroll
+  for (int q = 0; q < kRecPerThread; ++q) {
+    const int r = q * kT + tid;
+    if (r < n_ops) {
+      opbuf[2 * r] = __ldg(gops + 2 * r);
+      opbuf[2 * r + 1] = __ldg(gops + 2 * r + 1);
+    }
   }
   __syncthreads();
   const int n_chunks = (n_ops + kChunk - 1) / kChunk;
   for (int c = 0; c < n_chunks; ++c) {
     // prefetch the next chunk into registers while this one is walked
-    const int nxt = (c + 1) * kChunk + tid;
-    const bool pf = nxt < n_ops;
-    int4 na = make_int4(0, 0, 0, 0), nb = na;
-    if (pf) {
-      na = __ldg(gops + 2 * nxt);
-      nb = __ldg(gops + 2 * nxt + 1);
+    int4 na[kRecPerThread], nb[kRecPerThread];
+#pragma unroll
+    for (int q = 0; q < kRecPerThread; ++q) {
+      const int nxt = (c + 1) * kChunk + q * kT + tid;
+      if (nxt < n_ops) {
+        na[q] = __ldg(gops + 2 * nxt);
+        nb[q] = __ldg(gops + 2 * nxt + 1);
+      }
     }
     const int4* buf = opbuf + (c & 1) * 2 * kChunk;
     const int cnt = min(kChunk, n_ops - c * kChunk);
@@ -355,10 +362,14 @@ __global__ void __launch_bounds__(kThreads) replay_walk_kernel(WalkParams P) {
         i += 1;
       }
     }
-    if (pf) {
-      int4* nbuf = opbuf + ((c + 1) & 1) * 2 * kChunk;
-      nbuf[2 * tid] = na;
-      nbuf[2 * tid + 1] = nb;
+    int4* nbuf = opbuf + ((c + 1) & 1) * 2 * kChunk;
+#pragma unroll
+    for (int q = 0; q < kRecPerThread; ++q) {
+      const int r = q * kT + tid;
+      if ((c + 1) * kChunk + r < n_ops) {
+        nbuf[2 * r] = na[q];
+        nbuf[2 * r + 1] = nb[q];
+      }
     }
     __syncthreads();
   }
@@ -537,48 +548,68 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
 // ------------------------------------------------------------ launchers
 int walk_threads() { return kThreads; }
 
-template <int kMode, bool kS, bool kF>
+template <int kT, int kMode, bool kS, bool kF>
 static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
                                  cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kMode, kS, kF>,
+    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kS, kF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  replay_walk_kernel<kMode, kS, kF><<<blocks, kThreads, smem, stream>>>(p);
+  replay_walk_kernel<kT, kMode, kS, kF><<<blocks, kT, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int kMode>
+template <int kT, int kMode>
 static cudaError_t launch_walk_mode(const WalkParams& p, size_t smem, unsigned blocks,
                                     cudaStream_t stream) {
   const bool s = p.out_start != nullptr, f = p.out_fin != nullptr;
-  if (s && f) return launch_walk_t<kMode, true, true>(p, smem, blocks, stream);
-  if (f) return launch_walk_t<kMode, false, true>(p, smem, blocks, stream);
-  if (s) return launch_walk_t<kMode, true, false>(p, smem, blocks, stream);
-  return launch_walk_t<kMode, false, false>(p, smem, blocks, stream);
+  if (s && f) return launch_walk_t<kT, kMode, true, true>(p, smem, blocks, stream);
+  if (f) return launch_walk_t<kT, kMode, false, true>(p, smem, blocks, stream);
+  if (s) return launch_walk_t<kT, kMode, true, false>(p, smem, blocks, stream);
+  return launch_walk_t<kT, kMode, false, false>(p, smem, blocks, stream);
 }
 
-cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
-  const size_t smem = 4 * kChunk * sizeof(int4) +
-                      static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) *
-                          kSlotStride;
-  const int per_block = kThreads * kScenPerThread;
-  const int chunks = (p.sp.count + per_block - 1) / per_block;
-  const long long blocks = static_cast<long long>(chunks) * p.n_comps;
+template <int kT>
+static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStream_t stream) {
+  const int per_block = kT * kScenPerThread;
+  const long long chunks = (p.sp.count + per_block - 1) / per_block;
+  const long long blocks = chunks * p.n_comps;
   if (blocks <= 0) return cudaSuccess;
   const unsigned nb = static_cast<unsigned>(blocks);
   switch (p.sp.mode) {
-    case 0: return launch_walk_mode<0>(p, smem, nb, stream);
-    case kModeScale: return launch_walk_mode<kModeScale>(p, smem, nb, stream);
-    case kModeJitter: return launch_walk_mode<kModeJitter>(p, smem, nb, stream);
+    case 0: return launch_walk_mode<kT, 0>(p, smem, nb, stream);
+    case kModeScale: return launch_walk_mode<kT, kModeScale>(p, smem, nb, stream);
+    case kModeJitter: return launch_walk_mode<kT, kModeJitter>(p, smem, nb, stream);
     case kModeScale | kModeJitter:
-      return launch_walk_mode<kModeScale | kModeJitter>(p, smem, nb, stream);
-    default: return launch_walk_mode<kModeExplicit>(p, smem, nb, stream);
+      return launch_walk_mode<kT, kModeScale | kModeJitter>(p, smem, nb, stream);
+    default: return launch_walk_mode<kT, kModeExplicit>(p, smem, nb, stream);
   }
+}
+
+// shared memory of a walk CTA of t threads
+static size_t walk_smem(int n_slots, int t) {
+  return 4 * kChunk * sizeof(int4) +
+         static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * 16;
+}
+
+int walk_width(int n_slots) {
+  const size_t cap = 227 * 1024;
+  if (walk_smem(n_slots, 128) <= cap / 2) return 128;  // >= 2 CTAs per SM
+  if (walk_smem(n_slots, 64) <= cap / 2) return 64;
+  if (walk_smem(n_slots, 32) <= cap) return 32;
+  return 0;
+}
+
+cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
+  const int t = walk_width(n_slots);
+  if (t == 128) return launch_walk_width<128>(p, walk_smem(n_slots, 128), stream);
+  if (t == 64) return launch_walk_width<64>(p, walk_smem(n_slots, 64), stream);
+  if (t == 32) return launch_walk_width<32>(p, walk_smem(n_slots, 32), stream);
+  return cudaErrorInvalidConfiguration;
 }
 
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,

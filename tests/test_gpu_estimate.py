@@ -1,0 +1,64 @@
+"""GPU parity of the estimate (generator-semantics) mode: the batched replay of
+generate_graph(estimate=True) with scenario durations must reproduce the
+reference's build_pipeline(spec, DurationHook) (pipeline.cpp:361-477) event
+times bit-for-bit — p2p rendezvous and collective barriers included."""
+import numpy as np
+import pytest
+
+import refshim as R
+from paper_2504_09307_b200 import ScenarioSpec, simulate_batch
+from paper_2504_09307_b200.synth import generate_graph
+from test_synth_graph import FIELDS, _my_lane_sequences, _ref_pipeline, _spec
+
+pytestmark = pytest.mark.gpu
+
+
+def _orc_graph(g):
+    return R.Graph(**{k: getattr(g, k) for k in FIELDS}, window_start=g.window_start,
+                   window_end=g.window_end)
+
+
+def _check(shape, S, seed, jitter, every=1, tp=1):
+    pp, dp, m, layers, d, f = shape
+    sg = generate_graph(_spec(pp, dp, m, layers, d, f, tp=tp, estimate=True))
+    g = sg.graph
+    spec = ScenarioSpec(count=S, seed=seed, jitter=jitter)
+    res = simulate_batch(g, spec, breakdown=False)
+    og = _orc_graph(g)
+    sc = R.OrcScenarios(seed=seed, jitter=jitter)
+    spec_json = R.synth_spec(pp=pp, dp=dp, m=m, layers=layers, d_model=d, d_ffn=f)
+    for s in range(0, S, every):
+        dur = R.orc_durations(og, sc, s)
+        for t in range(tp):
+            sel = np.where(g.rank % tp == t)[0]
+            hook = np.zeros(sg.n_ops, np.int64)
+            hook[sg.op_index[sel]] = dur[sel]
+            ref, _ = _ref_pipeline(spec_json, hook)
+            sub = R.Graph(**{k: (getattr(g, k)[sel] if k in ("duration", "original_start",
+                                                              "rank", "lane_kind", "lane",
+                                                              "op_class", "task_kind")
+                                 else getattr(g, k)) for k in FIELDS},
+                          window_start=g.window_start, window_end=g.window_end)
+            sub.rank = sub.rank // tp
+            got = _my_lane_sequences(sub, res.start[sel, s], res.fin[sel, s])
+            assert got == ref, f"scenario {s} replica {t}"
+    return res
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 4, 4, 1024, 4096), (1, 2, 4, 4, 1024, 4096),
+                                   (4, 2, 8, 4, 1024, 4096), (2, 4, 4, 4, 1024, 4096),
+                                   (8, 1, 8, 8, 1024, 4096)])
+def test_estimate_batch_matches_build_pipeline(shape):
+    _check(shape, S=40, seed=21, jitter=0.3)
+
+
+def test_estimate_config3_44b_tp4_sampled():
+    # BASELINE config 3: 44B (48 L, d 12288, f 24576) pp4 dp4 m16 x TP4 replicas
+    res = _check((4, 4, 16, 48, 12288, 24576), S=6, seed=250409307, jitter=0.1, tp=4)
+    assert res.span.shape == (6, 3)
+
+
+def test_estimate_nominal_equals_generator_truth():
+    sg = generate_graph(_spec(4, 2, 8, 4, estimate=True))
+    res = simulate_batch(sg.graph, ScenarioSpec(count=2), breakdown=False)
+    assert (res.makespan == sg.truth_makespan).all()
