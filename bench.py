@@ -1,0 +1,403 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched Lumos replay on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[4], the one quoted at 1/2/4/8 GPUs): the
+512-rank GPT-3 175B graph — 96 layers, d_model 12288, d_ffn 49152, pp4 dp16,
+32 microbatches, x TP8 replicas = 4,952,576 tasks — replayed for a
+65,536-scenario Monte Carlo (every task duration jittered ±10%, Philox keyed
+by (task, scenario)).  A step is one pass over the whole batch: every
+scenario's start/finish timestamps of every task (written to HBM, 1,024
+scenarios per tile), its makespan, the per-rank 4-way breakdown and the
+per-stream busy time; for N > 1 the scenarios are split across ranks and the
+per-scenario results are gathered to rank 0 over NCCL (the only collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU replay (oracle/_ref, the
+unmodified tracesim compiled here) on the box's host cores on a bounded sample
+of the same workload ("Measurement").
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (model, parallelism, tp replicas, scenarios, label)
+    "config5": (dict(n_layers=96, d_model=12288, d_ffn=49152, n_heads=96, d_head=128),
+                dict(pp=4, dp=16, num_microbatches=32), 8, 65536,
+                "512-rank GPT-3 175B (96L d12288 f49152, pp4 dp16 m32 x TP8 replicas)"),
+    "config4": (dict(n_layers=96, d_model=12288, d_ffn=49152, n_heads=96, d_head=128),
+                dict(pp=4, dp=8, num_microbatches=32), 8, 16384,
+                "256-rank GPT-3 175B (pp4 dp8 m32 x TP8 replicas)"),
+    "config2": (dict(n_layers=48, d_model=6144, d_ffn=12288, n_heads=48, d_head=128),
+                dict(pp=2, dp=2, num_microbatches=4), 2, 1024,
+                "8-rank GPT-3 15B (pp2 dp2 m4 x TP2 replicas)"),
+}
+METRIC = "scenario-node relaxations/sec (replays/sec) at 1/2/4/8 B200; % HBM roofline"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config5", choices=sorted(CONFIGS))
+    ap.add_argument("--scenarios", type=int, default=0, help="override the batch size")
+    ap.add_argument("--tile", type=int, default=1024)
+    ap.add_argument("--jitter", type=float, default=0.1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def walk_traffic(config, tile):
+    """dram bytes per walk launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "walk_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(f"{config}/tile{tile}")
+        return e
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------ reference arm
+
+def cpu_sample_graph(args):
+    """The reference's own graph for the bounded CPU sample: one TP replica of
+    the workload (the tp=1 generator graph, identical per-replica structure)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refshim as R
+    model, par, tp, _, _ = CONFIGS[args.config]
+    spec = R.synth_spec(pp=par["pp"], dp=par["dp"], m=par["num_microbatches"],
+                        layers=model["n_layers"], d_model=model["d_model"], d_ffn=model["d_ffn"],
+                        heads=model["n_heads"])
+    h, _ = R.generate(spec, tp=1)
+    g = h.export()
+    return R, h, g
+
+
+def cpu_threads():
+    n = os.cpu_count() or 1
+    return max(1, min(n, 16))
+
+
+def run_cpu_sample(R, h, g, args, first, threads, per_thread=1):
+    sc = R.OrcScenarios(seed=250409307, jitter=args.jitter)
+    cls = g.default_scale_class()
+    count = threads * per_thread
+    secs, mk = h.bench_simulate(sc, first, count, cls, threads)
+    return secs, count
+
+
+def reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    R, h, g = cpu_sample_graph(args)
+    threads = cpu_threads()
+    for w in range(args.warmup):
+        run_cpu_sample(R, h, g, args, 10_000_000 + w * threads, threads)
+    # each step's clock covers the parallel simulate() region only; the
+    # per-thread graph copies are made before it starts (ref_shim.cpp)
+    wall = 0.0
+    total = 0
+    for k in range(args.steps):
+        secs, count = run_cpu_sample(R, h, g, args, k * threads, threads)
+        wall += secs
+        total += count
+    relax = g.n * total / wall
+    line = {"impl": "reference", "metric": METRIC, "value": relax, "unit": "relaxations/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (generator graph, Philox-jittered durations)",
+            "replays_per_s": total / wall,
+            "config": {"workload": CONFIGS[args.config][4] + " — reference CPU replay on a "
+                       "bounded sample", "sample_tasks": g.n},
+            "cpu_baseline": {"value": relax, "unit": "relaxations/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{threads} scenarios per step, one per host thread, each a "
+                                       f"full tracesim::simulate() of one TP replica "
+                                       f"({g.n} tasks) of the workload"},
+            "e2e": {"value": relax, "unit": "relaxations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2504_09307_b200 import DeviceGraph, ScenarioSpec
+    from paper_2504_09307_b200 import _native as N
+    from paper_2504_09307_b200.synth import SynthSpec, generate_graph
+
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    model, par, tp, scenarios, label = CONFIGS[args.config]
+    S_total = args.scenarios or scenarios
+    S_local = S_total // world
+    first = rank * S_local
+    tile = min(args.tile, S_local)
+    assert S_local % tile == 0, "scenarios per GPU must be a multiple of the tile"
+
+    t0 = time.time()
+    sg = generate_graph(SynthSpec(tp=tp, **model, **par))
+    g = sg.graph
+    t_gen = time.time() - t0
+    t0 = time.time()
+    dg = DeviceGraph(g, device=local)
+    t_compile = time.time() - t0
+    n = dg.n_tasks
+    R_, ST_ = dg.n_ranks, dg.n_streams
+
+    dev = torch.device("cuda", local)
+    start = torch.empty((n, tile), dtype=torch.int64, device=dev)
+    fin = torch.empty((n, tile), dtype=torch.int64, device=dev)
+    span = torch.empty((S_local, 3), dtype=torch.int64, device=dev)
+    bd = torch.empty((S_local, R_, 5), dtype=torch.int64, device=dev)
+    busy = torch.empty((S_local, ST_), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    if world > 1 and rank == 0:
+        span_all = torch.empty((S_total, 3), dtype=torch.int64, device=dev)
+        bd_all = torch.empty((S_total, R_, 5), dtype=torch.int64, device=dev)
+        busy_all = torch.empty((S_total, ST_), dtype=torch.int64, device=dev)
+
+    def gather():
+        if world == 1:
+            return
+        for loc, tot in ((span, span_all if rank == 0 else None),
+                         (bd, bd_all if rank == 0 else None),
+                         (busy, busy_all if rank == 0 else None)):
+            dist.gather(loc, list(tot.chunk(world)) if rank == 0 else None, dst=0)
+
+    def step():
+        for t0_ in range(0, S_local, tile):
+            spec = ScenarioSpec(count=tile, first=first + t0_, seed=250409307, jitter=args.jitter)
+            dg.replay_batch(spec, start=start, fin=fin, ld=tile, span=span[t0_:t0_ + tile],
+                            rank_breakdown=bd[t0_:t0_ + tile], stream_busy=busy[t0_:t0_ + tile],
+                            stream=sptr)
+        gather()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # timed region
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    dg.profile(True)
+    dg.profile_read()
+    launches0 = N.lib().ts_kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    ms = e0.elapsed_time(e1)
+    launches = (N.lib().ts_kernel_launches() - launches0) / args.steps
+    prof = dg.profile_read()
+    dg.profile(False)
+    clocks = sampler.stop()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    relax_per_step = n * S_total
+    value = relax_per_step / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (K1 walk): algorithmic bytes per launch =
+    # start + finish rows written (16 B per task per scenario); predecessor
+    # finishes are read from shared memory (0 HBM bytes) and durations are
+    # generated in registers (0 HBM bytes) — DESIGN.md "Roofline".
+    walk_bytes = n * tile * 16 + dg.info["program_bytes"]
+    walk_avg_ms = prof["walk_ms"] / max(1, prof["walk_launches"])
+    achieved = walk_bytes / (walk_avg_ms / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    traffic = walk_traffic(args.config, tile)
+    step_ms_dev = (prof["walk_ms"] + prof["reduce_ms"] + prof["other_ms"]) / args.steps
+
+    # end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_span = torch.empty((S_local, 3), dtype=torch.int64).pin_memory()
+        h_bd = torch.empty((S_local, R_, 5), dtype=torch.int64).pin_memory()
+        h_busy = torch.empty((S_local, ST_), dtype=torch.int64).pin_memory()
+        sc_bytes = 0
+
+        def e2e_step():
+            nonlocal sc_bytes
+            sc_bytes = 0
+            for t0_ in range(0, S_local, tile):
+                spec = ScenarioSpec(count=tile, first=first + t0_, seed=250409307,
+                                    jitter=args.jitter)
+                sc_bytes += 72  # the ts_scenarios descriptor read from host memory
+                dg.replay_batch(spec, start=start, fin=fin, ld=tile,
+                                span=h_span[t0_:t0_ + tile], rank_breakdown=h_bd[t0_:t0_ + tile],
+                                stream_busy=h_busy[t0_:t0_ + tile], stream=sptr)
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        tw = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e2e_s = (time.perf_counter() - tw) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        d2h = (h_span.numel() + h_bd.numel() + h_busy.numel()) * 8
+        e2e = {"value": relax_per_step / e2e_s, "unit": "relaxations/s",
+               "h2d_bytes_per_step": sc_bytes, "d2h_bytes_per_step": d2h * world,
+               "ms_per_step": e2e_s * 1e3,
+               "note": "host scenario descriptors in, per-scenario span + per-rank breakdown + "
+                       "per-stream busy copied to pinned host memory every step; timestamps "
+                       "stay in device memory"}
+
+    # CPU baseline (rank 0, N = 1 only): the reference on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            R, h, cg = cpu_sample_graph(args)
+            threads = cpu_threads()
+            secs, count = run_cpu_sample(R, h, cg, args, 0, threads, per_thread=1)
+            cpu = {"value": cg.n * count / secs, "unit": "relaxations/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"{count} scenarios ({threads} threads x 1), each a full "
+                             f"tracesim::simulate() of one TP replica ({cg.n} tasks) of the "
+                             f"workload, {secs:.1f} s wall"}
+        except Exception as exc:  # the oracle library is test infrastructure
+            cpu = {"value": None, "unit": "relaxations/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "relaxations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (GPT-3 generator graph, random-free base durations from the "
+                    "reference cost formulas; Philox-jittered scenarios)",
+            "replays_per_s": S_total / (ms_per_step / 1e3),
+            "config": {"workload": f"{args.config}: {label}, {S_total}-scenario Monte Carlo "
+                                   f"(jitter {args.jitter})",
+                       "tasks": n, "edges": int(g.edge_from.shape[0]), "ranks": R_,
+                       "scenarios": S_total, "tile": tile, "parallelism": f"scenario-shard x{world}",
+                       "outputs": "start+finish of every task x scenario (HBM), span, per-rank "
+                                  "breakdown, per-stream busy",
+                       "l2": "no flush needed: each tile writes 16 B x tasks x tile "
+                             f"= {n * tile * 16 / 1e9:.0f} GB >> 126 MB L2",
+                       "graph_gen_s": round(t_gen, 2), "compile_s": round(t_compile, 2)},
+            "gpu_launches": launches,
+            "device_ms_per_step": {"walk": prof["walk_ms"] / args.steps,
+                                   "reduce": prof["reduce_ms"] / args.steps,
+                                   "other": prof["other_ms"] / args.steps,
+                                   "sum": step_ms_dev},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "replay_walk (K1)", "bytes_per_launch": walk_bytes,
+                         "launch_ms": walk_avg_ms, "peak_source": peak_src},
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -236,6 +236,21 @@ int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, con
                         const int64_t* arg_stream, const char* names, int64_t gap_threshold_us,
                         ts_host_graph** inout);
 
+/* Device-time accounting: when enabled, CUDA events are recorded on the
+ * caller's stream around every kernel the engine launches for this graph;
+ * ts_profile_read waits for them, returns the accumulated milliseconds per
+ * kernel class and resets the counters. */
+typedef struct {
+  double walk_ms;          /* K1 replay walk (durations fused) */
+  int64_t walk_launches;
+  double reduce_ms;        /* K5 per-rank breakdown / stream busy */
+  int64_t reduce_launches;
+  double other_ms;         /* span init / finalize */
+  int64_t other_launches;
+} ts_profile_stats;
+int ts_profile_enable(ts_graph* g, int enable);
+int ts_profile_read(ts_graph* g, ts_profile_stats* out);
+
 /* Launch counters (kernels this library enqueued since creation). */
 int64_t ts_kernel_launches(void);
 const char* ts_last_error(void);

@@ -53,6 +53,12 @@ class TsScenarios(C.Structure):
                 ("scale_num", i32p), ("durations", i64p), ("durations_ld", C.c_int64)]
 
 
+class TsProfileStats(C.Structure):
+    _fields_ = [("walk_ms", C.c_double), ("walk_launches", C.c_int64), ("reduce_ms", C.c_double),
+                ("reduce_launches", C.c_int64), ("other_ms", C.c_double),
+                ("other_launches", C.c_int64)]
+
+
 class TsResult(C.Structure):
     _fields_ = [("start", i64p), ("fin", i64p), ("ld", C.c_int64), ("span", i64p),
                 ("rank_breakdown", i64p), ("stream_busy", i64p), ("status", i32p)]
@@ -90,6 +96,10 @@ def lib():
         L.ts_scenario_durations.restype = C.c_int
         L.ts_scenario_durations.argtypes = [C.c_void_p, C.POINTER(TsScenarios), i64p, C.c_int64,
                                             C.c_void_p]
+        L.ts_profile_enable.restype = C.c_int
+        L.ts_profile_enable.argtypes = [C.c_void_p, C.c_int]
+        L.ts_profile_read.restype = C.c_int
+        L.ts_profile_read.argtypes = [C.c_void_p, C.POINTER(TsProfileStats)]
         if L.ts_abi_version() != 1:
             raise RuntimeError("liblumos_b200.so ABI mismatch")
         _lib = L
@@ -102,4 +112,7 @@ def last_error() -> str:
 
 EXPORTED = ["ts_abi_version", "ts_last_error", "ts_kernel_launches", "ts_graph_create",
             "ts_graph_destroy", "ts_graph_get_info", "ts_graph_ranks", "ts_graph_streams",
-            "ts_replay_batch", "ts_simulate", "ts_scenario_durations"]
+            "ts_replay_batch", "ts_simulate", "ts_scenario_durations", "ts_profile_enable",
+            "ts_profile_read", "ts_synth_defaults", "ts_synth_graph", "ts_host_graph_desc",
+            "ts_host_graph_op_index", "ts_host_graph_n_ops", "ts_host_graph_name_ids",
+            "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph"]

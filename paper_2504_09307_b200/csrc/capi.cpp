@@ -107,8 +107,50 @@ struct ts_graph {
   int32_t* d_rank_stream_off = nullptr;
   int32_t* d_stream_node_off = nullptr;
   int32_t* d_stream_nodes = nullptr;
-  DevBuf span_lo, span_hi, status, scratch_ts, stage_out, stage_in;
+  DevBuf span_lo, span_hi, status, scratch_ts;
+  DevBuf stage[8];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur
+  // device-time accounting
+  bool profile = false;
+  struct Mark {
+    cudaEvent_t a, b;
+    int kind;  // 0 walk, 1 reduce, 2 other
+  };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
 };
+
+namespace {
+// records events around one launch when profiling is on
+struct Timed {
+  ts_graph* g;
+  cudaStream_t s;
+  int kind;
+  cudaEvent_t a = nullptr;
+  Timed(ts_graph* g_, cudaStream_t s_, int k) : g(g_), s(s_), kind(k) {
+    if (g->profile) {
+      a = g->get_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Timed() {
+    if (a) {
+      cudaEvent_t b = g->get_event();
+      cudaEventRecord(b, s);
+      g->marks.push_back({a, b, kind});
+    }
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -197,9 +239,13 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_stream_node_off),
                     static_cast<void*>(g->d_stream_nodes)})
       if (p) cudaFree(p);
-    for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts, &g->stage_out,
-                      &g->stage_in})
-      b->release();
+    for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts}) b->release();
+    for (DevBuf& b : g->stage) b.release();
+    for (auto& m : g->marks) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+    for (cudaEvent_t e : g->event_pool) cudaEventDestroy(e);
     if (prev >= 0) cudaSetDevice(prev);
   }
   delete g;
@@ -301,37 +347,25 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   cudaGetDevice(&prev_dev);
   if (prev_dev != g->device) CUDA_TRY(cudaSetDevice(g->device));
 
-  // inputs given as host memory are staged on the device
-  std::vector<void*> owned;
-  auto stage_in = [&](const void* host, size_t bytes, const void** dev) -> cudaError_t {
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
+  // inputs given as host memory are staged on the device (persistent buffers)
+  auto stage_in = [&](int slot, const void* host, size_t bytes, const void** dev) -> cudaError_t {
+    cudaError_t e = g->stage[slot].reserve(bytes);
     if (e != cudaSuccess) return e;
-    owned.push_back(p);
-    *dev = p;
-    return cudaMemcpyAsync(p, host, bytes, cudaMemcpyHostToDevice, stream);
+    *dev = g->stage[slot].p;
+    return cudaMemcpyAsync(g->stage[slot].p, host, bytes, cudaMemcpyHostToDevice, stream);
   };
-  auto cleanup = [&] {
-    for (void* p : owned) cudaFree(p);
-    owned.clear();
-  };
+  auto cleanup = [] {};
   if (sp.scale_num && !is_device_ptr(sp.scale_num)) {
     const void* d = nullptr;
-    cudaError_t e = stage_in(sp.scale_num, static_cast<size_t>(count) * sp.n_classes * 4, &d);
-    if (e != cudaSuccess) {
-      cleanup();
-      return fail(TS_E_CUDA, cudaGetErrorString(e));
-    }
+    cudaError_t e = stage_in(5, sp.scale_num, static_cast<size_t>(count) * sp.n_classes * 4, &d);
+    if (e != cudaSuccess) return fail(TS_E_CUDA, cudaGetErrorString(e));
     sp.scale_num = static_cast<const int32_t*>(d);
   }
   if (sp.durations && !is_device_ptr(sp.durations)) {
     const void* d = nullptr;
-    cudaError_t e = stage_in(sp.durations,
+    cudaError_t e = stage_in(6, sp.durations,
                              static_cast<size_t>(c.n_tasks) * sp.durations_ld * 8, &d);
-    if (e != cudaSuccess) {
-      cleanup();
-      return fail(TS_E_CUDA, cudaGetErrorString(e));
-    }
+    if (e != cudaSuccess) return fail(TS_E_CUDA, cudaGetErrorString(e));
     sp.durations = static_cast<const int64_t*>(d);
   }
 
@@ -346,23 +380,21 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     void* dev;
   };
   std::vector<OutBuf> copies;
-  auto out_ptr = [&](void* user, size_t bytes) -> void* {
+  auto out_ptr = [&](int slot, void* user, size_t bytes) -> void* {
     if (!user) return nullptr;
     if (is_device_ptr(user)) return user;
-    void* p = nullptr;
-    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-    owned.push_back(p);
-    copies.push_back({user, bytes, p});
-    return p;
+    if (g->stage[slot].reserve(bytes) != cudaSuccess) return nullptr;
+    copies.push_back({user, bytes, g->stage[slot].p});
+    return g->stage[slot].p;
   };
   const size_t ts_bytes = static_cast<size_t>(c.n_tasks) * static_cast<size_t>(out->ld) * 8;
-  int64_t* d_start = static_cast<int64_t*>(out_ptr(out->start, ts_bytes));
-  int64_t* d_fin = static_cast<int64_t*>(out_ptr(out->fin, ts_bytes));
-  int64_t* d_span = static_cast<int64_t*>(out_ptr(out->span, static_cast<size_t>(count) * 24));
+  int64_t* d_start = static_cast<int64_t*>(out_ptr(0, out->start, ts_bytes));
+  int64_t* d_fin = static_cast<int64_t*>(out_ptr(1, out->fin, ts_bytes));
+  int64_t* d_span = static_cast<int64_t*>(out_ptr(2, out->span, static_cast<size_t>(count) * 24));
   int64_t* d_bd = static_cast<int64_t*>(
-      out_ptr(out->rank_breakdown, static_cast<size_t>(count) * n_ranks * 40));
+      out_ptr(3, out->rank_breakdown, static_cast<size_t>(count) * n_ranks * 40));
   int64_t* d_busy = static_cast<int64_t*>(
-      out_ptr(out->stream_busy, static_cast<size_t>(count) * n_streams * 8));
+      out_ptr(4, out->stream_busy, static_cast<size_t>(count) * n_streams * 8));
   if ((out->start && !d_start) || (out->fin && !d_fin) || (out->span && !d_span) ||
       (out->rank_breakdown && !d_bd) || (out->stream_busy && !d_busy)) {
     cleanup();
@@ -393,7 +425,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     s_ld = sub;
   }
 
-  CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
+  {
+    Timed tm(g, stream, 2);
+    CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
+  }
   g_launches++;
   for (int32_t b0 = 0; b0 < count; b0 += sub) {
     const int32_t bn = std::min(sub, count - b0);
@@ -422,6 +457,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
                      (!wp.out_start || al(wp.out_start)) && (!wp.out_fin || al(wp.out_fin));
     }
     if (wp.n_comps > 0) {
+      Timed tm(g, stream, 0);
       CUDA_TRY(launch_replay_walk(wp, c.max_slots, stream));
       g_launches++;
     }
@@ -443,11 +479,15 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       rp.n_streams = n_streams;
       rp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
       rp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
-      CUDA_TRY(launch_rank_reduce(rp, stream));
+      {
+        Timed tm(g, stream, 1);
+        CUDA_TRY(launch_rank_reduce(rp, stream));
+      }
       g_launches++;
     }
   }
   if (d_span) {
+    Timed tm(g, stream, 2);
     CUDA_TRY(launch_span_finalize(lo, hi, c.window_start, d_span, nullptr, count, stream));
     g_launches++;
   }
@@ -478,6 +518,36 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
                 std::to_string(n_fail) +
                     " scenario(s) failed the static sync-binding certificate and need the "
                     "exact event-driven replay");
+  return TS_OK;
+}
+
+int ts_profile_enable(ts_graph* g, int enable) {
+  if (!g) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  g->profile = enable != 0;
+  return TS_OK;
+}
+
+int ts_profile_read(ts_graph* g, ts_profile_stats* out) {
+  if (!g || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  for (auto& m : g->marks) {
+    CUDA_TRY(cudaEventSynchronize(m.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, m.a, m.b));
+    if (m.kind == 0) {
+      out->walk_ms += ms;
+      out->walk_launches++;
+    } else if (m.kind == 1) {
+      out->reduce_ms += ms;
+      out->reduce_launches++;
+    } else {
+      out->other_ms += ms;
+      out->other_launches++;
+    }
+    g->event_pool.push_back(m.a);
+    g->event_pool.push_back(m.b);
+  }
+  g->marks.clear();
   return TS_OK;
 }
 

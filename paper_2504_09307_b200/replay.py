@@ -187,6 +187,18 @@ class DeviceGraph:
         if rc != N.TS_OK:
             _raise(rc)
 
+    def profile(self, enable: bool = True) -> None:
+        """Record CUDA events around every kernel this graph launches."""
+        N.lib().ts_profile_enable(self.h, 1 if enable else 0)
+
+    def profile_read(self) -> dict:
+        """Accumulated device milliseconds per kernel class since the last read."""
+        st = N.TsProfileStats()
+        rc = N.lib().ts_profile_read(self.h, C.byref(st))
+        if rc != N.TS_OK:
+            _raise(rc)
+        return {k: getattr(st, k) for k, _ in N.TsProfileStats._fields_}
+
     def scenario_durations(self, spec: ScenarioSpec, out=None, stream=None):
         """Materialise scenario durations [n_tasks][count] (the K4 kernel alone)."""
         if out is None:
