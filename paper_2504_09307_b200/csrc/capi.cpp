@@ -107,6 +107,8 @@ struct ts_graph {
   int32_t* d_rank_stream_off = nullptr;
   int32_t* d_stream_node_off = nullptr;
   int32_t* d_stream_nodes = nullptr;
+  int32_t* d_rank_lists = nullptr;                // ranks grouped by stream-count bucket
+  int32_t bucket_off[kReduceBuckets + 1] = {0};
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[8];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur
   // device-time accounting
@@ -217,6 +219,17 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   if (e == cudaSuccess) e = upload(&g->d_rank_stream_off, c.rank_stream_off);
   if (e == cudaSuccess) e = upload(&g->d_stream_node_off, c.stream_node_off);
   if (e == cudaSuccess) e = upload(&g->d_stream_nodes, c.stream_nodes);
+  {
+    std::vector<int32_t> lists;
+    for (int b = 0; b < kReduceBuckets; ++b) {
+      g->bucket_off[b] = static_cast<int32_t>(lists.size());
+      for (size_t r = 0; r + 1 < c.rank_stream_off.size(); ++r)
+        if (reduce_bucket(c.rank_stream_off[r + 1] - c.rank_stream_off[r]) == b)
+          lists.push_back(static_cast<int32_t>(r));
+    }
+    g->bucket_off[kReduceBuckets] = static_cast<int32_t>(lists.size());
+    if (e == cudaSuccess) e = upload(&g->d_rank_lists, lists);
+  }
   g->has_device = true;
   if (e != cudaSuccess) {
     ts_graph_destroy(g);
@@ -237,7 +250,7 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
                     static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
                     static_cast<void*>(g->d_stream_node_off),
-                    static_cast<void*>(g->d_stream_nodes)})
+                    static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists)})
       if (p) cudaFree(p);
     for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts}) b->release();
     for (DevBuf& b : g->stage) b.release();
@@ -479,11 +492,14 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       rp.n_streams = n_streams;
       rp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
       rp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
-      {
+      for (int b = 0; b < kReduceBuckets; ++b) {
+        const int nr = g->bucket_off[b + 1] - g->bucket_off[b];
+        if (nr == 0) continue;
+        rp.rank_list = g->d_rank_lists + g->bucket_off[b];
         Timed tm(g, stream, 1);
-        CUDA_TRY(launch_rank_reduce(rp, stream));
+        CUDA_TRY(launch_rank_reduce(rp, b, nr, stream));
+        g_launches++;
       }
-      g_launches++;
     }
   }
   if (d_span) {

@@ -1072,8 +1072,13 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
       if (lanes[l].kind != TS_LANE_CUDA_STREAM) continue;
       out.stream_rank.push_back(lanes[l].rank);
       out.stream_lane.push_back(lanes[l].lane);
-      for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k)
-        out.stream_nodes.push_back(lane_tasks[k]);
+      for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k) {
+        const int32_t t = lane_tasks[k];
+        // bit 31 carries OpClass::Communication for the reduction kernel
+        out.stream_nodes.push_back(out.is_comm[t] ? static_cast<int32_t>(
+                                                        static_cast<uint32_t>(t) | 0x80000000u)
+                                                  : t);
+      }
       out.stream_node_off.push_back(static_cast<int32_t>(out.stream_nodes.size()));
     }
     for (size_t r = ri + 1; r <= out.ranks.size(); ++r)

@@ -51,6 +51,7 @@ struct WalkParams {
 };
 
 struct ReduceParams {
+  const int32_t* rank_list;  // ranks (indices into rank_stream_off) of this launch
   const int32_t* rank_stream_off;
   const int32_t* stream_node_off;
   const int32_t* stream_nodes;
@@ -80,6 +81,9 @@ cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W
                                  int64_t* makespan, int32_t count, cudaStream_t stream);
 cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
                              int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream);
-cudaError_t launch_rank_reduce(const ReduceParams& p, cudaStream_t stream);
+constexpr int kReduceBuckets = 7;
+int reduce_bucket(int streams_in_rank);
+cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in_bucket,
+                               cudaStream_t stream);
 
 }  // namespace lumos

@@ -135,18 +135,6 @@ __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a
 __device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
-// One 32-byte record as two 16-byte read-only loads (every lane of the CTA
-// reads the same address: a broadcast, L1-resident after the first warp).
-struct Rec {
-  int4 a, b;
-};
-__device__ __forceinline__ Rec load_rec(const Op* p) {
-  Rec r;
-  r.a = __ldg(reinterpret_cast<const int4*>(p));
-  r.b = __ldg(reinterpret_cast<const int4*>(p) + 1);
-  return r;
-}
-
 // ------------------------------------------------------------------- K1
 // One thread replays two adjacent scenarios (columns c, c+1): the op record is
 // decoded once per pair, each operand is one 16-byte shared load, and each
@@ -427,60 +415,129 @@ __global__ void durations_kernel(ScenarioParams sp, const int64_t* __restrict__ 
 // ------------------------------------------------------------------- K5
 constexpr int kMaxStreamsPerRank = 32;
 
-__global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
-  if (col >= P.count) return;
-  const int s0 = P.rank_stream_off[r], s1 = P.rank_stream_off[r + 1];
-  const int ns = s1 - s0;
+// Each thread owns one scenario of one rank and merges the rank's stream
+// timelines (each stream's kernels are chain-ordered, hence time-ordered and
+// disjoint).  Per stream the thread keeps a private, double-buffered ring of
+// 2 x H intervals in shared memory; the half it is not reading is refilled
+// with cp.async (global -> shared, no registers), so the merge waits on memory
+// only when a refill issued ~H intervals earlier has not landed yet.  The
+// stream node lists carry the communication flag in bit 31.
+template <int NS>
+struct RingHalf {
+  static constexpr int value = NS <= 2 ? 4 : NS <= 4 ? 2 : 1;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int NS>
+__device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col, int r, int ns,
+                                                 int64_t* ring) {
+  constexpr int H = RingHalf<NS>::value;
+  const int tid = threadIdx.x;
+  const int s0 = P.rank_stream_off[r];
   const int64_t W = P.window_start;
-  const int64_t mk = P.span_hi[col] - P.span_lo[col];
   int64_t wend = P.window_end;
   {
-    int64_t a = P.span_lo[col], b = P.span_hi[col];
-    int64_t m = (a == kMaxI64) ? 0 : (b - a);
-    (void)mk;
+    const int64_t a = P.span_lo[col], b = P.span_hi[col];
+    const int64_t m = (a == kMaxI64) ? 0 : (b - a);
     if (W + m > wend) wend = W + m;
   }
   if (wend < W) wend = W;
-
-  int idx[kMaxStreamsPerRank];
-  int end[kMaxStreamsPerRank];
-  unsigned inside = 0;
-  int64_t busy_acc = 0;
-  for (int j = 0; j < ns; ++j) {
-    idx[j] = P.stream_node_off[s0 + j];
-    end[j] = P.stream_node_off[s0 + j + 1];
-  }
   const int64_t* __restrict__ S = P.start;
   const int64_t* __restrict__ F = P.fin;
   const int64_t ld = P.ld;
-  auto clip_s = [&](int node) { return imax(S[static_cast<int64_t>(node) * ld + col], W); };
-  auto clip_e = [&](int node) { return imin(F[static_cast<int64_t>(node) * ld + col], wend); };
-  // skip empty (after clipping) intervals at the front of every stream
-  int64_t next_t[kMaxStreamsPerRank];
-  for (int j = 0; j < ns; ++j) {
-    next_t[j] = kMaxI64;
-    while (idx[j] < end[j]) {
-      const int node = P.stream_nodes[idx[j]];
-      const int64_t a = clip_s(node), b = clip_e(node);
-      if (a < b) {
-        next_t[j] = a;
-        break;
+  const int* __restrict__ nodes = P.stream_nodes;
+  // ring layout [NS][2 halves][H][2 (start, fin)][kThreads]
+#define RING(j, h, q, k) ring[(((((j) * 2 + (h)) * H + (q)) * 2 + (k)) * kThreads) + tid]
+
+  int next_idx[NS], end_idx[NS];
+  int half[NS], pos[NS], avail[NS], pend[NS];
+  uint32_t cbits[NS], pbits[NS];  // comm flags of the current / prefetched half
+  auto prefetch = [&](int j, int h) {
+    const int base = next_idx[j];
+    const int n = min(H, end_idx[j] - base);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int q = 0; q < H; ++q)
+      if (q < n) {
+        const int e = nodes[base + q];
+        const int node = e & 0x7FFFFFFF;
+        bits |= static_cast<uint32_t>(e < 0) << q;
+        const int64_t off = static_cast<int64_t>(node) * ld + col;
+        cp_async8(&RING(j, h, q, 0), S + off);
+        cp_async8(&RING(j, h, q, 1), F + off);
       }
-      ++idx[j];
+    cp_async_commit();
+    next_idx[j] = base + n;
+    pend[j] = n;
+    pbits[j] = bits;
+  };
+  int64_t cs[NS], ce[NS];
+  bool cc[NS], inside[NS];
+  // move stream j to its next non-empty clipped interval (or exhaust it)
+  auto advance = [&](int j) {
+    for (;;) {
+      if (pos[j] >= avail[j]) {
+        if (pend[j] == 0) {
+          cs[j] = ce[j] = kMaxI64;
+          return;
+        }
+        cp_async_wait_all();
+        half[j] ^= 1;
+        avail[j] = pend[j];
+        cbits[j] = pbits[j];
+        pos[j] = 0;
+        pend[j] = 0;
+        if (next_idx[j] < end_idx[j]) prefetch(j, half[j] ^ 1);
+      }
+      const int q = pos[j]++;
+      const int64_t a = imax(RING(j, half[j], q, 0), W);
+      const int64_t b = imin(RING(j, half[j], q, 1), wend);
+      if (a < b) {
+        cs[j] = a;
+        ce[j] = b;
+        cc[j] = (cbits[j] >> q) & 1u;
+        return;
+      }
     }
+  };
+  int64_t busy[NS];
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    next_idx[j] = j < ns ? P.stream_node_off[s0 + j] : 0;
+    end_idx[j] = j < ns ? P.stream_node_off[s0 + j + 1] : 0;
+    half[j] = 1;  // the first switch moves to half 0
+    pos[j] = avail[j] = pend[j] = 0;
+    cbits[j] = pbits[j] = 0;
+    inside[j] = false;
+    busy[j] = 0;
+    if (next_idx[j] < end_idx[j]) prefetch(j, 0);
   }
+#pragma unroll
+  for (int j = 0; j < NS; ++j) advance(j);
+
   int compute = 0, comm = 0;
   int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
   for (;;) {
     int jm = -1;
     int64_t tm = kMaxI64;
-    for (int j = 0; j < ns; ++j)
-      if (next_t[j] < tm) {
-        tm = next_t[j];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      const int64_t t = inside[j] ? ce[j] : cs[j];
+      if (t < tm) {
+        tm = t;
         jm = j;
       }
+    }
     if (jm < 0) break;
     if (tm > prev) {
       const int64_t span = tm - prev;
@@ -490,30 +547,21 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
       else ot += span;
       prev = tm;
     }
-    const int node = P.stream_nodes[idx[jm]];
-    const bool c = P.is_comm[node] != 0;
-    if (!((inside >> jm) & 1u)) {
-      // interval opens
-      if (c) ++comm; else ++compute;
-      inside |= 1u << jm;
-      next_t[jm] = clip_e(node);
-    } else {
-      if (c) --comm; else --compute;
-      inside &= ~(1u << jm);
-      if (P.stream_busy) busy_acc = 0;
-      ++idx[jm];
-      next_t[jm] = kMaxI64;
-      while (idx[jm] < end[jm]) {
-        const int nn = P.stream_nodes[idx[jm]];
-        const int64_t a = clip_s(nn), b = clip_e(nn);
-        if (a < b) {
-          next_t[jm] = a;
-          break;
-        }
-        ++idx[jm];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) {
+      if (j != jm) continue;
+      if (!inside[j]) {
+        if (cc[j]) ++comm; else ++compute;
+        inside[j] = true;
+      } else {
+        if (cc[j]) --comm; else --compute;
+        busy[j] += ce[j] - cs[j];
+        inside[j] = false;
+        advance(j);
       }
     }
   }
+#undef RING
   if (wend > prev) {
     const int64_t span = wend - prev;
     if (compute > 0 && comm > 0) ov += span;
@@ -521,7 +569,6 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
     else if (comm > 0) em += span;
     else ot += span;
   }
-  (void)busy_acc;
   if (P.breakdown) {
     int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
     row[0] = wend - W;
@@ -531,16 +578,20 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
     row[4] = ot;
   }
   if (P.stream_busy) {
-    for (int j = 0; j < ns; ++j) {
-      int64_t b = 0;
-      for (int k = P.stream_node_off[s0 + j]; k < P.stream_node_off[s0 + j + 1]; ++k) {
-        const int node = P.stream_nodes[k];
-        const int64_t a = clip_s(node), e = clip_e(node);
-        if (a < e) b += e - a;
-      }
-      P.stream_busy[static_cast<int64_t>(col) * P.n_streams + s0 + j] = b;
-    }
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+      if (j < ns) P.stream_busy[static_cast<int64_t>(col) * P.n_streams + s0 + j] = busy[j];
   }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
+  extern __shared__ int64_t ring[];
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = P.rank_list[blockIdx.y];
+  if (col >= P.count) return;
+  const int ns = P.rank_stream_off[r + 1] - P.rank_stream_off[r];
+  rank_reduce_body<NS>(P, col, r, ns, ring);
 }
 
 }  // namespace
@@ -634,10 +685,36 @@ cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_rank_reduce(const ReduceParams& p, cudaStream_t stream) {
-  if (p.count <= 0 || p.n_ranks <= 0) return cudaSuccess;
-  dim3 grid((p.count + kThreads - 1) / kThreads, p.n_ranks);
-  rank_reduce_kernel<<<grid, kThreads, 0, stream>>>(p);
+int reduce_bucket(int ns) {
+  return ns <= 1 ? 0 : ns == 2 ? 1 : ns == 3 ? 2 : ns == 4 ? 3 : ns <= 8 ? 4 : ns <= 16 ? 5 : 6;
+}
+
+cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in_bucket,
+                               cudaStream_t stream) {
+  if (p.count <= 0 || n_ranks_in_bucket <= 0) return cudaSuccess;
+  dim3 grid((p.count + kThreads - 1) / kThreads, n_ranks_in_bucket);
+  auto go = [&](auto kern, int ns) -> cudaError_t {
+    const int h = ns <= 2 ? 4 : ns <= 4 ? 2 : 1;
+    const size_t smem = static_cast<size_t>(ns) * 2 * h * 2 * kThreads * sizeof(int64_t);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, kThreads, smem, stream>>>(p);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  switch (bucket) {
+    case 0: e = go(rank_reduce_kernel<1>, 1); break;
+    case 1: e = go(rank_reduce_kernel<2>, 2); break;
+    case 2: e = go(rank_reduce_kernel<3>, 3); break;
+    case 3: e = go(rank_reduce_kernel<4>, 4); break;
+    case 4: e = go(rank_reduce_kernel<8>, 8); break;
+    case 5: e = go(rank_reduce_kernel<16>, 16); break;
+    default: e = go(rank_reduce_kernel<kMaxStreamsPerRank>, kMaxStreamsPerRank); break;
+  }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
