@@ -108,6 +108,13 @@ struct ts_graph {
   int32_t* d_stream_node_off = nullptr;
   int32_t* d_stream_nodes = nullptr;
   int32_t* d_rank_lists = nullptr;                // ranks grouped by stream-count bucket
+  // event-driven path tables
+  int64_t* d_ostart = nullptr;
+  int32_t *d_lane_of = nullptr, *d_lane_off = nullptr, *d_lane_tasks = nullptr;
+  int32_t *d_succ_off = nullptr, *d_succ = nullptr, *d_indeg0 = nullptr, *d_rule_of = nullptr;
+  int32_t *d_rule_kind = nullptr, *d_rule_bound = nullptr, *d_rule_wl_off = nullptr;
+  int32_t *d_rule_wl = nullptr, *d_lane_rank = nullptr, *d_lane_stream = nullptr;
+  DevBuf des_scratch;
   int32_t bucket_off[kReduceBuckets + 1] = {0};
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[8];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur
@@ -190,7 +197,7 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     cudaGetDevice(&g->device);
   }
   const CompiledGraph& c = g->cg;
-  if (walk_width(c.max_slots) == 0) {
+  if (!c.des_only && walk_width(c.max_slots) == 0) {
     const std::string msg = "a component needs " + std::to_string(c.max_slots) +
                             " live values per scenario: more than shared memory holds";
     delete g;
@@ -230,6 +237,23 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     g->bucket_off[kReduceBuckets] = static_cast<int32_t>(lists.size());
     if (e == cudaSuccess) e = upload(&g->d_rank_lists, lists);
   }
+  {
+    const DesTables& T = c.des;
+    if (e == cudaSuccess) e = upload(&g->d_ostart, T.ostart);
+    if (e == cudaSuccess) e = upload(&g->d_lane_of, T.lane_of);
+    if (e == cudaSuccess) e = upload(&g->d_lane_off, T.lane_off);
+    if (e == cudaSuccess) e = upload(&g->d_lane_tasks, T.lane_tasks);
+    if (e == cudaSuccess) e = upload(&g->d_succ_off, T.succ_off);
+    if (e == cudaSuccess) e = upload(&g->d_succ, T.succ);
+    if (e == cudaSuccess) e = upload(&g->d_indeg0, T.indeg0);
+    if (e == cudaSuccess) e = upload(&g->d_rule_of, T.rule_of);
+    if (e == cudaSuccess) e = upload(&g->d_rule_kind, T.rule_kind);
+    if (e == cudaSuccess) e = upload(&g->d_rule_bound, T.rule_bound);
+    if (e == cudaSuccess) e = upload(&g->d_rule_wl_off, T.rule_wl_off);
+    if (e == cudaSuccess) e = upload(&g->d_rule_wl, T.rule_wl);
+    if (e == cudaSuccess) e = upload(&g->d_lane_rank, T.lane_rank);
+    if (e == cudaSuccess) e = upload(&g->d_lane_stream, T.lane_stream);
+  }
   g->has_device = true;
   if (e != cudaSuccess) {
     ts_graph_destroy(g);
@@ -250,8 +274,16 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
                     static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
                     static_cast<void*>(g->d_stream_node_off),
-                    static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists)})
+                    static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists),
+                    static_cast<void*>(g->d_ostart), static_cast<void*>(g->d_lane_of),
+                    static_cast<void*>(g->d_lane_off), static_cast<void*>(g->d_lane_tasks),
+                    static_cast<void*>(g->d_succ_off), static_cast<void*>(g->d_succ),
+                    static_cast<void*>(g->d_indeg0), static_cast<void*>(g->d_rule_of),
+                    static_cast<void*>(g->d_rule_kind), static_cast<void*>(g->d_rule_bound),
+                    static_cast<void*>(g->d_rule_wl_off), static_cast<void*>(g->d_rule_wl),
+                    static_cast<void*>(g->d_lane_rank), static_cast<void*>(g->d_lane_stream)})
       if (p) cudaFree(p);
+    g->des_scratch.release();
     for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts}) b->release();
     for (DevBuf& b : g->stage) b.release();
     for (auto& m : g->marks) {
@@ -394,7 +426,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   };
   std::vector<OutBuf> copies;
   auto out_ptr = [&](int slot, void* user, size_t bytes) -> void* {
-    if (!user) return nullptr;
+    if (!user || bytes == 0) return nullptr;
     if (is_device_ptr(user)) return user;
     if (g->stage[slot].reserve(bytes) != cudaSuccess) return nullptr;
     copies.push_back({user, bytes, g->stage[slot].p});
@@ -408,8 +440,9 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       out_ptr(3, out->rank_breakdown, static_cast<size_t>(count) * n_ranks * 40));
   int64_t* d_busy = static_cast<int64_t*>(
       out_ptr(4, out->stream_busy, static_cast<size_t>(count) * n_streams * 8));
-  if ((out->start && !d_start) || (out->fin && !d_fin) || (out->span && !d_span) ||
-      (out->rank_breakdown && !d_bd) || (out->stream_busy && !d_busy)) {
+  if ((out->start && ts_bytes && !d_start) || (out->fin && ts_bytes && !d_fin) ||
+      (out->span && !d_span) || (out->rank_breakdown && n_ranks && !d_bd) ||
+      (out->stream_busy && n_streams && !d_busy)) {
     cleanup();
     return fail(TS_E_NOMEM, "could not stage output buffers");
   }
@@ -469,12 +502,63 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       wp.vec_store = (wp.ld % 2 == 0) && (bn % 2 == 0) &&
                      (!wp.out_start || al(wp.out_start)) && (!wp.out_fin || al(wp.out_fin));
     }
-    if (wp.n_comps > 0) {
+    if (!c.des_only && wp.n_comps > 0) {
       Timed tm(g, stream, 0);
       CUDA_TRY(launch_replay_walk(wp, c.max_slots, stream));
       g_launches++;
     }
-    if (want_red) {
+    if (c.des_only || c.n_syncs > 0) {
+      // exact event-driven replay: every scenario of a graph outside the
+      // chained class, or (fix-up) the scenarios whose certificate failed
+      DesParams dp{};
+      const DesTables& T = c.des;
+      dp.n = c.n_tasks;
+      dp.nl = T.n_lanes;
+      dp.ostart = g->d_ostart;
+      dp.lane_of = g->d_lane_of;
+      dp.lane_off = g->d_lane_off;
+      dp.lane_tasks = g->d_lane_tasks;
+      dp.succ_off = g->d_succ_off;
+      dp.succ = g->d_succ;
+      dp.indeg0 = g->d_indeg0;
+      dp.rule_of = g->d_rule_of;
+      dp.rule_kind = g->d_rule_kind;
+      dp.rule_bound = g->d_rule_bound;
+      dp.rule_wl_off = g->d_rule_wl_off;
+      dp.rule_wl = g->d_rule_wl;
+      dp.base = g->d_base;
+      dp.cls = g->d_cls;
+      dp.is_comm = g->d_is_comm;
+      dp.lane_rank = g->d_lane_rank;
+      dp.lane_stream = g->d_lane_stream;
+      dp.n_ranks = n_ranks;
+      dp.n_streams = n_streams;
+      dp.W = c.window_start;
+      dp.window_end = c.window_end;
+      dp.sp = wp.sp;
+      dp.out_start = wp.out_start;
+      dp.out_fin = wp.out_fin;
+      dp.ld = wp.ld;
+      dp.span_lo = wp.span_lo;
+      dp.span_hi = wp.span_hi;
+      dp.status = wp.status;
+      dp.fixup = c.des_only ? 0 : 1;
+      if (c.des_only) {  // the walk's reductions are not valid here: DES does them
+        dp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
+        dp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
+      }
+      const size_t per = des_scratch_bytes(c.n_tasks, T.n_lanes);
+      const size_t budget = size_t(1) << 30;
+      dp.n_slots = static_cast<int32_t>(
+          std::max<size_t>(1, std::min<size_t>(static_cast<size_t>(bn), budget / per)));
+      CUDA_TRY(g->des_scratch.reserve(per * dp.n_slots));
+      dp.scratch = g->des_scratch.as<char>();
+      dp.scratch_bytes = static_cast<int64_t>(per);
+      Timed tm(g, stream, 2);
+      CUDA_TRY(launch_des(dp, stream));
+      g_launches++;
+    }
+    if (want_red && !c.des_only) {
       ReduceParams rp{};
       rp.rank_stream_off = g->d_rank_stream_off;
       rp.stream_node_off = g->d_stream_node_off;
@@ -508,9 +592,9 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     g_launches++;
   }
 
-  // certificate failures need the exact event-driven path
+  // deadlock (only possible outside the chained class) -> SimulationError
   std::vector<int32_t> host_status;
-  if (c.n_syncs > 0 || out->status) {
+  if (c.des_only || (out->status && !is_device_ptr(out->status))) {
     host_status.resize(count);
     CUDA_TRY(cudaMemcpyAsync(host_status.data(), status, static_cast<size_t>(count) * 4,
                              cudaMemcpyDeviceToHost, stream));
@@ -526,14 +610,12 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     else
       std::memcpy(out->status, host_status.data(), static_cast<size_t>(count) * 4);
   }
-  int64_t n_fail = 0;
-  for (int32_t s : host_status) n_fail += s != 0;
   if (prev_dev >= 0 && prev_dev != g->device) cudaSetDevice(prev_dev);
-  if (n_fail > 0)
-    return fail(TS_E_UNSUPPORTED,
-                std::to_string(n_fail) +
-                    " scenario(s) failed the static sync-binding certificate and need the "
-                    "exact event-driven replay");
+  int64_t n_dead = 0;
+  for (int32_t st : host_status) n_dead += st < 0;
+  if (c.des_only && n_dead > 0)
+    return fail(TS_E_SIMULATION, "deadlock: " + std::to_string(n_dead) +
+                                     " scenario(s) left tasks blocked");
   return TS_OK;
 }
 

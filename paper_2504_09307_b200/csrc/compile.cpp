@@ -104,7 +104,9 @@ struct CertEntry {
 
 }  // namespace
 
-int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
+namespace {
+
+int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
   const int32_t n = d.n_tasks;
   if (n < 0) {
     err = "n_tasks must be non-negative";
@@ -1041,10 +1043,17 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
     out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
   }
 
-  // ----------------------------------------------------- per-task arrays
+  return TS_OK;
+}
+
+// per-task arrays, reduction metadata and the event-driven (DES) tables — for
+// every graph, whichever replay path it takes
+void build_common(const ts_graph_desc& d, CompiledGraph& out) {
+  const int32_t n = d.n_tasks;
   out.base.assign(d.duration, d.duration + n);
   out.scale_class.resize(n);
   out.is_comm.resize(n);
+  out.n_gpu_tasks = 0;
   for (int32_t t = 0; t < n; ++t) {
     out.scale_class[t] = d.scale_class ? d.scale_class[t]
                                        : static_cast<uint8_t>(d.task_kind && d.task_kind[t]
@@ -1057,11 +1066,46 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
     if (d.lane_kind[t] == TS_LANE_CUDA_STREAM) out.n_gpu_tasks++;
   }
 
-  // -------------------------------------------- reduction metadata (K5)
+  // lanes = distinct processors in ProcessorId order (simulate.cpp:164-171)
+  std::vector<Proc> lanes(n);
+  for (int32_t i = 0; i < n; ++i) lanes[i] = {d.rank[i], d.lane_kind[i], d.lane[i]};
+  std::sort(lanes.begin(), lanes.end());
+  lanes.erase(std::unique(lanes.begin(), lanes.end()), lanes.end());
+  const int32_t nl = static_cast<int32_t>(lanes.size());
+  auto lane_index = [&](const Proc& p) -> int32_t {
+    auto it = std::lower_bound(lanes.begin(), lanes.end(), p);
+    return (it != lanes.end() && *it == p) ? static_cast<int32_t>(it - lanes.begin()) : -1;
+  };
+  std::vector<int32_t> lane_of(n), lane_off(nl + 1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    lane_of[i] = lane_index({d.rank[i], d.lane_kind[i], d.lane[i]});
+    lane_off[lane_of[i] + 1]++;
+  }
+  for (int32_t l = 0; l < nl; ++l) lane_off[l + 1] += lane_off[l];
+  std::vector<int32_t> lane_tasks(n);
+  {
+    std::vector<int32_t> fill(lane_off.begin(), lane_off.end() - 1);
+    for (int32_t i = 0; i < n; ++i) lane_tasks[fill[lane_of[i]]++] = i;
+  }
+  for (int32_t l = 0; l < nl; ++l)
+    std::sort(lane_tasks.begin() + lane_off[l], lane_tasks.begin() + lane_off[l + 1],
+              [&](int32_t x, int32_t y) {
+                return std::make_pair(d.original_start[x], x) <
+                       std::make_pair(d.original_start[y], y);
+              });
+
+  // reduction metadata (K5): ranks (ranks_in, build.cpp:582-590), their
+  // stream lanes and each stream's kernels in chain (= time) order
+  out.ranks.clear();
   for (int32_t l = 0; l < nl; ++l)
     if (out.ranks.empty() || out.ranks.back() != lanes[l].rank) out.ranks.push_back(lanes[l].rank);
   out.rank_stream_off.assign(out.ranks.size() + 1, 0);
-  out.stream_node_off.push_back(0);
+  out.stream_node_off.assign(1, 0);
+  out.stream_rank.clear();
+  out.stream_lane.clear();
+  out.stream_nodes.clear();
+  out.des.lane_stream.assign(nl, -1);
+  out.des.lane_rank.assign(nl, 0);
   {
     size_t ri = 0;
     for (int32_t l = 0; l < nl; ++l) {
@@ -1069,7 +1113,9 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
         ++ri;
         out.rank_stream_off[ri] = static_cast<int32_t>(out.stream_rank.size());
       }
+      out.des.lane_rank[l] = static_cast<int32_t>(ri);
       if (lanes[l].kind != TS_LANE_CUDA_STREAM) continue;
+      out.des.lane_stream[l] = static_cast<int32_t>(out.stream_rank.size());
       out.stream_rank.push_back(lanes[l].rank);
       out.stream_lane.push_back(lanes[l].lane);
       for (int32_t k = lane_off[l]; k < lane_off[l + 1]; ++k) {
@@ -1084,6 +1130,67 @@ int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) 
     for (size_t r = ri + 1; r <= out.ranks.size(); ++r)
       out.rank_stream_off[r] = static_cast<int32_t>(out.stream_rank.size());
   }
+
+  // event-driven replay tables (restating the Engine, simulate.cpp:162-196)
+  DesTables& T = out.des;
+  T.n_lanes = nl;
+  T.lane_of = lane_of;
+  T.lane_off = lane_off;
+  T.lane_tasks = lane_tasks;
+  T.ostart.assign(d.original_start, d.original_start + n);
+  std::vector<std::pair<int32_t, int32_t>> edges;
+  edges.reserve(static_cast<size_t>(d.n_edges));
+  for (int64_t e = 0; e < d.n_edges; ++e) edges.emplace_back(d.edge_from[e], d.edge_to[e]);
+  std::sort(edges.begin(), edges.end());
+  edges.erase(std::unique(edges.begin(), edges.end()), edges.end());
+  T.succ_off.assign(n + 1, 0);
+  T.indeg0.assign(n, 0);
+  for (const auto& e : edges) {
+    T.succ_off[e.first + 1]++;
+    T.indeg0[e.second]++;
+  }
+  for (int32_t i = 0; i < n; ++i) T.succ_off[i + 1] += T.succ_off[i];
+  T.succ.resize(edges.size());
+  {
+    std::vector<int32_t> fill(T.succ_off.begin(), T.succ_off.end() - 1);
+    for (const auto& e : edges) T.succ[fill[e.first]++] = e.second;
+  }
+  T.rule_of.assign(n, -1);
+  T.rule_kind.clear();
+  T.rule_bound.clear();
+  T.rule_wl_off.assign(1, 0);
+  T.rule_wl.clear();
+  for (int32_t r = 0; r < d.n_rules; ++r) {
+    T.rule_of[d.rule_task[r]] = r;  // a later rule on the same task wins
+    T.rule_kind.push_back(d.rule_kind[r]);
+    T.rule_bound.push_back(d.rule_bound ? d.rule_bound[r] : -1);
+    for (int32_t w = d.rule_watch_off[r]; w < d.rule_watch_off[r + 1]; ++w) {
+      const int32_t l = lane_index({d.watch_rank[w], d.watch_kind[w], d.watch_lane[w]});
+      if (l >= 0) T.rule_wl.push_back(l);  // processors without tasks are ignored
+    }
+    T.rule_wl_off.push_back(static_cast<int32_t>(T.rule_wl.size()));
+  }
+}
+
+}  // namespace
+
+int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
+  int rc = compile_programs(d, out, err);
+  if (rc == TS_E_UNSUPPORTED && d.n_gates == 0) {
+    // outside the chained class: every scenario takes the exact event-driven
+    // path (a restatement of the reference Engine on the device)
+    const int32_t n = d.n_tasks;
+    out = CompiledGraph{};
+    out.n_tasks = n;
+    out.window_start = d.window_start;
+    out.window_end = d.window_end;
+    out.des_only = true;
+    out.des_reason = err;
+    err.clear();
+    rc = TS_OK;
+  }
+  if (rc != TS_OK) return rc;
+  build_common(d, out);
   return TS_OK;
 }
 

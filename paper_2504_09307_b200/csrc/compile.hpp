@@ -10,6 +10,22 @@
 
 namespace lumos {
 
+// Tables of the exact event-driven replay (the reference Engine, restated on
+// the device for graphs outside the chained class and for scenarios whose
+// sync certificate fails).
+struct DesTables {
+  int32_t n_lanes = 0;
+  std::vector<int32_t> lane_of;     // [n]
+  std::vector<int32_t> lane_off;    // [n_lanes + 1]: each lane's ready-heap region
+  std::vector<int32_t> lane_tasks;  // [n] tasks of each lane, (original_start, id) order
+  std::vector<int64_t> ostart;      // [n] dispatch key (original_start)
+  std::vector<int32_t> succ_off, succ, indeg0;
+  std::vector<int32_t> rule_of;     // [n] -> rule or -1
+  std::vector<int32_t> rule_kind, rule_bound, rule_wl_off, rule_wl;  // watched lane ids
+  std::vector<int32_t> lane_rank;   // [n_lanes] rank slot
+  std::vector<int32_t> lane_stream; // [n_lanes] stream slot or -1 (CPU lane)
+};
+
 struct CompiledGraph {
   int32_t n_tasks = 0;
   int64_t window_start = 0;
@@ -34,6 +50,11 @@ struct CompiledGraph {
   std::vector<int32_t> stream_lane;
   std::vector<int32_t> stream_node_off;  // [n_streams + 1]
   std::vector<int32_t> stream_nodes;
+
+  // event-driven path
+  bool des_only = false;    // graph outside the chained class
+  std::string des_reason;   // why (the compiler's message)
+  DesTables des;
 };
 
 // Returns TS_OK or a TS_E_* code with `err` set to the reference-style message.

@@ -1,0 +1,333 @@
+// des.cu — exact event-driven replay on the device (one thread per scenario).
+//
+// A restatement of the reference Engine (/root/reference/proj/src/
+// simulate.cpp:145-337) for the cases the straight-line walk does not cover:
+//   * graphs outside the chained class (lanes not linked by fixed edges, rules
+//     watching CPU lanes, ...) — every scenario runs here, and
+//   * scenarios of chained graphs whose static sync-binding certificate failed
+//     in the walk — only those are re-run here (fix-up mode).
+// Per scenario: lane clocks, per-lane ready heaps keyed (original_start, id),
+// a completion heap keyed (end, id); each iteration starts the smallest-key
+// startable lane head (drain_startable) and then pops every completion at the
+// next end time.  Deadlock -> status -1 (SimulationError in the reference).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_common.cuh"
+#include "kernels.hpp"
+#include "lumos_b200.h"
+
+namespace lumos {
+
+namespace {
+
+struct DesScratch {
+  int64_t* sim_start;  // [n]  (INT64_MIN = not started)
+  int64_t* sim_end;    // [n]
+  int64_t* comp_t;     // [n]  completion heap keys
+  int64_t* clock;      // [nl]
+  int64_t* ev;         // [2n] breakdown events
+  int32_t* indeg;      // [n]
+  int32_t* heap;       // [n]  per-lane ready heaps (lane_off regions)
+  int32_t* comp_id;    // [n]
+  int32_t* hsize;      // [nl]
+};
+
+__device__ DesScratch carve(char* base, int32_t n, int32_t nl) {
+  DesScratch s;
+  int64_t* p64 = reinterpret_cast<int64_t*>(base);
+  s.sim_start = p64;
+  s.sim_end = p64 + n;
+  s.comp_t = p64 + 2 * static_cast<int64_t>(n);
+  s.clock = p64 + 3 * static_cast<int64_t>(n);
+  s.ev = s.clock + nl;
+  int32_t* p32 = reinterpret_cast<int32_t*>(s.ev + 2 * static_cast<int64_t>(n));
+  s.indeg = p32;
+  s.heap = p32 + n;
+  s.comp_id = p32 + 2 * static_cast<int64_t>(n);
+  s.hsize = p32 + 3 * static_cast<int64_t>(n);
+  return s;
+}
+
+struct Des {
+  const DesParams& P;
+  DesScratch s;
+
+  __device__ bool key_less(int32_t a, int32_t b) const {
+    const int64_t ka = P.ostart[a], kb = P.ostart[b];
+    return ka < kb || (ka == kb && a < b);
+  }
+  // ready heap of lane l (min by (original_start, id))
+  __device__ void ready_push(int32_t l, int32_t t) {
+    int32_t* h = s.heap + P.lane_off[l];
+    int32_t i = s.hsize[l]++;
+    h[i] = t;
+    while (i > 0) {
+      const int32_t p = (i - 1) >> 1;
+      if (!key_less(h[i], h[p])) break;
+      const int32_t x = h[i];
+      h[i] = h[p];
+      h[p] = x;
+      i = p;
+    }
+  }
+  __device__ void ready_pop(int32_t l) {
+    int32_t* h = s.heap + P.lane_off[l];
+    const int32_t n = --s.hsize[l];
+    h[0] = h[n];
+    int32_t i = 0;
+    for (;;) {
+      const int32_t a = 2 * i + 1, b = a + 1;
+      int32_t m = i;
+      if (a < n && key_less(h[a], h[m])) m = a;
+      if (b < n && key_less(h[b], h[m])) m = b;
+      if (m == i) break;
+      const int32_t x = h[i];
+      h[i] = h[m];
+      h[m] = x;
+      i = m;
+    }
+  }
+  __device__ bool comp_less(int32_t i, int32_t j) const {
+    return s.comp_t[i] < s.comp_t[j] || (s.comp_t[i] == s.comp_t[j] && s.comp_id[i] < s.comp_id[j]);
+  }
+  __device__ void comp_swap(int32_t i, int32_t j) {
+    const int64_t t = s.comp_t[i];
+    s.comp_t[i] = s.comp_t[j];
+    s.comp_t[j] = t;
+    const int32_t d = s.comp_id[i];
+    s.comp_id[i] = s.comp_id[j];
+    s.comp_id[j] = d;
+  }
+  __device__ void comp_push(int32_t& size, int64_t t, int32_t id) {
+    int32_t i = size++;
+    s.comp_t[i] = t;
+    s.comp_id[i] = id;
+    while (i > 0) {
+      const int32_t p = (i - 1) >> 1;
+      if (!comp_less(i, p)) break;
+      comp_swap(i, p);
+      i = p;
+    }
+  }
+  __device__ void comp_pop(int32_t& size) {
+    const int32_t n = --size;
+    s.comp_t[0] = s.comp_t[n];
+    s.comp_id[0] = s.comp_id[n];
+    int32_t i = 0;
+    for (;;) {
+      const int32_t a = 2 * i + 1, b = a + 1;
+      int32_t m = i;
+      if (a < n && comp_less(a, m)) m = a;
+      if (b < n && comp_less(b, m)) m = b;
+      if (m == i) break;
+      comp_swap(i, m);
+      i = m;
+    }
+  }
+  // rule_ok (simulate.cpp:202-217)
+  __device__ bool rule_ok(int32_t t, int32_t own, int64_t now) const {
+    const int32_t r = P.rule_of[t];
+    if (r < 0) return true;
+    if (P.rule_kind[r] == TS_RULE_EVENT_SYNC) {
+      const int32_t b = P.rule_bound[r];
+      if (b < 0) return true;
+      return s.sim_start[b] != kMinI64 && s.sim_end[b] <= now;
+    }
+    for (int32_t w = P.rule_wl_off[r]; w < P.rule_wl_off[r + 1]; ++w) {
+      const int32_t lw = P.rule_wl[w];
+      if (s.clock[lw] > now) return false;
+      const int32_t pending = s.hsize[lw] - (lw == own ? 1 : 0);
+      if (pending > 0) return false;
+    }
+    return true;
+  }
+  __device__ void complete(int32_t t) {
+    for (int32_t k = P.succ_off[t]; k < P.succ_off[t + 1]; ++k) {
+      const int32_t v = P.succ[k];
+      if (--s.indeg[v] == 0) ready_push(P.lane_of[v], v);
+    }
+  }
+};
+
+// heap sort of int64 keys (breakdown events)
+__device__ void sort_i64(int64_t* a, int32_t n) {
+  auto sift = [&](int32_t i, int32_t m) {
+    for (;;) {
+      int32_t c = 2 * i + 1;
+      if (c >= m) break;
+      if (c + 1 < m && a[c + 1] > a[c]) ++c;
+      if (a[c] <= a[i]) break;
+      const int64_t x = a[i];
+      a[i] = a[c];
+      a[c] = x;
+      i = c;
+    }
+  };
+  for (int32_t i = n / 2 - 1; i >= 0; --i) sift(i, n);
+  for (int32_t m = n - 1; m > 0; --m) {
+    const int64_t x = a[0];
+    a[0] = a[m];
+    a[m] = x;
+    sift(0, m);
+  }
+}
+
+__global__ void des_kernel(DesParams P) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= P.n_slots) return;
+  const int32_t n = P.n, nl = P.nl;
+  Des E{P, carve(P.scratch + static_cast<int64_t>(slot) * P.scratch_bytes, n, nl)};
+  DesScratch& s = E.s;
+  for (int col = slot; col < P.sp.count; col += P.n_slots) {
+    if (P.fixup && P.status[col] == 0) continue;
+    ThreadScen ts;
+    init_thread_scen(P.sp, col, ts);
+    const int64_t W = P.W;
+    for (int32_t l = 0; l < nl; ++l) {
+      s.clock[l] = W;
+      s.hsize[l] = 0;
+    }
+    for (int32_t t = 0; t < n; ++t) {
+      s.indeg[t] = P.indeg0[t];
+      s.sim_start[t] = kMinI64;
+    }
+    for (int32_t t = 0; t < n; ++t)
+      if (s.indeg[t] == 0) E.ready_push(P.lane_of[t], t);
+    int64_t now = W;
+    int32_t unstarted = n, comp = 0;
+    bool dead = false;
+    for (;;) {
+      // drain_startable (simulate.cpp:239-255)
+      for (;;) {
+        int32_t best = -1, best_lane = -1;
+        for (int32_t l = 0; l < nl; ++l) {
+          if (s.clock[l] > now || s.hsize[l] == 0) continue;
+          const int32_t head = s.heap[P.lane_off[l]];
+          if (!E.rule_ok(head, l, now)) continue;
+          if (best < 0 || E.key_less(head, best)) {
+            best = head;
+            best_lane = l;
+          }
+        }
+        if (best < 0) break;
+        E.ready_pop(best_lane);
+        const int64_t d = scenario_duration<-1>(P.sp, ts, best, P.base[best], P.cls[best]);
+        s.sim_start[best] = now;
+        s.sim_end[best] = now + d;
+        --unstarted;
+        if (d == 0) {
+          E.complete(best);
+        } else {
+          s.clock[best_lane] = now + d;
+          E.comp_push(comp, now + d, best);
+        }
+      }
+      if (comp == 0) {
+        dead = unstarted != 0;
+        break;
+      }
+      const int64_t t2 = s.comp_t[0];
+      while (comp > 0 && s.comp_t[0] == t2) {
+        const int32_t done = s.comp_id[0];
+        E.comp_pop(comp);
+        E.complete(done);
+      }
+      now = t2;
+    }
+    if (dead) {
+      P.status[col] = -1;
+      continue;
+    }
+    int64_t lo = W, hi = W;
+    if (n > 0) {
+      lo = kMaxI64;
+      hi = kMinI64;
+      for (int32_t t = 0; t < n; ++t) {
+        lo = imin(lo, s.sim_start[t]);
+        hi = imax(hi, s.sim_end[t]);
+        if (P.out_start) P.out_start[static_cast<int64_t>(t) * P.ld + col] = s.sim_start[t];
+        if (P.out_fin) P.out_fin[static_cast<int64_t>(t) * P.ld + col] = s.sim_end[t];
+      }
+      if (hi < lo) hi = lo;
+    }
+    P.span_lo[col] = lo;
+    P.span_hi[col] = hi;
+    P.status[col] = 1;
+    if (!P.breakdown && !P.stream_busy) continue;
+    // per-rank breakdown (metrics.cpp:43-103) on sorted interval endpoints
+    int64_t wend = P.window_end;
+    if (W + (hi - lo) > wend) wend = W + (hi - lo);
+    if (wend < W) wend = W;
+    int32_t l = 0;
+    while (l < nl) {
+      const int32_t r = P.lane_rank[l];
+      int32_t ne = 0;
+      int32_t l1 = l;
+      for (; l1 < nl && P.lane_rank[l1] == r; ++l1) {
+        const int32_t st = P.lane_stream[l1];
+        if (st < 0) continue;
+        int64_t busy = 0;
+        for (int32_t k = P.lane_off[l1]; k < P.lane_off[l1 + 1]; ++k) {
+          const int32_t t = P.lane_tasks[k];
+          const int64_t a = imax(s.sim_start[t], W), b = imin(s.sim_end[t], wend);
+          if (a >= b) continue;
+          busy += b - a;
+          const int64_t c = P.is_comm[t] ? 2 : 0;  // 0 compute, 2 comm; +1 = end
+          s.ev[ne++] = ((a - W) << 2) | c;
+          s.ev[ne++] = ((b - W) << 2) | (c + 1);
+        }
+        if (P.stream_busy) P.stream_busy[static_cast<int64_t>(col) * P.n_streams + st] = busy;
+      }
+      sort_i64(s.ev, ne);
+      int compute = 0, commc = 0;
+      int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
+      auto account = [&](int64_t upto) {
+        if (upto <= prev) return;
+        const int64_t span = upto - prev;
+        if (compute > 0 && commc > 0) ov += span;
+        else if (compute > 0) ec += span;
+        else if (commc > 0) em += span;
+        else ot += span;
+        prev = upto;
+      };
+      for (int32_t k = 0; k < ne; ++k) {
+        account(W + (s.ev[k] >> 2));
+        switch (s.ev[k] & 3) {
+          case 0: ++compute; break;
+          case 1: --compute; break;
+          case 2: ++commc; break;
+          default: --commc; break;
+        }
+      }
+      account(wend);
+      if (P.breakdown) {
+        int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
+        row[0] = wend - W;
+        row[1] = ec;
+        row[2] = em;
+        row[3] = ov;
+        row[4] = ot;
+      }
+      l = l1;
+    }
+  }
+}
+
+}  // namespace
+
+size_t des_scratch_bytes(int32_t n, int32_t nl) {
+  const size_t b = (static_cast<size_t>(n) * 3 + nl + 2 * static_cast<size_t>(n)) * 8 +
+                   (static_cast<size_t>(n) * 3 + nl) * 4;
+  return (b + 255) / 256 * 256;
+}
+
+cudaError_t launch_des(const DesParams& p, cudaStream_t stream) {
+  if (p.n_slots <= 0 || p.sp.count <= 0) return cudaSuccess;
+  const int threads = 64;
+  des_kernel<<<(p.n_slots + threads - 1) / threads, threads, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace lumos

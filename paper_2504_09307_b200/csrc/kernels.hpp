@@ -71,6 +71,44 @@ struct ReduceParams {
   int64_t* stream_busy;  // [count][n_streams]
 };
 
+struct DesParams {
+  int32_t n, nl;
+  const int64_t* ostart;
+  const int32_t* lane_of;
+  const int32_t* lane_off;
+  const int32_t* lane_tasks;
+  const int32_t* succ_off;
+  const int32_t* succ;
+  const int32_t* indeg0;
+  const int32_t* rule_of;
+  const int32_t* rule_kind;
+  const int32_t* rule_bound;
+  const int32_t* rule_wl_off;
+  const int32_t* rule_wl;
+  const int64_t* base;
+  const uint8_t* cls;
+  const uint8_t* is_comm;
+  const int32_t* lane_rank;
+  const int32_t* lane_stream;
+  int32_t n_ranks, n_streams;
+  int64_t W, window_end;
+  ScenarioParams sp;
+  int64_t* out_start;
+  int64_t* out_fin;
+  int64_t ld;
+  int64_t* span_lo;
+  int64_t* span_hi;
+  int32_t* status;
+  int64_t* breakdown;
+  int64_t* stream_busy;
+  int32_t fixup;    // only scenarios whose status is non-zero (certificate failed)
+  int32_t n_slots;  // concurrent scenarios (scratch slots)
+  char* scratch;
+  int64_t scratch_bytes;  // per slot
+};
+size_t des_scratch_bytes(int32_t n, int32_t nl);
+cudaError_t launch_des(const DesParams& p, cudaStream_t stream);
+
 int walk_threads();
 int walk_width(int n_slots);  // walk CTA width for a slot count (0: too many)
 int max_streams_per_rank();

@@ -21,6 +21,7 @@
 
 #include <cstdint>
 
+#include "device_common.cuh"
 #include "kernels.hpp"
 #include "program.hpp"
 
@@ -29,109 +30,8 @@ namespace lumos {
 namespace {
 
 constexpr int kThreads = kWalkThreads;  // widest walk CTA; K4/K5 block size
-constexpr int64_t kMinI64 = INT64_MIN;
-constexpr int64_t kMaxI64 = INT64_MAX;
 
-__device__ __forceinline__ void philox2x32_10(uint32_t& x0, uint32_t& x1, uint32_t key) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t hi = __umulhi(0xD256D193u, x0);
-    const uint32_t lo = 0xD256D193u * x0;
-    x0 = hi ^ key ^ x1;
-    x1 = lo;
-    key += 0x9E3779B9u;
-  }
-}
-
-// (a * num + den/2) / den for a >= 0, num >= 0 (transform.cpp:38-43)
-__device__ __forceinline__ int64_t mul_div_nonneg(int64_t a, int64_t num, int64_t den,
-                                                  int den_shift) {
-  const uint64_t ua = static_cast<uint64_t>(a), un = static_cast<uint64_t>(num);
-  uint64_t lo = ua * un;
-  uint64_t hi = __umul64hi(ua, un);
-  const uint64_t half = static_cast<uint64_t>(den / 2);
-  const uint64_t lo2 = lo + half;
-  hi += lo2 < lo ? 1 : 0;
-  lo = lo2;
-  if (den_shift >= 0) {
-    if (den_shift == 0) return static_cast<int64_t>(lo);
-    return static_cast<int64_t>((lo >> den_shift) | (hi << (64 - den_shift)));
-  }
-  const uint64_t ud = static_cast<uint64_t>(den);
-  if (hi == 0) return static_cast<int64_t>(lo / ud);
-  // 128 / 64 long division (rare: products beyond 2^64)
-  uint64_t q = 0, r = hi % ud;
-  for (int b = 63; b >= 0; --b) {
-    const bool top = (r >> 63) != 0;
-    r = (r << 1) | ((lo >> b) & 1u);
-    if (top || r >= ud) {
-      r -= ud;
-      q |= 1ull << b;
-    }
-  }
-  return static_cast<int64_t>(q);
-}
-
-struct ThreadScen {
-  int64_t scen;    // global scenario id
-  int32_t col;     // column in the batch
-  int32_t num[kMaxClasses];
-};
-
-__device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t scen, int col,
-                                             int cls) {
-  if (sp.scale_num) return sp.scale_num[static_cast<int64_t>(col) * sp.n_classes + cls];
-  uint32_t x0 = static_cast<uint32_t>(cls), x1 = static_cast<uint32_t>(scen);
-  philox2x32_10(x0, x1, sp.key_cls);
-  return sp.scale_lo + static_cast<int32_t>((static_cast<uint64_t>(x0) * sp.scale_span) >> 32);
-}
-
-// K4 semantics: the scenario's duration of one task (see lumos_b200.h).
-// kMode < 0: decided at run time from sp.mode.
-template <int kMode>
-__device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
-                                                     const ThreadScen& ts, int64_t task,
-                                                     int64_t base, int cls) {
-  const int mode = kMode >= 0 ? kMode : sp.mode;
-  if (mode & kModeExplicit) return __ldcs(sp.durations + task * sp.durations_ld + ts.col);
-  int64_t d = base;
-  if (mode & kModeScale) {
-    int32_t num = ts.num[0];
-    if (cls == 1) num = ts.num[1];
-    if (cls == 2) num = ts.num[2];
-    if (cls == 3) num = ts.num[3];
-    d = mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
-  }
-  if (mode & kModeJitter) {
-    if (d == 0) return 0;
-    uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
-    philox2x32_10(x0, x1, sp.key_jit);
-    const uint64_t bits = (static_cast<uint64_t>(x0) << 32) | x1;
-    const double u01 = __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
-    const double u = __dadd_rn(__dmul_rn(sp.two_j, u01), sp.neg_j);
-    const double f = __dadd_rn(1.0, u);
-    const double p = __dmul_rn(__ll2double_rn(d), f);
-    // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)
-    // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
-    // already an integer
-    if (p < 1.5) return 1;
-    if (p >= 0x1.0p52) return static_cast<int64_t>(p);
-    return __double2ll_rd(__dadd_rn(p, 0.5));
-  }
-  return d;
-}
-
-__device__ __forceinline__ void init_thread_scen(const ScenarioParams& sp, int col, ThreadScen& ts) {
-  ts.col = col;
-  ts.scen = sp.first + col;
-#pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c)
-    ts.num[c] = (sp.mode & kModeScale) && c < sp.n_classes_eff ? class_num(sp, ts.scen, col, c) : 0;
-}
-
-__device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ uint32_t tid_offset() { return threadIdx.x * 16u; }
-__device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
