@@ -212,9 +212,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     model, par, tp, scenarios, label = CONFIGS[args.config]
+    from paper_2504_09307_b200.shard import gather_rows, shard
     S_total = args.scenarios or scenarios
-    S_local = S_total // world
-    first = rank * S_local
+    first, S_local = shard(S_total, world, rank)
     tile = min(args.tile, S_local)
     assert S_local % tile == 0, "scenarios per GPU must be a multiple of the tile"
 
@@ -242,12 +242,12 @@ def main():
         busy_all = torch.empty((S_total, ST_), dtype=torch.int64, device=dev)
 
     def gather():
+        # the only collective: per-scenario results to rank 0 (NCCL)
         if world == 1:
             return
-        for loc, tot in ((span, span_all if rank == 0 else None),
-                         (bd, bd_all if rank == 0 else None),
-                         (busy, busy_all if rank == 0 else None)):
-            dist.gather(loc, list(tot.chunk(world)) if rank == 0 else None, dst=0)
+        gather_rows(span, world, rank, span_all if rank == 0 else None)
+        gather_rows(bd, world, rank, bd_all if rank == 0 else None)
+        gather_rows(busy, world, rank, busy_all if rank == 0 else None)
 
     def step():
         for t0_ in range(0, S_local, tile):
