@@ -1,0 +1,304 @@
+// tracesim_dropin.cpp — the reference-side binding: a replacement for
+// /root/reference/proj/src/simulate.cpp that keeps the tracesim C++ API of
+// include/tracesim/simulate.hpp verbatim and runs the replay on the B200
+// engine through its C ABI (include/lumos_b200.h).
+//
+// A maintainer swaps this file in for src/simulate.cpp in the tracesim
+// library and links liblumos_b200.so; every caller of
+// simulate() — CLI replay/whatif/analyze (cli.cpp:181, 224-225, 307), the
+// acceptance gate, the tests — then replays on the GPU.  Exceptions follow the
+// reference taxonomy (types.hpp:109-138): invalid graphs and deadlocks throw
+// SimulationError with the reference's message text.
+//
+// The batched entry point (not in the reference) is declared in
+// tracesim_b200.hpp: N duration scenarios of one graph in one call.
+#include <algorithm>
+#include <map>
+#include <queue>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "lumos_b200.h"
+#include "tracesim/simulate.hpp"
+#include "tracesim/trace_parse.hpp"
+#include "tracesim_b200.hpp"
+
+namespace tracesim {
+
+namespace {
+
+std::string ids_text(const std::vector<TaskId>& ids) {
+  std::ostringstream os;
+  for (std::size_t i = 0; i < ids.size(); ++i) os << (i ? " " : "") << ids[i];
+  return os.str();
+}
+
+// ExecutionGraph -> structure of arrays the C ABI takes (ts_graph_desc)
+struct Soa {
+  std::vector<int64_t> duration, original_start;
+  std::vector<int32_t> rank, lane_kind, lane;
+  std::vector<uint8_t> op_class, task_kind;
+  std::vector<int32_t> edge_from, edge_to;
+  std::vector<int32_t> rule_kind, rule_task, rule_bound, rule_watch_off{0};
+  std::vector<int32_t> watch_rank, watch_kind, watch_lane;
+  ts_graph_desc desc{};
+
+  explicit Soa(const ExecutionGraph& g) {
+    for (const Task& t : g.tasks) {
+      duration.push_back(t.duration);
+      original_start.push_back(t.original_start);
+      rank.push_back(t.processor.rank);
+      lane_kind.push_back(t.processor.kind == LaneKind::CudaStream ? TS_LANE_CUDA_STREAM
+                                                                   : TS_LANE_CPU_THREAD);
+      lane.push_back(t.processor.lane);
+      op_class.push_back(static_cast<uint8_t>(t.op_class));
+      task_kind.push_back(t.kind == TaskKind::Gpu ? 1 : 0);
+    }
+    for (const auto& [u, v] : g.fixed_edges) {
+      edge_from.push_back(u);
+      edge_to.push_back(v);
+    }
+    for (const RuntimeRule& r : g.rules) {
+      rule_kind.push_back(r.kind == RuntimeRule::Kind::StreamSync   ? TS_RULE_STREAM_SYNC
+                          : r.kind == RuntimeRule::Kind::DeviceSync ? TS_RULE_DEVICE_SYNC
+                                                                    : TS_RULE_EVENT_SYNC);
+      rule_task.push_back(r.waiting_task);
+      rule_bound.push_back(r.bound_task && *r.bound_task >= 0 ? *r.bound_task : -1);
+      for (const ProcessorId& p : r.watched) {
+        watch_rank.push_back(p.rank);
+        watch_kind.push_back(p.kind == LaneKind::CudaStream ? TS_LANE_CUDA_STREAM
+                                                            : TS_LANE_CPU_THREAD);
+        watch_lane.push_back(p.lane);
+      }
+      rule_watch_off.push_back(static_cast<int32_t>(watch_rank.size()));
+    }
+    desc.n_tasks = static_cast<int32_t>(g.tasks.size());
+    desc.duration = duration.data();
+    desc.original_start = original_start.data();
+    desc.rank = rank.data();
+    desc.lane_kind = lane_kind.data();
+    desc.lane = lane.data();
+    desc.op_class = op_class.data();
+    desc.task_kind = task_kind.data();
+    desc.n_edges = static_cast<int64_t>(edge_from.size());
+    desc.edge_from = edge_from.data();
+    desc.edge_to = edge_to.data();
+    desc.n_rules = static_cast<int32_t>(rule_kind.size());
+    desc.rule_kind = rule_kind.data();
+    desc.rule_task = rule_task.data();
+    desc.rule_bound = rule_bound.data();
+    desc.rule_watch_off = rule_watch_off.data();
+    desc.watch_rank = watch_rank.data();
+    desc.watch_kind = watch_kind.data();
+    desc.watch_lane = watch_lane.data();
+    desc.window_start = g.iteration_window.start;
+    desc.window_end = g.iteration_window.end;
+  }
+};
+
+[[noreturn]] void rethrow(int rc) {
+  const std::string msg = ts_last_error();
+  if (rc == TS_E_GRAPH) throw GraphError(msg);
+  if (rc == TS_E_SIMULATION) throw SimulationError(msg);
+  throw SimulationError("B200 replay engine: " + msg);
+}
+
+struct Handle {
+  ts_graph* g = nullptr;
+  explicit Handle(const ExecutionGraph& graph) {
+    Soa s(graph);
+    if (int rc = ts_graph_create(&s.desc, -1, &g)) rethrow(rc);
+  }
+  ~Handle() { ts_graph_destroy(g); }
+};
+
+}  // namespace
+
+std::vector<ValidationIssue> validate_graph(const ExecutionGraph& graph) {
+  using K = ValidationIssue::Kind;
+  std::vector<ValidationIssue> out;
+  const TaskId n = static_cast<TaskId>(graph.tasks.size());
+  for (const Task& t : graph.tasks)
+    if (t.duration < 0)
+      out.push_back({K::NegativeDuration, true,
+                     "task " + std::to_string(t.id) + " has negative duration", {t.id}});
+  auto in_range = [n](TaskId x) { return x >= 0 && x < n; };
+  bool edges_valid = true;
+  for (const auto& [u, v] : graph.fixed_edges)
+    if (!in_range(u) || !in_range(v) || u == v) {
+      edges_valid = false;
+      out.push_back({K::BadEdge, true,
+                     "edge " + std::to_string(u) + "->" + std::to_string(v) +
+                         " references an invalid task",
+                     {u, v}});
+    }
+  for (const RuntimeRule& r : graph.rules) {
+    const bool bad_bound = r.bound_task && *r.bound_task >= 0 && *r.bound_task >= n;
+    if (!in_range(r.waiting_task) || bad_bound) {
+      out.push_back({K::BadRule, true,
+                     "rule on task " + std::to_string(r.waiting_task) +
+                         " references an invalid task",
+                     {r.waiting_task}});
+    } else if (r.kind != RuntimeRule::Kind::EventSync && r.watched.empty()) {
+      out.push_back({K::EmptyScope, false,
+                     "sync task " + std::to_string(r.waiting_task) +
+                         " watches no lanes and will not block",
+                     {r.waiting_task}});
+    }
+  }
+  if (!edges_valid || n == 0) return out;
+  for (const auto& [u, v] : graph.fixed_edges) {
+    const Task& a = graph.tasks[u];
+    const Task& b = graph.tasks[v];
+    if (a.processor == b.processor && a.original_start > b.original_start)
+      out.push_back({K::ChainOrder, false,
+                     "edge " + std::to_string(u) + "->" + std::to_string(v) +
+                         " runs against original start order on " + to_string(a.processor),
+                     {u, v}});
+  }
+  // Kahn; on failure walk unmet predecessors (smallest id) until one repeats
+  std::vector<int> remaining(n, 0);
+  std::vector<std::vector<TaskId>> succ(n), pred(n);
+  for (const auto& [u, v] : graph.fixed_edges) {
+    succ[u].push_back(v);
+    pred[v].push_back(u);
+    ++remaining[v];
+  }
+  std::queue<TaskId> ready;
+  for (TaskId i = 0; i < n; ++i)
+    if (remaining[i] == 0) ready.push(i);
+  TaskId done = 0;
+  while (!ready.empty()) {
+    const TaskId u = ready.front();
+    ready.pop();
+    ++done;
+    for (TaskId v : succ[u])
+      if (--remaining[v] == 0) ready.push(v);
+  }
+  if (done == n) return out;
+  TaskId cur = -1;
+  for (TaskId i = 0; i < n && cur < 0; ++i)
+    if (remaining[i] > 0) cur = i;
+  std::vector<TaskId> path;
+  std::vector<char> seen(n, 0);
+  while (cur >= 0 && !seen[cur]) {
+    seen[cur] = 1;
+    path.push_back(cur);
+    TaskId next = -1;
+    for (TaskId p : pred[cur])
+      if (remaining[p] > 0 && (next < 0 || p < next)) next = p;
+    cur = next;
+  }
+  std::vector<TaskId> cycle;
+  if (cur >= 0) {
+    cycle.assign(std::find(path.begin(), path.end(), cur), path.end());
+    std::reverse(cycle.begin(), cycle.end());
+  }
+  out.push_back({K::Cycle, true, "dependency cycle: " + ids_text(cycle), cycle});
+  return out;
+}
+
+TaskId pick_ready(const ExecutionGraph& graph, std::span<const TaskId> ready) {
+  TaskId best = -1;
+  for (TaskId id : ready)
+    if (best < 0 || std::pair(graph.tasks[id].original_start, id) <
+                        std::pair(graph.tasks[best].original_start, best))
+      best = id;
+  return best;
+}
+
+SimulatedTrace simulate(const ExecutionGraph& graph) {
+  for (const ValidationIssue& issue : validate_graph(graph))
+    if (issue.error) throw SimulationError("invalid graph: " + issue.message);
+  const std::size_t n = graph.tasks.size();
+  SimulatedTrace out;
+  if (n == 0) {
+    out.start = out.end = graph.iteration_window.start;
+    return out;
+  }
+  Handle h(graph);
+  std::vector<int64_t> start(n), fin(n), span(3);
+  if (int rc = ts_simulate(h.g, start.data(), fin.data(), span.data())) rethrow(rc);
+  out.entries.reserve(n);
+  for (std::size_t i = 0; i < n; ++i)
+    out.entries.push_back(
+        {static_cast<TaskId>(i), start[i], fin[i], graph.tasks[i].processor});
+  std::sort(out.entries.begin(), out.entries.end(), [](const SimEntry& a, const SimEntry& b) {
+    return std::pair(a.sim_start, a.task_id) < std::pair(b.sim_start, b.task_id);
+  });
+  out.start = span[0];
+  out.end = span[1];
+  out.makespan = span[2];
+  return out;
+}
+
+std::string simulated_to_chrome_json(const ExecutionGraph& graph, const SimulatedTrace& sim) {
+  std::vector<TraceEvent> events;
+  events.reserve(sim.entries.size());
+  for (const SimEntry& e : sim.entries) {
+    const Task& t = graph.tasks[e.task_id];
+    TraceEvent ev;
+    ev.name = t.name;
+    if (t.kind == TaskKind::Gpu) {
+      ev.category = EventCategory::GpuKernel;
+      ev.stream_id = t.processor.lane;
+    } else {
+      const bool runtime = t.op_class == OpClass::Launch || t.op_class == OpClass::Sync ||
+                           t.op_class == OpClass::EventRecord ||
+                           t.op_class == OpClass::EventWait;
+      ev.category = runtime ? EventCategory::CudaRuntime : EventCategory::CpuOp;
+    }
+    ev.timestamp = e.sim_start;
+    ev.duration = e.sim_end - e.sim_start;
+    ev.process_id = t.processor.rank;
+    ev.thread_id = t.processor.lane;
+    ev.correlation_id = t.correlation_id;
+    ev.args = t.meta;
+    if (t.layer_tag) ev.args["layer"] = std::to_string(*t.layer_tag);
+    if (t.microbatch_tag) ev.args["microbatch"] = std::to_string(*t.microbatch_tag);
+    events.push_back(std::move(ev));
+  }
+  return chrome_json(events);
+}
+
+namespace b200 {
+
+BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                           bool timestamps) {
+  for (const ValidationIssue& issue : validate_graph(graph))
+    if (issue.error) throw SimulationError("invalid graph: " + issue.message);
+  Handle h(graph);
+  ts_graph_info info{};
+  ts_graph_get_info(h.g, &info);
+  BatchResult r;
+  const std::size_t S = static_cast<std::size_t>(spec.count);
+  r.span.assign(S * 3, 0);
+  r.rank_breakdown.assign(S * static_cast<std::size_t>(info.n_ranks) * 5, 0);
+  r.ranks.resize(static_cast<std::size_t>(info.n_ranks));
+  ts_graph_ranks(h.g, r.ranks.data());
+  if (timestamps) {
+    r.start.assign(graph.tasks.size() * S, 0);
+    r.fin.assign(graph.tasks.size() * S, 0);
+  }
+  ts_scenarios sc{};
+  sc.first = spec.first;
+  sc.count = spec.count;
+  sc.seed = spec.seed;
+  sc.jitter = spec.jitter;
+  sc.scale_lo = spec.scale_lo;
+  sc.scale_hi = spec.scale_hi;
+  sc.scale_den = spec.scale_den;
+  ts_result res{};
+  res.start = timestamps ? r.start.data() : nullptr;
+  res.fin = timestamps ? r.fin.data() : nullptr;
+  res.ld = spec.count;
+  res.span = r.span.data();
+  res.rank_breakdown = info.n_ranks ? r.rank_breakdown.data() : nullptr;
+  if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc);
+  return r;
+}
+
+}  // namespace b200
+
+}  // namespace tracesim
