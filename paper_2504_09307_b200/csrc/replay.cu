@@ -338,30 +338,31 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-template <int NS>
-__device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col, int r, int ns,
-                                                 int64_t* ring) {
+// T: the time type of the merge — uint32 offsets from W when the accounting
+// window fits 32 bits (then every compare is one 32-bit op), else int64.
+template <int NS, typename T>
+__device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col, int r, int ns,
+                                                  int64_t* ring, int64_t W, int64_t wend) {
   constexpr int H = RingHalf<NS>::value;
+  constexpr T kInf = static_cast<T>(sizeof(T) == 4 ? 0xFFFFFFFFu : INT64_MAX);
   const int tid = threadIdx.x;
   const int s0 = P.rank_stream_off[r];
-  const int64_t W = P.window_start;
-  int64_t wend = P.window_end;
-  {
-    const int64_t a = P.span_lo[col], b = P.span_hi[col];
-    const int64_t m = (a == kMaxI64) ? 0 : (b - a);
-    if (W + m > wend) wend = W + m;
-  }
-  if (wend < W) wend = W;
+  const int64_t span = wend - W;
   const int64_t* __restrict__ S = P.start;
   const int64_t* __restrict__ F = P.fin;
   const int64_t ld = P.ld;
   const int* __restrict__ nodes = P.stream_nodes;
   // ring layout [NS][2 halves][H][2 (start, fin)][kThreads]
 #define RING(j, h, q, k) ring[(((((j) * 2 + (h)) * H + (q)) * 2 + (k)) * kThreads) + tid]
+  auto rel = [&](int64_t v) -> T {
+    int64_t x = v - W;
+    x = x < 0 ? 0 : (x > span ? span : x);
+    return static_cast<T>(x);
+  };
 
   int next_idx[NS], end_idx[NS];
   int half[NS], pos[NS], avail[NS], pend[NS];
-  uint32_t cbits[NS], pbits[NS];  // comm flags of the current / prefetched half
+  uint32_t cbits[NS], pbits[NS];
   auto prefetch = [&](int j, int h) {
     const int base = next_idx[j];
     const int n = min(H, end_idx[j] - base);
@@ -381,14 +382,13 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
     pend[j] = n;
     pbits[j] = bits;
   };
-  int64_t cs[NS], ce[NS];
-  bool cc[NS], inside[NS];
-  // move stream j to its next non-empty clipped interval (or exhaust it)
+  T cs[NS], ce[NS];
+  uint32_t cc = 0, inside = 0;  // per-stream bits: current interval is comm / open
   auto advance = [&](int j) {
     for (;;) {
       if (pos[j] >= avail[j]) {
         if (pend[j] == 0) {
-          cs[j] = ce[j] = kMaxI64;
+          cs[j] = ce[j] = kInf;
           return;
         }
         cp_async_wait_all();
@@ -400,12 +400,11 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
         if (next_idx[j] < end_idx[j]) prefetch(j, half[j] ^ 1);
       }
       const int q = pos[j]++;
-      const int64_t a = imax(RING(j, half[j], q, 0), W);
-      const int64_t b = imin(RING(j, half[j], q, 1), wend);
+      const T a = rel(RING(j, half[j], q, 0)), b = rel(RING(j, half[j], q, 1));
       if (a < b) {
         cs[j] = a;
         ce[j] = b;
-        cc[j] = (cbits[j] >> q) & 1u;
+        cc = (cc & ~(1u << j)) | (((cbits[j] >> q) & 1u) << j);
         return;
       }
     }
@@ -418,7 +417,6 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
     half[j] = 1;  // the first switch moves to half 0
     pos[j] = avail[j] = pend[j] = 0;
     cbits[j] = pbits[j] = 0;
-    inside[j] = false;
     busy[j] = 0;
     if (next_idx[j] < end_idx[j]) prefetch(j, 0);
   }
@@ -426,13 +424,14 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
   for (int j = 0; j < NS; ++j) advance(j);
 
   int compute = 0, comm = 0;
-  int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
+  T prev = 0;
+  int64_t ec = 0, em = 0, ov = 0, ot = 0;
   for (;;) {
     int jm = -1;
-    int64_t tm = kMaxI64;
+    T tm = kInf;
 #pragma unroll
     for (int j = 0; j < NS; ++j) {
-      const int64_t t = inside[j] ? ce[j] : cs[j];
+      const T t = ((inside >> j) & 1u) ? ce[j] : cs[j];
       if (t < tm) {
         tm = t;
         jm = j;
@@ -440,38 +439,43 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
     }
     if (jm < 0) break;
     if (tm > prev) {
-      const int64_t span = tm - prev;
-      if (compute > 0 && comm > 0) ov += span;
-      else if (compute > 0) ec += span;
-      else if (comm > 0) em += span;
-      else ot += span;
+      const int64_t d = static_cast<int64_t>(tm - prev);
+      if (compute > 0) {
+        if (comm > 0) ov += d; else ec += d;
+      } else {
+        if (comm > 0) em += d; else ot += d;
+      }
       prev = tm;
     }
+    const bool is_comm = (cc >> jm) & 1u;
+    if (!((inside >> jm) & 1u)) {
+      if (is_comm) ++comm; else ++compute;
+      inside |= 1u << jm;
+    } else {
+      if (is_comm) --comm; else --compute;
+      inside &= ~(1u << jm);
 #pragma unroll
-    for (int j = 0; j < NS; ++j) {
-      if (j != jm) continue;
-      if (!inside[j]) {
-        if (cc[j]) ++comm; else ++compute;
-        inside[j] = true;
-      } else {
-        if (cc[j]) --comm; else --compute;
-        busy[j] += ce[j] - cs[j];
-        inside[j] = false;
-        advance(j);
-      }
+      for (int j = 0; j < NS; ++j)
+        if (j == jm) {
+          busy[j] += static_cast<int64_t>(ce[j] - cs[j]);
+          advance(j);
+        }
     }
   }
 #undef RING
-  if (wend > prev) {
-    const int64_t span = wend - prev;
-    if (compute > 0 && comm > 0) ov += span;
-    else if (compute > 0) ec += span;
-    else if (comm > 0) em += span;
-    else ot += span;
+  {
+    const int64_t d = span - static_cast<int64_t>(prev);
+    if (d > 0) {
+      if (compute > 0) {
+        if (comm > 0) ov += d; else ec += d;
+      } else {
+        if (comm > 0) em += d; else ot += d;
+      }
+    }
   }
   if (P.breakdown) {
     int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
-    row[0] = wend - W;
+    row[0] = span;
     row[1] = ec;
     row[2] = em;
     row[3] = ov;
@@ -482,6 +486,23 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
     for (int j = 0; j < NS; ++j)
       if (j < ns) P.stream_busy[static_cast<int64_t>(col) * P.n_streams + s0 + j] = busy[j];
   }
+}
+
+template <int NS>
+__device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col, int r, int ns,
+                                                 int64_t* ring) {
+  const int64_t W = P.window_start;
+  int64_t wend = P.window_end;
+  {
+    const int64_t a = P.span_lo[col], b = P.span_hi[col];
+    const int64_t m = (a == kMaxI64) ? 0 : (b - a);
+    if (W + m > wend) wend = W + m;
+  }
+  if (wend < W) wend = W;
+  if (wend - W < 0xFFFFFFFFll)
+    rank_reduce_merge<NS, uint32_t>(P, col, r, ns, ring, W, wend);
+  else
+    rank_reduce_merge<NS, int64_t>(P, col, r, ns, ring, W, wend);
 }
 
 template <int NS>
