@@ -227,12 +227,38 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   if (e == cudaSuccess) e = upload(&g->d_stream_node_off, c.stream_node_off);
   if (e == cudaSuccess) e = upload(&g->d_stream_nodes, c.stream_nodes);
   {
+    // per rank: generic merge bucket, or the fast path when the rank has one
+    // compute-only stream and <= 3 comm-only streams
+    const size_t n_ranks = c.rank_stream_off.size() - 1;
+    std::vector<int> bucket(n_ranks);
+    std::vector<int32_t> entry(n_ranks);
+    for (size_t r = 0; r < n_ranks; ++r) {
+      const int s0 = c.rank_stream_off[r], ns = c.rank_stream_off[r + 1] - s0;
+      int n_compute = 0, n_comm = 0, ci = -1;
+      for (int j = 0; j < ns; ++j) {
+        bool any_comm = false, any_compute = false;
+        for (int32_t q = c.stream_node_off[s0 + j]; q < c.stream_node_off[s0 + j + 1]; ++q)
+          (c.stream_nodes[q] < 0 ? any_comm : any_compute) = true;
+        if (any_compute && !any_comm) {
+          ++n_compute;
+          ci = j;
+        } else if (any_comm && !any_compute) {
+          ++n_comm;
+        }
+      }
+      if (n_compute == 1 && n_compute + n_comm == ns && n_comm <= kReduceFastMaxComm) {
+        bucket[r] = kReduceGenericBuckets + n_comm;
+        entry[r] = static_cast<int32_t>(r) | (ci << 24);
+      } else {
+        bucket[r] = reduce_bucket(ns);
+        entry[r] = static_cast<int32_t>(r);
+      }
+    }
     std::vector<int32_t> lists;
     for (int b = 0; b < kReduceBuckets; ++b) {
       g->bucket_off[b] = static_cast<int32_t>(lists.size());
-      for (size_t r = 0; r + 1 < c.rank_stream_off.size(); ++r)
-        if (reduce_bucket(c.rank_stream_off[r + 1] - c.rank_stream_off[r]) == b)
-          lists.push_back(static_cast<int32_t>(r));
+      for (size_t r = 0; r < n_ranks; ++r)
+        if (bucket[r] == b) lists.push_back(entry[r]);
     }
     g->bucket_off[kReduceBuckets] = static_cast<int32_t>(lists.size());
     if (e == cudaSuccess) e = upload(&g->d_rank_lists, lists);

@@ -119,7 +119,12 @@ cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W
                                  int64_t* makespan, int32_t count, cudaStream_t stream);
 cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
                              int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream);
-constexpr int kReduceBuckets = 7;
+// buckets 0..6: event merge by stream count (reduce_bucket); 7..10: the
+// one-compute-stream fast path with 0..3 comm streams (rank_list entries then
+// carry the compute stream's index in bits 24..31)
+constexpr int kReduceGenericBuckets = 7;
+constexpr int kReduceFastMaxComm = 3;
+constexpr int kReduceBuckets = kReduceGenericBuckets + kReduceFastMaxComm + 1;
 int reduce_bucket(int streams_in_rank);
 cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in_bucket,
                                cudaStream_t stream);

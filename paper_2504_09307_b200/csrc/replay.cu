@@ -515,6 +515,206 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
   rank_reduce_body<NS>(P, col, r, ns, ring);
 }
 
+// ---------------------------------------------------------------- K5 fast path
+// Ranks with exactly one compute-only stream A and NC comm-only streams (every
+// generator rank): the four categories follow from |A|, |U| (U = union of the
+// comm intervals) and |A ∩ U|:
+//   overlap = |A∩U|, exposed compute = |A| - overlap, exposed comm = |U| - overlap,
+//   other = span - |A| - |U| + overlap
+// — the same numbers the event merge produces, since A's intervals are
+// disjoint (one stream is one chain) and the categories only ask whether any
+// compute / any comm kernel is running.  A is walked by a pointer (two loads
+// and a compare per kernel); only the few comm intervals go through a merge.
+template <int H, typename T>
+struct Cursor {
+  int next, end, half, pos, avail, pend;
+  int64_t* ring;  // [2 halves][H][2][kThreads] + tid
+  __device__ __forceinline__ int64_t& at(int h, int q, int k) {
+    return ring[((h * H + q) * 2 + k) * kThreads];
+  }
+  __device__ __forceinline__ void prefetch(const int* __restrict__ nodes,
+                                           const int64_t* __restrict__ S,
+                                           const int64_t* __restrict__ F, int64_t ld, int col,
+                                           int h) {
+    const int base = next;
+    const int n = min(H, end - base);
+#pragma unroll
+    for (int q = 0; q < H; ++q)
+      if (q < n) {
+        const int node = nodes[base + q] & 0x7FFFFFFF;
+        const int64_t off = static_cast<int64_t>(node) * ld + col;
+        cp_async8(&at(h, q, 0), S + off);
+        cp_async8(&at(h, q, 1), F + off);
+      }
+    cp_async_commit();
+    next = base + n;
+    pend = n;
+  }
+  __device__ __forceinline__ void init(int b, int e, int64_t* rb, const int* nodes,
+                                       const int64_t* S, const int64_t* F, int64_t ld, int col) {
+    next = b;
+    end = e;
+    half = 1;
+    pos = avail = pend = 0;
+    ring = rb;
+    if (next < end) prefetch(nodes, S, F, ld, col, 0);
+  }
+  // next non-empty clipped interval [a, b); false when the stream is done
+  template <typename Rel>
+  __device__ __forceinline__ bool get(T& a, T& b, const int* nodes, const int64_t* S,
+                                      const int64_t* F, int64_t ld, int col, Rel rel) {
+    for (;;) {
+      if (pos >= avail) {
+        if (pend == 0) return false;
+        cp_async_wait_all();
+        half ^= 1;
+        avail = pend;
+        pos = 0;
+        pend = 0;
+        if (next < end) prefetch(nodes, S, F, ld, col, half ^ 1);
+      }
+      const int q = pos++;
+      a = rel(at(half, q, 0));
+      b = rel(at(half, q, 1));
+      if (a < b) return true;
+    }
+  }
+};
+
+constexpr int kFastHA = 8;  // ring half of the compute stream
+constexpr int kFastHC = 2;  // ring half of a comm stream
+
+template <int NC>
+constexpr size_t fast_ring_words() {
+  return static_cast<size_t>(2 * kFastHA * 2 + NC * 2 * kFastHC * 2);
+}
+
+template <int NC, typename T>
+__device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int col, int r,
+                                                      int ci, int64_t* ring, int64_t W,
+                                                      int64_t wend) {
+  constexpr T kInf = static_cast<T>(sizeof(T) == 4 ? 0xFFFFFFFFu : INT64_MAX);
+  const int tid = threadIdx.x;
+  const int s0 = P.rank_stream_off[r];
+  const int64_t span = wend - W;
+  const int64_t* __restrict__ S = P.start;
+  const int64_t* __restrict__ F = P.fin;
+  const int64_t ld = P.ld;
+  const int* __restrict__ nodes = P.stream_nodes;
+  auto rel = [&](int64_t v) -> T {
+    int64_t x = v - W;
+    x = x < 0 ? 0 : (x > span ? span : x);
+    return static_cast<T>(x);
+  };
+  Cursor<kFastHA, T> A;
+  A.init(P.stream_node_off[s0 + ci], P.stream_node_off[s0 + ci + 1], ring + tid, nodes, S, F,
+         ld, col);
+  Cursor<kFastHC, T> C[NC > 0 ? NC : 1];
+  T cs[NC > 0 ? NC : 1], ce[NC > 0 ? NC : 1];
+  int64_t cbusy[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int s = s0 + j + (j >= ci ? 1 : 0);
+    C[j].init(P.stream_node_off[s], P.stream_node_off[s + 1],
+              ring + (2 * kFastHA * 2 + j * 2 * kFastHC * 2) * kThreads + tid, nodes, S, F, ld,
+              col);
+    cbusy[j] = 0;
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j)
+    if (!C[j].get(cs[j], ce[j], nodes, S, F, ld, col, rel)) cs[j] = ce[j] = kInf;
+
+  // union of the comm intervals, produced in time order
+  T us = kInf, ue = kInf;
+  int64_t m = 0;
+  auto next_union = [&]() {
+    int jm = -1;
+    T tm = kInf;
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+      if (cs[j] < tm) {
+        tm = cs[j];
+        jm = j;
+      }
+    if (jm < 0) {
+      us = ue = kInf;
+      return;
+    }
+    us = tm;
+    ue = tm;
+    for (;;) {
+      // absorb every comm interval starting inside [us, ue] (the first pass
+      // takes the earliest one, whose start is us)
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < NC; ++j)
+        if (cs[j] <= ue) {
+          if (ce[j] > ue) ue = ce[j];
+          cbusy[j] += static_cast<int64_t>(ce[j] - cs[j]);
+          if (!C[j].get(cs[j], ce[j], nodes, S, F, ld, col, rel)) cs[j] = ce[j] = kInf;
+          any = true;
+        }
+      if (!any) break;
+    }
+    m += static_cast<int64_t>(ue - us);
+  };
+  if (NC > 0) next_union();
+
+  int64_t busy_a = 0, ov = 0;
+  T as, ae;
+  while (A.get(as, ae, nodes, S, F, ld, col, rel)) {
+    busy_a += static_cast<int64_t>(ae - as);
+    if (NC > 0) {
+      while (ue <= as) next_union();
+      while (us < ae) {
+        const T lo = us > as ? us : as;
+        const T hi = ue < ae ? ue : ae;
+        ov += static_cast<int64_t>(hi - lo);
+        if (ue <= ae) next_union(); else break;
+      }
+    }
+  }
+  if (NC > 0)
+    while (us != kInf) next_union();
+
+  if (P.breakdown) {
+    int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
+    row[0] = span;
+    row[1] = busy_a - ov;
+    row[2] = m - ov;
+    row[3] = ov;
+    row[4] = span - busy_a - m + ov;
+  }
+  if (P.stream_busy) {
+    int64_t* b = P.stream_busy + static_cast<int64_t>(col) * P.n_streams + s0;
+    b[ci] = busy_a;
+#pragma unroll
+    for (int j = 0; j < NC; ++j) b[j + (j >= ci ? 1 : 0)] = cbusy[j];
+  }
+}
+
+// rank_list entries: rank | compute-stream index << 24
+template <int NC>
+__global__ void __launch_bounds__(kThreads) rank_reduce_fast_kernel(ReduceParams P) {
+  extern __shared__ int64_t ring[];
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = P.rank_list[blockIdx.y];
+  if (col >= P.count) return;
+  const int r = e & 0xFFFFFF, ci = e >> 24;
+  const int64_t W = P.window_start;
+  int64_t wend = P.window_end;
+  {
+    const int64_t a = P.span_lo[col], b = P.span_hi[col];
+    const int64_t m = (a == kMaxI64) ? 0 : (b - a);
+    if (W + m > wend) wend = W + m;
+  }
+  if (wend < W) wend = W;
+  if (wend - W < 0xFFFFFFFFll)
+    rank_reduce_fast_body<NC, uint32_t>(P, col, r, ci, ring, W, wend);
+  else
+    rank_reduce_fast_body<NC, int64_t>(P, col, r, ci, ring, W, wend);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ launchers
@@ -633,7 +833,25 @@ cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in
     case 3: e = go(rank_reduce_kernel<4>, 4); break;
     case 4: e = go(rank_reduce_kernel<8>, 8); break;
     case 5: e = go(rank_reduce_kernel<16>, 16); break;
-    default: e = go(rank_reduce_kernel<kMaxStreamsPerRank>, kMaxStreamsPerRank); break;
+    case 6: e = go(rank_reduce_kernel<kMaxStreamsPerRank>, kMaxStreamsPerRank); break;
+    default: {
+      auto fast = [&](auto kern, size_t words) -> cudaError_t {
+        const size_t smem = words * kThreads * sizeof(int64_t);
+        if (smem > 48 * 1024) {
+          cudaError_t e2 = cudaFuncSetAttribute(
+              kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+          if (e2 != cudaSuccess) return e2;
+        }
+        kern<<<grid, kThreads, smem, stream>>>(p);
+        return cudaSuccess;
+      };
+      switch (bucket - kReduceGenericBuckets) {
+        case 0: e = fast(rank_reduce_fast_kernel<0>, fast_ring_words<0>()); break;
+        case 1: e = fast(rank_reduce_fast_kernel<1>, fast_ring_words<1>()); break;
+        case 2: e = fast(rank_reduce_fast_kernel<2>, fast_ring_words<2>()); break;
+        default: e = fast(rank_reduce_fast_kernel<3>, fast_ring_words<3>()); break;
+      }
+    }
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

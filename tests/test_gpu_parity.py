@@ -229,8 +229,21 @@ def test_generated_traces_replay_exactly(shape, jitter):
     assert np.array_equal(rs, g.original_start)
 
 
+def _expected_stream_busy(g, dg, rs, rf, wend):
+    """Per-stream busy time: sum of the stream's kernel intervals clipped to
+    [window_start, wend) (the union is the sum: one stream is one chain)."""
+    a = np.clip(rs, g.window_start, wend)
+    b = np.clip(rf, g.window_start, wend)
+    out = np.zeros(dg.n_streams, np.int64)
+    for k in range(dg.n_streams):
+        m = (g.rank == dg.stream_rank[k]) & (g.lane_kind == 1) & (g.lane == dg.stream_lane[k])
+        out[k] = int(np.maximum(b[m] - a[m], 0).sum())
+    return out
+
+
 def _check_batch(h, g, spec, sc, check_breakdown=True, every=1):
     res = simulate_batch(g, spec, timestamps=True, breakdown=check_breakdown)
+    dg = DeviceGraph(g) if check_breakdown else None
     for s in range(0, spec.count, every):
         dur = R.orc_durations(g, sc, spec.first + s)
         rs, rf, rspan = h.simulate(dur)
@@ -243,6 +256,8 @@ def _check_batch(h, g, spec, sc, check_breakdown=True, every=1):
             ranks = sorted(ref_bd)
             for i, r in enumerate(ranks):
                 assert tuple(res.rank_breakdown[s, i]) == ref_bd[r], f"scenario {s} rank {r}"
+            assert np.array_equal(res.stream_busy[s, :dg.n_streams],
+                                  _expected_stream_busy(g, dg, rs, rf, wend)), f"scenario {s} busy"
     return res
 
 
@@ -366,6 +381,7 @@ def test_random_graphs_batched_scenarios():
             res = simulate_batch(g, ScenarioSpec(count=16, seed=3, jitter=0.45))
         except SimulationError:
             continue
+        dg = DeviceGraph(g)
         for s_ in range(16):
             dur = R.orc_durations(g, sc, s_)
             rs, rf, rspan = h.simulate(dur)
@@ -374,6 +390,8 @@ def test_random_graphs_batched_scenarios():
             ref_bd = h.breakdown_by_rank(rs, rf, g.window_start, wend)
             for i, r in enumerate(sorted(ref_bd)):
                 assert tuple(res.rank_breakdown[s_, i]) == ref_bd[r]
+            assert np.array_equal(res.stream_busy[s_, :dg.n_streams],
+                                  _expected_stream_busy(g, dg, rs, rf, wend))
 
 
 def test_large_config4_sampled():
@@ -384,3 +402,25 @@ def test_large_config4_sampled():
     assert truth == 2183270773
     spec = ScenarioSpec(count=4, first=123, seed=9, jitter=0.1)
     _check_batch(h, g, spec, R.OrcScenarios(seed=9, jitter=0.1), check_breakdown=True)
+
+
+def test_reduce_fast_and_generic_ranks():
+    # K5 has two paths: ranks with one compute-only stream and <= 3 comm-only
+    # streams (interval sweep) and everything else (event merge).  Mixing a
+    # comm kernel into rank 0's compute stream and a compute kernel into rank
+    # 1's p2p stream sends those ranks to the merge while ranks 2/3 stay on the
+    # sweep; breakdown and per-stream busy must match the reference on both.
+    h0, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h0.export()
+    kern = g.task_kind == 1
+    r0 = np.flatnonzero(kern & (g.rank == 0) & (g.op_class == 0))
+    r1 = np.flatnonzero(kern & (g.rank == 1) & (g.op_class == 1))
+    assert len(r0) and len(r1)
+    g.op_class = g.op_class.copy()
+    g.op_class[r0[len(r0) // 2]] = 1
+    g.op_class[r1[len(r1) // 2]] = 0
+    h = R.from_graph(g)
+    spec = ScenarioSpec(count=64, first=5, seed=21, jitter=0.3)
+    _check_batch(h, g, spec, R.OrcScenarios(seed=21, jitter=0.3))
+    # and the unmodified graph (every rank on the sweep)
+    _check_batch(h0, h0.export(), spec, R.OrcScenarios(seed=21, jitter=0.3))
