@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -359,6 +360,7 @@ static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioPa
   sp.first = sc->first;
   sp.count = sc->count;
   sp.key_jit = seed_key(sc->seed, 0u);
+  for (int r = 0; r < 10; ++r) sp.rk_jit[r] = sp.key_jit + static_cast<uint32_t>(r) * 0x9E3779B9u;
   sp.key_cls = seed_key(sc->seed, 0x5CA1E000u);
   sp.den_shift = -1;
   sp.n_classes = 0;
@@ -376,6 +378,7 @@ static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioPa
     sp.mode |= kModeJitter;
     sp.two_j = 2.0 * sc->jitter;
     sp.neg_j = -sc->jitter;
+    sp.two_j_ulp = std::ldexp(sp.two_j, -53);
   }
   if (sc->scale_den > 0) {
     sp.mode |= kModeScale;

@@ -27,6 +27,19 @@ __device__ __forceinline__ void philox2x32_10(uint32_t& x0, uint32_t& x1, uint32
   }
 }
 
+// the same permutation with the round keys precomputed (kernel-parameter
+// constants: each round is one IMAD.WIDE and one three-input XOR)
+__device__ __forceinline__ void philox2x32_10_rk(uint32_t& x0, uint32_t& x1,
+                                                 const uint32_t (&rk)[10]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi = __umulhi(0xD256D193u, x0);
+    const uint32_t lo = 0xD256D193u * x0;
+    x0 = hi ^ rk[r] ^ x1;
+    x1 = lo;
+  }
+}
+
 // (a * num + den/2) / den for a >= 0, num >= 0 (transform.cpp:38-43)
 __device__ __forceinline__ int64_t mul_div_nonneg(int64_t a, int64_t num, int64_t den,
                                                   int den_shift) {
@@ -89,10 +102,11 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
   if (mode & kModeJitter) {
     if (d == 0) return 0;
     uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
-    philox2x32_10(x0, x1, sp.key_jit);
+    philox2x32_10_rk(x0, x1, sp.rk_jit);
     const uint64_t bits = (static_cast<uint64_t>(x0) << 32) | x1;
-    const double u01 = __dmul_rn(__ull2double_rn(bits >> 11), 0x1.0p-53);
-    const double u = __dadd_rn(__dmul_rn(sp.two_j, u01), sp.neg_j);
+    // two_j * (k * 2^-53) == (two_j * 2^-53) * k exactly (power-of-two
+    // scaling commutes with rounding while nothing is subnormal)
+    const double u = __dadd_rn(__dmul_rn(sp.two_j_ulp, __ull2double_rn(bits >> 11)), sp.neg_j);
     const double f = __dadd_rn(1.0, u);
     const double p = __dmul_rn(__ll2double_rn(d), f);
     // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)

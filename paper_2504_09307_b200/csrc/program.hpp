@@ -41,7 +41,7 @@ constexpr uint16_t kSlotTrash = 1;
 constexpr int kFirstSlot = 2;
 // Programs are streamed through shared memory in chunks of kChunk records; no
 // op group (an op plus its auxiliary records) straddles a chunk boundary.
-constexpr int kChunk = 128;
+constexpr int kChunk = 64;
 // Each walk thread replays kScenPerThread adjacent scenarios.  The slot table
 // is [slot][T] of int64 x kScenPerThread (16 bytes) for a CTA of T threads
 // (128, 64 or 32, chosen at launch from the slot count), so slot s of a thread

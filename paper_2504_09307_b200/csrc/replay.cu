@@ -49,13 +49,16 @@ __device__ __forceinline__ I64x2 max2(I64x2 a, I64x2 b) { return {imax(a.x, b.x)
 
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin>
 __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
-  constexpr int kRecPerThread = kChunk / kT;  // chunk refill: records per thread
+  constexpr int kRecPerThread = (kChunk + kT - 1) / kT;  // chunk refill: records per thread
   constexpr int kShift = kT == 128 ? 4 : kT == 64 ? 3 : 2;  // s*128 -> s*kT*16 bytes
-  static_assert(kChunk % kT == 0 && kT >= 32, "");
+  static_assert(kT >= 32, "");
   static_assert(kScenPerThread == 2, "pair layout");
   extern __shared__ int4 smem[];
-  int4* opbuf = smem;  // [2][kChunk][2]
-  char* slot_base = reinterpret_cast<char*>(smem + 4 * kChunk) + tid_offset();
+  // [2][kChunk][4]: the raw 32-byte record, then its eight 16-bit slot fields
+  // (pred[4], dst, x0, x1, x2) widened to byte offsets by the loader, so the
+  // walk adds one register per operand address
+  int4* opbuf = smem;
+  char* slot_base = reinterpret_cast<char*>(smem + 8 * kChunk) + tid_offset();
   const int tid = threadIdx.x;
   const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
   const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   const int64_t W = P.window_start;
 #define SLOT2(off) \
   (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
+#define SLOTB(boff) (*reinterpret_cast<I64x2*>(slot_base + static_cast<uint32_t>(boff)))
   SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
 
   ThreadScen ts0, ts1;
@@ -88,13 +92,19 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   const uint32_t ld = static_cast<uint32_t>(P.ld);
   const int64_t dcol = c1 - c0;
 
+  auto stage = [&](int4* dstbuf, int r, int4 a, int4 b) {
+    dstbuf[4 * r] = a;
+    dstbuf[4 * r + 1] = b;
+    const uint32_t x = b.x, y = b.y, z = b.z, w = b.w;
+    dstbuf[4 * r + 2] = make_int4(lo16(x) << kShift, hi16(x) << kShift, lo16(y) << kShift,
+                                  hi16(y) << kShift);
+    dstbuf[4 * r + 3] = make_int4(lo16(z) << kShift, hi16(z) << kShift, lo16(w) << kShift,
+                                  hi16(w) << kShift);
+  };
 #pragma unroll
   for (int q = 0; q < kRecPerThread; ++q) {
     const int r = q * kT + tid;
-    if (r < n_ops) {
-      opbuf[2 * r] = __ldg(gops + 2 * r);
-      opbuf[2 * r + 1] = __ldg(gops + 2 * r + 1);
-    }
+    if (r < kChunk && r < n_ops) stage(opbuf, r, __ldg(gops + 2 * r), __ldg(gops + 2 * r + 1));
   }
   __syncthreads();
   const int n_chunks = (n_ops + kChunk - 1) / kChunk;
@@ -104,28 +114,28 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
 #pragma unroll
     for (int q = 0; q < kRecPerThread; ++q) {
       const int nxt = (c + 1) * kChunk + q * kT + tid;
-      if (nxt < n_ops) {
+      if (q * kT + tid < kChunk && nxt < n_ops) {
         na[q] = __ldg(gops + 2 * nxt);
         nb[q] = __ldg(gops + 2 * nxt + 1);
       }
     }
-    const int4* buf = opbuf + (c & 1) * 2 * kChunk;
+    const int4* buf = opbuf + (c & 1) * 4 * kChunk;
     const int cnt = min(kChunk, n_ops - c * kChunk);
     for (int i = 0; i < cnt; ++i) {
-      const int4 ra = buf[2 * i], rb = buf[2 * i + 1];
+      const int4 ra = buf[4 * i], rb = buf[4 * i + 1];
+      const int4 oa = buf[4 * i + 2], ob = buf[4 * i + 3];
       const uint32_t hdr = static_cast<uint32_t>(ra.w);
       const uint32_t kind = hdr & 0xFFu;
       const uint32_t cls_b = (hdr >> 16) & 0xFFu;
       const uint32_t flags = hdr >> 24;
-      const uint32_t w0 = static_cast<uint32_t>(rb.x), w1 = static_cast<uint32_t>(rb.y);
-      const uint32_t w2 = static_cast<uint32_t>(rb.z), w3 = static_cast<uint32_t>(rb.w);
+      const uint32_t w2 = static_cast<uint32_t>(rb.z);
       // every operand is read before any result is written (results may
       // reuse the slot of an operand that dies at this op)
-      const I64x2 p0 = SLOT2(lo16(w0)), p1 = SLOT2(hi16(w0));
-      const I64x2 p2 = SLOT2(lo16(w1)), p3 = SLOT2(hi16(w1));
-      const uint32_t dst = lo16(w2);
+      const I64x2 p0 = SLOTB(oa.x), p1 = SLOTB(oa.y);
+      const I64x2 p2 = SLOTB(oa.z), p3 = SLOTB(oa.w);
+      const uint32_t dst = ob.x;
       I64x2 cov_src = {kMaxI64, kMaxI64};
-      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOT2(hi16(w2));
+      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOTB(ob.y);
       I64x2 st, gate;
       if (kind == OP_NODE || kind == OP_SYNC || kind == OP_START || kind == OP_ACC) {
         st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
@@ -145,7 +155,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         continue;  // OP_NOP
       }
       if (kind == OP_ACC) {
-        SLOT2(dst) = st;
+        SLOTB(dst) = st;
         continue;
       }
       if (kind == OP_SYNC) {
@@ -154,8 +164,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         I64x2 S = rs;
         const int n_ext = static_cast<int>(hi16(w2));
         for (int e = 0; e < n_ext; ++e) {
-          const int4 xa = buf[2 * (i + 1 + e)];
-          const int n = buf[2 * (i + 1 + e) + 1].z & 0xFFFF;
+          const int4 xa = buf[4 * (i + 1 + e)];
+          const int n = buf[4 * (i + 1 + e) + 1].z & 0xFFFF;
           const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
 #pragma unroll
           for (int k = 0; k < kCertPerExt; ++k)
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         }
         bool cov0 = S.x == rs.x, cov1 = S.y == rs.y;
         for (int e = 0; e < n_ext; ++e) {
-          const int4 xa = buf[2 * (i + 1 + e)], xb = buf[2 * (i + 1 + e) + 1];
+          const int4 xa = buf[4 * (i + 1 + e)], xb = buf[4 * (i + 1 + e) + 1];
           const int n = xb.z & 0xFFFF;
           const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
           const uint32_t cv[4] = {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)};
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         i += n_ext;
       }
       if (kind == OP_START) {
-        SLOT2(dst) = st;
+        SLOTB(dst) = st;
       } else {
         const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
         const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
@@ -198,8 +208,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int64_t d0 = scenario_duration<kMode>(P.sp, ts0, task, base, cls);
         const int64_t d1 = scenario_duration<kMode>(P.sp, ts1, task, base, cls);
         const I64x2 fin = {imax(st.x, gate.x) + d0, imax(st.y, gate.y) + d1};
-        SLOT2(dst) = fin;
-        if (flags & F_STORE_START) SLOT2(hi16(w3)) = st;
+        SLOTB(dst) = fin;
+        if (flags & F_STORE_START) SLOTB(ob.w) = st;
         if (flags & F_SINK) {
           hi0 = imax(hi0, fin.x);
           hi1 = imax(hi1, fin.y);
@@ -222,11 +232,11 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         }
       }
       if (flags & F_TRACK1) {
-        SLOT2(lo16(w3)) = I64x2{p0.x >= st.x ? imin(st.x, cov_src.x) : st.x,
+        SLOTB(ob.z) = I64x2{p0.x >= st.x ? imin(st.x, cov_src.x) : st.x,
                                 p0.y >= st.y ? imin(st.y, cov_src.y) : st.y};
       } else if (flags & F_TRACK) {
         // coverage of this kernel per watched set (program.hpp, OpCov)
-        const int4 xa = buf[2 * (i + 1)], xb = buf[2 * (i + 1) + 1];
+        const int4 xa = buf[4 * (i + 1)], xb = buf[4 * (i + 1) + 1];
         const uint32_t src[2][4] = {{lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)},
                                     {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)}};
         const uint32_t cdst[2] = {lo16(xb.x), hi16(xb.x)};
@@ -250,18 +260,16 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         i += 1;
       }
     }
-    int4* nbuf = opbuf + ((c + 1) & 1) * 2 * kChunk;
+    int4* nbuf = opbuf + ((c + 1) & 1) * 4 * kChunk;
 #pragma unroll
     for (int q = 0; q < kRecPerThread; ++q) {
       const int r = q * kT + tid;
-      if ((c + 1) * kChunk + r < n_ops) {
-        nbuf[2 * r] = na[q];
-        nbuf[2 * r + 1] = nb[q];
-      }
+      if (r < kChunk && (c + 1) * kChunk + r < n_ops) stage(nbuf, r, na[q], nb[q]);
     }
     __syncthreads();
   }
 #undef SLOT2
+#undef SLOTB
   if (hi0 != kMinI64) {
     atomicMin(reinterpret_cast<long long*>(P.span_lo) + c0, static_cast<long long>(W));
     atomicMax(reinterpret_cast<long long*>(P.span_hi) + c0, static_cast<long long>(hi0));
@@ -764,7 +772,7 @@ static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStrea
 
 // shared memory of a walk CTA of t threads
 static size_t walk_smem(int n_slots, int t) {
-  return 4 * kChunk * sizeof(int4) +
+  return 8 * kChunk * sizeof(int4) +
          static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * 16;
 }
 
