@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "liblumos_b200.so")
+LIB_PATH = os.environ.get("LUMOS_B200_LIB") or os.path.join(HERE, "lib", "liblumos_b200.so")
 
 i64p = C.POINTER(C.c_int64)
 i32p = C.POINTER(C.c_int32)

@@ -112,9 +112,8 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
     // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)
     // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
     // already an integer
-    if (p < 1.5) return 1;
-    if (p >= 0x1.0p52) return static_cast<int64_t>(p);
-    return __double2ll_rd(__dadd_rn(p, 0.5));
+    const int64_t r = __double2ll_rd(p >= 0x1.0p52 ? p : __dadd_rn(p, 0.5));
+    return r < 1 ? 1 : r;
   }
   return d;
 }

@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   int64_t* const fin_c0 = P.out_fin + c0;
   const uint32_t ld = static_cast<uint32_t>(P.ld);
   const int64_t dcol = c1 - c0;
+  char* const sbase = reinterpret_cast<char*>(start_c0);
+  char* const fbase = reinterpret_cast<char*>(fin_c0);
+  const uint64_t ld8 = static_cast<uint64_t>(ld) * 8u;
 
   auto stage = [&](int4* dstbuf, int r, int4 a, int4 b) {
     dstbuf[4 * r] = a;
@@ -210,16 +213,17 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const I64x2 fin = {imax(st.x, gate.x) + d0, imax(st.y, gate.y) + d1};
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
-        if (flags & F_SINK) {
+        if (__builtin_expect((flags & F_SINK) != 0, 0)) {
           hi0 = imax(hi0, fin.x);
           hi1 = imax(hi1, fin.y);
         }
         const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
         if (vec_store) {
+          const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
           if (kWriteStart)
-            __stcs(reinterpret_cast<longlong2*>(start_c0 + at), make_longlong2(st.x, st.y));
+            __stcs(reinterpret_cast<longlong2*>(sbase + at8), make_longlong2(st.x, st.y));
           if (kWriteFin)
-            __stcs(reinterpret_cast<longlong2*>(fin_c0 + at), make_longlong2(fin.x, fin.y));
+            __stcs(reinterpret_cast<longlong2*>(fbase + at8), make_longlong2(fin.x, fin.y));
         } else {
           if (kWriteStart) {
             __stcs(start_c0 + at, st.x);
