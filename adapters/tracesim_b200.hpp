@@ -4,9 +4,11 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <vector>
 
 #include "tracesim/build.hpp"
+#include "tracesim/metrics.hpp"
 
 namespace tracesim::b200 {
 
@@ -21,14 +23,37 @@ struct ScenarioSpec {
   int32_t scale_lo = 0, scale_hi = 0, scale_den = 0;  // den <= 0: no class scaling
 };
 
+struct BatchOptions {
+  bool timestamps = false;
+  int64_t util_bin_width = 0;  // > 0: utilization_by_rank bins (metrics.cpp:105-155)
+  int32_t util_max_bins = 0;   // bins kept per rank
+  bool deltas = false;         // compare_replay start deltas (metrics.cpp:189-221)
+};
+
 struct BatchResult {
   std::vector<int64_t> start, fin;     // [task][scenario] (when requested)
   std::vector<int64_t> span;           // [scenario][3] {start, end, makespan}
   std::vector<int64_t> rank_breakdown; // [scenario][rank][5] (metrics.hpp:33-39 order)
   std::vector<int32_t> ranks;          // rank of each breakdown row
+  int64_t util_bin_width = 0;
+  int32_t util_max_bins = 0;
+  std::vector<int64_t> util_covered;   // [scenario][rank][util_max_bins] covered us
+  std::vector<int32_t> util_n_bins;    // [scenario] bins each window needs
+  std::vector<int64_t> delta_abs_sum;  // [scenario] sum |sim_start - original_start|
+  std::vector<int64_t> delta_worst;    // [scenario][3] {max |delta|, task, delta}
 };
 
 BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
                            bool timestamps = false);
+BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                           const BatchOptions& options);
+
+// Scenario s of a batch in the reference's metric types.
+// utilization_by_rank over [window.start, max(window.end, window.start + makespan))
+// (cli.cpp:303-316); bins past util_max_bins are not returned.
+std::map<int, UtilizationSeries> utilization_by_rank(const BatchResult& r, std::size_t s,
+                                                     IterationWindow window);
+// compare_replay with the worst list cut to one task (the batch keeps one).
+ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, std::size_t s);
 
 }  // namespace tracesim::b200

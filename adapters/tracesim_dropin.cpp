@@ -13,6 +13,8 @@
 // The batched entry point (not in the reference) is declared in
 // tracesim_b200.hpp: N duration scenarios of one graph in one call.
 #include <algorithm>
+#include <limits>
+#include <stdexcept>
 #include <map>
 #include <queue>
 #include <sstream>
@@ -266,6 +268,13 @@ namespace b200 {
 
 BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
                            bool timestamps) {
+  BatchOptions o;
+  o.timestamps = timestamps;
+  return simulate_batch(graph, spec, o);
+}
+
+BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                           const BatchOptions& o) {
   for (const ValidationIssue& issue : validate_graph(graph))
     if (issue.error) throw SimulationError("invalid graph: " + issue.message);
   Handle h(graph);
@@ -273,11 +282,12 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   ts_graph_get_info(h.g, &info);
   BatchResult r;
   const std::size_t S = static_cast<std::size_t>(spec.count);
+  const std::size_t R = static_cast<std::size_t>(info.n_ranks);
   r.span.assign(S * 3, 0);
-  r.rank_breakdown.assign(S * static_cast<std::size_t>(info.n_ranks) * 5, 0);
-  r.ranks.resize(static_cast<std::size_t>(info.n_ranks));
+  r.rank_breakdown.assign(S * R * 5, 0);
+  r.ranks.resize(R);
   ts_graph_ranks(h.g, r.ranks.data());
-  if (timestamps) {
+  if (o.timestamps) {
     r.start.assign(graph.tasks.size() * S, 0);
     r.fin.assign(graph.tasks.size() * S, 0);
   }
@@ -290,13 +300,74 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   sc.scale_hi = spec.scale_hi;
   sc.scale_den = spec.scale_den;
   ts_result res{};
-  res.start = timestamps ? r.start.data() : nullptr;
-  res.fin = timestamps ? r.fin.data() : nullptr;
+  res.start = o.timestamps ? r.start.data() : nullptr;
+  res.fin = o.timestamps ? r.fin.data() : nullptr;
   res.ld = spec.count;
   res.span = r.span.data();
-  res.rank_breakdown = info.n_ranks ? r.rank_breakdown.data() : nullptr;
+  res.rank_breakdown = R ? r.rank_breakdown.data() : nullptr;
+  if (o.util_bin_width > 0) {
+    r.util_bin_width = o.util_bin_width;
+    r.util_max_bins = std::max<int32_t>(1, o.util_max_bins);
+    r.util_covered.assign(S * std::max<std::size_t>(1, R) * r.util_max_bins, 0);
+    r.util_n_bins.assign(S, 0);
+    res.util_bin_width = r.util_bin_width;
+    res.util_max_bins = r.util_max_bins;
+    res.util_covered = R ? r.util_covered.data() : nullptr;
+    res.util_n_bins = r.util_n_bins.data();
+  }
+  if (o.deltas) {
+    r.delta_abs_sum.assign(S, 0);
+    r.delta_worst.assign(S * 3, 0);
+    res.delta_abs_sum = r.delta_abs_sum.data();
+    res.delta_worst = r.delta_worst.data();
+  }
   if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc);
   return r;
+}
+
+std::map<int, UtilizationSeries> utilization_by_rank(const BatchResult& r, std::size_t s,
+                                                     IterationWindow window) {
+  std::map<int, UtilizationSeries> out;
+  if (r.util_bin_width <= 0) throw std::invalid_argument("bin_width must be positive");
+  window.end = std::max(window.end, window.start + r.span[3 * s + 2]);
+  if (window.end <= window.start) return out;  // metrics.cpp:108
+  const std::size_t kept = std::min<std::size_t>(r.util_n_bins[s], r.util_max_bins);
+  for (std::size_t k = 0; k < r.ranks.size(); ++k) {
+    UtilizationSeries series;
+    series.bin_width = r.util_bin_width;
+    const int64_t* row =
+        r.util_covered.data() + (s * r.ranks.size() + k) * static_cast<std::size_t>(r.util_max_bins);
+    for (std::size_t i = 0; i < kept; ++i) {
+      const Micros bin_start = window.start + static_cast<Micros>(i) * r.util_bin_width;
+      const Micros span = std::min(r.util_bin_width, window.end - bin_start);
+      series.bins.push_back({bin_start, static_cast<double>(row[i]) / span});
+    }
+    out[r.ranks[k]] = std::move(series);
+  }
+  return out;
+}
+
+ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, std::size_t s) {
+  ReplayReport rep;
+  Micros lo = std::numeric_limits<Micros>::max(), hi = std::numeric_limits<Micros>::min();
+  for (const Task& t : graph.tasks) {
+    lo = std::min(lo, t.original_start);
+    hi = std::max(hi, t.original_start + t.duration);
+  }
+  rep.reference_makespan = graph.tasks.empty() ? 0 : hi - lo;
+  rep.simulated_makespan = r.span[3 * s + 2];
+  rep.relative_error =
+      relative_error(rep.reference_makespan, rep.simulated_makespan, &rep.zero_reference);
+  const std::size_t n = graph.tasks.size();
+  rep.mean_abs_delta = n ? static_cast<double>(r.delta_abs_sum[s]) / static_cast<double>(n) : 0.0;
+  rep.max_abs_delta = r.delta_worst[3 * s];
+  const int64_t task = r.delta_worst[3 * s + 1];
+  if (task >= 0) {
+    const Micros rs = graph.tasks[static_cast<std::size_t>(task)].original_start;
+    rep.worst.push_back({static_cast<TaskId>(task), rs, rs + r.delta_worst[3 * s + 2],
+                         r.delta_worst[3 * s + 2]});
+  }
+  return rep;
 }
 
 }  // namespace b200

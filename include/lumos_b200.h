@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 /* error codes (0 = success) */
 enum {
@@ -163,6 +163,19 @@ typedef struct {
   int64_t* stream_busy;    /* [count][n_streams] summed kernel time per stream */
   int32_t* status;         /* [count] 0 = exact fast path, 1 = resolved by the
                               exact event-driven path, <0 = error */
+  /* utilization_by_rank (metrics.cpp:105-155) over the breakdown's window
+   * [W, max(window.end, W + makespan)): per rank, the microseconds of bin b
+   * = [W + b*w, min(W + (b+1)*w, end)) covered by >= 1 kernel on any of the
+   * rank's streams (value = covered / bin span, computed by the caller). */
+  int64_t util_bin_width;  /* w > 0 to produce util_covered */
+  int32_t util_max_bins;   /* bins stored per rank (later bins are dropped) */
+  int32_t util_pad;
+  int64_t* util_covered;   /* [count][n_ranks][util_max_bins] */
+  int32_t* util_n_bins;    /* [count] bins the window needs */
+  /* compare_replay (metrics.cpp:189-221): delta = sim_start - original_start */
+  int64_t* delta_abs_sum;  /* [count] sum of |delta| over all tasks (exact) */
+  int64_t* delta_worst;    /* [count][3] {max |delta|, its task (smallest id on
+                              ties, the report's sort order), signed delta} */
 } ts_result;
 
 /* Replays `sc->count` scenarios on `stream` (cudaStream_t, NULL = legacy

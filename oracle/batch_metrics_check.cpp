@@ -1,0 +1,85 @@
+// batch_metrics_check.cpp — TEST INFRASTRUCTURE (built into oracle/_ref/ by
+// oracle/Makefile, run by tests/test_gpu_dropin.py on a B200).
+//
+// Drives the C++ batched API of the drop-in (adapters/tracesim_b200.hpp) with
+// the utilization and compare_replay outputs, and checks every scenario
+// against the reference's own code on the same durations: the tick oracle
+// (tests/oracles.cpp) replays the perturbed graph, and the reference
+// metrics.cpp computes utilization_by_rank (metrics.cpp:105-155) and
+// compare_replay (metrics.cpp:189-221) from it.  Scenario durations come from
+// the C restatement of the scenario formula (lumos_oracle.c).
+#include <cstdio>
+#include <map>
+#include <vector>
+
+#include "json.hpp"
+#include "lumos_oracle.h"
+#include "oracles.hpp"
+#include "tracesim/build.hpp"
+#include "tracesim/metrics.hpp"
+#include "tracesim/synth.hpp"
+#include "tracesim/trace_parse.hpp"
+#include "tracesim_b200.hpp"
+
+using namespace tracesim;
+
+int main() {
+  nlohmann::json j;
+  j["parallelism"] = {{"pp", 2}, {"dp", 2}, {"num_microbatches", 4}};
+  j["model"] = {{"n_layers", 4}, {"d_model", 1024}, {"d_ffn", 4096}, {"n_heads", 16},
+                {"d_head", 64}};
+  SynthResult gen = generate(SynthSpec::from_json(j.dump()));
+  std::map<int, ExecutionGraph> parts;
+  for (const auto& [rank, evs] : split_by_rank(gen.events))
+    parts[rank] = build_graph(evs, BuildPolicy(), rank);
+  const ExecutionGraph g = merge_ranks(parts);
+
+  b200::ScenarioSpec spec;
+  spec.first = 40;
+  spec.count = 24;
+  spec.seed = 99;
+  spec.jitter = 0.2;
+  b200::BatchOptions opt;
+  opt.util_bin_width = 4000;
+  opt.util_max_bins = 1024;
+  opt.deltas = true;
+  const b200::BatchResult r = b200::simulate_batch(g, spec, opt);
+
+  orc_scenarios sc{};
+  sc.seed = spec.seed;
+  sc.jitter = spec.jitter;
+  std::vector<int64_t> base, dur(g.tasks.size());
+  for (const Task& t : g.tasks) base.push_back(t.duration);
+  std::vector<uint8_t> cls(g.tasks.size(), 0);
+  int bad = 0;
+  for (int s = 0; s < spec.count; ++s) {
+    orc_fill_durations(&sc, spec.first + s, static_cast<int32_t>(g.tasks.size()), base.data(),
+                       cls.data(), dur.data());
+    ExecutionGraph gs = g;
+    for (std::size_t t = 0; t < gs.tasks.size(); ++t) gs.tasks[t].duration = dur[t];
+    const SimulatedTrace sim = oracle::tick_simulate(gs);
+    if (sim.makespan != r.span[3 * s + 2]) ++bad;
+    IterationWindow w = g.iteration_window;
+    w.end = std::max(w.end, w.start + sim.makespan);
+    auto want = utilization_by_rank(task_intervals(gs, &sim), w, opt.util_bin_width);
+    auto got = b200::utilization_by_rank(r, s, g.iteration_window);
+    if (want.size() != got.size()) ++bad;
+    for (const auto& [rank, ws] : want) {
+      const auto& gs_ = got.at(rank);
+      if (ws.bins.size() != gs_.bins.size()) { ++bad; continue; }
+      for (std::size_t b = 0; b < ws.bins.size(); ++b)
+        if (ws.bins[b].start != gs_.bins[b].start || ws.bins[b].value != gs_.bins[b].value) ++bad;
+    }
+    const ReplayReport a = compare_replay(g, sim, 1), b = b200::replay_report(g, r, s);
+    if (a.reference_makespan != b.reference_makespan || a.simulated_makespan != b.simulated_makespan ||
+        a.max_abs_delta != b.max_abs_delta || a.mean_abs_delta != b.mean_abs_delta ||
+        a.relative_error != b.relative_error || a.worst.size() != b.worst.size() ||
+        (!a.worst.empty() && (a.worst[0].task != b.worst[0].task ||
+                              a.worst[0].delta != b.worst[0].delta ||
+                              a.worst[0].simulated_start != b.worst[0].simulated_start)))
+      ++bad;
+  }
+  std::printf("%s: %d scenarios, %zu tasks, %d mismatches\n", bad ? "FAIL" : "PASS", spec.count,
+              g.tasks.size(), bad);
+  return bad ? 1 : 0;
+}

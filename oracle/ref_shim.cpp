@@ -16,7 +16,9 @@
 //   breakdown_by_rank             (src/metrics.cpp:96-103)
 //   build_pipeline + DurationHook (src/pipeline.cpp:474-477)
 
+#include <algorithm>
 #include <chrono>
+#include <limits>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -300,6 +302,66 @@ int ref_breakdown_by_rank(void* h, const int64_t* start, const int64_t* fin, int
     ++k;
   }
   return k;
+}
+
+// utilization_by_rank (metrics.cpp:105-155) over the simulated intervals:
+// values[k][b] (double) for the k-th rank (ascending), ranks[k], n_bins[k].
+int ref_utilization_by_rank(void* h, const int64_t* start, const int64_t* fin, int64_t wstart,
+                            int64_t wend, int64_t bin_width, double* values, int32_t* ranks,
+                            int32_t* n_bins, int max_ranks, int max_bins) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  SimulatedTrace sim;
+  for (std::size_t i = 0; i < g.tasks.size(); ++i)
+    sim.entries.push_back({static_cast<TaskId>(i), start[i], fin[i], g.tasks[i].processor});
+  auto util = utilization_by_rank(task_intervals(g, &sim), IterationWindow{wstart, wend}, bin_width);
+  int k = 0;
+  for (const auto& [rank, series] : util) {
+    if (k >= max_ranks) break;
+    ranks[k] = rank;
+    n_bins[k] = static_cast<int32_t>(series.bins.size());
+    for (std::size_t b = 0; b < series.bins.size() && static_cast<int>(b) < max_bins; ++b)
+      values[static_cast<std::size_t>(k) * max_bins + b] = series.bins[b].value;
+    ++k;
+  }
+  return k;
+}
+
+// compare_replay (metrics.cpp:189-221) of one replay given as per-task
+// start/fin: out_i = {reference_makespan, simulated_makespan, max_abs_delta,
+// zero_reference, n_worst, worst task ids..., worst deltas...}, out_d =
+// {mean_abs_delta, relative_error}.  Entries are ordered (sim_start, id) as
+// simulate() emits them (simulate.cpp:320-326).
+int ref_compare_replay(void* h, const int64_t* start, const int64_t* fin, int32_t worst_n,
+                       int64_t* out_i, double* out_d) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  SimulatedTrace sim;
+  for (std::size_t i = 0; i < g.tasks.size(); ++i)
+    sim.entries.push_back({static_cast<TaskId>(i), start[i], fin[i], g.tasks[i].processor});
+  std::sort(sim.entries.begin(), sim.entries.end(), [](const SimEntry& a, const SimEntry& b) {
+    return std::pair(a.sim_start, a.task_id) < std::pair(b.sim_start, b.task_id);
+  });
+  if (!sim.entries.empty()) {
+    sim.start = std::numeric_limits<Micros>::max();
+    sim.end = std::numeric_limits<Micros>::min();
+    for (const auto& e : sim.entries) {
+      sim.start = std::min(sim.start, e.sim_start);
+      sim.end = std::max(sim.end, e.sim_end);
+    }
+    sim.makespan = sim.end - sim.start;
+  }
+  ReplayReport rep = compare_replay(g, sim, static_cast<std::size_t>(worst_n));
+  out_i[0] = rep.reference_makespan;
+  out_i[1] = rep.simulated_makespan;
+  out_i[2] = rep.max_abs_delta;
+  out_i[3] = rep.zero_reference ? 1 : 0;
+  out_i[4] = static_cast<int64_t>(rep.worst.size());
+  for (std::size_t k = 0; k < rep.worst.size(); ++k) {
+    out_i[5 + k] = rep.worst[k].task;
+    out_i[5 + worst_n + k] = rep.worst[k].delta;
+  }
+  out_d[0] = rep.mean_abs_delta;
+  out_d[1] = rep.relative_error;
+  return 0;
 }
 
 // ------------------------------------------------------ CPU baseline timing

@@ -61,9 +61,13 @@ class TsProfileStats(C.Structure):
 
 class TsResult(C.Structure):
     _fields_ = [("start", i64p), ("fin", i64p), ("ld", C.c_int64), ("span", i64p),
-                ("rank_breakdown", i64p), ("stream_busy", i64p), ("status", i32p)]
+                ("rank_breakdown", i64p), ("stream_busy", i64p), ("status", i32p),
+                ("util_bin_width", C.c_int64), ("util_max_bins", C.c_int32),
+                ("util_pad", C.c_int32), ("util_covered", i64p), ("util_n_bins", i32p),
+                ("delta_abs_sum", i64p), ("delta_worst", i64p)]
 
 
+ABI_VERSION = 2  # TS_ABI_VERSION in include/lumos_b200.h
 _lib = None
 
 
@@ -100,7 +104,7 @@ def lib():
         L.ts_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.ts_profile_read.restype = C.c_int
         L.ts_profile_read.argtypes = [C.c_void_p, C.POINTER(TsProfileStats)]
-        if L.ts_abi_version() != 1:
+        if L.ts_abi_version() != ABI_VERSION:
             raise RuntimeError("liblumos_b200.so ABI mismatch")
         _lib = L
     return _lib

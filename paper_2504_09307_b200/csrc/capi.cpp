@@ -118,7 +118,9 @@ struct ts_graph {
   DevBuf des_scratch;
   int32_t bucket_off[kReduceBuckets + 1] = {0};
   DevBuf span_lo, span_hi, status, scratch_ts;
-  DevBuf stage[8];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur
+  DevBuf stage[12];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur,
+                     // util, util bins, delta sum, delta worst
+  DevBuf delta_scratch;
   // device-time accounting
   bool profile = false;
   struct Mark {
@@ -311,7 +313,8 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_lane_rank), static_cast<void*>(g->d_lane_stream)})
       if (p) cudaFree(p);
     g->des_scratch.release();
-    for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts}) b->release();
+    for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts, &g->delta_scratch})
+      b->release();
     for (DevBuf& b : g->stage) b.release();
     for (auto& m : g->marks) {
       cudaEventDestroy(m.a);
@@ -417,6 +420,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   if (count == 0) return TS_OK;
   if ((out->start || out->fin) && out->ld < count)
     return fail(TS_E_INVALID_ARGUMENT, "ld must be >= count");
+  if ((out->util_covered || out->util_n_bins) && out->util_bin_width <= 0)
+    return fail(TS_E_INVALID_ARGUMENT, "bin_width must be positive");  // metrics.cpp:107
+  if (out->util_covered && out->util_max_bins <= 0)
+    return fail(TS_E_INVALID_ARGUMENT, "util_max_bins must be positive");
   int prev_dev = -1;
   cudaGetDevice(&prev_dev);
   if (prev_dev != g->device) CUDA_TRY(cudaSetDevice(g->device));
@@ -445,7 +452,8 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
 
   // outputs: device pointers are written in place, host pointers staged
   const bool want_ts = out->start || out->fin;
-  const bool want_red = out->rank_breakdown || out->stream_busy;
+  const bool want_red = out->rank_breakdown || out->stream_busy || out->util_covered;
+  const bool want_delta = out->delta_abs_sum || out->delta_worst;
   const int32_t n_ranks = static_cast<int32_t>(c.ranks.size());
   const int32_t n_streams = static_cast<int32_t>(c.stream_rank.size());
   struct OutBuf {
@@ -469,9 +477,18 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       out_ptr(3, out->rank_breakdown, static_cast<size_t>(count) * n_ranks * 40));
   int64_t* d_busy = static_cast<int64_t*>(
       out_ptr(4, out->stream_busy, static_cast<size_t>(count) * n_streams * 8));
+  const int32_t ubins = out->util_covered ? out->util_max_bins : 0;
+  int64_t* d_util = static_cast<int64_t*>(
+      out_ptr(7, out->util_covered, static_cast<size_t>(count) * n_ranks * ubins * 8));
+  int32_t* d_nbins = static_cast<int32_t*>(out_ptr(8, out->util_n_bins, static_cast<size_t>(count) * 4));
+  int64_t* d_dsum = static_cast<int64_t*>(out_ptr(9, out->delta_abs_sum, static_cast<size_t>(count) * 8));
+  int64_t* d_dworst =
+      static_cast<int64_t*>(out_ptr(10, out->delta_worst, static_cast<size_t>(count) * 24));
   if ((out->start && ts_bytes && !d_start) || (out->fin && ts_bytes && !d_fin) ||
       (out->span && !d_span) || (out->rank_breakdown && n_ranks && !d_bd) ||
-      (out->stream_busy && n_streams && !d_busy)) {
+      (out->stream_busy && n_streams && !d_busy) || (out->util_covered && n_ranks && !d_util) ||
+      (out->util_n_bins && !d_nbins) || (out->delta_abs_sum && !d_dsum) ||
+      (out->delta_worst && !d_dworst)) {
     cleanup();
     return fail(TS_E_NOMEM, "could not stage output buffers");
   }
@@ -489,15 +506,25 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   int64_t* s_start = d_start;
   int64_t* s_fin = d_fin;
   int64_t s_ld = out->ld;
-  if (want_red && !want_ts) {
-    const size_t budget = size_t(4) << 30;
-    const size_t per_col = static_cast<size_t>(c.n_tasks) * 16 + 1;
-    size_t cols = std::max<size_t>(128, budget / per_col / 128 * 128);
-    sub = static_cast<int32_t>(std::min<size_t>(cols, static_cast<size_t>(count)));
-    CUDA_TRY(g->scratch_ts.reserve(static_cast<size_t>(sub) * per_col));
-    s_start = g->scratch_ts.as<int64_t>();
-    s_fin = s_start + static_cast<size_t>(c.n_tasks) * sub;
-    s_ld = sub;
+  // compare_replay deltas need the starts, the reductions both timestamps
+  const bool need_start = want_red || want_delta, need_fin = want_red;
+  if ((need_start && !d_start) || (need_fin && !d_fin)) {
+    if (!want_ts) {
+      // none requested: sub-batch through an internal scratch tile
+      const size_t budget = size_t(4) << 30;
+      const size_t per_col = static_cast<size_t>(c.n_tasks) * 16 + 1;
+      size_t cols = std::max<size_t>(128, budget / per_col / 128 * 128);
+      sub = static_cast<int32_t>(std::min<size_t>(cols, static_cast<size_t>(count)));
+      CUDA_TRY(g->scratch_ts.reserve(static_cast<size_t>(sub) * per_col));
+      s_start = g->scratch_ts.as<int64_t>();
+      s_fin = s_start + static_cast<size_t>(c.n_tasks) * sub;
+      s_ld = sub;
+    } else {
+      // one of them requested: the other lives in scratch at the caller's ld
+      CUDA_TRY(g->scratch_ts.reserve(ts_bytes + 1));
+      if (!d_start) s_start = g->scratch_ts.as<int64_t>();
+      if (need_fin && !d_fin) s_fin = g->scratch_ts.as<int64_t>();
+    }
   }
 
   {
@@ -519,9 +546,15 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.sp.count = bn;
     if (sp.scale_num) wp.sp.scale_num = sp.scale_num + static_cast<size_t>(b0) * sp.n_classes;
     if (sp.durations) wp.sp.durations = sp.durations + b0;
-    const bool own_tile = s_start != d_start || s_fin != d_fin;
-    wp.out_start = own_tile ? s_start : (d_start ? d_start + b0 : nullptr);
-    wp.out_fin = own_tile ? s_fin : (d_fin ? d_fin + b0 : nullptr);
+    // b0 > 0 only when sub-batching through the scratch tile, whose pointers
+    // are tile-local; otherwise there is one tile at b0 = 0
+    if (d_util) {
+      const size_t row = static_cast<size_t>(n_ranks) * ubins;
+      CUDA_TRY(cudaMemsetAsync(d_util + static_cast<size_t>(b0) * row, 0,
+                               static_cast<size_t>(bn) * row * 8, stream));
+    }
+    wp.out_start = s_start;
+    wp.out_fin = s_fin;
     wp.ld = s_ld;
     wp.span_lo = lo + b0;
     wp.span_hi = hi + b0;
@@ -575,6 +608,9 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       if (c.des_only) {  // the walk's reductions are not valid here: DES does them
         dp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
         dp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
+        dp.util = d_util ? d_util + static_cast<size_t>(b0) * n_ranks * ubins : nullptr;
+        dp.util_bw = out->util_bin_width;
+        dp.util_max_bins = ubins;
       }
       const size_t per = des_scratch_bytes(c.n_tasks, T.n_lanes);
       const size_t budget = size_t(1) << 30;
@@ -605,6 +641,9 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       rp.n_streams = n_streams;
       rp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
       rp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
+      rp.util = d_util ? d_util + static_cast<size_t>(b0) * n_ranks * ubins : nullptr;
+      rp.util_bw = out->util_bin_width;
+      rp.util_max_bins = ubins;
       for (int b = 0; b < kReduceBuckets; ++b) {
         const int nr = g->bucket_off[b + 1] - g->bucket_off[b];
         if (nr == 0) continue;
@@ -614,6 +653,31 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
         g_launches++;
       }
     }
+    if (want_delta) {
+      DeltaParams dl{};
+      dl.start = wp.out_start;
+      dl.ld = wp.ld;
+      dl.ostart = g->d_ostart;
+      dl.n_tasks = c.n_tasks;
+      dl.count = bn;
+      const int col_blocks = (bn + 127) / 128;
+      const int64_t want = (4 * 148 * 8 + col_blocks - 1) / col_blocks;
+      dl.n_chunks = static_cast<int32_t>(
+          std::max<int64_t>(1, std::min<int64_t>(want, (c.n_tasks + 255) / 256)));
+      CUDA_TRY(g->delta_scratch.reserve(static_cast<size_t>(dl.n_chunks) * bn * 32));
+      dl.partial = g->delta_scratch.as<int64_t>();
+      dl.abs_sum = d_dsum ? d_dsum + b0 : nullptr;
+      dl.worst = d_dworst ? d_dworst + static_cast<size_t>(b0) * 3 : nullptr;
+      Timed tm(g, stream, 1);
+      CUDA_TRY(launch_deltas(dl, stream));
+      g_launches += 2;
+    }
+  }
+  if (d_nbins) {
+    Timed tm(g, stream, 2);
+    CUDA_TRY(launch_util_nbins(lo, hi, c.window_start, c.window_end, out->util_bin_width, d_nbins,
+                               count, stream));
+    g_launches++;
   }
   if (d_span) {
     Timed tm(g, stream, 2);

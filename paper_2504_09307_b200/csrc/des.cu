@@ -255,7 +255,7 @@ __global__ void des_kernel(DesParams P) {
     P.span_lo[col] = lo;
     P.span_hi[col] = hi;
     P.status[col] = 1;
-    if (!P.breakdown && !P.stream_busy) continue;
+    if (!P.breakdown && !P.stream_busy && !P.util) continue;
     // per-rank breakdown (metrics.cpp:43-103) on sorted interval endpoints
     int64_t wend = P.window_end;
     if (W + (hi - lo) > wend) wend = W + (hi - lo);
@@ -283,6 +283,9 @@ __global__ void des_kernel(DesParams P) {
       sort_i64(s.ev, ne);
       int compute = 0, commc = 0;
       int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
+      BinAcc ua;
+      if (P.util) ua.init(P.util + (static_cast<int64_t>(col) * P.n_ranks + r) * P.util_max_bins,
+                          P.util_bw, P.util_max_bins);
       auto account = [&](int64_t upto) {
         if (upto <= prev) return;
         const int64_t span = upto - prev;
@@ -290,6 +293,7 @@ __global__ void des_kernel(DesParams P) {
         else if (compute > 0) ec += span;
         else if (commc > 0) em += span;
         else ot += span;
+        if (P.util && (compute > 0 || commc > 0)) ua.add(prev - W, upto - W, 1);
         prev = upto;
       };
       for (int32_t k = 0; k < ne; ++k) {
@@ -302,6 +306,7 @@ __global__ void des_kernel(DesParams P) {
         }
       }
       account(wend);
+      if (P.util) ua.flush();
       if (P.breakdown) {
         int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
         row[0] = wend - W;

@@ -128,5 +128,40 @@ __device__ __forceinline__ void init_thread_scen(const ScenarioParams& sp, int c
 
 __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
 
+// Utilization bins (metrics.cpp:105-155): adds covered microseconds of
+// [from, to) (window-relative, non-decreasing `from` across calls) to the bins
+// of width bw, accumulating the current bin in a register and flushing it to
+// row[bin] (read-modify-write: several accumulators of one thread may share a
+// row).  sign -1 subtracts (the overlap term of |A u U| = |A| + |U| - |A n U|).
+struct BinAcc {
+  int64_t* row;
+  int64_t bw, bin_end, acc;
+  int32_t bin, max_bins;
+  __device__ __forceinline__ void init(int64_t* r, int64_t w, int32_t mb) {
+    row = r;
+    bw = w;
+    bin_end = w;
+    acc = 0;
+    bin = 0;
+    max_bins = mb;
+  }
+  __device__ __forceinline__ void flush() {
+    if (acc != 0 && bin < max_bins) row[bin] += acc;
+    acc = 0;
+  }
+  __device__ __forceinline__ void add(int64_t from, int64_t to, int64_t sign) {
+    while (from < to) {
+      while (from >= bin_end) {
+        flush();
+        ++bin;
+        bin_end += bw;
+      }
+      const int64_t e = to < bin_end ? to : bin_end;
+      acc += sign * (e - from);
+      from = e;
+    }
+  }
+};
+
 }  // namespace
 }  // namespace lumos

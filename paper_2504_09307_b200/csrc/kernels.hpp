@@ -71,6 +71,10 @@ struct ReduceParams {
   int32_t pad;
   int64_t* breakdown;    // [count][n_ranks][5]
   int64_t* stream_busy;  // [count][n_streams]
+  int64_t* util;         // [count][n_ranks][util_max_bins] (zeroed), or null
+  int64_t util_bw;
+  int32_t util_max_bins;
+  int32_t pad2;
 };
 
 struct DesParams {
@@ -103,6 +107,9 @@ struct DesParams {
   int32_t* status;
   int64_t* breakdown;
   int64_t* stream_busy;
+  int64_t* util;  // as ReduceParams
+  int64_t util_bw;
+  int32_t util_max_bins;
   int32_t fixup;    // only scenarios whose status is non-zero (certificate failed)
   int32_t n_slots;  // concurrent scenarios (scratch slots)
   char* scratch;
@@ -117,6 +124,24 @@ int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
                              cudaStream_t stream);
+// compare_replay deltas of one tile: partial[chunk][count][3] then per column
+// {sum |d|, max |d|, worst task, signed delta} (see ts_result)
+struct DeltaParams {
+  const int64_t* start;  // [n_tasks][ld]
+  int64_t ld;
+  const int64_t* ostart;  // [n_tasks]
+  int32_t n_tasks;
+  int32_t count;
+  int32_t n_chunks;
+  int32_t pad;
+  int64_t* partial;  // [n_chunks][count][4]
+  int64_t* abs_sum;  // [count] or null
+  int64_t* worst;    // [count][3] or null
+};
+cudaError_t launch_deltas(const DeltaParams& p, cudaStream_t stream);
+// n_bins[i] = ceil(window span / w) for the utilization bins
+cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, int64_t window_end,
+                              int64_t w, int32_t* n_bins, int32_t count, cudaStream_t stream);
 cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W, int64_t* span,
                                  int64_t* makespan, int32_t count, cudaStream_t stream);
 cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,

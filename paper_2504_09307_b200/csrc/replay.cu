@@ -352,7 +352,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 // T: the time type of the merge — uint32 offsets from W when the accounting
 // window fits 32 bits (then every compare is one 32-bit op), else int64.
-template <int NS, typename T>
+template <int NS, typename T, bool kUtil>
 __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col, int r, int ns,
                                                   int64_t* ring, int64_t W, int64_t wend) {
   constexpr int H = RingHalf<NS>::value;
@@ -438,6 +438,9 @@ __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col
   int compute = 0, comm = 0;
   T prev = 0;
   int64_t ec = 0, em = 0, ov = 0, ot = 0;
+  BinAcc ua;
+  if (kUtil) ua.init(P.util + (static_cast<int64_t>(col) * P.n_ranks + r) * P.util_max_bins,
+                     P.util_bw, P.util_max_bins);
   for (;;) {
     int jm = -1;
     T tm = kInf;
@@ -457,6 +460,8 @@ __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col
       } else {
         if (comm > 0) em += d; else ot += d;
       }
+      if (kUtil && (compute > 0 || comm > 0))
+        ua.add(static_cast<int64_t>(prev), static_cast<int64_t>(tm), 1);
       prev = tm;
     }
     const bool is_comm = (cc >> jm) & 1u;
@@ -475,6 +480,7 @@ __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col
     }
   }
 #undef RING
+  if (kUtil) ua.flush();
   {
     const int64_t d = span - static_cast<int64_t>(prev);
     if (d > 0) {
@@ -500,7 +506,7 @@ __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col
   }
 }
 
-template <int NS>
+template <int NS, bool kUtil>
 __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col, int r, int ns,
                                                  int64_t* ring) {
   const int64_t W = P.window_start;
@@ -512,19 +518,19 @@ __device__ __forceinline__ void rank_reduce_body(const ReduceParams& P, int col,
   }
   if (wend < W) wend = W;
   if (wend - W < 0xFFFFFFFFll)
-    rank_reduce_merge<NS, uint32_t>(P, col, r, ns, ring, W, wend);
+    rank_reduce_merge<NS, uint32_t, kUtil>(P, col, r, ns, ring, W, wend);
   else
-    rank_reduce_merge<NS, int64_t>(P, col, r, ns, ring, W, wend);
+    rank_reduce_merge<NS, int64_t, kUtil>(P, col, r, ns, ring, W, wend);
 }
 
-template <int NS>
+template <int NS, bool kUtil>
 __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
   extern __shared__ int64_t ring[];
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = P.rank_list[blockIdx.y];
   if (col >= P.count) return;
   const int ns = P.rank_stream_off[r + 1] - P.rank_stream_off[r];
-  rank_reduce_body<NS>(P, col, r, ns, ring);
+  rank_reduce_body<NS, kUtil>(P, col, r, ns, ring);
 }
 
 // ---------------------------------------------------------------- K5 fast path
@@ -601,7 +607,7 @@ constexpr size_t fast_ring_words() {
   return static_cast<size_t>(2 * kFastHA * 2 + NC * 2 * kFastHC * 2);
 }
 
-template <int NC, typename T>
+template <int NC, typename T, bool kUtil>
 __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int col, int r,
                                                       int ci, int64_t* ring, int64_t W,
                                                       int64_t wend) {
@@ -636,6 +642,14 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
   for (int j = 0; j < NC; ++j)
     if (!C[j].get(cs[j], ce[j], nodes, S, F, ld, col, rel)) cs[j] = ce[j] = kInf;
 
+  // utilization = |A| + |U| - |A n U| per bin, one accumulator per term
+  BinAcc ua, uu, uo;
+  if (kUtil) {
+    int64_t* row = P.util + (static_cast<int64_t>(col) * P.n_ranks + r) * P.util_max_bins;
+    ua.init(row, P.util_bw, P.util_max_bins);
+    uu.init(row, P.util_bw, P.util_max_bins);
+    uo.init(row, P.util_bw, P.util_max_bins);
+  }
   // union of the comm intervals, produced in time order
   T us = kInf, ue = kInf;
   int64_t m = 0;
@@ -669,6 +683,7 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
       if (!any) break;
     }
     m += static_cast<int64_t>(ue - us);
+    if (kUtil) uu.add(static_cast<int64_t>(us), static_cast<int64_t>(ue), 1);
   };
   if (NC > 0) next_union();
 
@@ -676,18 +691,25 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
   T as, ae;
   while (A.get(as, ae, nodes, S, F, ld, col, rel)) {
     busy_a += static_cast<int64_t>(ae - as);
+    if (kUtil) ua.add(static_cast<int64_t>(as), static_cast<int64_t>(ae), 1);
     if (NC > 0) {
       while (ue <= as) next_union();
       while (us < ae) {
         const T lo = us > as ? us : as;
         const T hi = ue < ae ? ue : ae;
         ov += static_cast<int64_t>(hi - lo);
+        if (kUtil) uo.add(static_cast<int64_t>(lo), static_cast<int64_t>(hi), -1);
         if (ue <= ae) next_union(); else break;
       }
     }
   }
   if (NC > 0)
     while (us != kInf) next_union();
+  if (kUtil) {
+    ua.flush();
+    uu.flush();
+    uo.flush();
+  }
 
   if (P.breakdown) {
     int64_t* row = P.breakdown + (static_cast<int64_t>(col) * P.n_ranks + r) * 5;
@@ -706,7 +728,7 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
 }
 
 // rank_list entries: rank | compute-stream index << 24
-template <int NC>
+template <int NC, bool kUtil>
 __global__ void __launch_bounds__(kThreads) rank_reduce_fast_kernel(ReduceParams P) {
   extern __shared__ int64_t ring[];
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
@@ -722,14 +744,94 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_fast_kernel(ReduceParams
   }
   if (wend < W) wend = W;
   if (wend - W < 0xFFFFFFFFll)
-    rank_reduce_fast_body<NC, uint32_t>(P, col, r, ci, ring, W, wend);
+    rank_reduce_fast_body<NC, uint32_t, kUtil>(P, col, r, ci, ring, W, wend);
   else
-    rank_reduce_fast_body<NC, int64_t>(P, col, r, ci, ring, W, wend);
+    rank_reduce_fast_body<NC, int64_t, kUtil>(P, col, r, ci, ring, W, wend);
+}
+
+// ------------------------------------------------------------------- K6
+// compare_replay deltas (metrics.cpp:189-221).  Pass 1: thread = (scenario
+// column, task chunk), tasks ascending, strict '>' so the first maximum (the
+// smallest task id) wins; pass 2 folds the chunks in ascending order.
+__global__ void delta_partial_kernel(DeltaParams P) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  if (col >= P.count) return;
+  const int32_t per = (P.n_tasks + P.n_chunks - 1) / P.n_chunks;
+  const int32_t t0 = chunk * per, t1 = min(P.n_tasks, t0 + per);
+  int64_t sum = 0, best = -1, best_d = 0;
+  int32_t best_t = -1;
+  for (int32_t t = t0; t < t1; ++t) {
+    const int64_t d = __ldcs(P.start + static_cast<int64_t>(t) * P.ld + col) - __ldg(P.ostart + t);
+    const int64_t a = d < 0 ? -d : d;
+    sum += a;
+    if (a > best) {
+      best = a;
+      best_t = t;
+      best_d = d;
+    }
+  }
+  int64_t* o = P.partial + (static_cast<int64_t>(chunk) * P.count + col) * 4;
+  o[0] = sum;
+  o[1] = best;
+  o[2] = best_t;
+  o[3] = best_d;
+}
+
+__global__ void delta_final_kernel(DeltaParams P) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= P.count) return;
+  int64_t sum = 0, best = -1, best_t = -1, best_d = 0;
+  for (int c = 0; c < P.n_chunks; ++c) {
+    const int64_t* o = P.partial + (static_cast<int64_t>(c) * P.count + col) * 4;
+    sum += o[0];
+    if (o[1] > best) {
+      best = o[1];
+      best_t = o[2];
+      best_d = o[3];
+    }
+  }
+  if (P.abs_sum) P.abs_sum[col] = sum;
+  if (P.worst) {
+    P.worst[3 * static_cast<int64_t>(col) + 0] = best < 0 ? 0 : best;
+    P.worst[3 * static_cast<int64_t>(col) + 1] = best_t;
+    P.worst[3 * static_cast<int64_t>(col) + 2] = best_d;
+  }
+}
+
+__global__ void util_nbins_kernel(const int64_t* lo, const int64_t* hi, int64_t W,
+                                  int64_t window_end, int64_t w, int32_t* n_bins, int32_t count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int64_t m = lo[i] == kMaxI64 ? 0 : hi[i] - lo[i];
+  int64_t wend = window_end > W + m ? window_end : W + m;
+  if (wend < W) wend = W;
+  n_bins[i] = static_cast<int32_t>((wend - W + w - 1) / w);
 }
 
 }  // namespace
 
 // ------------------------------------------------------------ launchers
+cudaError_t launch_deltas(const DeltaParams& p, cudaStream_t stream) {
+  if (p.count <= 0) return cudaSuccess;
+  DeltaParams q = p;
+  if (q.n_tasks > 0 && q.n_chunks > 0) {
+    dim3 grid((q.count + 127) / 128, q.n_chunks);
+    delta_partial_kernel<<<grid, 128, 0, stream>>>(q);
+  } else {
+    q.n_chunks = 0;  // no entries: sum 0, worst {0, -1, 0}
+  }
+  delta_final_kernel<<<(q.count + 127) / 128, 128, 0, stream>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, int64_t window_end,
+                              int64_t w, int32_t* n_bins, int32_t count, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  util_nbins_kernel<<<(count + 255) / 256, 256, 0, stream>>>(lo, hi, W, window_end, w, n_bins,
+                                                             count);
+  return cudaGetLastError();
+}
 int walk_threads() { return kThreads; }
 
 template <int kT, int kMode, bool kS, bool kF>
@@ -837,34 +939,37 @@ cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in
     kern<<<grid, kThreads, smem, stream>>>(p);
     return cudaSuccess;
   };
+  const bool u = p.util != nullptr;
   cudaError_t e;
-  switch (bucket) {
-    case 0: e = go(rank_reduce_kernel<1>, 1); break;
-    case 1: e = go(rank_reduce_kernel<2>, 2); break;
-    case 2: e = go(rank_reduce_kernel<3>, 3); break;
-    case 3: e = go(rank_reduce_kernel<4>, 4); break;
-    case 4: e = go(rank_reduce_kernel<8>, 8); break;
-    case 5: e = go(rank_reduce_kernel<16>, 16); break;
-    case 6: e = go(rank_reduce_kernel<kMaxStreamsPerRank>, kMaxStreamsPerRank); break;
-    default: {
-      auto fast = [&](auto kern, size_t words) -> cudaError_t {
-        const size_t smem = words * kThreads * sizeof(int64_t);
-        if (smem > 48 * 1024) {
-          cudaError_t e2 = cudaFuncSetAttribute(
-              kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-          if (e2 != cudaSuccess) return e2;
-        }
-        kern<<<grid, kThreads, smem, stream>>>(p);
-        return cudaSuccess;
-      };
-      switch (bucket - kReduceGenericBuckets) {
-        case 0: e = fast(rank_reduce_fast_kernel<0>, fast_ring_words<0>()); break;
-        case 1: e = fast(rank_reduce_fast_kernel<1>, fast_ring_words<1>()); break;
-        case 2: e = fast(rank_reduce_fast_kernel<2>, fast_ring_words<2>()); break;
-        default: e = fast(rank_reduce_fast_kernel<3>, fast_ring_words<3>()); break;
-      }
+#define LUMOS_GEN(NS_) (u ? go(rank_reduce_kernel<NS_, true>, NS_) : go(rank_reduce_kernel<NS_, false>, NS_))
+#define LUMOS_FAST(NC_)                                                      \
+  (u ? fast(rank_reduce_fast_kernel<NC_, true>, fast_ring_words<NC_>()) \
+     : fast(rank_reduce_fast_kernel<NC_, false>, fast_ring_words<NC_>()))
+  auto fast = [&](auto kern, size_t words) -> cudaError_t {
+    const size_t smem = words * kThreads * sizeof(int64_t);
+    if (smem > 48 * 1024) {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem));
+      if (e2 != cudaSuccess) return e2;
     }
+    kern<<<grid, kThreads, smem, stream>>>(p);
+    return cudaSuccess;
+  };
+  switch (bucket) {
+    case 0: e = LUMOS_GEN(1); break;
+    case 1: e = LUMOS_GEN(2); break;
+    case 2: e = LUMOS_GEN(3); break;
+    case 3: e = LUMOS_GEN(4); break;
+    case 4: e = LUMOS_GEN(8); break;
+    case 5: e = LUMOS_GEN(16); break;
+    case 6: e = LUMOS_GEN(kMaxStreamsPerRank); break;
+    case kReduceGenericBuckets + 0: e = LUMOS_FAST(0); break;
+    case kReduceGenericBuckets + 1: e = LUMOS_FAST(1); break;
+    case kReduceGenericBuckets + 2: e = LUMOS_FAST(2); break;
+    default: e = LUMOS_FAST(3); break;
   }
+#undef LUMOS_GEN
+#undef LUMOS_FAST
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -169,7 +169,9 @@ class DeviceGraph:
         return SimulatedTrace.from_task_arrays(start[:n], fin[:n], span)
 
     def replay_batch(self, spec: ScenarioSpec, start=None, fin=None, ld: int = 0, span=None,
-                     rank_breakdown=None, stream_busy=None, status=None, stream=None) -> None:
+                     rank_breakdown=None, stream_busy=None, status=None, stream=None,
+                     util_bin_width: int = 0, util_covered=None, util_n_bins=None,
+                     delta_abs_sum=None, delta_worst=None) -> None:
         """Raw ts_replay_batch: outputs are caller-owned numpy (host) or torch
         (device or host) buffers; see include/lumos_b200.h for shapes."""
         sc = spec.to_c()
@@ -182,6 +184,12 @@ class DeviceGraph:
         r.rank_breakdown = _ptr(rank_breakdown, N.i64p)
         r.stream_busy = _ptr(stream_busy, N.i64p)
         r.status = _ptr(status, N.i32p)
+        r.util_bin_width = int(util_bin_width)
+        r.util_max_bins = int(util_covered.shape[-1]) if util_covered is not None else 0
+        r.util_covered = _ptr(util_covered, N.i64p)
+        r.util_n_bins = _ptr(util_n_bins, N.i32p)
+        r.delta_abs_sum = _ptr(delta_abs_sum, N.i64p)
+        r.delta_worst = _ptr(delta_worst, N.i64p)
         s = C.c_void_p(stream) if isinstance(stream, int) else stream
         rc = N.lib().ts_replay_batch(self.h, C.byref(sc), C.byref(r), s)
         if rc != N.TS_OK:
@@ -219,10 +227,39 @@ class BatchResult:
     fin: Optional[np.ndarray]
     rank_breakdown: Optional[np.ndarray]  # [count][n_ranks][5]
     stream_busy: Optional[np.ndarray]     # [count][n_streams]
+    util_bin_width: int = 0
+    util_covered: Optional[np.ndarray] = None  # [count][n_ranks][max_bins] covered us
+    util_n_bins: Optional[np.ndarray] = None   # [count] bins of each scenario's window
+    delta_abs_sum: Optional[np.ndarray] = None  # [count] sum |sim_start - original_start|
+    delta_worst: Optional[np.ndarray] = None    # [count][3] {max |delta|, task, delta}
 
     @property
     def makespan(self) -> np.ndarray:
         return self.span[:, 2]
+
+    def utilization(self, s: int, window_start: int, window_end: int) -> np.ndarray:
+        """utilization_by_rank values of scenario s (metrics.cpp:145-150):
+        covered / bin span, the last bin normalised by its actual span.
+        window = [window_start, max(window_end, window_start + makespan))."""
+        w = self.util_bin_width
+        end = max(window_end, window_start + int(self.span[s, 2]))
+        nb = int(self.util_n_bins[s])
+        nb_kept = min(nb, self.util_covered.shape[-1])
+        spans = np.minimum(w, end - (window_start + w * np.arange(nb_kept, dtype=np.int64)))
+        return self.util_covered[s, :, :nb_kept] / spans
+
+    def replay_report(self, s: int, n_tasks: int, reference_makespan: int) -> dict:
+        """compare_replay fields of scenario s (metrics.cpp:189-221), worst
+        list truncated to one entry."""
+        sim = int(self.span[s, 2])
+        zero = reference_makespan == 0
+        return {"reference_makespan": reference_makespan, "simulated_makespan": sim,
+                "relative_error": 0.0 if zero else abs(sim - reference_makespan) / reference_makespan,
+                "zero_reference": zero,
+                "mean_abs_delta": 0.0 if n_tasks == 0 else float(self.delta_abs_sum[s]) / n_tasks,
+                "max_abs_delta": int(self.delta_worst[s, 0]),
+                "worst": [] if self.delta_worst[s, 1] < 0 else
+                [{"task": int(self.delta_worst[s, 1]), "delta": int(self.delta_worst[s, 2])}]}
 
 
 def simulate(graph, device: Optional[int] = None) -> SimulatedTrace:
@@ -232,18 +269,30 @@ def simulate(graph, device: Optional[int] = None) -> SimulatedTrace:
 
 
 def simulate_batch(graph, spec: ScenarioSpec, timestamps: bool = True, breakdown: bool = True,
-                   device: Optional[int] = None) -> BatchResult:
-    """Replay ``spec.count`` scenarios; results in host numpy arrays."""
+                   device: Optional[int] = None, util_bin_width: int = 0,
+                   util_max_bins: int = 0, deltas: bool = False) -> BatchResult:
+    """Replay ``spec.count`` scenarios; results in host numpy arrays.
+    util_bin_width > 0 adds utilization_by_rank bins (util_max_bins per rank);
+    deltas adds the compare_replay start-delta statistics."""
     dg = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
     S = spec.count
     span = np.zeros((S, 3), np.int64)
-    start = fin = bd = busy = None
+    start = fin = bd = busy = util = nbins = dsum = dworst = None
     if timestamps:
         start = np.zeros((dg.n_tasks, S), np.int64)
         fin = np.zeros((dg.n_tasks, S), np.int64)
     if breakdown:
         bd = np.zeros((S, dg.n_ranks, 5), np.int64)
         busy = np.zeros((S, max(1, dg.n_streams)), np.int64)
+    if util_bin_width > 0:
+        util = np.zeros((S, max(1, dg.n_ranks), max(1, util_max_bins)), np.int64)
+        nbins = np.zeros(S, np.int32)
+    if deltas:
+        dsum = np.zeros(S, np.int64)
+        dworst = np.zeros((S, 3), np.int64)
     dg.replay_batch(spec, start=start, fin=fin, ld=S, span=span, rank_breakdown=bd,
-                    stream_busy=busy)
-    return BatchResult(span=span, start=start, fin=fin, rank_breakdown=bd, stream_busy=busy)
+                    stream_busy=busy, util_bin_width=util_bin_width, util_covered=util,
+                    util_n_bins=nbins, delta_abs_sum=dsum, delta_worst=dworst)
+    return BatchResult(span=span, start=start, fin=fin, rank_breakdown=bd, stream_busy=busy,
+                       util_bin_width=util_bin_width, util_covered=util, util_n_bins=nbins,
+                       delta_abs_sum=dsum, delta_worst=dworst)

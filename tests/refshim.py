@@ -123,6 +123,13 @@ def ref():
         lib.ref_breakdown_by_rank.restype = C.c_int
         lib.ref_breakdown_by_rank.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64,
                                               _i64p, C.c_int]
+        lib.ref_utilization_by_rank.restype = C.c_int
+        lib.ref_utilization_by_rank.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int64, C.c_int64,
+                                                C.c_int64, C.POINTER(C.c_double), _i32p, _i32p,
+                                                C.c_int, C.c_int]
+        lib.ref_compare_replay.restype = C.c_int
+        lib.ref_compare_replay.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int32, _i64p,
+                                           C.POINTER(C.c_double)]
         lib.ref_bench_simulate.restype = C.c_double
         lib.ref_bench_simulate.argtypes = [C.c_void_p, C.POINTER(OrcScenarios), C.c_int64,
                                            C.c_int32, _u8p, C.c_int, _i64p]
@@ -215,6 +222,30 @@ class RefGraphHandle:
         k = ref().ref_breakdown_by_rank(self.h, _p(start, _i64p), _p(fin, _i64p), wstart, wend,
                                         _p(out, _i64p), max_ranks)
         return {int(row[0]): tuple(int(x) for x in row[1:]) for row in out[:k]}
+
+    def utilization_by_rank(self, start, fin, wstart, wend, bin_width, max_ranks=1024,
+                            max_bins=4096):
+        """{rank: np.array of bin values} from the reference metrics.cpp:105-155."""
+        vals = np.zeros((max_ranks, max_bins), np.float64)
+        ranks = np.zeros(max_ranks, np.int32)
+        nb = np.zeros(max_ranks, np.int32)
+        k = ref().ref_utilization_by_rank(self.h, _p(start, _i64p), _p(fin, _i64p), wstart, wend,
+                                          bin_width, vals.ctypes.data_as(C.POINTER(C.c_double)),
+                                          _p(ranks, _i32p), _p(nb, _i32p), max_ranks, max_bins)
+        return {int(ranks[i]): vals[i, :nb[i]].copy() for i in range(k)}
+
+    def compare_replay(self, start, fin, worst_n=5):
+        """ReplayReport of the reference compare_replay (metrics.cpp:189-221)."""
+        oi = np.zeros(5 + 2 * worst_n, np.int64)
+        od = np.zeros(2, np.float64)
+        ref().ref_compare_replay(self.h, _p(start, _i64p), _p(fin, _i64p), worst_n,
+                                 _p(oi, _i64p), od.ctypes.data_as(C.POINTER(C.c_double)))
+        nw = int(oi[4])
+        return {"reference_makespan": int(oi[0]), "simulated_makespan": int(oi[1]),
+                "max_abs_delta": int(oi[2]), "zero_reference": bool(oi[3]),
+                "mean_abs_delta": float(od[0]), "relative_error": float(od[1]),
+                "worst": [{"task": int(oi[5 + k]), "delta": int(oi[5 + worst_n + k])}
+                          for k in range(nw)]}
 
     def bench_simulate(self, sc: OrcScenarios, first: int, count: int, cls, threads: int):
         mk = np.zeros(count, np.int64)

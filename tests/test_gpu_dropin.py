@@ -26,3 +26,14 @@ def test_reference_acceptance_gate_on_the_b200_engine():
     m = re.search(r"C9 \w+ .*\[(\d+) events, ([\d.]+) s .*start delta (\d+) us\]", out)
     assert m, out
     assert int(m.group(1)) >= 900000 and float(m.group(2)) <= 60.0 and int(m.group(3)) == 0
+
+
+CHECK = os.path.join(ROOT, "oracle", "_ref", "batch_metrics_check")
+
+
+@pytest.mark.skipif(not os.path.exists(CHECK), reason="batched-API check not built")
+def test_cpp_batched_metrics_match_reference_metrics():
+    # tracesim::b200::simulate_batch with utilization + compare_replay outputs
+    # vs the reference metrics.cpp on tick-oracle replays of the same durations
+    p = subprocess.run([CHECK], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and p.stdout.startswith("PASS"), p.stdout + p.stderr

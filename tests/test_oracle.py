@@ -209,3 +209,25 @@ def test_jitter_formula_exact():
         R.orc().orc_philox2x32_10(task, scen, key, out)
         bits = (out[0] << 32) | out[1]
         assert got == _jitter_exact(d, bits, 0.37)
+
+
+def test_reference_metric_shims_golden():
+    # the checker for the device metric reductions (tests/test_gpu_metrics.py)
+    # is the reference's own metrics.cpp; pin the shim on its unit-test values:
+    # utilization bins test_metrics.cpp:98-109, compare_replay :167-193
+    from test_gpu_parity import _graph
+    g = _graph([(1, 7, 0, 500), (0, 1, 0, 1000), (1, 9, 1000, 250)], edges=[(1, 2)],
+               window=(0, 1500))
+    g.op_class[2] = 1
+    h = R.from_graph(g)
+    rs, rf, _ = h.simulate()
+    util = h.utilization_by_rank(rs, rf, 0, 1500, 1000)
+    assert list(util) == [0] and util[0].tolist() == [0.5, 0.5]
+    g = _graph([(0, 1, 0, 10), (0, 1, 30, 10), (0, 2, 5, 20)], edges=[(0, 1)], window=(0, 40))
+    h = R.from_graph(g)
+    rs, rf, _ = h.simulate()
+    rep = h.compare_replay(rs, rf, worst_n=2)
+    assert rep["reference_makespan"] == 40 and rep["simulated_makespan"] == 20
+    assert rep["max_abs_delta"] == 20 and rep["mean_abs_delta"] == pytest.approx(25.0 / 3)
+    assert rep["worst"] == [{"task": 1, "delta": -20}, {"task": 2, "delta": -5}]
+    assert rep["relative_error"] == pytest.approx(0.5)
