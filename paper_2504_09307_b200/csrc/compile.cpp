@@ -874,6 +874,14 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       for (int k = 0; k < o.op.npred; ++k) o.op.pred[k] = read_slot(o.v_pred[k]);
       for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kSlotOrigin;
       const uint16_t cov_src = (o.op.flags & F_TRACK1) ? read_slot(o.v_cov1_src) : kNoSlot;
+      // the walk reads an F_TRACK1 coverage source after writing the op's
+      // results, so a dying source is released only after they are placed
+      int64_t late_free = -1;
+      if ((o.op.flags & F_TRACK1) && o.v_cov1_src >= 0 &&
+          std::find(dying.begin(), dying.end(), o.v_cov1_src) != dying.end()) {
+        dying.erase(std::remove(dying.begin(), dying.end(), o.v_cov1_src), dying.end());
+        late_free = o.v_cov1_src;
+      }
       if (group_end) flush();
       ensure(o.v_dst >= 0 ? o.v_dst : 0);
       if (o.v_dst >= 0 && o.v_dst < V_ACC && last_use[o.v_dst] <= at &&
@@ -884,10 +892,14 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       if (o.op.kind != OP_SYNC) o.op.x0 = kNoSlot;
       o.op.x1 = kNoSlot;
       if (o.op.flags & F_TRACK1) {
-        o.op.x0 = cov_src;
+        o.op.x0 = cov_src == kNoSlot ? kSlotInf : cov_src;
         o.op.x1 = write_slot(o.v_cov1_dst);
       }
       o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
+      if (late_free >= 0) {
+        free_slots.push(slot_of[late_free]);
+        slot_of[late_free] = kNoSlot;
+      }
     }
     if (std::getenv("LUMOS_DEBUG_SLOTS") && c == 0) {
       // replay the allocation to find the peak live set (debug only)

@@ -35,10 +35,12 @@ constexpr int kMaxClasses = 4;
 constexpr int kCertPerExt = 4;
 // Reserved slots: slot 0 always holds W (the replay origin) and is what unused
 // predecessor fields point at, so every op reads exactly four slots with no
-// branch on the fan-in; slot 1 is a write-only sink for results nobody reads.
+// branch on the fan-in; slot 1 is a write-only sink for results nobody reads;
+// slot 2 holds +inf, the coverage source of an F_TRACK1 op without one.
 constexpr uint16_t kSlotOrigin = 0;
 constexpr uint16_t kSlotTrash = 1;
-constexpr int kFirstSlot = 2;
+constexpr uint16_t kSlotInf = 2;
+constexpr int kFirstSlot = 3;
 // Programs are streamed through shared memory in chunks of kChunk records; no
 // op group (an op plus its auxiliary records) straddles a chunk boundary.
 constexpr int kChunk = 64;

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
 #define SLOTB(boff) (*reinterpret_cast<I64x2*>(slot_base + static_cast<uint32_t>(boff)))
   SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
+  SLOT2(slot_off(kSlotInf)) = I64x2{kMaxI64, kMaxI64};
 
   ThreadScen ts0, ts1;
   init_thread_scen(P.sp, c0, ts0);
@@ -137,23 +138,24 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
       const I64x2 p0 = SLOTB(oa.x), p1 = SLOTB(oa.y);
       const I64x2 p2 = SLOTB(oa.z), p3 = SLOTB(oa.w);
       const uint32_t dst = ob.x;
-      I64x2 cov_src = {kMaxI64, kMaxI64};
-      if ((flags & F_TRACK1) && hi16(w2) != kNoSlot) cov_src = SLOTB(ob.y);
-      I64x2 st, gate;
+      // st = the task's start; fb = what its finish adds the duration to
+      // (max(start, gate) for gated kinds, else the start itself: st >= W)
+      I64x2 st, fb;
       if (kind == OP_NODE || kind == OP_SYNC || kind == OP_START || kind == OP_ACC) {
         st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
-        gate = I64x2{W, W};
+        fb = st;
       } else if (kind == OP_FINISH) {
         st = p0;
-        gate = max2(max2(p1, p2), p3);
+        fb = max2(max2(p0, p1), max2(p2, p3));
       } else if (kind == OP_GATED) {
         const int nfixed = static_cast<int>(cls_b >> 4);
         st = I64x2{W, W};
-        gate = st;
+        I64x2 gate = st;
         if (nfixed > 0) st = max2(st, p0); else gate = max2(gate, p0);
         if (nfixed > 1) st = max2(st, p1); else gate = max2(gate, p1);
         if (nfixed > 2) st = max2(st, p2); else gate = max2(gate, p2);
         gate = max2(gate, p3);
+        fb = max2(st, gate);
       } else {
         continue;  // OP_NOP
       }
@@ -199,6 +201,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         fail0 = fail0 || !cov0;
         fail1 = fail1 || !cov1;
         st = S;
+        fb = S;
         i += n_ext;
       }
       if (kind == OP_START) {
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int cls = cls_b & 15u;
         const int64_t d0 = scenario_duration<kMode>(P.sp, ts0, task, base, cls);
         const int64_t d1 = scenario_duration<kMode>(P.sp, ts1, task, base, cls);
-        const I64x2 fin = {imax(st.x, gate.x) + d0, imax(st.y, gate.y) + d1};
+        const I64x2 fin = {fb.x + d0, fb.y + d1};
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
         if (__builtin_expect((flags & F_SINK) != 0, 0)) {
@@ -236,8 +239,11 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         }
       }
       if (flags & F_TRACK1) {
+        // the source slot outlives this op's results (compile.cpp), so it is
+        // read here; kSlotInf when the kernel has no coverage source
+        const I64x2 cov_src = SLOTB(ob.y);
         SLOTB(ob.z) = I64x2{p0.x >= st.x ? imin(st.x, cov_src.x) : st.x,
-                                p0.y >= st.y ? imin(st.y, cov_src.y) : st.y};
+                            p0.y >= st.y ? imin(st.y, cov_src.y) : st.y};
       } else if (flags & F_TRACK) {
         // coverage of this kernel per watched set (program.hpp, OpCov)
         const int4 xa = buf[4 * (i + 1)], xb = buf[4 * (i + 1) + 1];
