@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   const int64_t W = P.window_start;
 #define SLOT2(off) \
   (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
-#define SLOTB(boff) (*reinterpret_cast<I64x2*>(slot_base + static_cast<uint32_t>(boff)))
+#define SLOTB(boff) \
+  (*static_cast<I64x2*>(__builtin_assume_aligned(slot_base + static_cast<uint32_t>(boff), 16)))
   SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
   SLOT2(slot_off(kSlotInf)) = I64x2{kMaxI64, kMaxI64};
 
