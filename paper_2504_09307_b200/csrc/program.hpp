@@ -58,12 +58,13 @@ LUMOS_HD constexpr uint16_t slot_off(int s) {
 }
 
 enum OpKind : uint8_t {
+  // kinds 0..3 take start = max(W, preds) (the walk tests kind <= OP_ACC)
   OP_NODE = 0,    // start = max(W, preds); fin = start + d
-  OP_GATED = 1,   // start = max(W, preds[0..nfixed)); fin = max(start, preds[nfixed..)) + d
+  OP_SYNC = 1,    // OP_NODE over fixed preds, then static sync edges + certificate
   OP_START = 2,   // start = max(W, preds) -> dst (first half of a collective member)
-  OP_FINISH = 3,  // start = slot[pred0]; fin = max(start, preds[1..)) + d
-  OP_ACC = 4,     // dst = max(preds)  (fan-in > 4 folding; no task)
-  OP_SYNC = 5,    // OP_NODE over fixed preds, then static sync edges + certificate
+  OP_ACC = 3,     // dst = max(preds)  (fan-in > 4 folding; no task)
+  OP_FINISH = 4,  // start = slot[pred0]; fin = max(start, preds[1..)) + d
+  OP_GATED = 5,   // start = max(W, preds[0..nfixed)); fin = max(start, preds[nfixed..)) + d
   OP_NOP = 6,     // padding to a chunk boundary
 };
 

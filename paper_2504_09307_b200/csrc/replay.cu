@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
       // st = the task's start; fb = what its finish adds the duration to
       // (max(start, gate) for gated kinds, else the start itself: st >= W)
       I64x2 st, fb;
-      if (kind == OP_NODE || kind == OP_SYNC || kind == OP_START || kind == OP_ACC) {
+      if (kind <= OP_ACC) {  // OP_NODE, OP_SYNC, OP_START, OP_ACC
         st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
         fb = st;
       } else if (kind == OP_FINISH) {
