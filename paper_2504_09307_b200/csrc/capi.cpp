@@ -510,10 +510,13 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   const bool need_start = want_red || want_delta, need_fin = want_red;
   if ((need_start && !d_start) || (need_fin && !d_fin)) {
     if (!want_ts) {
-      // none requested: sub-batch through an internal scratch tile
-      const size_t budget = size_t(4) << 30;
+      // none requested: sub-batch through an internal scratch tile of up to
+      // half the free device memory (wide tiles keep the walk grid full)
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) cudaGetLastError();
+      const size_t budget = std::max<size_t>(size_t(4) << 30, (free_b + g->scratch_ts.bytes) / 2);
       const size_t per_col = static_cast<size_t>(c.n_tasks) * 16 + 1;
-      size_t cols = std::max<size_t>(128, budget / per_col / 128 * 128);
+      size_t cols = std::max<size_t>(128, budget / per_col / 256 * 256);
       sub = static_cast<int32_t>(std::min<size_t>(cols, static_cast<size_t>(count)));
       CUDA_TRY(g->scratch_ts.reserve(static_cast<size_t>(sub) * per_col));
       s_start = g->scratch_ts.as<int64_t>();
