@@ -200,7 +200,7 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     cudaGetDevice(&g->device);
   }
   const CompiledGraph& c = g->cg;
-  if (!c.des_only && walk_width(c.max_slots) == 0) {
+  if (!c.des_only && walk_width(c.max_slots, false) == 0) {
     const std::string msg = "a component needs " + std::to_string(c.max_slots) +
                             " live values per scenario: more than shared memory holds";
     delete g;
@@ -530,6 +530,21 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     }
   }
 
+  // uint32 offsets from W in the walk when no time can reach W + 2^32 - 1:
+  // per component, sum of the largest possible durations (class scale
+  // mul_div <= d*num/den + 1, jitter <= d*(1+j) + 1, transform.cpp:38-43,
+  // synth.cpp:150-155) bounds every start and finish
+  bool rel32 = false;
+  if (!(sp.mode & kModeExplicit) && !sp.scale_num) {
+    double f = 1.0;
+    if (sp.mode & kModeScale)
+      f *= static_cast<double>(sp.scale_lo + static_cast<int64_t>(sp.scale_span) - 1) /
+           static_cast<double>(sp.scale_den);
+    if (sp.mode & kModeJitter) f *= 1.0 + 0.5 * sp.two_j;
+    const double bound = static_cast<double>(c.max_comp_dur_sum) * f +
+                         3.0 * static_cast<double>(c.max_comp_tasks) + 16.0;
+    rel32 = f >= 0.0 && bound < 4.2e9 && walk_width(c.max_slots, true) > 0;
+  }
   {
     Timed tm(g, stream, 2);
     CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
@@ -562,6 +577,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.span_lo = lo + b0;
     wp.span_hi = hi + b0;
     wp.status = status + b0;
+    wp.rel32 = rel32 ? 1 : 0;
     {
       auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
       wp.vec_store = (wp.ld % 2 == 0) && (bn % 2 == 0) &&

@@ -1052,6 +1052,15 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       if (contiguous) prog_by_hash[h].push_back(prog);
     }
     out.max_slots = std::max(out.max_slots, n_slots);
+    {
+      int64_t sum = 0;
+      for (int32_t t : comp_tasks) {
+        const int64_t dt = d.duration[t] > 0 ? d.duration[t] : 0;
+        sum = sum > INT64_MAX - dt ? INT64_MAX : sum + dt;
+      }
+      out.max_comp_dur_sum = std::max(out.max_comp_dur_sum, sum);
+      out.max_comp_tasks = std::max(out.max_comp_tasks, static_cast<int32_t>(comp_tasks.size()));
+    }
     out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
   }
 

@@ -34,6 +34,12 @@ struct CompiledGraph {
   std::vector<ProgramDesc> programs;
   std::vector<ComponentDesc> comps;
   int32_t max_slots = 0;
+  // largest per-component sum of base durations and task count: with the
+  // scenario's worst-case duration factor they bound every time of a replay
+  // (W + any path <= W + sum of the component's durations), which decides
+  // whether the walk may keep uint32 offsets from W
+  int64_t max_comp_dur_sum = 0;
+  int32_t max_comp_tasks = 0;
   int32_t n_syncs = 0;
   int32_t n_gpu_tasks = 0;
 

@@ -49,7 +49,7 @@ struct WalkParams {
   int64_t* span_hi;
   int32_t* status;
   int32_t vec_store;   // 16-byte output stores allowed (ld, count even; aligned)
-  int32_t pad2;
+  int32_t rel32;       // slot values are uint32 offsets from W (bound proven on the host)
 };
 
 struct ReduceParams {
@@ -119,7 +119,7 @@ size_t des_scratch_bytes(int32_t n, int32_t nl);
 cudaError_t launch_des(const DesParams& p, cudaStream_t stream);
 
 int walk_threads();
-int walk_width(int n_slots);  // walk CTA width for a slot count (0: too many)
+int walk_width(int n_slots, bool rel32);  // walk CTA width for a slot count (0: too many)
 int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,

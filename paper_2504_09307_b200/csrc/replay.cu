@@ -31,26 +31,43 @@ namespace {
 
 constexpr int kThreads = kWalkThreads;  // widest walk CTA; K4/K5 block size
 
-__device__ __forceinline__ uint32_t tid_offset() { return threadIdx.x * 16u; }
 __device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
 // ------------------------------------------------------------------- K1
 // One thread replays two adjacent scenarios (columns c, c+1): the op record is
-// decoded once per pair, each operand is one 16-byte shared load, and each
-// output row is written with one 16-byte streaming store per thread (512
+// decoded once per pair, each operand is one 8- or 16-byte shared load, and
+// each output row is written with one 16-byte streaming store per thread (512
 // contiguous bytes per warp).
-// Shared memory: two program chunks (2 x kChunk x 32 B, refilled one chunk
-// ahead through registers) followed by the slot table [n_slots][kThreads] x 2.
-struct I64x2 {
-  int64_t x, y;
+// Shared memory: two program chunks (2 x kChunk x 64 B, refilled one chunk
+// ahead through registers) followed by the slot table [n_slots][kT] x 2 values.
+//
+// Value type V: int64 absolute times, or uint32 offsets from W when the
+// launch proves every time of every component stays below W + 2^32 - 1 (the
+// sum of the component's largest possible durations bounds any path; checked
+// on the host, capi.cpp).  Offsets halve the slot table and turn the int64
+// max/add chains into single 32-bit instructions; stores add W back.
+template <typename V>
+struct alignas(2 * sizeof(V)) VPair {
+  V x, y;
 };
-__device__ __forceinline__ I64x2 max2(I64x2 a, I64x2 b) { return {imax(a.x, b.x), imax(a.y, b.y)}; }
+template <typename V>
+__device__ __forceinline__ V vmax(V a, V b) { return a > b ? a : b; }
+template <typename V>
+__device__ __forceinline__ V vmin(V a, V b) { return a < b ? a : b; }
+template <typename V>
+__device__ __forceinline__ VPair<V> max2(VPair<V> a, VPair<V> b) {
+  return {vmax(a.x, b.x), vmax(a.y, b.y)};
+}
 
-template <int kT, int kMode, bool kWriteStart, bool kWriteFin>
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V>
 __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
+  using VP = VPair<V>;
+  constexpr bool kRel = sizeof(V) == 4;
   constexpr int kRecPerThread = (kChunk + kT - 1) / kT;  // chunk refill: records per thread
-  constexpr int kShift = kT == 128 ? 4 : kT == 64 ? 3 : 2;  // s*128 -> s*kT*16 bytes
+  // record slot fields hold s * 128; a slot is kT pairs of 2 * sizeof(V) bytes
+  constexpr int kShift = (kT == 128 ? 4 : kT == 64 ? 3 : 2) - (kRel ? 1 : 0);
+  constexpr V kInfV = kRel ? static_cast<V>(0xFFFFFFFFu) : static_cast<V>(kMaxI64);
   static_assert(kT >= 32, "");
   static_assert(kScenPerThread == 2, "pair layout");
   extern __shared__ int4 smem[];
@@ -58,7 +75,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   // (pred[4], dst, x0, x1, x2) widened to byte offsets by the loader, so the
   // walk adds one register per operand address
   int4* opbuf = smem;
-  char* slot_base = reinterpret_cast<char*>(smem + 8 * kChunk) + tid_offset();
+  char* slot_base =
+      reinterpret_cast<char*>(smem + 8 * kChunk) + threadIdx.x * static_cast<uint32_t>(sizeof(VP));
   const int tid = threadIdx.x;
   const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
   const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
@@ -76,12 +94,14 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
   const int64_t W = P.window_start;
+  const V w0 = kRel ? V(0) : static_cast<V>(W);  // the origin in V
+  auto absv = [&](V v) -> int64_t { return kRel ? W + static_cast<int64_t>(v) : static_cast<int64_t>(v); };
 #define SLOT2(off) \
-  (*reinterpret_cast<I64x2*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
+  (*reinterpret_cast<VP*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
 #define SLOTB(boff) \
-  (*static_cast<I64x2*>(__builtin_assume_aligned(slot_base + static_cast<uint32_t>(boff), 16)))
-  SLOT2(slot_off(kSlotOrigin)) = I64x2{W, W};
-  SLOT2(slot_off(kSlotInf)) = I64x2{kMaxI64, kMaxI64};
+  (*static_cast<VP*>(__builtin_assume_aligned(slot_base + static_cast<uint32_t>(boff), sizeof(VP))))
+  SLOT2(slot_off(kSlotOrigin)) = VP{w0, w0};
+  SLOT2(slot_off(kSlotInf)) = VP{kInfV, kInfV};
 
   ThreadScen ts0, ts1;
   init_thread_scen(P.sp, c0, ts0);
@@ -136,12 +156,12 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
       const uint32_t w2 = static_cast<uint32_t>(rb.z);
       // every operand is read before any result is written (results may
       // reuse the slot of an operand that dies at this op)
-      const I64x2 p0 = SLOTB(oa.x), p1 = SLOTB(oa.y);
-      const I64x2 p2 = SLOTB(oa.z), p3 = SLOTB(oa.w);
+      const VP p0 = SLOTB(oa.x), p1 = SLOTB(oa.y);
+      const VP p2 = SLOTB(oa.z), p3 = SLOTB(oa.w);
       const uint32_t dst = ob.x;
       // st = the task's start; fb = what its finish adds the duration to
       // (max(start, gate) for gated kinds, else the start itself: st >= W)
-      I64x2 st, fb;
+      VP st, fb;
       if (kind <= OP_ACC) {  // OP_NODE, OP_SYNC, OP_START, OP_ACC
         st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
         fb = st;
@@ -150,8 +170,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         fb = max2(max2(p0, p1), max2(p2, p3));
       } else if (kind == OP_GATED) {
         const int nfixed = static_cast<int>(cls_b >> 4);
-        st = I64x2{W, W};
-        I64x2 gate = st;
+        st = VP{w0, w0};
+        VP gate = st;
         if (nfixed > 0) st = max2(st, p0); else gate = max2(gate, p0);
         if (nfixed > 1) st = max2(st, p1); else gate = max2(gate, p1);
         if (nfixed > 2) st = max2(st, p2); else gate = max2(gate, p2);
@@ -166,8 +186,8 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
       }
       if (kind == OP_SYNC) {
         // static binding S = max(r_s, finish(k*_w)) and its certificate
-        const I64x2 rs = st;
-        I64x2 S = rs;
+        const VP rs = st;
+        VP S = rs;
         const int n_ext = static_cast<int>(hi16(w2));
         for (int e = 0; e < n_ext; ++e) {
           const int4 xa = buf[4 * (i + 1 + e)];
@@ -188,12 +208,12 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
           for (int k = 0; k < kCertPerExt; ++k) {
             if (k >= n) continue;
             if (f[k] != kNoSlot && cv[k] != kNoSlot) {
-              const I64x2 fk = SLOT2(f[k]), ck = SLOT2(cv[k]);
+              const VP fk = SLOT2(f[k]), ck = SLOT2(cv[k]);
               cov0 = cov0 || (fk.x == S.x && ck.x <= rs.x);
               cov1 = cov1 || (fk.y == S.y && ck.y <= rs.y);
             }
             if (nx[k] != kNoSlot) {
-              const I64x2 nk = SLOT2(nx[k]);
+              const VP nk = SLOT2(nx[k]);
               fail0 = fail0 || nk.x <= S.x;
               fail1 = fail1 || nk.y <= S.y;
             }
@@ -214,37 +234,39 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int cls = cls_b & 15u;
         const int64_t d0 = scenario_duration<kMode>(P.sp, ts0, task, base, cls);
         const int64_t d1 = scenario_duration<kMode>(P.sp, ts1, task, base, cls);
-        const I64x2 fin = {fb.x + d0, fb.y + d1};
+        const VP fin = {static_cast<V>(fb.x + static_cast<V>(d0)),
+                        static_cast<V>(fb.y + static_cast<V>(d1))};
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
         if (__builtin_expect((flags & F_SINK) != 0, 0)) {
-          hi0 = imax(hi0, fin.x);
-          hi1 = imax(hi1, fin.y);
+          hi0 = imax(hi0, absv(fin.x));
+          hi1 = imax(hi1, absv(fin.y));
         }
         const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
         if (vec_store) {
           const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
           if (kWriteStart)
-            __stcs(reinterpret_cast<longlong2*>(sbase + at8), make_longlong2(st.x, st.y));
+            __stcs(reinterpret_cast<longlong2*>(sbase + at8), make_longlong2(absv(st.x), absv(st.y)));
           if (kWriteFin)
-            __stcs(reinterpret_cast<longlong2*>(fbase + at8), make_longlong2(fin.x, fin.y));
+            __stcs(reinterpret_cast<longlong2*>(fbase + at8),
+                   make_longlong2(absv(fin.x), absv(fin.y)));
         } else {
           if (kWriteStart) {
-            __stcs(start_c0 + at, st.x);
-            __stcs(start_c0 + at + dcol, st.y);
+            __stcs(start_c0 + at, absv(st.x));
+            __stcs(start_c0 + at + dcol, absv(st.y));
           }
           if (kWriteFin) {
-            __stcs(fin_c0 + at, fin.x);
-            __stcs(fin_c0 + at + dcol, fin.y);
+            __stcs(fin_c0 + at, absv(fin.x));
+            __stcs(fin_c0 + at + dcol, absv(fin.y));
           }
         }
       }
       if (flags & F_TRACK1) {
         // the source slot outlives this op's results (compile.cpp), so it is
         // read here; kSlotInf when the kernel has no coverage source
-        const I64x2 cov_src = SLOTB(ob.y);
-        SLOTB(ob.z) = I64x2{p0.x >= st.x ? imin(st.x, cov_src.x) : st.x,
-                            p0.y >= st.y ? imin(st.y, cov_src.y) : st.y};
+        const VP cov_src = SLOTB(ob.y);
+        SLOTB(ob.z) = VP{p0.x >= st.x ? vmin(st.x, cov_src.x) : st.x,
+                         p0.y >= st.y ? vmin(st.y, cov_src.y) : st.y};
       } else if (flags & F_TRACK) {
         // coverage of this kernel per watched set (program.hpp, OpCov)
         const int4 xa = buf[4 * (i + 1)], xb = buf[4 * (i + 1) + 1];
@@ -252,17 +274,17 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
                                     {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)}};
         const uint32_t cdst[2] = {lo16(xb.x), hi16(xb.x)};
         const int n_sets = xb.y & 0xFFFF;
-        const I64x2 pv[4] = {p0, p1, p2, p3};
-        I64x2 cvj[kCovSets];
+        const VP pv[4] = {p0, p1, p2, p3};
+        VP cvj[kCovSets];
 #pragma unroll
         for (int j = 0; j < kCovSets; ++j) {
           cvj[j] = st;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (j < n_sets && src[j][k] != kNoSlot) {
-              const I64x2 sv = SLOT2(src[j][k]);
-              if (pv[k].x >= st.x) cvj[j].x = imin(cvj[j].x, sv.x);
-              if (pv[k].y >= st.y) cvj[j].y = imin(cvj[j].y, sv.y);
+              const VP sv = SLOT2(src[j][k]);
+              if (pv[k].x >= st.x) cvj[j].x = vmin(cvj[j].x, sv.x);
+              if (pv[k].y >= st.y) cvj[j].y = vmin(cvj[j].y, sv.y);
             }
         }
 #pragma unroll
@@ -841,32 +863,32 @@ cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, i
 }
 int walk_threads() { return kThreads; }
 
-template <int kT, int kMode, bool kS, bool kF>
+template <int kT, int kMode, bool kS, bool kF, typename V>
 static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
                                  cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kS, kF>,
+    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kS, kF, V>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  replay_walk_kernel<kT, kMode, kS, kF><<<blocks, kT, smem, stream>>>(p);
+  replay_walk_kernel<kT, kMode, kS, kF, V><<<blocks, kT, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int kT, int kMode>
+template <int kT, int kMode, typename V>
 static cudaError_t launch_walk_mode(const WalkParams& p, size_t smem, unsigned blocks,
                                     cudaStream_t stream) {
   const bool s = p.out_start != nullptr, f = p.out_fin != nullptr;
-  if (s && f) return launch_walk_t<kT, kMode, true, true>(p, smem, blocks, stream);
-  if (f) return launch_walk_t<kT, kMode, false, true>(p, smem, blocks, stream);
-  if (s) return launch_walk_t<kT, kMode, true, false>(p, smem, blocks, stream);
-  return launch_walk_t<kT, kMode, false, false>(p, smem, blocks, stream);
+  if (s && f) return launch_walk_t<kT, kMode, true, true, V>(p, smem, blocks, stream);
+  if (f) return launch_walk_t<kT, kMode, false, true, V>(p, smem, blocks, stream);
+  if (s) return launch_walk_t<kT, kMode, true, false, V>(p, smem, blocks, stream);
+  return launch_walk_t<kT, kMode, false, false, V>(p, smem, blocks, stream);
 }
 
-template <int kT>
+template <int kT, typename V>
 static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStream_t stream) {
   const int per_block = kT * kScenPerThread;
   const long long chunks = (p.sp.count + per_block - 1) / per_block;
@@ -874,34 +896,43 @@ static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStrea
   if (blocks <= 0) return cudaSuccess;
   const unsigned nb = static_cast<unsigned>(blocks);
   switch (p.sp.mode) {
-    case 0: return launch_walk_mode<kT, 0>(p, smem, nb, stream);
-    case kModeScale: return launch_walk_mode<kT, kModeScale>(p, smem, nb, stream);
-    case kModeJitter: return launch_walk_mode<kT, kModeJitter>(p, smem, nb, stream);
+    case 0: return launch_walk_mode<kT, 0, V>(p, smem, nb, stream);
+    case kModeScale: return launch_walk_mode<kT, kModeScale, V>(p, smem, nb, stream);
+    case kModeJitter: return launch_walk_mode<kT, kModeJitter, V>(p, smem, nb, stream);
     case kModeScale | kModeJitter:
-      return launch_walk_mode<kT, kModeScale | kModeJitter>(p, smem, nb, stream);
-    default: return launch_walk_mode<kT, kModeExplicit>(p, smem, nb, stream);
+      return launch_walk_mode<kT, kModeScale | kModeJitter, V>(p, smem, nb, stream);
+    default: return launch_walk_mode<kT, kModeExplicit, V>(p, smem, nb, stream);
   }
 }
 
-// shared memory of a walk CTA of t threads
-static size_t walk_smem(int n_slots, int t) {
+// shared memory of a walk CTA of t threads with `vbytes`-byte slot values
+static size_t walk_smem(int n_slots, int t, int vbytes) {
   return 8 * kChunk * sizeof(int4) +
-         static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * 16;
+         static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * 2 * vbytes;
 }
 
-int walk_width(int n_slots) {
+int walk_width(int n_slots, bool rel32) {
   const size_t cap = 227 * 1024;
-  if (walk_smem(n_slots, 128) <= cap / 2) return 128;  // >= 2 CTAs per SM
-  if (walk_smem(n_slots, 64) <= cap / 2) return 64;
-  if (walk_smem(n_slots, 32) <= cap) return 32;
+  const int vb = rel32 ? 4 : 8;
+  if (walk_smem(n_slots, 128, vb) <= cap / 2) return 128;  // >= 2 CTAs per SM
+  if (walk_smem(n_slots, 64, vb) <= cap / 2) return 64;
+  if (walk_smem(n_slots, 32, vb) <= cap) return 32;
   return 0;
 }
 
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
-  const int t = walk_width(n_slots);
-  if (t == 128) return launch_walk_width<128>(p, walk_smem(n_slots, 128), stream);
-  if (t == 64) return launch_walk_width<64>(p, walk_smem(n_slots, 64), stream);
-  if (t == 32) return launch_walk_width<32>(p, walk_smem(n_slots, 32), stream);
+  const bool rel = p.rel32 != 0;
+  const int t = walk_width(n_slots, rel);
+  const int vb = rel ? 4 : 8;
+  if (rel) {
+    if (t == 128) return launch_walk_width<128, uint32_t>(p, walk_smem(n_slots, 128, vb), stream);
+    if (t == 64) return launch_walk_width<64, uint32_t>(p, walk_smem(n_slots, 64, vb), stream);
+    if (t == 32) return launch_walk_width<32, uint32_t>(p, walk_smem(n_slots, 32, vb), stream);
+  } else {
+    if (t == 128) return launch_walk_width<128, int64_t>(p, walk_smem(n_slots, 128, vb), stream);
+    if (t == 64) return launch_walk_width<64, int64_t>(p, walk_smem(n_slots, 64, vb), stream);
+    if (t == 32) return launch_walk_width<32, int64_t>(p, walk_smem(n_slots, 32, vb), stream);
+  }
   return cudaErrorInvalidConfiguration;
 }
 

@@ -424,3 +424,20 @@ def test_reduce_fast_and_generic_ranks():
     _check_batch(h, g, spec, R.OrcScenarios(seed=21, jitter=0.3))
     # and the unmodified graph (every rank on the sweep)
     _check_batch(h0, h0.export(), spec, R.OrcScenarios(seed=21, jitter=0.3))
+
+
+def test_walk_value_width_paths():
+    # the walk keeps uint32 offsets from W when the per-component duration sum
+    # bounds every time below W + 2^32 - 1, else int64: one long task pushes
+    # the same graph onto the int64 path; both must match the reference
+    h0, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h0.export()
+    spec = ScenarioSpec(count=32, first=3, seed=17, jitter=0.2)
+    sc = R.OrcScenarios(seed=17, jitter=0.2)
+    _check_batch(h0, g, spec, sc, every=4)          # uint32 path
+    g2 = h0.export()
+    g2.duration = g2.duration.copy()
+    t = int(np.flatnonzero(g2.task_kind == 1)[-1])  # a late kernel
+    g2.duration[t] = 5_000_000_000                  # > 2^32 us on its own
+    h2 = R.from_graph(g2)
+    _check_batch(h2, g2, spec, sc, every=4)         # int64 path
