@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 2
+#define TS_ABI_VERSION 3
 
 /* error codes (0 = success) */
 enum {
@@ -101,7 +101,25 @@ typedef struct {
   const int32_t* gate_from;
   const int32_t* gate_to;
   const uint8_t* gate_kind;      /* TS_GATE_* */
+  /* Optional retime metadata (Task.meta keys bytes / collective / group_size /
+   * m n k / region / dir, types.hpp:84-86), NULL when absent; needed only by
+   * ts_retime scenarios.  rt_kind classifies each task the way change_hidden
+   * and scale_dp read its metadata (transform.cpp:219-349). */
+  const uint8_t* rt_kind;        /* [n] TS_RT_*                                 */
+  const int64_t* rt_bytes;       /* [n] meta "bytes" (0 when absent)            */
+  const int32_t* rt_group;       /* [n] meta "group_size" (0 when absent)       */
+  const int64_t* rt_mnk;         /* [n][3] meta m, n, k (0 when absent)         */
 } ts_graph_desc;
+
+/* retime classes of a task (transform.cpp:279-349, scale_dp :219-258) */
+enum {
+  TS_RT_NONE = 0,
+  TS_RT_GEMM = 1,       /* GPU compute with m, n, k > 0                        */
+  TS_RT_OPT = 2,        /* GPU compute, region "opt", with bytes               */
+  TS_RT_ALLREDUCE = 3,  /* GPU communication, collective "allreduce", bytes    */
+  TS_RT_P2P_SEND = 4,   /* GPU communication, region "p2p", bytes, dir != recv */
+  TS_RT_P2P_RECV = 5    /* GPU communication, region "p2p", bytes, dir == recv */
+};
 
 typedef struct ts_graph ts_graph;
 
@@ -148,7 +166,26 @@ typedef struct {
   const int32_t* scale_num; /* [count][n_classes] or NULL */
   const int64_t* durations; /* [n_tasks][durations_ld] or NULL */
   int64_t durations_ld;
+  const struct ts_retime* retime; /* per-scenario what-if retime, or NULL */
 } ts_scenarios;
+
+/* Device-side what-if retiming: scenario s replays the
+ * graph apply_whatif would return for a width / data-parallel change that
+ * needs no pipeline rebuild (transform.cpp:713-760): change_hidden
+ * (transform.cpp:279-349) then scale_dp (:219-258), with the analytical cost
+ * model collective_cost_us (cost.cpp:55-62) at that scenario's alpha / beta.
+ * Class scale and jitter then apply to the retimed durations.  All arrays
+ * are host memory, [count] entries (target_model [count][3]).  Errors follow
+ * the reference's TransformError messages (TS_E_INVALID_ARGUMENT). */
+typedef struct ts_retime {
+  const double* alpha_us;       /* [count] cost model alpha (us)              */
+  const double* bytes_per_us;   /* [count] cost model bandwidth (> 0)         */
+  int32_t source_dp;            /* scale_dp: collectives sized for this group  */
+  int32_t pad;
+  const int32_t* target_dp;     /* [count] or NULL: no data-parallel retime   */
+  int64_t source_model[3];      /* change_hidden source {d_model, d_ffn, n_params} */
+  const int64_t* target_model;  /* [count][3] or NULL: no width retime        */
+} ts_retime;
 
 /* Outputs; any pointer may be NULL (not produced).  start/fin are the
  * SimEntry sim_start/sim_end (simulate.hpp:12-17) of every task, stored

@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <optional>
 #include <random>
 #include <string>
 #include <thread>
@@ -30,6 +31,7 @@
 #include "json.hpp"
 #include "oracles.hpp"
 #include "tracesim/build.hpp"
+#include "tracesim/cost.hpp"
 #include "tracesim/metrics.hpp"
 #include "tracesim/pipeline.hpp"
 #include "tracesim/simulate.hpp"
@@ -398,6 +400,87 @@ double ref_bench_simulate(void* h, const orc_scenarios* sc, int64_t first, int32
   }
   for (auto& t : pool) t.join();
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+// ------------------------------------------------------------- what-if retime
+// Per-task retime metadata as the device takes it (ts_graph_desc.rt_*): the
+// TS_RT_* class the reference's change_hidden / scale_dp would apply to the
+// task (transform.cpp:219-349), read with their own strict integer parsing.
+static std::optional<int64_t> shim_meta_i64(const Task& t, const char* key) {
+  auto it = t.meta.find(key);
+  if (it == t.meta.end()) return std::nullopt;
+  try {
+    std::size_t pos = 0;
+    int64_t v = std::stoll(it->second, &pos);
+    if (pos != it->second.size()) return std::nullopt;
+    return v;
+  } catch (const std::exception&) {
+    return std::nullopt;
+  }
+}
+static std::string shim_meta_str(const Task& t, const char* key) {
+  auto it = t.meta.find(key);
+  return it == t.meta.end() ? std::string() : it->second;
+}
+
+int ref_graph_retime_meta(void* h, uint8_t* kind, int64_t* bytes, int32_t* group, int64_t* mnk) {
+  const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+  for (std::size_t i = 0; i < g.tasks.size(); ++i) {
+    const Task& t = g.tasks[i];
+    kind[i] = 0;
+    auto b = shim_meta_i64(t, "bytes");
+    bytes[i] = b ? *b : -1;
+    auto gs = shim_meta_i64(t, "group_size");
+    group[i] = gs ? static_cast<int32_t>(*gs) : 0;
+    const int64_t m = shim_meta_i64(t, "m").value_or(0), n = shim_meta_i64(t, "n").value_or(0),
+                  k = shim_meta_i64(t, "k").value_or(0);
+    mnk[3 * i] = m;
+    mnk[3 * i + 1] = n;
+    mnk[3 * i + 2] = k;
+    if (t.kind != TaskKind::Gpu) continue;
+    if (t.op_class == OpClass::Compute) {
+      if (m > 0 && n > 0 && k > 0) kind[i] = 1;                        // TS_RT_GEMM
+      else if (shim_meta_str(t, "region") == "opt" && b) kind[i] = 2;  // TS_RT_OPT
+    } else if (t.op_class == OpClass::Communication) {
+      if (shim_meta_str(t, "collective") == "allreduce") {
+        kind[i] = 3;  // TS_RT_ALLREDUCE (scale_dp checks bytes itself)
+      } else if (shim_meta_str(t, "region") == "p2p" && b) {
+        kind[i] = shim_meta_str(t, "dir") != "recv" ? 4 : 5;  // TS_RT_P2P_SEND / _RECV
+      }
+    }
+  }
+  return 0;
+}
+
+// apply_whatif's non-structural retime (transform.cpp:741-755): change_hidden
+// (when d_model or d_ffn change) then scale_dp (when the sizes differ), with
+// AnalyticalCostModel(alpha, bytes_per_us).  Returns a new handle or NULL
+// (message in ref_last_error()).
+void* ref_apply_retime(void* h, const int64_t* src_model, const int64_t* tgt_model, int src_dp,
+                       int tgt_dp, double alpha, double bytes_per_us) {
+  try {
+    const ExecutionGraph& g = static_cast<RefGraph*>(h)->g;
+    AnalyticalCostModel model(alpha, bytes_per_us);
+    ExecutionGraph out = g;
+    if (tgt_model) {
+      ModelConfig sm, tm;
+      sm.d_model = static_cast<int>(src_model[0]);
+      sm.d_ffn = static_cast<int>(src_model[1]);
+      sm.n_params = src_model[2];
+      tm.d_model = static_cast<int>(tgt_model[0]);
+      tm.d_ffn = static_cast<int>(tgt_model[1]);
+      tm.n_params = tgt_model[2];
+      out = change_hidden(out, sm, tm, model);
+    }
+    if (src_dp != tgt_dp) out = scale_dp(out, src_dp, tgt_dp, model);
+    auto* r = new RefGraph;
+    r->g = std::move(out);
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
 }
 
 }  // extern "C"

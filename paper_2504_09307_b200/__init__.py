@@ -8,9 +8,10 @@ generator and graph builder (:mod:`.synth`), all over the C ABI of
 from .graph import (COMMUNICATION, COMPUTE, CPU_THREAD, CUDA_STREAM, DEVICE_SYNC, EVENT_SYNC,
                     STREAM_SYNC, DeviceError, ExecutionGraph, GraphError, SimulatedTrace,
                     SimulationError, UnsupportedGraphError)
-from .replay import BatchResult, DeviceGraph, ScenarioSpec, simulate, simulate_batch
+from .replay import BatchResult, DeviceGraph, Retime, ScenarioSpec, simulate, simulate_batch
 
 __all__ = [
+    "Retime",
     "ExecutionGraph", "SimulatedTrace", "SimulationError", "GraphError", "UnsupportedGraphError",
     "DeviceError", "DeviceGraph", "ScenarioSpec", "BatchResult", "simulate", "simulate_batch",
     "CPU_THREAD", "CUDA_STREAM", "STREAM_SYNC", "DEVICE_SYNC", "EVENT_SYNC", "COMPUTE",

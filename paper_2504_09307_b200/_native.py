@@ -35,7 +35,8 @@ class TsGraphDesc(C.Structure):
                 ("rule_watch_off", i32p), ("watch_rank", i32p), ("watch_kind", i32p),
                 ("watch_lane", i32p), ("window_start", C.c_int64), ("window_end", C.c_int64),
                 ("n_gates", C.c_int64), ("gate_from", i32p), ("gate_to", i32p),
-                ("gate_kind", u8p)]
+                ("gate_kind", u8p), ("rt_kind", u8p), ("rt_bytes", i64p), ("rt_group", i32p),
+                ("rt_mnk", i64p)]
 
 
 class TsGraphInfo(C.Structure):
@@ -50,7 +51,14 @@ class TsScenarios(C.Structure):
     _fields_ = [("first", C.c_int64), ("count", C.c_int32), ("flags", C.c_int32),
                 ("seed", C.c_uint64), ("jitter", C.c_double), ("scale_lo", C.c_int32),
                 ("scale_hi", C.c_int32), ("scale_den", C.c_int32), ("n_classes", C.c_int32),
-                ("scale_num", i32p), ("durations", i64p), ("durations_ld", C.c_int64)]
+                ("scale_num", i32p), ("durations", i64p), ("durations_ld", C.c_int64),
+                ("retime", C.c_void_p)]
+
+
+class TsRetime(C.Structure):
+    _fields_ = [("alpha_us", C.POINTER(C.c_double)), ("bytes_per_us", C.POINTER(C.c_double)),
+                ("source_dp", C.c_int32), ("pad", C.c_int32), ("target_dp", i32p),
+                ("source_model", C.c_int64 * 3), ("target_model", i64p)]
 
 
 class TsProfileStats(C.Structure):
@@ -67,7 +75,7 @@ class TsResult(C.Structure):
                 ("delta_abs_sum", i64p), ("delta_worst", i64p)]
 
 
-ABI_VERSION = 2  # TS_ABI_VERSION in include/lumos_b200.h
+ABI_VERSION = 3  # TS_ABI_VERSION in include/lumos_b200.h
 _lib = None
 
 

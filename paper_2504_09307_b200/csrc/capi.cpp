@@ -103,6 +103,11 @@ struct ts_graph {
   ComponentDesc* d_comps = nullptr;
   int32_t* d_comp_order = nullptr;
   int64_t* d_base = nullptr;
+  uint8_t* d_rt_kind = nullptr;  // retime metadata (empty when absent)
+  int64_t* d_rt_bytes = nullptr;
+  int32_t* d_rt_group = nullptr;
+  int64_t* d_rt_mnk = nullptr;
+  DevBuf retime_dur, retime_par;  // retimed durations tile, per-scenario parameters
   uint8_t* d_cls = nullptr;
   uint8_t* d_is_comm = nullptr;
   int32_t* d_rank_stream_off = nullptr;
@@ -224,6 +229,10 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   if (e == cudaSuccess) e = upload(&g->d_comps, c.comps);
   if (e == cudaSuccess) e = upload(&g->d_comp_order, order);
   if (e == cudaSuccess) e = upload(&g->d_base, c.base);
+  if (e == cudaSuccess) e = upload(&g->d_rt_kind, c.rt_kind);
+  if (e == cudaSuccess) e = upload(&g->d_rt_bytes, c.rt_bytes);
+  if (e == cudaSuccess) e = upload(&g->d_rt_group, c.rt_group);
+  if (e == cudaSuccess) e = upload(&g->d_rt_mnk, c.rt_mnk);
   if (e == cudaSuccess) e = upload(&g->d_cls, c.scale_class);
   if (e == cudaSuccess) e = upload(&g->d_is_comm, c.is_comm);
   if (e == cudaSuccess) e = upload(&g->d_rank_stream_off, c.rank_stream_off);
@@ -301,6 +310,8 @@ void ts_graph_destroy(ts_graph* g) {
     for (void* p : {static_cast<void*>(g->d_ops), static_cast<void*>(g->d_progs),
                     static_cast<void*>(g->d_comps), static_cast<void*>(g->d_comp_order),
                     static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
+                    static_cast<void*>(g->d_rt_kind), static_cast<void*>(g->d_rt_bytes),
+                    static_cast<void*>(g->d_rt_group), static_cast<void*>(g->d_rt_mnk),
                     static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
                     static_cast<void*>(g->d_stream_node_off),
                     static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists),
@@ -313,6 +324,8 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_lane_rank), static_cast<void*>(g->d_lane_stream)})
       if (p) cudaFree(p);
     g->des_scratch.release();
+    g->retime_dur.release();
+    g->retime_par.release();
     for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts, &g->delta_scratch})
       b->release();
     for (DevBuf& b : g->stage) b.release();
@@ -409,6 +422,104 @@ static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioPa
   return TS_OK;
 }
 
+// Validates a ts_retime against the graph the way change_hidden / scale_dp
+// reject their inputs (transform.cpp:219-258, 279-349, cost.cpp:55-62) and
+// stages its per-scenario arrays on the device: [alpha][bpu][target_dp][model].
+static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStream_t stream,
+                        RetimeParams& p) {
+  const CompiledGraph& c = g->cg;
+  if (c.rt_kind.empty())
+    return fail(TS_E_INVALID_ARGUMENT, "graph carries no retime metadata (ts_graph_desc.rt_kind)");
+  if (!rt->alpha_us || !rt->bytes_per_us)
+    return fail(TS_E_INVALID_ARGUMENT, "retime needs alpha_us and bytes_per_us per scenario");
+  bool any_dp_change = false, any_hidden = false;
+  for (int32_t s = 0; s < count; ++s) {
+    if (!(rt->bytes_per_us[s] > 0))
+      return fail(TS_E_INVALID_ARGUMENT,
+                  "cost model cannot retime collective: bytes_per_us must be positive");
+    if (rt->target_dp) {
+      const int32_t sd = rt->source_dp, td = rt->target_dp[s];
+      if (sd < 1 || td < 1) return fail(TS_E_INVALID_ARGUMENT, "data-parallel sizes must be >= 1");
+      if (sd != td) {
+        if (sd == 1)
+          return fail(TS_E_INVALID_ARGUMENT,
+                      "source trace has no gradient collectives to rescale; use apply_whatif to "
+                      "introduce them");
+        if (td == 1)
+          return fail(TS_E_INVALID_ARGUMENT,
+                      "cannot drop gradient collectives by retiming; use apply_whatif to rebuild "
+                      "without them");
+        any_dp_change = true;
+      }
+    }
+    if (rt->target_model) {
+      const int64_t* tm = rt->target_model + 3 * static_cast<size_t>(s);
+      if (tm[0] != rt->source_model[0] || tm[1] != rt->source_model[1]) {
+        if (rt->source_model[0] <= 0 || tm[0] <= 0)
+          return fail(TS_E_INVALID_ARGUMENT, "hidden-size rescale needs both model widths");
+        for (int32_t t = 0; t < c.n_tasks; ++t) {
+          const uint8_t k = c.rt_kind[t];
+          if ((k == TS_RT_OPT || k == TS_RT_ALLREDUCE) &&
+              (rt->source_model[2] <= 0 || tm[2] <= 0))
+            return fail(TS_E_INVALID_ARGUMENT,
+                        k == TS_RT_OPT
+                            ? "hidden-size rescale of optimizer work needs n_params on both models"
+                            : "hidden-size rescale of collectives needs n_params on both models");
+          if (k == TS_RT_ALLREDUCE && c.rt_group[t] <= 0)
+            return fail(TS_E_INVALID_ARGUMENT,
+                        "collective task " + std::to_string(t) + " carries no group size");
+        }
+        any_hidden = true;
+      }
+    }
+  }
+  if (any_dp_change) {
+    int changed = 0;
+    for (int32_t t = 0; t < c.n_tasks; ++t)
+      if (c.rt_kind[t] == TS_RT_ALLREDUCE && c.rt_group[t] == rt->source_dp) {
+        if (c.rt_bytes[t] < 0)
+          return fail(TS_E_INVALID_ARGUMENT,
+                      "collective task " + std::to_string(t) + " carries no byte count");
+        ++changed;
+      }
+    if (changed == 0)
+      return fail(TS_E_INVALID_ARGUMENT, "no gradient collectives sized for data-parallel group " +
+                                             std::to_string(rt->source_dp) + " found");
+  }
+  (void)any_hidden;
+  const size_t n = static_cast<size_t>(count);
+  const size_t bytes = n * 8 * 2 + n * 4 + (rt->target_model ? n * 24 : 0) + 64;
+  if (g->retime_par.reserve(bytes) != cudaSuccess)
+    return fail(TS_E_NOMEM, "could not stage retime parameters");
+  char* base = g->retime_par.as<char>();
+  double* d_alpha = reinterpret_cast<double*>(base);
+  double* d_bpu = d_alpha + n;
+  int64_t* d_tm = reinterpret_cast<int64_t*>(d_bpu + n);
+  int32_t* d_tdp = reinterpret_cast<int32_t*>(d_tm + (rt->target_model ? 3 * n : 0));
+  auto cp = [&](void* dst, const void* src, size_t b) {
+    return cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, stream);
+  };
+  cudaError_t e = cp(d_alpha, rt->alpha_us, n * 8);
+  if (e == cudaSuccess) e = cp(d_bpu, rt->bytes_per_us, n * 8);
+  if (e == cudaSuccess && rt->target_model) e = cp(d_tm, rt->target_model, n * 24);
+  if (e == cudaSuccess && rt->target_dp) e = cp(d_tdp, rt->target_dp, n * 4);
+  if (e != cudaSuccess) return fail(TS_E_CUDA, cudaGetErrorString(e));
+  p.base = g->d_base;
+  p.cls = g->d_cls;
+  p.kind = g->d_rt_kind;
+  p.bytes = g->d_rt_bytes;
+  p.group = g->d_rt_group;
+  p.mnk = g->d_rt_mnk;
+  p.alpha = d_alpha;
+  p.bpu = d_bpu;
+  p.target_dp = rt->target_dp ? d_tdp : nullptr;
+  p.target_model = rt->target_model ? d_tm : nullptr;
+  for (int k = 0; k < 3; ++k) p.src_model[k] = rt->source_model[k];
+  p.source_dp = rt->source_dp;
+  p.n_tasks = c.n_tasks;
+  return TS_OK;
+}
+
 int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, void* stream_) {
   if (!g || !sc || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
   if (!g->has_device) return fail(TS_E_CUDA, "graph was compiled without a device");
@@ -420,6 +531,13 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   if (count == 0) return TS_OK;
   if ((out->start || out->fin) && out->ld < count)
     return fail(TS_E_INVALID_ARGUMENT, "ld must be >= count");
+  RetimeParams rtp{};
+  const bool retime = sc->retime != nullptr;
+  if (retime) {
+    if (sp.mode & kModeExplicit)
+      return fail(TS_E_INVALID_ARGUMENT, "retime cannot be combined with explicit durations");
+    if (int rc = retime_stage(g, sc->retime, count, stream, rtp)) return rc;
+  }
   if ((out->util_covered || out->util_n_bins) && out->util_bin_width <= 0)
     return fail(TS_E_INVALID_ARGUMENT, "bin_width must be positive");  // metrics.cpp:107
   if (out->util_covered && out->util_max_bins <= 0)
@@ -503,6 +621,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   // timestamps needed for the reductions but not requested: sub-batch through
   // an internal scratch tile
   int32_t sub = count;
+  bool tile_local = false;  // timestamp pointers address the current tile only
   int64_t* s_start = d_start;
   int64_t* s_fin = d_fin;
   int64_t s_ld = out->ld;
@@ -522,6 +641,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       s_start = g->scratch_ts.as<int64_t>();
       s_fin = s_start + static_cast<size_t>(c.n_tasks) * sub;
       s_ld = sub;
+      tile_local = true;
     } else {
       // one of them requested: the other lives in scratch at the caller's ld
       CUDA_TRY(g->scratch_ts.reserve(ts_bytes + 1));
@@ -534,8 +654,17 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   // per component, sum of the largest possible durations (class scale
   // mul_div <= d*num/den + 1, jitter <= d*(1+j) + 1, transform.cpp:38-43,
   // synth.cpp:150-155) bounds every start and finish
+  // retimed durations: materialised per tile (K4r), the walk reads them
+  if (retime) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) cudaGetLastError();
+    const size_t per_col = static_cast<size_t>(c.n_tasks) * 8 + 1;
+    const size_t cap = std::max<size_t>(128, (free_b + g->retime_dur.bytes) / 4 / per_col / 128 * 128);
+    sub = static_cast<int32_t>(std::min<size_t>(static_cast<size_t>(sub), cap));
+    CUDA_TRY(g->retime_dur.reserve(static_cast<size_t>(sub) * per_col));
+  }
   bool rel32 = false;
-  if (!(sp.mode & kModeExplicit) && !sp.scale_num) {
+  if (!retime && !(sp.mode & kModeExplicit) && !sp.scale_num) {
     double f = 1.0;
     if (sp.mode & kModeScale)
       f *= static_cast<double>(sp.scale_lo + static_cast<int64_t>(sp.scale_span) - 1) /
@@ -564,15 +693,33 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.sp.count = bn;
     if (sp.scale_num) wp.sp.scale_num = sp.scale_num + static_cast<size_t>(b0) * sp.n_classes;
     if (sp.durations) wp.sp.durations = sp.durations + b0;
-    // b0 > 0 only when sub-batching through the scratch tile, whose pointers
-    // are tile-local; otherwise there is one tile at b0 = 0
+    if (retime) {
+      // what-if retime + class scale + jitter of this tile, then an explicit walk
+      RetimeParams rp_ = rtp;
+      rp_.sp = wp.sp;
+      rp_.alpha = rtp.alpha + b0;
+      rp_.bpu = rtp.bpu + b0;
+      if (rtp.target_dp) rp_.target_dp = rtp.target_dp + b0;
+      if (rtp.target_model) rp_.target_model = rtp.target_model + 3 * static_cast<size_t>(b0);
+      rp_.dur = g->retime_dur.as<int64_t>();
+      rp_.ld = bn;
+      {
+        Timed tm(g, stream, 2);
+        CUDA_TRY(launch_retime_durations(rp_, stream));
+      }
+      g_launches++;
+      wp.sp.mode = kModeExplicit;
+      wp.sp.durations = rp_.dur;
+      wp.sp.durations_ld = bn;
+      wp.sp.scale_num = nullptr;
+    }
     if (d_util) {
       const size_t row = static_cast<size_t>(n_ranks) * ubins;
       CUDA_TRY(cudaMemsetAsync(d_util + static_cast<size_t>(b0) * row, 0,
                                static_cast<size_t>(bn) * row * 8, stream));
     }
-    wp.out_start = s_start;
-    wp.out_fin = s_fin;
+    wp.out_start = s_start ? s_start + (tile_local ? 0 : b0) : nullptr;
+    wp.out_fin = s_fin ? s_fin + (tile_local ? 0 : b0) : nullptr;
     wp.ld = s_ld;
     wp.span_lo = lo + b0;
     wp.span_hi = hi + b0;
@@ -797,7 +944,23 @@ int ts_scenario_durations(ts_graph* g, const ts_scenarios* sc, int64_t* dur, int
     staged_num = static_cast<const int32_t*>(tmp_num);
     sp.scale_num = staged_num;
   }
-  CUDA_TRY(launch_durations(sp, g->d_base, g->d_cls, g->cg.n_tasks, d, ld, stream));
+  if (sc->retime) {
+    if (sp.mode & kModeExplicit) {
+      if (tmp) cudaFree(tmp);
+      return fail(TS_E_INVALID_ARGUMENT, "retime cannot be combined with explicit durations");
+    }
+    RetimeParams rtp{};
+    if (int rc = retime_stage(g, sc->retime, sc->count, stream, rtp)) {
+      if (tmp) cudaFree(tmp);
+      return rc;
+    }
+    rtp.sp = sp;
+    rtp.dur = d;
+    rtp.ld = ld;
+    CUDA_TRY(launch_retime_durations(rtp, stream));
+  } else {
+    CUDA_TRY(launch_durations(sp, g->d_base, g->d_cls, g->cg.n_tasks, d, ld, stream));
+  }
   g_launches++;
   if (tmp) {
     CUDA_TRY(cudaMemcpyAsync(dur, d, bytes, cudaMemcpyDeviceToHost, stream));

@@ -1072,6 +1072,19 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
 void build_common(const ts_graph_desc& d, CompiledGraph& out) {
   const int32_t n = d.n_tasks;
   out.base.assign(d.duration, d.duration + n);
+  out.rt_kind.clear();
+  out.rt_bytes.clear();
+  out.rt_group.clear();
+  out.rt_mnk.clear();
+  if (d.rt_kind) {
+    out.rt_kind.assign(d.rt_kind, d.rt_kind + n);
+    out.rt_bytes.assign(n, 0);
+    out.rt_group.assign(n, 0);
+    out.rt_mnk.assign(static_cast<size_t>(n) * 3, 0);
+    if (d.rt_bytes) std::copy(d.rt_bytes, d.rt_bytes + n, out.rt_bytes.begin());
+    if (d.rt_group) std::copy(d.rt_group, d.rt_group + n, out.rt_group.begin());
+    if (d.rt_mnk) std::copy(d.rt_mnk, d.rt_mnk + static_cast<size_t>(n) * 3, out.rt_mnk.begin());
+  }
   out.scale_class.resize(n);
   out.is_comm.resize(n);
   out.n_gpu_tasks = 0;

@@ -47,6 +47,11 @@ struct CompiledGraph {
   std::vector<int64_t> base;
   std::vector<uint8_t> scale_class;
   std::vector<uint8_t> is_comm;
+  // retime metadata (ts_graph_desc.rt_*), empty when the graph carries none
+  std::vector<uint8_t> rt_kind;
+  std::vector<int64_t> rt_bytes;
+  std::vector<int32_t> rt_group;
+  std::vector<int64_t> rt_mnk;  // [n][3]
 
   // reductions: ranks (sorted, = ranks_in(graph), build.cpp:582-590), their
   // CUDA-stream lanes and each stream's kernels in chain (= time) order

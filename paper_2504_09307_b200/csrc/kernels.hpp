@@ -144,6 +144,27 @@ cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, i
                               int64_t w, int32_t* n_bins, int32_t count, cudaStream_t stream);
 cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W, int64_t* span,
                                  int64_t* makespan, int32_t count, cudaStream_t stream);
+// what-if retime of every (task, scenario) duration (ts_retime), then the
+// scenario's class scale and jitter; writes dur[task * ld + s]
+struct RetimeParams {
+  ScenarioParams sp;        // mode without kModeExplicit
+  const int64_t* base;
+  const uint8_t* cls;
+  const uint8_t* kind;      // TS_RT_*
+  const int64_t* bytes;
+  const int32_t* group;
+  const int64_t* mnk;       // [n][3]
+  const double* alpha;      // [count] (device)
+  const double* bpu;        // [count]
+  const int32_t* target_dp; // [count] or null
+  const int64_t* target_model;  // [count][3] or null
+  int64_t src_model[3];
+  int32_t source_dp;
+  int32_t n_tasks;
+  int64_t* dur;
+  int64_t ld;
+};
+cudaError_t launch_retime_durations(const RetimeParams& p, cudaStream_t stream);
 cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
                              int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream);
 // buckets 0..6: event merge by stream count (reduce_bucket); 7..10: the

@@ -23,6 +23,7 @@
 
 #include "device_common.cuh"
 #include "kernels.hpp"
+#include "lumos_b200.h"
 #include "program.hpp"
 
 namespace lumos {
@@ -353,6 +354,74 @@ __global__ void durations_kernel(ScenarioParams sp, const int64_t* __restrict__ 
     dur[static_cast<int64_t>(t) * ld + col] = scenario_duration<-1>(sp, ts, t, base[t], cls[t]);
 }
 
+// ------------------------------------------------------------------- K4r
+// What-if retime (transform.cpp:219-349 through apply_whatif :713-760):
+// change_hidden then scale_dp with the analytical collective cost
+// (cost.cpp:40-62), evaluated in double with explicitly rounded operations in
+// the reference's order, then llround (round half away from zero).
+__device__ __forceinline__ int64_t llround_exact(double t) {
+  if (t >= 0x1.0p52 || t <= -0x1.0p52) return static_cast<int64_t>(t);  // integral
+  const int64_t r = __double2ll_rz(t);
+  const double fr = __dadd_rn(t, -static_cast<double>(r));  // exact (Sterbenz)
+  return fr >= 0.5 ? r + 1 : (fr <= -0.5 ? r - 1 : r);
+}
+// collective_cost_us: max(0, llround(alpha + bytes * scale(c, g) / beta))
+__device__ __forceinline__ int64_t coll_cost(bool allreduce, int64_t bytes, int32_t g,
+                                             double alpha, double bpu) {
+  double scale = 1.0;  // SendRecv
+  if (allreduce) {
+    const double gd = static_cast<double>(g);
+    scale = __ddiv_rn(__dmul_rn(2.0, __dadd_rn(gd, -1.0)), gd);
+  }
+  const double t = __dadd_rn(alpha, __ddiv_rn(__dmul_rn(static_cast<double>(bytes), scale), bpu));
+  const int64_t r = llround_exact(t);
+  return r < 0 ? 0 : r;
+}
+
+__global__ void retime_durations_kernel(RetimeParams P) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= P.sp.count) return;
+  ThreadScen ts;
+  init_thread_scen(P.sp, col, ts);
+  const double alpha = P.alpha[col], bpu = P.bpu[col];
+  const int32_t tdp = P.target_dp ? P.target_dp[col] : P.source_dp;
+  const bool dp = P.target_dp && tdp != P.source_dp;
+  int64_t tm[3] = {P.src_model[0], P.src_model[1], P.src_model[2]};
+  if (P.target_model)
+    for (int k = 0; k < 3; ++k) tm[k] = P.target_model[3 * static_cast<int64_t>(col) + k];
+  // change_hidden is a no-op unless d_model or d_ffn change (transform.cpp:282)
+  const bool hid = P.target_model && (tm[0] != P.src_model[0] || tm[1] != P.src_model[1]);
+  for (int32_t t = blockIdx.y; t < P.n_tasks; t += gridDim.y) {
+    int64_t d = P.base[t];
+    const uint8_t kd = P.kind[t];
+    if (kd != TS_RT_NONE && (hid || dp)) {
+      int64_t bytes = P.bytes[t];
+      if (hid) {
+        if (kd == TS_RT_GEMM) {
+          const int64_t* mnk = P.mnk + 3 * static_cast<int64_t>(t);
+          int64_t nd[3];
+          for (int k = 0; k < 3; ++k)
+            nd[k] = mnk[k] == P.src_model[0] ? tm[0] : (mnk[k] == P.src_model[1] ? tm[1] : mnk[k]);
+          d = mul_div_nonneg(d, nd[0] * nd[1] * nd[2], mnk[0] * mnk[1] * mnk[2], -1);
+        } else if (kd == TS_RT_OPT) {
+          d = mul_div_nonneg(d, tm[2], P.src_model[2], -1);
+        } else if (kd == TS_RT_ALLREDUCE) {
+          bytes = mul_div_nonneg(bytes, tm[2], P.src_model[2], -1);
+          d = coll_cost(true, bytes, P.group[t], alpha, bpu);
+        } else if (kd == TS_RT_P2P_SEND || kd == TS_RT_P2P_RECV) {
+          bytes = mul_div_nonneg(bytes, tm[0], P.src_model[0], -1);
+          if (kd == TS_RT_P2P_SEND) d = coll_cost(false, bytes, 2, alpha, bpu);
+          // a receive keeps its recorded duration (arrival skew), transform.cpp:342
+        }
+      }
+      if (dp && kd == TS_RT_ALLREDUCE && P.group[t] == P.source_dp)
+        d = coll_cost(true, bytes, tdp, alpha, bpu);
+    }
+    P.dur[static_cast<int64_t>(t) * P.ld + col] =
+        scenario_duration<-1>(P.sp, ts, t, d, P.cls[t]);
+  }
+}
+
 // ------------------------------------------------------------------- K5
 constexpr int kMaxStreamsPerRank = 32;
 
@@ -628,8 +697,14 @@ struct Cursor {
   }
 };
 
-constexpr int kFastHA = 8;  // ring half of the compute stream
-constexpr int kFastHC = 2;  // ring half of a comm stream
+#ifndef LUMOS_FAST_HA
+#define LUMOS_FAST_HA 8
+#endif
+#ifndef LUMOS_FAST_HC
+#define LUMOS_FAST_HC 2
+#endif
+constexpr int kFastHA = LUMOS_FAST_HA;  // ring half of the compute stream
+constexpr int kFastHC = LUMOS_FAST_HC;  // ring half of a comm stream
 
 template <int NC>
 constexpr size_t fast_ring_words() {
@@ -947,6 +1022,13 @@ cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W
                                  int64_t* makespan, int32_t count, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
   span_finalize_kernel<<<(count + 255) / 256, 256, 0, stream>>>(lo, hi, W, span, makespan, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_retime_durations(const RetimeParams& p, cudaStream_t stream) {
+  if (p.sp.count <= 0 || p.n_tasks <= 0) return cudaSuccess;
+  dim3 grid((p.sp.count + 127) / 128, p.n_tasks < 4096 ? p.n_tasks : 4096);
+  retime_durations_kernel<<<grid, 128, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

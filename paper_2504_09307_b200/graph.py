@@ -75,6 +75,11 @@ class ExecutionGraph:
     gate_kind: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
     scale_class: Optional[np.ndarray] = None
     names: list = field(default_factory=list)
+    # retime metadata (ts_graph_desc.rt_*; TS_RT_* classes of Task.meta), or None
+    rt_kind: Optional[np.ndarray] = None   # [n] uint8
+    rt_bytes: Optional[np.ndarray] = None  # [n] int64 (-1: no byte count)
+    rt_group: Optional[np.ndarray] = None  # [n] int32
+    rt_mnk: Optional[np.ndarray] = None    # [n][3] int64
 
     def __post_init__(self):
         self.duration = _i64(self.duration)
@@ -100,6 +105,15 @@ class ExecutionGraph:
         self.gate_kind = _u8(self.gate_kind)
         if self.scale_class is not None:
             self.scale_class = _u8(self.scale_class)
+        if self.rt_kind is not None:
+            self.rt_kind = _u8(self.rt_kind)
+            n = self.rt_kind.shape[0]
+            self.rt_bytes = (_i64(self.rt_bytes) if self.rt_bytes is not None
+                             else np.zeros(n, np.int64))
+            self.rt_group = (_i32(self.rt_group) if self.rt_group is not None
+                             else np.zeros(n, np.int32))
+            self.rt_mnk = (np.ascontiguousarray(self.rt_mnk, np.int64).reshape(n, 3)
+                           if self.rt_mnk is not None else np.zeros((n, 3), np.int64))
         self.window_start = int(self.window_start)
         self.window_end = int(self.window_end)
 

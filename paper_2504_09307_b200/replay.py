@@ -67,6 +67,7 @@ class ScenarioSpec:
     scale_num: Optional[object] = None  # [count][n_classes] int32 (numpy or torch)
     durations: Optional[object] = None  # [n_tasks][ld] int64
     durations_ld: int = 0
+    retime: Optional["Retime"] = None   # per-scenario what-if retime (ts_retime)
 
     def to_c(self) -> N.TsScenarios:
         sc = N.TsScenarios()
@@ -81,7 +82,42 @@ class ScenarioSpec:
         if self.durations is not None:
             sc.durations = _ptr(self.durations, N.i64p)
             sc.durations_ld = self.durations_ld or int(self.durations.shape[1])
+        if self.retime is not None:
+            self._rt = self.retime.to_c(self.count)  # kept alive with the spec
+            sc.retime = C.cast(C.pointer(self._rt), C.c_void_p)
         return sc
+
+
+@dataclass
+class Retime:
+    """Device-side what-if retime per scenario (ts_retime): apply_whatif's
+    non-structural width / data-parallel change (transform.cpp:713-760) —
+    change_hidden then scale_dp with the analytical cost model alpha + bytes *
+    scale / beta (cost.cpp:40-62).  Arrays are per scenario (host memory)."""
+    alpha_us: object                      # [count] float64
+    bytes_per_us: object                  # [count] float64
+    source_dp: int = 1
+    target_dp: Optional[object] = None    # [count] int32
+    source_model: tuple = (0, 0, 0)       # (d_model, d_ffn, n_params)
+    target_model: Optional[object] = None  # [count][3] int64
+
+    def to_c(self, count: int) -> N.TsRetime:
+        self._a = np.ascontiguousarray(np.broadcast_to(np.asarray(self.alpha_us, np.float64), (count,)))
+        self._b = np.ascontiguousarray(np.broadcast_to(np.asarray(self.bytes_per_us, np.float64), (count,)))
+        r = N.TsRetime()
+        r.alpha_us = self._a.ctypes.data_as(C.POINTER(C.c_double))
+        r.bytes_per_us = self._b.ctypes.data_as(C.POINTER(C.c_double))
+        r.source_dp = int(self.source_dp)
+        if self.target_dp is not None:
+            self._t = np.ascontiguousarray(np.broadcast_to(np.asarray(self.target_dp, np.int32), (count,)))
+            r.target_dp = self._t.ctypes.data_as(N.i32p)
+        for k in range(3):
+            r.source_model[k] = int(self.source_model[k])
+        if self.target_model is not None:
+            self._m = np.ascontiguousarray(
+                np.broadcast_to(np.asarray(self.target_model, np.int64), (count, 3)))
+            r.target_model = self._m.ctypes.data_as(N.i64p)
+        return r
 
 
 class DeviceGraph:
@@ -123,6 +159,11 @@ class DeviceGraph:
         d.gate_from = _ptr(g.gate_from, N.i32p)
         d.gate_to = _ptr(g.gate_to, N.i32p)
         d.gate_kind = _ptr(g.gate_kind, N.u8p)
+        if g.rt_kind is not None:
+            d.rt_kind = _ptr(g.rt_kind, N.u8p)
+            d.rt_bytes = _ptr(g.rt_bytes, N.i64p) if g.rt_bytes is not None else None
+            d.rt_group = _ptr(g.rt_group, N.i32p) if g.rt_group is not None else None
+            d.rt_mnk = _ptr(g.rt_mnk, N.i64p) if g.rt_mnk is not None else None
         h = C.c_void_p()
         dev = N.DEVICE_NONE if compile_only else (-1 if device is None else int(device))
         rc = N.lib().ts_graph_create(C.byref(d), dev, C.byref(h))

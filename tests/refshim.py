@@ -130,6 +130,11 @@ def ref():
         lib.ref_compare_replay.restype = C.c_int
         lib.ref_compare_replay.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int32, _i64p,
                                            C.POINTER(C.c_double)]
+        lib.ref_graph_retime_meta.restype = C.c_int
+        lib.ref_graph_retime_meta.argtypes = [C.c_void_p, _u8p, _i64p, _i32p, _i64p]
+        lib.ref_apply_retime.restype = C.c_void_p
+        lib.ref_apply_retime.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int, C.c_int, C.c_double,
+                                         C.c_double]
         lib.ref_bench_simulate.restype = C.c_double
         lib.ref_bench_simulate.argtypes = [C.c_void_p, C.POINTER(OrcScenarios), C.c_int64,
                                            C.c_int32, _u8p, C.c_int, _i64p]
@@ -246,6 +251,28 @@ class RefGraphHandle:
                 "mean_abs_delta": float(od[0]), "relative_error": float(od[1]),
                 "worst": [{"task": int(oi[5 + k]), "delta": int(oi[5 + worst_n + k])}
                           for k in range(nw)]}
+
+    def retime_meta(self):
+        """(rt_kind, rt_bytes, rt_group, rt_mnk) arrays of ts_graph_desc from Task.meta."""
+        n = self.export().n
+        kind = np.zeros(n, np.uint8)
+        nb = np.zeros(n, np.int64)
+        grp = np.zeros(n, np.int32)
+        mnk = np.zeros((n, 3), np.int64)
+        ref().ref_graph_retime_meta(self.h, _p(kind, _u8p), _p(nb, _i64p), _p(grp, _i32p),
+                                    _p(mnk, _i64p))
+        return kind, nb, grp, mnk
+
+    def apply_retime(self, src_model=None, tgt_model=None, src_dp=1, tgt_dp=1, alpha=10.0,
+                     bytes_per_us=50000.0):
+        """The reference change_hidden then scale_dp (apply_whatif's retime path)."""
+        sm = np.asarray(src_model if src_model is not None else (0, 0, 0), np.int64)
+        tm = np.asarray(tgt_model, np.int64) if tgt_model is not None else None
+        p = ref().ref_apply_retime(self.h, _p(sm, _i64p), _p(tm, _i64p) if tm is not None else None,
+                                   src_dp, tgt_dp, alpha, bytes_per_us)
+        if not p:
+            raise RefError(3, ref().ref_last_error().decode())
+        return RefGraphHandle(p)
 
     def bench_simulate(self, sc: OrcScenarios, first: int, count: int, cls, threads: int):
         mk = np.zeros(count, np.int64)
