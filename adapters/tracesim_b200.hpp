@@ -21,6 +21,16 @@ struct ScenarioSpec {
   uint64_t seed = 250409307;
   double jitter = 0.0;
   int32_t scale_lo = 0, scale_hi = 0, scale_den = 0;  // den <= 0: no class scaling
+  // What-if retime per scenario (non-empty alpha_us enables it): scenario s
+  // replays apply_whatif's retime of the graph — change_hidden(source_model ->
+  // target_model[s]) then scale_dp(source_dp -> target_dp[s]) with
+  // AnalyticalCostModel(alpha_us[s], bytes_per_us[s]) (transform.cpp:741-755).
+  // Errors throw TransformError with the reference's messages.
+  std::vector<double> alpha_us, bytes_per_us;  // [count]
+  int32_t source_dp = 1;
+  std::vector<int32_t> target_dp;              // [count] or empty
+  int64_t source_model[3] = {0, 0, 0};         // {d_model, d_ffn, n_params}
+  std::vector<int64_t> target_model;           // [count * 3] or empty
 };
 
 struct BatchOptions {

@@ -16,6 +16,7 @@
 #include <limits>
 #include <stdexcept>
 #include <map>
+#include <optional>
 #include <queue>
 #include <sstream>
 #include <string>
@@ -24,6 +25,7 @@
 #include "lumos_b200.h"
 #include "tracesim/simulate.hpp"
 #include "tracesim/trace_parse.hpp"
+#include "tracesim/transform.hpp"
 #include "tracesim_b200.hpp"
 
 namespace tracesim {
@@ -96,11 +98,56 @@ struct Soa {
     desc.watch_lane = watch_lane.data();
     desc.window_start = g.iteration_window.start;
     desc.window_end = g.iteration_window.end;
+    // retime metadata: the TS_RT_* class change_hidden / scale_dp would apply
+    // (transform.cpp:219-349), from Task.meta with strict integer parsing
+    auto meta_i64 = [](const Task& t, const char* key) -> std::optional<int64_t> {
+      auto it = t.meta.find(key);
+      if (it == t.meta.end()) return std::nullopt;
+      try {
+        std::size_t pos = 0;
+        const int64_t v = std::stoll(it->second, &pos);
+        if (pos != it->second.size()) return std::nullopt;
+        return v;
+      } catch (const std::exception&) {
+        return std::nullopt;
+      }
+    };
+    auto meta_str = [](const Task& t, const char* key) {
+      auto it = t.meta.find(key);
+      return it == t.meta.end() ? std::string() : it->second;
+    };
+    for (const Task& t : g.tasks) {
+      const auto b = meta_i64(t, "bytes");
+      const auto gs = meta_i64(t, "group_size");
+      const int64_t m = meta_i64(t, "m").value_or(0), n = meta_i64(t, "n").value_or(0),
+                    k = meta_i64(t, "k").value_or(0);
+      uint8_t kind = TS_RT_NONE;
+      if (t.kind == TaskKind::Gpu && t.op_class == OpClass::Compute) {
+        if (m > 0 && n > 0 && k > 0) kind = TS_RT_GEMM;
+        else if (meta_str(t, "region") == "opt" && b) kind = TS_RT_OPT;
+      } else if (t.kind == TaskKind::Gpu && t.op_class == OpClass::Communication) {
+        if (meta_str(t, "collective") == "allreduce") kind = TS_RT_ALLREDUCE;
+        else if (meta_str(t, "region") == "p2p" && b)
+          kind = meta_str(t, "dir") != "recv" ? TS_RT_P2P_SEND : TS_RT_P2P_RECV;
+      }
+      rt_kind.push_back(kind);
+      rt_bytes.push_back(b ? *b : -1);
+      rt_group.push_back(gs ? static_cast<int32_t>(*gs) : 0);
+      rt_mnk.insert(rt_mnk.end(), {m, n, k});
+    }
+    desc.rt_kind = rt_kind.data();
+    desc.rt_bytes = rt_bytes.data();
+    desc.rt_group = rt_group.data();
+    desc.rt_mnk = rt_mnk.data();
   }
+  std::vector<uint8_t> rt_kind;
+  std::vector<int64_t> rt_bytes, rt_mnk;
+  std::vector<int32_t> rt_group;
 };
 
-[[noreturn]] void rethrow(int rc) {
+[[noreturn]] void rethrow(int rc, bool transform = false) {
   const std::string msg = ts_last_error();
+  if (transform && rc == TS_E_INVALID_ARGUMENT) throw TransformError(msg);
   if (rc == TS_E_GRAPH) throw GraphError(msg);
   if (rc == TS_E_SIMULATION) throw SimulationError(msg);
   throw SimulationError("B200 replay engine: " + msg);
@@ -299,6 +346,17 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   sc.scale_lo = spec.scale_lo;
   sc.scale_hi = spec.scale_hi;
   sc.scale_den = spec.scale_den;
+  ts_retime rt{};
+  const bool retime = !spec.alpha_us.empty();
+  if (retime) {
+    rt.alpha_us = spec.alpha_us.data();
+    rt.bytes_per_us = spec.bytes_per_us.data();
+    rt.source_dp = spec.source_dp;
+    rt.target_dp = spec.target_dp.empty() ? nullptr : spec.target_dp.data();
+    for (int k = 0; k < 3; ++k) rt.source_model[k] = spec.source_model[k];
+    rt.target_model = spec.target_model.empty() ? nullptr : spec.target_model.data();
+    sc.retime = &rt;
+  }
   ts_result res{};
   res.start = o.timestamps ? r.start.data() : nullptr;
   res.fin = o.timestamps ? r.fin.data() : nullptr;
@@ -321,7 +379,7 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
     res.delta_abs_sum = r.delta_abs_sum.data();
     res.delta_worst = r.delta_worst.data();
   }
-  if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc);
+  if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc, retime);
   return r;
 }
 

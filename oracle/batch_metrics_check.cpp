@@ -19,6 +19,8 @@
 #include "tracesim/metrics.hpp"
 #include "tracesim/synth.hpp"
 #include "tracesim/trace_parse.hpp"
+#include "tracesim/transform.hpp"
+#include "tracesim/cost.hpp"
 #include "tracesim_b200.hpp"
 
 using namespace tracesim;
@@ -79,7 +81,60 @@ int main() {
                               a.worst[0].simulated_start != b.worst[0].simulated_start)))
       ++bad;
   }
-  std::printf("%s: %d scenarios, %zu tasks, %d mismatches\n", bad ? "FAIL" : "PASS", spec.count,
-              g.tasks.size(), bad);
+  // what-if retime through the C++ API vs the reference transforms
+  // (change_hidden then scale_dp, transform.cpp:741-755) replayed by the tick oracle
+  b200::ScenarioSpec rs;
+  rs.count = 6;
+  rs.source_dp = 2;
+  rs.source_model[0] = 1024;
+  rs.source_model[1] = 4096;
+  rs.source_model[2] = 350000000;
+  const int tdp[6] = {2, 4, 8, 2, 4, 16};
+  const int64_t tm[6][3] = {{1024, 4096, 350000000}, {1536, 6144, 780000000},
+                            {2048, 8192, 1380000000}, {1024, 8192, 600000000},
+                            {1024, 4096, 350000000}, {1536, 4096, 500000000}};
+  for (int s = 0; s < rs.count; ++s) {
+    rs.alpha_us.push_back(s % 2 ? 10.0 : 4.5);
+    rs.bytes_per_us.push_back(s < 3 ? 50000.0 : 22222.2);
+    rs.target_dp.push_back(tdp[s]);
+    for (int k = 0; k < 3; ++k) rs.target_model.push_back(tm[s][k]);
+  }
+  b200::BatchOptions ro;
+  ro.timestamps = true;
+  const b200::BatchResult rr = b200::simulate_batch(g, rs, ro);
+  int bad_rt = 0;
+  for (int s = 0; s < rs.count; ++s) {
+    AnalyticalCostModel model(rs.alpha_us[s], rs.bytes_per_us[s]);
+    ModelConfig sm, tmc;
+    sm.d_model = 1024;
+    sm.d_ffn = 4096;
+    sm.n_params = 350000000;
+    tmc.d_model = static_cast<int>(tm[s][0]);
+    tmc.d_ffn = static_cast<int>(tm[s][1]);
+    tmc.n_params = tm[s][2];
+    ExecutionGraph gt = change_hidden(g, sm, tmc, model);
+    if (tdp[s] != 2) gt = scale_dp(gt, 2, tdp[s], model);
+    const SimulatedTrace sim = oracle::tick_simulate(gt);
+    std::vector<int64_t> st(g.tasks.size());
+    for (const auto& e : sim.entries) st[e.task_id] = e.sim_start;
+    for (std::size_t t = 0; t < g.tasks.size(); ++t)
+      if (st[t] != rr.start[t * rs.count + s]) {
+        ++bad_rt;
+        break;
+      }
+    if (sim.makespan != rr.span[3 * s + 2]) ++bad_rt;
+  }
+  bool threw = false;
+  try {
+    b200::ScenarioSpec e1 = rs;
+    e1.target_dp.assign(rs.count, 1);
+    b200::simulate_batch(g, e1, ro);
+  } catch (const TransformError& e) {
+    threw = std::string(e.what()).find("cannot drop gradient collectives") != std::string::npos;
+  }
+  if (!threw) ++bad_rt;
+  bad += bad_rt;
+  std::printf("%s: %d scenarios, %zu tasks, %d mismatches (retime: %d scenarios, %d)\n",
+              bad ? "FAIL" : "PASS", spec.count, g.tasks.size(), bad, rs.count, bad_rt);
   return bad ? 1 : 0;
 }
