@@ -92,6 +92,12 @@ ts_graph_desc HostGraph::desc() const {
   d.gate_from = gate_from.data();
   d.gate_to = gate_to.data();
   d.gate_kind = gate_kind.data();
+  if (!rt_kind.empty() && rt_kind.size() == duration.size()) {
+    d.rt_kind = rt_kind.data();
+    d.rt_bytes = rt_bytes.data();
+    d.rt_group = rt_group.data();
+    d.rt_mnk = rt_mnk.data();
+  }
   return d;
 }
 

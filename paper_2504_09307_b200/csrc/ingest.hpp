@@ -63,6 +63,11 @@ struct HostGraph {
   std::vector<uint8_t> gate_kind;
   std::vector<int32_t> name;      // per task: index into the shared Names
   std::vector<int64_t> op_index;  // per task: generator cost index (-1 = none)
+  // retime metadata (ts_graph_desc.rt_*), empty when unknown
+  std::vector<uint8_t> rt_kind;
+  std::vector<int64_t> rt_bytes;
+  std::vector<int32_t> rt_group;
+  std::vector<int64_t> rt_mnk;
   int32_t n_diagnostics = 0;
 
   int32_t n() const { return static_cast<int32_t>(duration.size()); }

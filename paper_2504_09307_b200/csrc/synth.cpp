@@ -49,9 +49,21 @@ int64_t collective_cost_us(Coll c, int64_t bytes, int group, double alpha, doubl
   return std::max<int64_t>(0, llr(t));
 }
 
+// retime metadata of a kernel: what the reference generator puts in the
+// event args (synth.cpp:46-48 m/n/k; :122-124 allreduce bytes / collective /
+// group_size; :133 optimizer bytes with region "opt", pipeline.cpp:297;
+// pipeline.cpp:162-166 p2p region / dir / bytes), classified as TS_RT_*
+struct KMeta {
+  uint8_t kind = TS_RT_NONE;
+  int64_t bytes = -1;
+  int32_t group = 0;
+  int64_t m = 0, n = 0, k = 0;
+};
+
 struct KSpec {
   int32_t name;
   int64_t dur;
+  KMeta meta{};
 };
 
 struct StageSpec {
@@ -64,6 +76,7 @@ struct PSpec {
   std::vector<StageSpec> stages;
   int64_t launch = 5, record = 2, wait = 2, sync = 5;
   int64_t p2p_send = 0, p2p_recv_base = 0;
+  int64_t act_bytes = 0;  // p2p transfer size (formulas::activation_bytes)
   int64_t origin = 0;
   int compute_stream = 7, reduce_stream = 9, p2p_stream = 11;
   int main_thread = 100, helper_thread = 200;
@@ -129,6 +142,7 @@ class Builder {
   }
 
   std::vector<GenEvent> events;
+  std::vector<KMeta> kmeta;  // by kernel cost index (op_index)
   std::vector<std::pair<int64_t, int64_t>> edges;             // estimate graph, event ids
   std::vector<std::tuple<int64_t, int64_t, uint8_t>> gates;  // (from, to, kind)
   int64_t end = 0;
@@ -156,6 +170,10 @@ class Builder {
     op.cpu_index = op_index_;
     op.cpu_dur = cost(s_.launch);
     op.kernel_index = op_index_;
+    if (k.meta.kind != TS_RT_NONE) {
+      if (kmeta.size() <= static_cast<size_t>(op_index_)) kmeta.resize(op_index_ + 1);
+      kmeta[op_index_] = k.meta;
+    }
     op.kernel_dur = cost(k.dur);
     op.kname = k.name;
     op.corr = next_corr_++;
@@ -191,7 +209,10 @@ class Builder {
 
   void emit_recv(std::vector<POp>& ops, bool fwd, int stage, int dp, int mb) {
     int from = fwd ? stage - 1 : stage + 1;
-    POp r = launch({n_sendrecv_, s_.p2p_recv_base});
+    KMeta rm;
+    rm.kind = TS_RT_P2P_RECV;
+    rm.bytes = s_.act_bytes;
+    POp r = launch({n_sendrecv_, s_.p2p_recv_base, rm});
     r.stream = s_.p2p_stream;
     r.recv_key = key(1, fwd, from, dp, mb);
     ops.push_back(r);
@@ -205,7 +226,10 @@ class Builder {
     int64_t ev = rec.event_id;
     ops.push_back(rec);
     ops.push_back(wait(s_.p2p_stream, ev));
-    POp snd = launch({n_sendrecv_, s_.p2p_send});
+    KMeta sm;
+    sm.kind = TS_RT_P2P_SEND;
+    sm.bytes = s_.act_bytes;
+    POp snd = launch({n_sendrecv_, s_.p2p_send, sm});
     snd.stream = s_.p2p_stream;
     snd.send_key = key(1, fwd, stage, dp, mb);
     ops.push_back(snd);
@@ -473,10 +497,16 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
   const int64_t t = sp.tokens_per_microbatch, d = sp.d_model, f = sp.d_ffn;
   const int64_t act = t * d * 2;  // formulas::activation_bytes (cost.cpp:83-85)
   ps.p2p_send = collective_cost_us(SENDRECV, act, 2, sp.alpha_us, sp.bytes_per_us);
+  ps.act_bytes = act;
   ps.p2p_recv_base = sp.p2p_recv_base_us;
   auto gemm = [&](const char* name, int64_t m, int64_t n, int64_t k, double factor) {
     int64_t base = gemm_scaled_us(sp.gemm_ref_us, sp.gemm_ref_mnk, 1, 1, m, n, k);
-    return KSpec{names.get(name), llr(static_cast<double>(base) * factor)};
+    KMeta g;
+    g.kind = TS_RT_GEMM;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    return KSpec{names.get(name), llr(static_cast<double>(base) * factor), g};
   };
   std::vector<KSpec> lf{gemm("gemm_qkv", t, d, d, 1.0), {names.get("attn_core"), sp.attn_misc_us},
                         gemm("gemm_mlp", t, f, d, 1.0)};
@@ -502,14 +532,23 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
     int64_t rbytes = layer_bytes * per_stage;  // synth_stage_reduce_bytes (synth.cpp:61-69)
     if (s == 0) rbytes += vocab_bytes;
     if (s == sp.pp - 1) rbytes += vocab_bytes;
+    KMeta ar;
+    ar.kind = TS_RT_ALLREDUCE;
+    ar.bytes = rbytes;
+    ar.group = sp.dp;
     if (sp.dp > 1)
       st.reduce.push_back({names.get("ncclDevKernel_AllReduce_Sum_f16"),
                            collective_cost_us(ALLREDUCE, rbytes, sp.dp, sp.alpha_us,
-                                              sp.bytes_per_us)});
+                                              sp.bytes_per_us),
+                           ar});
+    KMeta om;
+    om.kind = TS_RT_OPT;
+    om.bytes = rbytes;
     st.optimizer.push_back(
-        {names.get("adam_step"), llr(static_cast<double>(sp.optimizer_ref_us) *
-                                     static_cast<double>(rbytes) /
-                                     static_cast<double>(sp.optimizer_ref_bytes))});
+        {names.get("adam_step"),
+         llr(static_cast<double>(sp.optimizer_ref_us) * static_cast<double>(rbytes) /
+             static_cast<double>(sp.optimizer_ref_bytes)),
+         om});
     ps.stages.push_back(std::move(st));
   }
   return ps;
@@ -685,6 +724,25 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
   } else if (sp.estimate) {
     err = "estimate graphs couple ranks; slice_rank is not supported";
     return TS_E_INVALID_ARGUMENT;
+  }
+  // retime metadata per task through its generator cost index
+  {
+    const int32_t n = G.n();
+    G.rt_kind.assign(n, TS_RT_NONE);
+    G.rt_bytes.assign(n, -1);
+    G.rt_group.assign(n, 0);
+    G.rt_mnk.assign(static_cast<size_t>(n) * 3, 0);
+    for (int32_t t = 0; t < n; ++t) {
+      const int64_t oi = G.op_index[t];
+      if (G.task_kind[t] != 1 || oi < 0 || static_cast<size_t>(oi) >= b.kmeta.size()) continue;
+      const KMeta& km = b.kmeta[oi];
+      G.rt_kind[t] = km.kind;
+      G.rt_bytes[t] = km.bytes;
+      G.rt_group[t] = km.group;
+      G.rt_mnk[3 * static_cast<size_t>(t)] = km.m;
+      G.rt_mnk[3 * static_cast<size_t>(t) + 1] = km.n;
+      G.rt_mnk[3 * static_cast<size_t>(t) + 2] = km.k;
+    }
   }
   out.n_ops = b.events.empty() ? 0 : 0;
   int64_t max_idx = -1;

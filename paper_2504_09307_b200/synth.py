@@ -120,6 +120,11 @@ def _from_host(h, names: bool) -> tuple:
         window_end=d.window_end, gate_from=_arr(d.gate_from, d.n_gates, np.int32),
         gate_to=_arr(d.gate_to, d.n_gates, np.int32),
         gate_kind=_arr(d.gate_kind, d.n_gates, np.uint8))
+    if d.rt_kind:
+        g.rt_kind = _arr(d.rt_kind, n, np.uint8)
+        g.rt_bytes = _arr(d.rt_bytes, n, np.int64)
+        g.rt_group = _arr(d.rt_group, n, np.int32)
+        g.rt_mnk = _arr(d.rt_mnk, 3 * n, np.int64).reshape(n, 3)
     op_index = np.zeros(max(1, n), np.int64)
     L.ts_host_graph_op_index(h, op_index.ctypes.data_as(N.i64p))
     nm = []

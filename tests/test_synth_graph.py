@@ -242,3 +242,19 @@ def test_estimate_graph_with_hook_matches_build_pipeline(shape):
         start, fin = longest_path_with_gates(g, dur)
         ref, _ = _ref_pipeline(R.synth_spec(pp=pp, dp=dp, m=m, layers=layers), hook)
         assert _my_lane_sequences(g, start, fin) == ref
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 4), (2, 2, 4), (4, 1, 8), (2, 4, 4)])
+def test_generator_retime_metadata_matches_reference(shape):
+    # the per-task retime metadata (ts_graph_desc.rt_*) our generator attaches
+    # equals what the reference's Task.meta yields (synth.cpp:46-48, 122-133,
+    # pipeline.cpp:162-166, 297), task for task
+    pp, dp, m = shape
+    sg = generate_graph(SynthSpec(pp=pp, dp=dp, num_microbatches=m, n_layers=4))
+    h, _ = R.generate(R.synth_spec(pp=pp, dp=dp, m=m, layers=4))
+    kind, nbytes, group, mnk = h.retime_meta()
+    g = sg.graph
+    assert np.array_equal(g.rt_kind, kind)
+    assert np.array_equal(g.rt_bytes, nbytes)
+    assert np.array_equal(g.rt_group, group)
+    assert np.array_equal(g.rt_mnk, mnk)
