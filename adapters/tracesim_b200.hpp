@@ -9,6 +9,7 @@
 
 #include "tracesim/build.hpp"
 #include "tracesim/metrics.hpp"
+#include "tracesim/simulate.hpp"
 
 namespace tracesim::b200 {
 
@@ -65,5 +66,15 @@ std::map<int, UtilizationSeries> utilization_by_rank(const BatchResult& r, std::
                                                      IterationWindow window);
 // compare_replay with the worst list cut to one task (the batch keeps one).
 ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, std::size_t s);
+
+// Scenario s of a batch run with timestamps as a SimulatedTrace (entries in
+// (sim_start, task_id) order, simulate.hpp:12-24) — e.g. for
+// simulated_to_chrome_json (simulate.hpp:55) to audit a scenario visually.
+SimulatedTrace scenario_trace(const ExecutionGraph& graph, const BatchResult& r, std::size_t s);
+// Replays only the listed global scenario ids of `spec` (a scenario's
+// durations are a pure function of its id, so these equal the same ids of any
+// larger batch) and returns their traces; one compiled graph for all ids.
+std::vector<SimulatedTrace> replay_scenarios(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                                             const std::vector<int64_t>& ids);
 
 }  // namespace tracesim::b200

@@ -428,6 +428,70 @@ ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, st
   return rep;
 }
 
+SimulatedTrace scenario_trace(const ExecutionGraph& graph, const BatchResult& r, std::size_t s) {
+  const std::size_t S = r.span.size() / 3, n = graph.tasks.size();
+  if (r.start.size() != n * S || r.fin.size() != n * S || s >= S)
+    throw std::invalid_argument("scenario_trace needs a batch run with timestamps");
+  SimulatedTrace out;
+  out.entries.reserve(n);
+  for (std::size_t i = 0; i < n; ++i)
+    out.entries.push_back({static_cast<TaskId>(i), r.start[i * S + s], r.fin[i * S + s],
+                           graph.tasks[i].processor});
+  std::sort(out.entries.begin(), out.entries.end(), [](const SimEntry& a, const SimEntry& b) {
+    return std::pair(a.sim_start, a.task_id) < std::pair(b.sim_start, b.task_id);
+  });
+  out.start = r.span[3 * s];
+  out.end = r.span[3 * s + 1];
+  out.makespan = r.span[3 * s + 2];
+  return out;
+}
+
+std::vector<SimulatedTrace> replay_scenarios(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                                             const std::vector<int64_t>& ids) {
+  for (const ValidationIssue& issue : validate_graph(graph))
+    if (issue.error) throw SimulationError("invalid graph: " + issue.message);
+  Handle h(graph);
+  const std::size_t n = graph.tasks.size();
+  std::vector<SimulatedTrace> out;
+  std::vector<int64_t> start(n), fin(n), span(3);
+  for (int64_t id : ids) {
+    ts_scenarios sc{};
+    sc.first = id;
+    sc.count = 1;
+    sc.seed = spec.seed;
+    sc.jitter = spec.jitter;
+    sc.scale_lo = spec.scale_lo;
+    sc.scale_hi = spec.scale_hi;
+    sc.scale_den = spec.scale_den;
+    ts_retime rt{};
+    const bool retime = !spec.alpha_us.empty();
+    if (retime) {  // per-scenario retime arrays are indexed from spec.first
+      const std::size_t k = static_cast<std::size_t>(id - spec.first);
+      if (id < spec.first || k >= spec.alpha_us.size())
+        throw std::invalid_argument("scenario id outside the retime arrays");
+      rt.alpha_us = &spec.alpha_us[k];
+      rt.bytes_per_us = &spec.bytes_per_us[k];
+      rt.source_dp = spec.source_dp;
+      rt.target_dp = spec.target_dp.empty() ? nullptr : &spec.target_dp[k];
+      for (int j = 0; j < 3; ++j) rt.source_model[j] = spec.source_model[j];
+      rt.target_model = spec.target_model.empty() ? nullptr : &spec.target_model[3 * k];
+      sc.retime = &rt;
+    }
+    ts_result res{};
+    res.start = start.data();
+    res.fin = fin.data();
+    res.ld = 1;
+    res.span = span.data();
+    if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc, retime);
+    BatchResult one;
+    one.start = start;
+    one.fin = fin;
+    one.span = span;
+    out.push_back(scenario_trace(graph, one, 0));
+  }
+  return out;
+}
+
 }  // namespace b200
 
 }  // namespace tracesim

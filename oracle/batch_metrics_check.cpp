@@ -17,6 +17,7 @@
 #include "oracles.hpp"
 #include "tracesim/build.hpp"
 #include "tracesim/metrics.hpp"
+#include "tracesim/simulate.hpp"
 #include "tracesim/synth.hpp"
 #include "tracesim/trace_parse.hpp"
 #include "tracesim/transform.hpp"
@@ -123,6 +124,24 @@ int main() {
         break;
       }
     if (sim.makespan != rr.span[3 * s + 2]) ++bad_rt;
+  }
+  // selected-scenario traces (for simulated_to_chrome_json) equal the batch's
+  {
+    const std::vector<int64_t> ids = {spec.first + 3, spec.first + 17};
+    b200::BatchOptions to;
+    to.timestamps = true;
+    const b200::BatchResult full = b200::simulate_batch(g, spec, to);
+    const auto traces = b200::replay_scenarios(g, spec, ids);
+    for (std::size_t q = 0; q < ids.size(); ++q) {
+      const SimulatedTrace a = b200::scenario_trace(g, full, static_cast<std::size_t>(ids[q] - spec.first));
+      const SimulatedTrace& b = traces[q];
+      bool same = a.makespan == b.makespan && a.entries.size() == b.entries.size();
+      for (std::size_t i = 0; same && i < a.entries.size(); ++i)
+        same = a.entries[i].task_id == b.entries[i].task_id &&
+               a.entries[i].sim_start == b.entries[i].sim_start &&
+               a.entries[i].sim_end == b.entries[i].sim_end;
+      if (!same || simulated_to_chrome_json(g, b).size() < 100) ++bad;
+    }
   }
   bool threw = false;
   try {

@@ -289,6 +289,36 @@ class BatchResult:
         spans = np.minimum(w, end - (window_start + w * np.arange(nb_kept, dtype=np.int64)))
         return self.util_covered[s, :, :nb_kept] / spans
 
+    def trace(self, s: int) -> SimulatedTrace:
+        """Scenario s as a SimulatedTrace (needs a batch run with timestamps)."""
+        if self.start is None or self.fin is None:
+            raise ValueError("trace() needs a batch run with timestamps=True")
+        return SimulatedTrace.from_task_arrays(self.start[:, s], self.fin[:, s], self.span[s])
+
+    def chrome_trace(self, graph, s: int) -> str:
+        """Scenario s as Chrome trace-event JSON for visual audit, in the layout
+        of chrome_json / simulated_to_chrome_json (trace_parse.cpp:230-256,
+        simulate.cpp:349-382): one "X" event per task, kernels on their stream.
+        Names come from graph.names when present; args carry the stream only
+        (the C++ drop-in's simulated_to_chrome_json also emits Task.meta)."""
+        import json
+        g = graph if isinstance(graph, ExecutionGraph) else ExecutionGraph.from_any(graph)
+        tr = self.trace(s)
+        out = ['{"schema_version":1,"traceEvents":[']
+        first = True
+        for tid, a, b in zip(tr.task_id.tolist(), tr.sim_start.tolist(), tr.sim_end.tolist()):
+            gpu = int(g.task_kind[tid]) == 1
+            cat = "kernel" if gpu else ("cuda_runtime" if int(g.op_class[tid]) in (2, 3, 4, 5)
+                                        else "cpu_op")
+            ev = {"name": g.names[tid] if g.names else f"task{tid}", "cat": cat, "ph": "X",
+                  "ts": a, "dur": b - a, "pid": int(g.rank[tid]), "tid": int(g.lane[tid])}
+            if gpu:
+                ev["args"] = {"stream": int(g.lane[tid])}
+            out.append(("" if first else ",") + json.dumps(ev, separators=(",", ":")) + "\n")
+            first = False
+        out.append("]}\n")
+        return "".join(out)
+
     def replay_report(self, s: int, n_tasks: int, reference_makespan: int) -> dict:
         """compare_replay fields of scenario s (metrics.cpp:189-221), worst
         list truncated to one entry."""

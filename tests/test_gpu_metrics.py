@@ -156,3 +156,25 @@ def test_util_without_timestamps_tiles():
     assert np.array_equal(full.util_n_bins, lean.util_n_bins)
     assert np.array_equal(full.delta_abs_sum, lean.delta_abs_sum)
     assert np.array_equal(full.delta_worst, lean.delta_worst)
+
+
+def test_scenario_trace_and_chrome_export():
+    # a selected scenario of a batch as a SimulatedTrace
+    # (entries in (sim_start, task_id) order like simulate()) and as Chrome
+    # trace-event JSON for visual audit
+    import json
+    h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h.export(names=True)
+    spec = ScenarioSpec(count=8, first=100, seed=3, jitter=0.2)
+    res = simulate_batch(g, spec)
+    rs, rf, rspan = h.simulate(R.orc_durations(g, R.OrcScenarios(seed=3, jitter=0.2), 105))
+    tr = res.trace(5)
+    order = np.lexsort((np.arange(g.n), rs))
+    assert tr.task_id.tolist() == order.tolist()
+    assert tr.sim_start.tolist() == rs[order].tolist() and tr.sim_end.tolist() == rf[order].tolist()
+    assert (tr.start, tr.end, tr.makespan) == tuple(int(x) for x in rspan)
+    doc = json.loads(res.chrome_trace(g, 5))
+    evs = doc["traceEvents"]
+    assert len(evs) == g.n and doc["schema_version"] == 1
+    assert [e["ts"] for e in evs] == rs[order].tolist()
+    assert all(e["cat"] == "kernel" for e in evs if "args" in e)
