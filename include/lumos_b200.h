@@ -286,6 +286,17 @@ int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, con
                         const int64_t* arg_stream, const char* names, int64_t gap_threshold_us,
                         ts_host_graph** inout);
 
+/* Native parallel ingest of recorded traces: the
+ * reference's input path with default options (cli.cpp:93-137, window
+ * "full") — parse_trace of each Chrome-trace JSON file (trace_parse.cpp:79-154,
+ * default category table), one rank per rank_<N> file or per process id,
+ * build_graph per rank (build.cpp:338-510) and merge_ranks (:512-542) — with
+ * files parsed and ranks built on n_threads host threads (<= 0: all cores).
+ * The graph carries the retime metadata (rt_*) of its Task.meta.  Errors:
+ * TS_E_INVALID_ARGUMENT with the ParseError text, TS_E_GRAPH for cycles. */
+int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_threads,
+                     int64_t gap_threshold_us, ts_host_graph** out);
+
 /* Device-time accounting: when enabled, CUDA events are recorded on the
  * caller's stream around every kernel the engine launches for this graph;
  * ts_profile_read waits for them, returns the accumulated milliseconds per

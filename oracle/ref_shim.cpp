@@ -21,7 +21,10 @@
 #include <limits>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <map>
+#include <cctype>
+#include <sstream>
 #include <optional>
 #include <random>
 #include <string>
@@ -402,6 +405,63 @@ double ref_bench_simulate(void* h, const orc_scenarios* sc, int64_t first, int32
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+
+// ------------------------------------------------------------ trace ingest
+// Writes the reference generator's trace (generate(spec).events) as Chrome
+// JSON, one file per rank: <dir>/rank_<r>.json (chrome_json,
+// trace_parse.cpp:230-256).  Returns the number of files or -1.
+int ref_write_rank_traces(const char* spec_json, const char* dir) {
+  try {
+    SynthResult res = generate(SynthSpec::from_json(spec_json));
+    int k = 0;
+    for (const auto& [rank, evs] : split_by_rank(res.events)) {
+      std::ofstream out(std::string(dir) + "/rank_" + std::to_string(rank) + ".json");
+      out << chrome_json(evs);
+      ++k;
+    }
+    return k;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The reference's own input path with default options (cli.cpp:93-137,
+// window "full"): load_multirank of rank_<N> files, build_graph per rank,
+// merge_ranks.  Returns a handle or NULL (message in ref_last_error()).
+void* ref_ingest_traces(const char* const* paths, int n) {
+  try {
+    // load_multirank (trace_parse.cpp:286-296) with the file read into a
+    // string first and the rank_<N> marker scanned by hand: the same events
+    // and ranks, without std::regex / istream parsing, which crash in a
+    // process that has numpy's bundled runtime loaded
+    CategoryTable cats;
+    std::map<int, ExecutionGraph> graphs;
+    for (int i = 0; i < n; ++i) {
+      const std::string path = paths[i];
+      int rank = -1;
+      for (std::size_t p = path.find("rank"); p != std::string::npos; p = path.find("rank", p + 1)) {
+        std::size_t q = p + 4;
+        if (q < path.size() && path[q] == '_') ++q;
+        std::size_t e = q;
+        while (e < path.size() && std::isdigit(static_cast<unsigned char>(path[e]))) ++e;
+        if (e > q) rank = std::stoi(path.substr(q, e - q));
+      }
+      if (rank < 0) throw std::runtime_error("cannot derive a rank from filename '" + path + "'");
+      std::ifstream in(path, std::ios::binary);
+      std::stringstream ss;
+      ss << in.rdbuf();
+      if (graphs.count(rank)) throw std::runtime_error("duplicate rank " + std::to_string(rank));
+      graphs.emplace(rank, build_graph(parse_trace(ss.str(), cats), BuildPolicy(), rank));
+    }
+    auto* r = new RefGraph;
+    r->g = merge_ranks(graphs);
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 // ------------------------------------------------------------- what-if retime
 // Per-task retime metadata as the device takes it (ts_graph_desc.rt_*): the

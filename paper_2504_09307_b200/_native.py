@@ -127,4 +127,5 @@ EXPORTED = ["ts_abi_version", "ts_last_error", "ts_kernel_launches", "ts_graph_c
             "ts_replay_batch", "ts_simulate", "ts_scenario_durations", "ts_profile_enable",
             "ts_profile_read", "ts_synth_defaults", "ts_synth_graph", "ts_host_graph_desc",
             "ts_host_graph_op_index", "ts_host_graph_n_ops", "ts_host_graph_name_ids",
-            "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph"]
+            "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph",
+            "ts_ingest_traces"]

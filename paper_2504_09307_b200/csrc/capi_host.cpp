@@ -7,6 +7,7 @@
 #include "ingest.hpp"
 #include "lumos_b200.h"
 #include "synth.hpp"
+#include "trace_ingest.hpp"
 
 using namespace lumos;
 
@@ -65,6 +66,27 @@ const char* ts_host_graph_name(const ts_host_graph* g, int32_t id) {
 }
 
 void ts_host_graph_free(ts_host_graph* g) { delete g; }
+
+int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_threads,
+                     int64_t gap_threshold_us, ts_host_graph** out) {
+  if (!out || (n_paths > 0 && !paths)) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  std::vector<std::string> ps;
+  for (int32_t i = 0; i < n_paths; ++i) ps.emplace_back(paths[i] ? paths[i] : "");
+  auto* h = new ts_host_graph;
+  BuildPolicyLite pol;
+  pol.gap_threshold_us = gap_threshold_us;
+  std::vector<RtMeta> rt;
+  std::string err;
+  const int rc = ingest_trace_files(ps, n_threads, pol, h->s.names, h->s.graph, rt, err);
+  if (rc != TS_OK) {
+    delete h;
+    *out = nullptr;
+    return set_error(rc, err);
+  }
+  fill_retime_arrays(h->s.graph, rt);
+  *out = h;
+  return TS_OK;
+}
 
 int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, const uint8_t* cat,
                         const int64_t* ts, const int64_t* dur, const int32_t* tid,

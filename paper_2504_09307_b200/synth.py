@@ -52,6 +52,9 @@ def _lib():
         L.ts_host_graph_name.restype = C.c_char_p
         L.ts_host_graph_name.argtypes = [C.c_void_p, C.c_int32]
         L.ts_host_graph_free.argtypes = [C.c_void_p]
+        L.ts_ingest_traces.restype = C.c_int
+        L.ts_ingest_traces.argtypes = [C.POINTER(C.c_char_p), C.c_int32, C.c_int32, C.c_int64,
+                                       C.POINTER(C.c_void_p)]
         L.ts_build_rank_graph.restype = C.c_int
         L.ts_build_rank_graph.argtypes = [C.c_int32, C.c_int64, N.i32p, N.u8p, N.i64p, N.i64p,
                                           N.i32p, N.i64p, N.i32p, N.i64p, N.i64p, C.c_char_p,
@@ -248,3 +251,25 @@ def events_from_chrome(trace: dict, categories: Optional[dict] = None) -> dict:
     for r in out:  # parse_trace output order: (pid, ts, tid), stable
         out[r].sort(key=lambda e: (e["ts"], e["tid"]))
     return out
+
+
+def ingest_traces(paths, threads: int = 0, gap_threshold_us: int = 1000,
+                  names: bool = False) -> ExecutionGraph:
+    """Native parallel ingest of recorded Chrome traces (ts_ingest_traces): the
+    reference's parse_trace + build_graph + merge_ranks path for default options
+    (cli.cpp:93-137, window "full"), one rank per rank_<N> file or per process id,
+    files parsed and ranks built on ``threads`` host threads (0: all cores).
+    Raises ValueError (ParseError text) or GraphError (cycles)."""
+    L = _lib()
+    arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+    h = C.c_void_p()
+    rc = L.ts_ingest_traces(arr, len(paths), int(threads), int(gap_threshold_us), C.byref(h))
+    if rc != N.TS_OK:
+        from .replay import _raise
+        _raise(rc)
+    try:
+        g, _, _ = _from_host(h, names=names)
+    finally:
+        L.ts_host_graph_free(h)
+    return g
+

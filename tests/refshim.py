@@ -135,6 +135,10 @@ def ref():
         lib.ref_apply_retime.restype = C.c_void_p
         lib.ref_apply_retime.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int, C.c_int, C.c_double,
                                          C.c_double]
+        lib.ref_write_rank_traces.restype = C.c_int
+        lib.ref_write_rank_traces.argtypes = [C.c_char_p, C.c_char_p]
+        lib.ref_ingest_traces.restype = C.c_void_p
+        lib.ref_ingest_traces.argtypes = [C.POINTER(C.c_char_p), C.c_int]
         lib.ref_bench_simulate.restype = C.c_double
         lib.ref_bench_simulate.argtypes = [C.c_void_p, C.POINTER(OrcScenarios), C.c_int64,
                                            C.c_int32, _u8p, C.c_int, _i64p]
@@ -306,6 +310,23 @@ def generate(spec_json: str, tp: int = 1, slice_rank: int = -1):
 
 def from_trace(trace_json: str, rank: int = -1):
     return RefGraphHandle(ref().ref_graph_from_trace(trace_json.encode(), rank))
+
+
+def write_rank_traces(spec_json: str, directory: str) -> int:
+    """The reference generator's trace as rank_<r>.json Chrome files."""
+    k = ref().ref_write_rank_traces(spec_json.encode(), directory.encode())
+    if k < 0:
+        raise RefError(3, ref().ref_last_error().decode())
+    return k
+
+
+def ingest_traces(paths) -> "RefGraphHandle":
+    """The reference's load_multirank + build_graph + merge_ranks on files."""
+    arr = (C.c_char_p * len(paths))(*[p.encode() for p in paths])
+    h = ref().ref_ingest_traces(arr, len(paths))
+    if not h:
+        raise RefError(3, ref().ref_last_error().decode())
+    return RefGraphHandle(h)
 
 
 def from_graph(g: Graph):
