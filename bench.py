@@ -35,6 +35,12 @@ CONFIGS = {
     "config4": (dict(n_layers=96, d_model=12288, d_ffn=49152, n_heads=96, d_head=128),
                 dict(pp=4, dp=8, num_microbatches=32), 8, 16384,
                 "256-rank GPT-3 175B (pp4 dp8 m32 x TP8 replicas)"),
+    # estimate() semantics (build_pipeline + DurationHook): the generator's own
+    # dependency graph with p2p rendezvous / collective barrier gates
+    "config3": (dict(n_layers=48, d_model=12288, d_ffn=24576, n_heads=96, d_head=128,
+                     estimate=True),
+                dict(pp=4, dp=4, num_microbatches=16), 4, 4096,
+                "64-rank 44B estimate() pipeline (48L d12288 f24576, pp4 dp4 m16 x TP4 replicas)"),
     "config2": (dict(n_layers=48, d_model=6144, d_ffn=12288, n_heads=48, d_head=128),
                 dict(pp=2, dp=2, num_microbatches=4), 2, 1024,
                 "8-rank GPT-3 15B (pp2 dp2 m4 x TP2 replicas)"),
@@ -51,7 +57,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config5", choices=sorted(CONFIGS))
     ap.add_argument("--scenarios", type=int, default=0, help="override the batch size")
-    ap.add_argument("--tile", type=int, default=1024)
+    ap.add_argument("--tile", type=int, default=0,
+                    help="scenarios per replay call (default: 1024; the whole shard for "
+                         "config3, whose 4 components need wide launches)")
     ap.add_argument("--jitter", type=float, default=0.1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -215,7 +223,7 @@ def main():
     from paper_2504_09307_b200.shard import gather_rows, shard
     S_total = args.scenarios or scenarios
     first, S_local = shard(S_total, world, rank)
-    tile = min(args.tile, S_local)
+    tile = min(args.tile or (S_local if args.config == "config3" else 1024), S_local)
     assert S_local % tile == 0, "scenarios per GPU must be a multiple of the tile"
 
     t0 = time.time()
