@@ -36,41 +36,53 @@ __device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
 // ------------------------------------------------------------------- K1
-// One thread replays two adjacent scenarios (columns c, c+1): the op record is
-// decoded once per pair, each operand is one 8- or 16-byte shared load, and
-// each output row is written with one 16-byte streaming store per thread (512
-// contiguous bytes per warp).
+// One thread replays kS adjacent scenarios (2 normally: columns c, c+1; 1 when
+// a launch has too few (component, scenario) pairs to fill the GPU): the op
+// record is decoded once per thread, each operand is one shared load of kS
+// values, and each output row is written with one 8- or 16-byte streaming
+// store per thread (256 / 512 contiguous bytes per warp).
 // Shared memory: two program chunks (2 x kChunk x 64 B, refilled one chunk
-// ahead through registers) followed by the slot table [n_slots][kT] x 2 values.
+// ahead through registers) followed by the slot table [n_slots][kT] x kS values.
 //
 // Value type V: int64 absolute times, or uint32 offsets from W when the
 // launch proves every time of every component stays below W + 2^32 - 1 (the
 // sum of the component's largest possible durations bounds any path; checked
 // on the host, capi.cpp).  Offsets halve the slot table and turn the int64
 // max/add chains into single 32-bit instructions; stores add W back.
-template <typename V>
-struct alignas(2 * sizeof(V)) VPair {
-  V x, y;
+template <typename V, int kS>
+struct alignas(kS * sizeof(V)) VPack {
+  V v[kS];
 };
 template <typename V>
 __device__ __forceinline__ V vmax(V a, V b) { return a > b ? a : b; }
 template <typename V>
 __device__ __forceinline__ V vmin(V a, V b) { return a < b ? a : b; }
-template <typename V>
-__device__ __forceinline__ VPair<V> max2(VPair<V> a, VPair<V> b) {
-  return {vmax(a.x, b.x), vmax(a.y, b.y)};
+template <typename V, int kS>
+__device__ __forceinline__ VPack<V, kS> maxp(VPack<V, kS> a, VPack<V, kS> b) {
+  VPack<V, kS> r;
+#pragma unroll
+  for (int k = 0; k < kS; ++k) r.v[k] = vmax(a.v[k], b.v[k]);
+  return r;
 }
+template <typename V, int kS>
+__device__ __forceinline__ VPack<V, kS> splat(V x) {
+  VPack<V, kS> r;
+#pragma unroll
+  for (int k = 0; k < kS; ++k) r.v[k] = x;
+  return r;
+}
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
-template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V>
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
 __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
-  using VP = VPair<V>;
+  using VP = VPack<V, kS>;
   constexpr bool kRel = sizeof(V) == 4;
   constexpr int kRecPerThread = (kChunk + kT - 1) / kT;  // chunk refill: records per thread
-  // record slot fields hold s * 128; a slot is kT pairs of 2 * sizeof(V) bytes
-  constexpr int kShift = (kT == 128 ? 4 : kT == 64 ? 3 : 2) - (kRel ? 1 : 0);
+  // record slot fields hold s * 128; a slot is kT packs of kS * sizeof(V) bytes
+  constexpr int kShift = ilog2(kT) - 7 + ilog2(kS * static_cast<int>(sizeof(V)));
   constexpr V kInfV = kRel ? static_cast<V>(0xFFFFFFFFu) : static_cast<V>(kMaxI64);
-  static_assert(kT >= 32, "");
-  static_assert(kScenPerThread == 2, "pair layout");
+  static_assert(kT >= 32 && kShift >= 0, "");
+  static_assert(kS == 1 || kS == 2, "");
   extern __shared__ int4 smem[];
   // [2][kChunk][4]: the raw 32-byte record, then its eight 16-bit slot fields
   // (pred[4], dst, x0, x1, x2) widened to byte offsets by the loader, so the
@@ -84,11 +96,17 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   // lanes past the last scenario replay the last scenario again: identical
   // values, so their (duplicate) stores and atomics need no predication
   const int last = P.sp.count - 1;
-  int c0 = chunk * kT * 2 + 2 * tid;
-  if (c0 > last - 1)  // keep pairs even-aligned when the count is even
-    c0 = P.sp.count < 2 ? 0 : ((P.sp.count & 1) ? min(c0, last) : last - 1);
-  const int c1 = min(c0 + 1, last);
-  const bool vec_store = P.vec_store;  // ld even, count even, aligned buffers
+  int col[kS];
+  if (kS == 2) {
+    int c0 = chunk * kT * 2 + 2 * tid;
+    if (c0 > last - 1)  // keep pairs even-aligned when the count is even
+      c0 = P.sp.count < 2 ? 0 : ((P.sp.count & 1) ? min(c0, last) : last - 1);
+    col[0] = c0;
+    col[kS - 1] = min(c0 + 1, last);
+  } else {
+    col[0] = min(chunk * kT + tid, last);
+  }
+  const bool vec_store = kS == 2 && P.vec_store;  // ld even, count even, aligned buffers
 
   const ComponentDesc cd = P.comps[P.comp_order ? P.comp_order[comp] : comp];
   const ProgramDesc pd = P.progs[cd.program];
@@ -101,19 +119,24 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   (*reinterpret_cast<VP*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
 #define SLOTB(boff) \
   (*static_cast<VP*>(__builtin_assume_aligned(slot_base + static_cast<uint32_t>(boff), sizeof(VP))))
-  SLOT2(slot_off(kSlotOrigin)) = VP{w0, w0};
-  SLOT2(slot_off(kSlotInf)) = VP{kInfV, kInfV};
+  SLOT2(slot_off(kSlotOrigin)) = splat<V, kS>(w0);
+  SLOT2(slot_off(kSlotInf)) = splat<V, kS>(kInfV);
 
-  ThreadScen ts0, ts1;
-  init_thread_scen(P.sp, c0, ts0);
-  init_thread_scen(P.sp, c1, ts1);
+  ThreadScen ts[kS];
+#pragma unroll
+  for (int k = 0; k < kS; ++k) init_thread_scen(P.sp, col[k], ts[k]);
 
-  int64_t hi0 = kMinI64, hi1 = kMinI64;
-  bool fail0 = false, fail1 = false;
-  int64_t* const start_c0 = P.out_start + c0;
-  int64_t* const fin_c0 = P.out_fin + c0;
+  int64_t hi[kS];
+  bool fail[kS];
+#pragma unroll
+  for (int k = 0; k < kS; ++k) {
+    hi[k] = kMinI64;
+    fail[k] = false;
+  }
+  int64_t* const start_c0 = P.out_start + col[0];
+  int64_t* const fin_c0 = P.out_fin + col[0];
   const uint32_t ld = static_cast<uint32_t>(P.ld);
-  const int64_t dcol = c1 - c0;
+  const int64_t dcol = col[kS - 1] - col[0];
   char* const sbase = reinterpret_cast<char*>(start_c0);
   char* const fbase = reinterpret_cast<char*>(fin_c0);
   const uint64_t ld8 = static_cast<uint64_t>(ld) * 8u;
@@ -164,20 +187,20 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
       // (max(start, gate) for gated kinds, else the start itself: st >= W)
       VP st, fb;
       if (kind <= OP_ACC) {  // OP_NODE, OP_SYNC, OP_START, OP_ACC
-        st = max2(max2(p0, p1), max2(p2, p3));  // unused preds read the origin W
+        st = maxp(maxp(p0, p1), maxp(p2, p3));  // unused preds read the origin W
         fb = st;
       } else if (kind == OP_FINISH) {
         st = p0;
-        fb = max2(max2(p0, p1), max2(p2, p3));
+        fb = maxp(maxp(p0, p1), maxp(p2, p3));
       } else if (kind == OP_GATED) {
         const int nfixed = static_cast<int>(cls_b >> 4);
-        st = VP{w0, w0};
+        st = splat<V, kS>(w0);
         VP gate = st;
-        if (nfixed > 0) st = max2(st, p0); else gate = max2(gate, p0);
-        if (nfixed > 1) st = max2(st, p1); else gate = max2(gate, p1);
-        if (nfixed > 2) st = max2(st, p2); else gate = max2(gate, p2);
-        gate = max2(gate, p3);
-        fb = max2(st, gate);
+        if (nfixed > 0) st = maxp(st, p0); else gate = maxp(gate, p0);
+        if (nfixed > 1) st = maxp(st, p1); else gate = maxp(gate, p1);
+        if (nfixed > 2) st = maxp(st, p2); else gate = maxp(gate, p2);
+        gate = maxp(gate, p3);
+        fb = maxp(st, gate);
       } else {
         continue;  // OP_NOP
       }
@@ -196,9 +219,11 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
           const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
 #pragma unroll
           for (int k = 0; k < kCertPerExt; ++k)
-            if (k < n && f[k] != kNoSlot) S = max2(S, SLOT2(f[k]));
+            if (k < n && f[k] != kNoSlot) S = maxp(S, SLOT2(f[k]));
         }
-        bool cov0 = S.x == rs.x, cov1 = S.y == rs.y;
+        bool cov[kS];
+#pragma unroll
+        for (int s = 0; s < kS; ++s) cov[s] = S.v[s] == rs.v[s];
         for (int e = 0; e < n_ext; ++e) {
           const int4 xa = buf[4 * (i + 1 + e)], xb = buf[4 * (i + 1 + e) + 1];
           const int n = xb.z & 0xFFFF;
@@ -210,18 +235,19 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
             if (k >= n) continue;
             if (f[k] != kNoSlot && cv[k] != kNoSlot) {
               const VP fk = SLOT2(f[k]), ck = SLOT2(cv[k]);
-              cov0 = cov0 || (fk.x == S.x && ck.x <= rs.x);
-              cov1 = cov1 || (fk.y == S.y && ck.y <= rs.y);
+#pragma unroll
+              for (int s = 0; s < kS; ++s)
+                cov[s] = cov[s] || (fk.v[s] == S.v[s] && ck.v[s] <= rs.v[s]);
             }
             if (nx[k] != kNoSlot) {
               const VP nk = SLOT2(nx[k]);
-              fail0 = fail0 || nk.x <= S.x;
-              fail1 = fail1 || nk.y <= S.y;
+#pragma unroll
+              for (int s = 0; s < kS; ++s) fail[s] = fail[s] || nk.v[s] <= S.v[s];
             }
           }
         }
-        fail0 = fail0 || !cov0;
-        fail1 = fail1 || !cov1;
+#pragma unroll
+        for (int s = 0; s < kS; ++s) fail[s] = fail[s] || !cov[s];
         st = S;
         fb = S;
         i += n_ext;
@@ -233,32 +259,35 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
                              static_cast<uint32_t>(ra.x);
         const int cls = cls_b & 15u;
-        const int64_t d0 = scenario_duration<kMode>(P.sp, ts0, task, base, cls);
-        const int64_t d1 = scenario_duration<kMode>(P.sp, ts1, task, base, cls);
-        const VP fin = {static_cast<V>(fb.x + static_cast<V>(d0)),
-                        static_cast<V>(fb.y + static_cast<V>(d1))};
+        VP fin;
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+          const int64_t d = scenario_duration<kMode>(P.sp, ts[s], task, base, cls);
+          fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
+        }
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
         if (__builtin_expect((flags & F_SINK) != 0, 0)) {
-          hi0 = imax(hi0, absv(fin.x));
-          hi1 = imax(hi1, absv(fin.y));
+#pragma unroll
+          for (int s = 0; s < kS; ++s) hi[s] = imax(hi[s], absv(fin.v[s]));
         }
         const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
         if (vec_store) {
           const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
           if (kWriteStart)
-            __stcs(reinterpret_cast<longlong2*>(sbase + at8), make_longlong2(absv(st.x), absv(st.y)));
+            __stcs(reinterpret_cast<longlong2*>(sbase + at8),
+                   make_longlong2(absv(st.v[0]), absv(st.v[kS - 1])));
           if (kWriteFin)
             __stcs(reinterpret_cast<longlong2*>(fbase + at8),
-                   make_longlong2(absv(fin.x), absv(fin.y)));
+                   make_longlong2(absv(fin.v[0]), absv(fin.v[kS - 1])));
         } else {
           if (kWriteStart) {
-            __stcs(start_c0 + at, absv(st.x));
-            __stcs(start_c0 + at + dcol, absv(st.y));
+            __stcs(start_c0 + at, absv(st.v[0]));
+            if (kS == 2) __stcs(start_c0 + at + dcol, absv(st.v[kS - 1]));
           }
           if (kWriteFin) {
-            __stcs(fin_c0 + at, absv(fin.x));
-            __stcs(fin_c0 + at + dcol, absv(fin.y));
+            __stcs(fin_c0 + at, absv(fin.v[0]));
+            if (kS == 2) __stcs(fin_c0 + at + dcol, absv(fin.v[kS - 1]));
           }
         }
       }
@@ -266,8 +295,11 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         // the source slot outlives this op's results (compile.cpp), so it is
         // read here; kSlotInf when the kernel has no coverage source
         const VP cov_src = SLOTB(ob.y);
-        SLOTB(ob.z) = VP{p0.x >= st.x ? vmin(st.x, cov_src.x) : st.x,
-                         p0.y >= st.y ? vmin(st.y, cov_src.y) : st.y};
+        VP cv;
+#pragma unroll
+        for (int s = 0; s < kS; ++s)
+          cv.v[s] = p0.v[s] >= st.v[s] ? vmin(st.v[s], cov_src.v[s]) : st.v[s];
+        SLOTB(ob.z) = cv;
       } else if (flags & F_TRACK) {
         // coverage of this kernel per watched set (program.hpp, OpCov)
         const int4 xa = buf[4 * (i + 1)], xb = buf[4 * (i + 1) + 1];
@@ -284,8 +316,9 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
           for (int k = 0; k < 4; ++k)
             if (j < n_sets && src[j][k] != kNoSlot) {
               const VP sv = SLOT2(src[j][k]);
-              if (pv[k].x >= st.x) cvj[j].x = vmin(cvj[j].x, sv.x);
-              if (pv[k].y >= st.y) cvj[j].y = vmin(cvj[j].y, sv.y);
+#pragma unroll
+              for (int s = 0; s < kS; ++s)
+                if (pv[k].v[s] >= st.v[s]) cvj[j].v[s] = vmin(cvj[j].v[s], sv.v[s]);
             }
         }
 #pragma unroll
@@ -304,14 +337,14 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   }
 #undef SLOT2
 #undef SLOTB
-  if (hi0 != kMinI64) {
-    atomicMin(reinterpret_cast<long long*>(P.span_lo) + c0, static_cast<long long>(W));
-    atomicMax(reinterpret_cast<long long*>(P.span_hi) + c0, static_cast<long long>(hi0));
-    atomicMin(reinterpret_cast<long long*>(P.span_lo) + c1, static_cast<long long>(W));
-    atomicMax(reinterpret_cast<long long*>(P.span_hi) + c1, static_cast<long long>(hi1));
+#pragma unroll
+  for (int s = 0; s < kS; ++s) {
+    if (hi[s] != kMinI64) {
+      atomicMin(reinterpret_cast<long long*>(P.span_lo) + col[s], static_cast<long long>(W));
+      atomicMax(reinterpret_cast<long long*>(P.span_hi) + col[s], static_cast<long long>(hi[s]));
+    }
+    if (fail[s]) atomicOr(P.status + col[s], 1);
   }
-  if (fail0) atomicOr(P.status + c0, 1);
-  if (fail1) atomicOr(P.status + c1, 1);
 }
 
 __global__ void span_init_kernel(int64_t* lo, int64_t* hi, int32_t* status, int32_t count) {
@@ -938,77 +971,88 @@ cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, i
 }
 int walk_threads() { return kThreads; }
 
-template <int kT, int kMode, bool kS, bool kF, typename V>
+template <int kT, int kMode, bool kWS, bool kWF, typename V, int kS>
 static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
                                  cudaStream_t stream) {
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kS, kF, V>,
+    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kWS, kWF, V, kS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  replay_walk_kernel<kT, kMode, kS, kF, V><<<blocks, kT, smem, stream>>>(p);
+  replay_walk_kernel<kT, kMode, kWS, kWF, V, kS><<<blocks, kT, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int kT, int kMode, typename V>
+template <int kT, int kMode, typename V, int kS>
 static cudaError_t launch_walk_mode(const WalkParams& p, size_t smem, unsigned blocks,
                                     cudaStream_t stream) {
   const bool s = p.out_start != nullptr, f = p.out_fin != nullptr;
-  if (s && f) return launch_walk_t<kT, kMode, true, true, V>(p, smem, blocks, stream);
-  if (f) return launch_walk_t<kT, kMode, false, true, V>(p, smem, blocks, stream);
-  if (s) return launch_walk_t<kT, kMode, true, false, V>(p, smem, blocks, stream);
-  return launch_walk_t<kT, kMode, false, false, V>(p, smem, blocks, stream);
+  if (s && f) return launch_walk_t<kT, kMode, true, true, V, kS>(p, smem, blocks, stream);
+  if (f) return launch_walk_t<kT, kMode, false, true, V, kS>(p, smem, blocks, stream);
+  if (s) return launch_walk_t<kT, kMode, true, false, V, kS>(p, smem, blocks, stream);
+  return launch_walk_t<kT, kMode, false, false, V, kS>(p, smem, blocks, stream);
 }
 
-template <int kT, typename V>
+template <int kT, typename V, int kS>
 static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStream_t stream) {
-  const int per_block = kT * kScenPerThread;
+  const int per_block = kT * kS;
   const long long chunks = (p.sp.count + per_block - 1) / per_block;
   const long long blocks = chunks * p.n_comps;
   if (blocks <= 0) return cudaSuccess;
   const unsigned nb = static_cast<unsigned>(blocks);
   switch (p.sp.mode) {
-    case 0: return launch_walk_mode<kT, 0, V>(p, smem, nb, stream);
-    case kModeScale: return launch_walk_mode<kT, kModeScale, V>(p, smem, nb, stream);
-    case kModeJitter: return launch_walk_mode<kT, kModeJitter, V>(p, smem, nb, stream);
+    case 0: return launch_walk_mode<kT, 0, V, kS>(p, smem, nb, stream);
+    case kModeScale: return launch_walk_mode<kT, kModeScale, V, kS>(p, smem, nb, stream);
+    case kModeJitter: return launch_walk_mode<kT, kModeJitter, V, kS>(p, smem, nb, stream);
     case kModeScale | kModeJitter:
-      return launch_walk_mode<kT, kModeScale | kModeJitter, V>(p, smem, nb, stream);
-    default: return launch_walk_mode<kT, kModeExplicit, V>(p, smem, nb, stream);
+      return launch_walk_mode<kT, kModeScale | kModeJitter, V, kS>(p, smem, nb, stream);
+    default: return launch_walk_mode<kT, kModeExplicit, V, kS>(p, smem, nb, stream);
   }
 }
 
-// shared memory of a walk CTA of t threads with `vbytes`-byte slot values
+// shared memory of a walk CTA of t threads with `vbytes` bytes of slot values
+// per thread and slot
 static size_t walk_smem(int n_slots, int t, int vbytes) {
   return 8 * kChunk * sizeof(int4) +
-         static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * 2 * vbytes;
+         static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * vbytes;
 }
 
 int walk_width(int n_slots, bool rel32) {
   const size_t cap = 227 * 1024;
-  const int vb = rel32 ? 4 : 8;
+  const int vb = (rel32 ? 4 : 8) * 2;
   if (walk_smem(n_slots, 128, vb) <= cap / 2) return 128;  // >= 2 CTAs per SM
   if (walk_smem(n_slots, 64, vb) <= cap / 2) return 64;
   if (walk_smem(n_slots, 32, vb) <= cap) return 32;
   return 0;
 }
 
+// One scenario per thread when two per thread would leave the GPU short of
+// warps: fewer than ~8 warps per SM of (component, scenario-pair) work.
+static bool single_scenario(const WalkParams& p) {
+  const long long pairs = static_cast<long long>(p.n_comps) * ((p.sp.count + 1) / 2);
+  return pairs < 148LL * 8 * 32;
+}
+
+template <typename V, int kS>
+static cudaError_t launch_walk_v(const WalkParams& p, int n_slots, int t, cudaStream_t stream) {
+  const int vb = static_cast<int>(sizeof(V)) * kS;
+  if (t == 128) return launch_walk_width<128, V, kS>(p, walk_smem(n_slots, 128, vb), stream);
+  if (t == 64) return launch_walk_width<64, V, kS>(p, walk_smem(n_slots, 64, vb), stream);
+  if (t == 32) return launch_walk_width<32, V, kS>(p, walk_smem(n_slots, 32, vb), stream);
+  return cudaErrorInvalidConfiguration;
+}
+
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
   const bool rel = p.rel32 != 0;
   const int t = walk_width(n_slots, rel);
-  const int vb = rel ? 4 : 8;
-  if (rel) {
-    if (t == 128) return launch_walk_width<128, uint32_t>(p, walk_smem(n_slots, 128, vb), stream);
-    if (t == 64) return launch_walk_width<64, uint32_t>(p, walk_smem(n_slots, 64, vb), stream);
-    if (t == 32) return launch_walk_width<32, uint32_t>(p, walk_smem(n_slots, 32, vb), stream);
-  } else {
-    if (t == 128) return launch_walk_width<128, int64_t>(p, walk_smem(n_slots, 128, vb), stream);
-    if (t == 64) return launch_walk_width<64, int64_t>(p, walk_smem(n_slots, 64, vb), stream);
-    if (t == 32) return launch_walk_width<32, int64_t>(p, walk_smem(n_slots, 32, vb), stream);
-  }
-  return cudaErrorInvalidConfiguration;
+  if (single_scenario(p))
+    return rel ? launch_walk_v<uint32_t, 1>(p, n_slots, t, stream)
+               : launch_walk_v<int64_t, 1>(p, n_slots, t, stream);
+  return rel ? launch_walk_v<uint32_t, 2>(p, n_slots, t, stream)
+             : launch_walk_v<int64_t, 2>(p, n_slots, t, stream);
 }
 
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
