@@ -432,7 +432,16 @@ static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStr
     return fail(TS_E_INVALID_ARGUMENT, "graph carries no retime metadata (ts_graph_desc.rt_kind)");
   if (!rt->alpha_us || !rt->bytes_per_us)
     return fail(TS_E_INVALID_ARGUMENT, "retime needs alpha_us and bytes_per_us per scenario");
-  bool any_dp_change = false, any_hidden = false;
+  // the first task change_hidden would stop at (transform.cpp:279-349): the
+  // first optimizer / allreduce task (n_params check), the first allreduce
+  // without a group size
+  int32_t first_np = -1, first_nogroup = -1;
+  for (int32_t t = 0; t < c.n_tasks && (first_np < 0 || first_nogroup < 0); ++t) {
+    const uint8_t k = c.rt_kind[t];
+    if (first_np < 0 && (k == TS_RT_OPT || k == TS_RT_ALLREDUCE)) first_np = t;
+    if (first_nogroup < 0 && k == TS_RT_ALLREDUCE && c.rt_group[t] <= 0) first_nogroup = t;
+  }
+  bool any_dp_change = false;
   for (int32_t s = 0; s < count; ++s) {
     if (!(rt->bytes_per_us[s] > 0))
       return fail(TS_E_INVALID_ARGUMENT,
@@ -457,19 +466,14 @@ static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStr
       if (tm[0] != rt->source_model[0] || tm[1] != rt->source_model[1]) {
         if (rt->source_model[0] <= 0 || tm[0] <= 0)
           return fail(TS_E_INVALID_ARGUMENT, "hidden-size rescale needs both model widths");
-        for (int32_t t = 0; t < c.n_tasks; ++t) {
-          const uint8_t k = c.rt_kind[t];
-          if ((k == TS_RT_OPT || k == TS_RT_ALLREDUCE) &&
-              (rt->source_model[2] <= 0 || tm[2] <= 0))
-            return fail(TS_E_INVALID_ARGUMENT,
-                        k == TS_RT_OPT
-                            ? "hidden-size rescale of optimizer work needs n_params on both models"
-                            : "hidden-size rescale of collectives needs n_params on both models");
-          if (k == TS_RT_ALLREDUCE && c.rt_group[t] <= 0)
-            return fail(TS_E_INVALID_ARGUMENT,
-                        "collective task " + std::to_string(t) + " carries no group size");
-        }
-        any_hidden = true;
+        if (first_np >= 0 && (rt->source_model[2] <= 0 || tm[2] <= 0))
+          return fail(TS_E_INVALID_ARGUMENT,
+                      c.rt_kind[first_np] == TS_RT_OPT
+                          ? "hidden-size rescale of optimizer work needs n_params on both models"
+                          : "hidden-size rescale of collectives needs n_params on both models");
+        if (first_nogroup >= 0)
+          return fail(TS_E_INVALID_ARGUMENT, "collective task " + std::to_string(first_nogroup) +
+                                                 " carries no group size");
       }
     }
   }
@@ -486,7 +490,6 @@ static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStr
       return fail(TS_E_INVALID_ARGUMENT, "no gradient collectives sized for data-parallel group " +
                                              std::to_string(rt->source_dp) + " found");
   }
-  (void)any_hidden;
   const size_t n = static_cast<size_t>(count);
   const size_t bytes = n * 8 * 2 + n * 4 + (rt->target_model ? n * 24 : 0) + 64;
   if (g->retime_par.reserve(bytes) != cudaSuccess)
