@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -101,7 +102,12 @@ struct ts_graph {
   Op* d_ops = nullptr;
   ProgramDesc* d_progs = nullptr;
   ComponentDesc* d_comps = nullptr;
-  int32_t* d_comp_order = nullptr;
+  int32_t* d_comp_order = nullptr;   // single-program components, longest first
+  int32_t n_single = 0;
+  int32_t* d_coop_comps = nullptr;   // cooperative (multi-rank) components
+  int32_t n_coop = 0;
+  int32_t* d_coop_prog_off = nullptr;
+  int32_t* d_coop_progs = nullptr;
   int64_t* d_base = nullptr;
   uint8_t* d_rt_kind = nullptr;  // retime metadata (empty when absent)
   int64_t* d_rt_bytes = nullptr;
@@ -223,11 +229,35 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
     return c.programs[c.comps[a].program].n_ops > c.programs[c.comps[b].program].n_ops;
   });
+  // components walked by one program vs cooperatively by one warp per rank
+  std::vector<int32_t> single, coop;
+  for (int32_t ci : order) {
+    const bool multi = !c.coop_prog_off.empty() &&
+                       c.coop_prog_off[ci + 1] - c.coop_prog_off[ci] > 1;
+    (multi ? coop : single).push_back(ci);
+  }
+  g->n_single = static_cast<int32_t>(single.size());
+  g->n_coop = static_cast<int32_t>(coop.size());
+  if (g->n_coop > 0) {  // shared memory of a cooperative CTA with uint32 values
+    const size_t smem = static_cast<size_t>((c.max_mailboxes * 4 + 15) / 16) * 16 +
+                        static_cast<size_t>(c.max_mailboxes) * 32 * 4 +
+                        static_cast<size_t>(c.max_coop_ranks) * c.max_slots * 32 * 4;
+    if (c.max_coop_ranks > 32 || smem > 227 * 1024) {
+      delete g;
+      return fail(TS_E_UNSUPPORTED,
+                  "a component couples " + std::to_string(c.max_coop_ranks) + " ranks through " +
+                      std::to_string(c.max_mailboxes) +
+                      " values: more than one CTA holds (compile with LUMOS_COOP=0)");
+    }
+  }
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&g->d_ops, c.ops);
   if (e == cudaSuccess) e = upload(&g->d_progs, c.programs);
   if (e == cudaSuccess) e = upload(&g->d_comps, c.comps);
-  if (e == cudaSuccess) e = upload(&g->d_comp_order, order);
+  if (e == cudaSuccess) e = upload(&g->d_comp_order, single);
+  if (e == cudaSuccess) e = upload(&g->d_coop_comps, coop);
+  if (e == cudaSuccess) e = upload(&g->d_coop_prog_off, c.coop_prog_off);
+  if (e == cudaSuccess) e = upload(&g->d_coop_progs, c.coop_progs);
   if (e == cudaSuccess) e = upload(&g->d_base, c.base);
   if (e == cudaSuccess) e = upload(&g->d_rt_kind, c.rt_kind);
   if (e == cudaSuccess) e = upload(&g->d_rt_bytes, c.rt_bytes);
@@ -309,6 +339,8 @@ void ts_graph_destroy(ts_graph* g) {
     if (g->device >= 0) cudaSetDevice(g->device);
     for (void* p : {static_cast<void*>(g->d_ops), static_cast<void*>(g->d_progs),
                     static_cast<void*>(g->d_comps), static_cast<void*>(g->d_comp_order),
+                    static_cast<void*>(g->d_coop_comps), static_cast<void*>(g->d_coop_prog_off),
+                    static_cast<void*>(g->d_coop_progs),
                     static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
                     static_cast<void*>(g->d_rt_kind), static_cast<void*>(g->d_rt_bytes),
                     static_cast<void*>(g->d_rt_group), static_cast<void*>(g->d_rt_mnk),
@@ -677,6 +709,19 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
                          3.0 * static_cast<double>(c.max_comp_tasks) + 16.0;
     rel32 = f >= 0.0 && bound < 4.2e9 && walk_width(c.max_slots, true) > 0;
   }
+  // cooperative walks size their uint32 window by the nominal longest path
+  // and check every addition (a wrap sends the scenario to the fix-up)
+  bool coop_rel32 = false;
+  if (!retime && !(sp.mode & kModeExplicit) && !sp.scale_num && g->n_coop > 0) {
+    double f = 1.0;
+    if (sp.mode & kModeScale)
+      f *= static_cast<double>(sp.scale_lo + static_cast<int64_t>(sp.scale_span) - 1) /
+           static_cast<double>(sp.scale_den);
+    if (sp.mode & kModeJitter) f *= 1.0 + 0.5 * sp.two_j;
+    coop_rel32 = static_cast<double>(c.max_coop_path) * f * 1.25 + 1e6 < 4.0e9;
+    const char* force = std::getenv("LUMOS_COOP_FORCE_U32");  // tests: exercise the wrap fix-up
+    if (force && force[0] == '1') coop_rel32 = true;
+  }
   {
     Timed tm(g, stream, 2);
     CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
@@ -689,7 +734,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.progs = g->d_progs;
     wp.comps = g->d_comps;
     wp.comp_order = g->d_comp_order;
-    wp.n_comps = static_cast<int32_t>(c.comps.size());
+    wp.n_comps = g->n_single;
     wp.window_start = c.window_start;
     wp.sp = sp;
     wp.sp.first = sp.first + b0;
@@ -737,6 +782,30 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       Timed tm(g, stream, 0);
       CUDA_TRY(launch_replay_walk(wp, c.max_slots, stream));
       g_launches++;
+    }
+    if (!c.des_only && g->n_coop > 0) {
+      WalkParams cw = wp;
+      cw.comp_order = g->d_coop_comps;
+      cw.n_comps = g->n_coop;
+      CoopParams cp{};
+      cp.prog_off = g->d_coop_prog_off;
+      cp.progs = g->d_coop_progs;
+      cp.max_ranks = c.max_coop_ranks;
+      cp.n_mail = c.max_mailboxes;
+      cp.n_slots = c.max_slots;
+      cp.rel32 = coop_rel32 ? 1 : 0;
+      {
+        Timed tm(g, stream, 0);
+        CUDA_TRY(launch_coop_walk(cw, cp, stream));
+      }
+      g_launches++;
+      if (coop_rel32) {  // exact int64 re-run of any chunk whose window wrapped
+        cp.rel32 = 0;
+        cp.fixup = 1;
+        Timed tm(g, stream, 2);
+        CUDA_TRY(launch_coop_walk(cw, cp, stream));
+        g_launches++;
+      }
     }
     if (c.des_only || c.n_syncs > 0) {
       // exact event-driven replay: every scenario of a graph outside the

@@ -495,6 +495,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   // kernels by finish keeps a p2p receive — which starts early and then waits
   // inside its duration — from dragging every earlier launch forward.
   std::vector<int64_t> demand(na, INT64_MAX);
+  std::vector<int64_t> comp_path;
   {
     std::vector<int32_t> by_topo(na);
     for (int32_t a = 0; a < na; ++a) by_topo[topo[a]] = a;
@@ -522,6 +523,12 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         nfin[t] = f + d.duration[t];
       }
     }
+    // nominal longest path per component (W-relative): sizes the uint32
+    // window of cooperative walks, which also check every addition
+    comp_path.assign(n_comp, 0);
+    for (int32_t t = 0; t < n; ++t)
+      comp_path[comp_of[t]] = std::max(comp_path[comp_of[t]], nfin[t] - d.window_start);
+
     for (int64_t k = na - 1; k >= 0; --k) {
       const int32_t a = by_topo[k];
       const int32_t t = real_task(a);
@@ -590,6 +597,14 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
   };
 
+  // cooperative multi-rank walks (LUMOS_COOP=0 disables them)
+  const char* coop_env = std::getenv("LUMOS_COOP");
+  const bool coop = !(coop_env && coop_env[0] == '0');
+  out.coop_prog_off.clear();
+  out.coop_progs.clear();
+  out.max_mailboxes = 0;
+  out.max_coop_ranks = 1;
+  out.max_coop_path = 0;
   for (int32_t c = 0; c < n_comp; ++c) {
     ir.clear();
     comp_tasks.clear();
@@ -752,306 +767,473 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       }
     }
 
-    // ---- liveness: last use of each value; auxiliary records (certificate,
-    // coverage) belong to the op before them
-    auto ensure = [&](int64_t v) {
-      if (v >= static_cast<int64_t>(last_use.size())) {
-        last_use.resize(static_cast<size_t>(v + 1), -1);
-        slot_of.resize(static_cast<size_t>(v + 1), kNoSlot);
-      }
-    };
-    std::vector<int32_t> anchor(ir.size());
-    for (size_t i = 0; i < ir.size(); ++i)
-      anchor[i] = ir[i].aux() ? anchor[i - 1] : static_cast<int32_t>(i);
-    auto each_read = [&](const IrOp& o, auto&& f) {
-      if (o.is_ext) {
-        for (int k = 0; k < o.n_ent; ++k) {
-          if (o.v_fin[k] >= 0) f(o.v_fin[k]);
-          if (o.v_bs[k] >= 0) f(o.v_bs[k]);
-          if (o.v_next[k] >= 0) f(o.v_next[k]);
+    // ---- one straight-line program from an op sequence: liveness, slots,
+    // byte offsets, chunk padding, de-duplication.  Returns the program id,
+    // or -1 with finish_rc / err set.
+    int finish_rc = TS_OK;
+    auto finish_program = [&](std::vector<IrOp>& ir, int32_t& n_slots_out) -> int32_t {
+      // ---- liveness: last use of each value; auxiliary records (certificate,
+      // coverage) belong to the op before them
+      auto ensure = [&](int64_t v) {
+        if (v >= static_cast<int64_t>(last_use.size())) {
+          last_use.resize(static_cast<size_t>(v + 1), -1);
+          slot_of.resize(static_cast<size_t>(v + 1), kNoSlot);
         }
-        return;
-      }
-      if (o.is_cov) {
-        for (int j = 0; j < o.n_sets; ++j)
-          for (int k = 0; k < 4; ++k)
-            if (o.v_cov_src[j][k] >= 0) f(o.v_cov_src[j][k]);
-        return;
-      }
-      for (int k = 0; k < o.op.npred; ++k) f(o.v_pred[k]);
-      if (o.v_cov1_src >= 0) f(o.v_cov1_src);
-    };
-    auto each_write = [&](const IrOp& o, auto&& f) {
-      if (o.is_ext) return;
-      if (o.is_cov) {
-        for (int j = 0; j < o.n_sets; ++j)
-          if (o.v_cov_dst[j] >= 0) f(o.v_cov_dst[j]);
-        return;
-      }
-      if (o.v_dst >= 0) f(o.v_dst);
-      if ((o.op.flags & F_STORE_START) && o.v_x2 >= 0) f(o.v_x2);
-      if (o.v_cov1_dst >= 0) f(o.v_cov1_dst);
-    };
-    for (size_t i = 0; i < ir.size(); ++i)
-      each_read(ir[i], [&](int64_t v) {
-        ensure(v);
-        last_use[v] = std::max(last_use[v], anchor[i]);
-      });
-
-    // ---- linear-scan slot assignment.  An op group (op + its auxiliary
-    // records) reads every operand before it writes.  Operands dying in the
-    // group are released at the group's end; the op's own results are placed
-    // before that (so they never alias a group operand), the coverage results
-    // after it.
-    std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> free_slots;
-    int32_t n_slots = kFirstSlot;
-    std::vector<int64_t> dying;
-    bool broken = false;
-    auto flush = [&] {
-      std::sort(dying.begin(), dying.end());
-      dying.erase(std::unique(dying.begin(), dying.end()), dying.end());
-      for (int64_t v : dying) {
-        free_slots.push(slot_of[v]);
-        slot_of[v] = kNoSlot;
-      }
-      dying.clear();
-    };
-    for (size_t i = 0; i < ir.size(); ++i) {
-      IrOp& o = ir[i];
-      const int32_t at = anchor[i];
-      auto read_slot = [&](int64_t v) -> uint16_t {
-        if (v < 0) return kNoSlot;
-        if (slot_of[v] == kNoSlot) {
-          broken = true;
-          return kNoSlot;
-        }
-        if (last_use[v] == at) dying.push_back(v);
-        return static_cast<uint16_t>(slot_of[v]);
       };
-      auto write_slot = [&](int64_t v) -> uint16_t {
-        if (v < 0) return kSlotTrash;
-        ensure(v);
-        if (last_use[v] <= at) return kSlotTrash;  // nobody reads it later
-        int32_t s;
-        if (!free_slots.empty()) {
-          s = free_slots.top();
-          free_slots.pop();
-        } else {
-          s = n_slots++;
-        }
-        slot_of[v] = s;
-        return static_cast<uint16_t>(s);
-      };
-      const bool group_end = i + 1 >= ir.size() || !ir[i + 1].aux();
-      if (o.is_ext) {
-        OpExt x{};
-        for (int k = 0; k < kCertPerExt; ++k) x.fin[k] = x.bs[k] = x.next[k] = kNoSlot;
-        for (int k = 0; k < o.n_ent; ++k) {
-          x.fin[k] = read_slot(o.v_fin[k]);
-          x.bs[k] = read_slot(o.v_bs[k]);
-          x.next[k] = read_slot(o.v_next[k]);
-        }
-        x.n = static_cast<uint16_t>(o.n_ent);
-        std::memcpy(&o.op, &x, sizeof(Op));
-        if (group_end) flush();
-        continue;
-      }
-      if (o.is_cov) {
-        OpCov x{};
-        for (int j = 0; j < kCovSets; ++j) {
-          x.dst[j] = kNoSlot;
-          for (int k = 0; k < 4; ++k) x.src[j][k] = kNoSlot;
-        }
-        for (int j = 0; j < o.n_sets; ++j)
-          for (int k = 0; k < 4; ++k) x.src[j][k] = read_slot(o.v_cov_src[j][k]);
-        if (group_end) flush();
-        for (int j = 0; j < o.n_sets; ++j) x.dst[j] = write_slot(o.v_cov_dst[j]);
-        for (int j = o.n_sets; j < kCovSets; ++j) x.dst[j] = kSlotTrash;
-        x.n_sets = static_cast<uint16_t>(o.n_sets);
-        std::memcpy(&o.op, &x, sizeof(Op));
-        continue;
-      }
-      for (int k = 0; k < o.op.npred; ++k) o.op.pred[k] = read_slot(o.v_pred[k]);
-      for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kSlotOrigin;
-      const uint16_t cov_src = (o.op.flags & F_TRACK1) ? read_slot(o.v_cov1_src) : kNoSlot;
-      // the walk reads an F_TRACK1 coverage source after writing the op's
-      // results, so a dying source is released only after they are placed
-      int64_t late_free = -1;
-      if ((o.op.flags & F_TRACK1) && o.v_cov1_src >= 0 &&
-          std::find(dying.begin(), dying.end(), o.v_cov1_src) != dying.end()) {
-        dying.erase(std::remove(dying.begin(), dying.end(), o.v_cov1_src), dying.end());
-        late_free = o.v_cov1_src;
-      }
-      if (group_end) flush();
-      ensure(o.v_dst >= 0 ? o.v_dst : 0);
-      if (o.v_dst >= 0 && o.v_dst < V_ACC && last_use[o.v_dst] <= at &&
-          (o.op.kind == OP_NODE || o.op.kind == OP_GATED || o.op.kind == OP_FINISH ||
-           o.op.kind == OP_SYNC))
-        o.op.flags |= F_SINK;
-      o.op.dst = write_slot(o.v_dst);
-      if (o.op.kind != OP_SYNC) o.op.x0 = kNoSlot;
-      o.op.x1 = kNoSlot;
-      if (o.op.flags & F_TRACK1) {
-        o.op.x0 = cov_src == kNoSlot ? kSlotInf : cov_src;
-        o.op.x1 = write_slot(o.v_cov1_dst);
-      }
-      o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
-      if (late_free >= 0) {
-        free_slots.push(slot_of[late_free]);
-        slot_of[late_free] = kNoSlot;
-      }
-    }
-    if (std::getenv("LUMOS_DEBUG_SLOTS") && c == 0) {
-      // replay the allocation to find the peak live set (debug only)
-      std::vector<int64_t> live;
-      std::vector<int64_t> peak;
-      std::vector<char> alive(last_use.size(), 0);
-      for (size_t i = 0; i < ir.size(); ++i) {
-        each_write(ir[i], [&](int64_t v) {
-          if (last_use[v] > anchor[i]) alive[v] = 1, live.push_back(v);
-        });
-        live.erase(std::remove_if(live.begin(), live.end(),
-                                  [&](int64_t v) { return last_use[v] <= anchor[i]; }),
-                   live.end());
-        if (live.size() > peak.size()) peak = live;
-      }
-      int kinds[5] = {0, 0, 0, 0, 0};
-      std::map<std::string, int> by;
-      for (int64_t v : peak) {
-        int k = v < n ? 0 : v < V_COV ? 1 : v < V_ACC ? 2 : 3;
-        kinds[k]++;
-        if (k <= 1) {
-          int32_t t = static_cast<int32_t>(k == 0 ? v : v - n);
-          std::string key = std::string(k ? "START " : "FIN ") +
-                            (d.lane_kind[t] ? "stream" : "thread") + std::to_string(d.lane[t]) +
-                            " op" + std::to_string(d.op_class ? d.op_class[t] : 9);
-          by[key]++;
-        }
-      }
-      fprintf(stderr, "[slots] comp 0 peak %zu: fin %d start %d cov %d acc %d\n", peak.size(),
-              kinds[0], kinds[1], kinds[2], kinds[3]);
-      for (auto& [k, cnt] : by) fprintf(stderr, "[slots]   %s x%d\n", k.c_str(), cnt);
-    }
-    if (broken) {
-      err = "internal: compiled order reads a value before it is defined";
-      return TS_E_UNSUPPORTED;
-    }
-    if (n_slots > kMaxSlots) {
-      err = "unsupported graph: a component needs " + std::to_string(n_slots) +
-            " live values per scenario (limit " + std::to_string(kMaxSlots) + ")";
-      return TS_E_UNSUPPORTED;
-    }
-    // slot numbers -> byte offsets into the [slot][thread] table
-    {
-      auto off = [](uint16_t& s) {
-        if (s != kNoSlot) s = slot_off(s);
-      };
-      for (IrOp& o : ir) {
+      std::vector<int32_t> anchor(ir.size());
+      for (size_t i = 0; i < ir.size(); ++i)
+        anchor[i] = ir[i].aux() ? anchor[i - 1] : static_cast<int32_t>(i);
+      auto each_read = [&](const IrOp& o, auto&& f) {
         if (o.is_ext) {
-          OpExt x;
-          std::memcpy(&x, &o.op, sizeof(x));
-          for (int k = 0; k < kCertPerExt; ++k) {
-            off(x.fin[k]);
-            off(x.bs[k]);
-            off(x.next[k]);
+          for (int k = 0; k < o.n_ent; ++k) {
+            if (o.v_fin[k] >= 0) f(o.v_fin[k]);
+            if (o.v_bs[k] >= 0) f(o.v_bs[k]);
+            if (o.v_next[k] >= 0) f(o.v_next[k]);
           }
-          std::memcpy(&o.op, &x, sizeof(x));
-        } else if (o.is_cov) {
-          OpCov x;
-          std::memcpy(&x, &o.op, sizeof(x));
-          for (int j = 0; j < kCovSets; ++j) {
-            off(x.dst[j]);
-            for (int k = 0; k < 4; ++k) off(x.src[j][k]);
-          }
-          std::memcpy(&o.op, &x, sizeof(x));
-        } else {
-          for (int k = 0; k < 4; ++k) off(o.op.pred[k]);
-          off(o.op.dst);
-          if (o.op.kind != OP_SYNC) off(o.op.x0);
-          off(o.op.x1);
-          off(o.op.x2);
+          return;
         }
-      }
-    }
-    // reset per-value state touched by this component (keeps arrays reusable)
-    for (const IrOp& o : ir) {
-      each_read(o, [&](int64_t v) {
-        last_use[v] = -1;
-        slot_of[v] = kNoSlot;
-      });
-      each_write(o, [&](int64_t v) {
-        if (v < static_cast<int64_t>(last_use.size())) {
-          last_use[v] = -1;
+        if (o.is_cov) {
+          for (int j = 0; j < o.n_sets; ++j)
+            for (int k = 0; k < 4; ++k)
+              if (o.v_cov_src[j][k] >= 0) f(o.v_cov_src[j][k]);
+          return;
+        }
+        for (int k = 0; k < o.op.npred; ++k) f(o.v_pred[k]);
+        if (o.v_cov1_src >= 0) f(o.v_cov1_src);
+      };
+      auto each_write = [&](const IrOp& o, auto&& f) {
+        if (o.is_ext) return;
+        if (o.is_cov) {
+          for (int j = 0; j < o.n_sets; ++j)
+            if (o.v_cov_dst[j] >= 0) f(o.v_cov_dst[j]);
+          return;
+        }
+        if (o.v_dst >= 0) f(o.v_dst);
+        if ((o.op.flags & F_STORE_START) && o.v_x2 >= 0) f(o.v_x2);
+        if (o.v_cov1_dst >= 0) f(o.v_cov1_dst);
+      };
+      for (size_t i = 0; i < ir.size(); ++i)
+        each_read(ir[i], [&](int64_t v) {
+          ensure(v);
+          last_use[v] = std::max(last_use[v], anchor[i]);
+        });
+
+      // ---- linear-scan slot assignment.  An op group (op + its auxiliary
+      // records) reads every operand before it writes.  Operands dying in the
+      // group are released at the group's end; the op's own results are placed
+      // before that (so they never alias a group operand), the coverage results
+      // after it.
+      std::priority_queue<int32_t, std::vector<int32_t>, std::greater<>> free_slots;
+      int32_t n_slots = kFirstSlot;
+      std::vector<int64_t> dying;
+      bool broken = false;
+      auto flush = [&] {
+        std::sort(dying.begin(), dying.end());
+        dying.erase(std::unique(dying.begin(), dying.end()), dying.end());
+        for (int64_t v : dying) {
+          free_slots.push(slot_of[v]);
           slot_of[v] = kNoSlot;
         }
-      });
-    }
+        dying.clear();
+      };
+      for (size_t i = 0; i < ir.size(); ++i) {
+        IrOp& o = ir[i];
+        const int32_t at = anchor[i];
+        auto read_slot = [&](int64_t v) -> uint16_t {
+          if (v < 0) return kNoSlot;
+          if (slot_of[v] == kNoSlot) {
+            broken = true;
+            return kNoSlot;
+          }
+          if (last_use[v] == at) dying.push_back(v);
+          return static_cast<uint16_t>(slot_of[v]);
+        };
+        auto write_slot = [&](int64_t v) -> uint16_t {
+          if (v < 0) return kSlotTrash;
+          ensure(v);
+          if (last_use[v] <= at) return kSlotTrash;  // nobody reads it later
+          int32_t s;
+          if (!free_slots.empty()) {
+            s = free_slots.top();
+            free_slots.pop();
+          } else {
+            s = n_slots++;
+          }
+          slot_of[v] = s;
+          return static_cast<uint16_t>(s);
+        };
+        const bool group_end = i + 1 >= ir.size() || !ir[i + 1].aux();
+        if (o.is_ext) {
+          OpExt x{};
+          for (int k = 0; k < kCertPerExt; ++k) x.fin[k] = x.bs[k] = x.next[k] = kNoSlot;
+          for (int k = 0; k < o.n_ent; ++k) {
+            x.fin[k] = read_slot(o.v_fin[k]);
+            x.bs[k] = read_slot(o.v_bs[k]);
+            x.next[k] = read_slot(o.v_next[k]);
+          }
+          x.n = static_cast<uint16_t>(o.n_ent);
+          std::memcpy(&o.op, &x, sizeof(Op));
+          if (group_end) flush();
+          continue;
+        }
+        if (o.is_cov) {
+          OpCov x{};
+          for (int j = 0; j < kCovSets; ++j) {
+            x.dst[j] = kNoSlot;
+            for (int k = 0; k < 4; ++k) x.src[j][k] = kNoSlot;
+          }
+          for (int j = 0; j < o.n_sets; ++j)
+            for (int k = 0; k < 4; ++k) x.src[j][k] = read_slot(o.v_cov_src[j][k]);
+          if (group_end) flush();
+          for (int j = 0; j < o.n_sets; ++j) x.dst[j] = write_slot(o.v_cov_dst[j]);
+          for (int j = o.n_sets; j < kCovSets; ++j) x.dst[j] = kSlotTrash;
+          x.n_sets = static_cast<uint16_t>(o.n_sets);
+          std::memcpy(&o.op, &x, sizeof(Op));
+          continue;
+        }
+        for (int k = 0; k < o.op.npred; ++k) o.op.pred[k] = read_slot(o.v_pred[k]);
+        for (int k = o.op.npred; k < 4; ++k) o.op.pred[k] = kSlotOrigin;
+        const uint16_t cov_src = (o.op.flags & F_TRACK1) ? read_slot(o.v_cov1_src) : kNoSlot;
+        // the walk reads an F_TRACK1 coverage source after writing the op's
+        // results, so a dying source is released only after they are placed
+        int64_t late_free = -1;
+        if ((o.op.flags & F_TRACK1) && o.v_cov1_src >= 0 &&
+            std::find(dying.begin(), dying.end(), o.v_cov1_src) != dying.end()) {
+          dying.erase(std::remove(dying.begin(), dying.end(), o.v_cov1_src), dying.end());
+          late_free = o.v_cov1_src;
+        }
+        if (group_end) flush();
+        ensure(o.v_dst >= 0 ? o.v_dst : 0);
+        if (o.v_dst >= 0 && o.v_dst < V_ACC && last_use[o.v_dst] <= at &&
+            (o.op.kind == OP_NODE || o.op.kind == OP_GATED || o.op.kind == OP_FINISH ||
+             o.op.kind == OP_SYNC))
+          o.op.flags |= F_SINK;
+        o.op.dst = write_slot(o.v_dst);
+        if (o.op.kind != OP_SYNC) o.op.x0 = kNoSlot;
+        o.op.x1 = kNoSlot;
+        if (o.op.flags & F_TRACK1) {
+          o.op.x0 = cov_src == kNoSlot ? kSlotInf : cov_src;
+          o.op.x1 = write_slot(o.v_cov1_dst);
+        }
+        o.op.x2 = (o.op.flags & F_STORE_START) ? write_slot(o.v_x2) : kNoSlot;
+        if (o.op.kind == OP_POST || o.op.kind == OP_WAIT)
+          o.op.x1 = static_cast<uint16_t>(o.v_x1);  // mailbox id, not a slot
+        if (late_free >= 0) {
+          free_slots.push(slot_of[late_free]);
+          slot_of[late_free] = kNoSlot;
+        }
+      }
+      if (std::getenv("LUMOS_DEBUG_SLOTS") && c == 0) {
+        // replay the allocation to find the peak live set (debug only)
+        std::vector<int64_t> live;
+        std::vector<int64_t> peak;
+        std::vector<char> alive(last_use.size(), 0);
+        for (size_t i = 0; i < ir.size(); ++i) {
+          each_write(ir[i], [&](int64_t v) {
+            if (last_use[v] > anchor[i]) alive[v] = 1, live.push_back(v);
+          });
+          live.erase(std::remove_if(live.begin(), live.end(),
+                                    [&](int64_t v) { return last_use[v] <= anchor[i]; }),
+                     live.end());
+          if (live.size() > peak.size()) peak = live;
+        }
+        int kinds[5] = {0, 0, 0, 0, 0};
+        std::map<std::string, int> by;
+        for (int64_t v : peak) {
+          int k = v < n ? 0 : v < V_COV ? 1 : v < V_ACC ? 2 : 3;
+          kinds[k]++;
+          if (k <= 1) {
+            int32_t t = static_cast<int32_t>(k == 0 ? v : v - n);
+            std::string key = std::string(k ? "START " : "FIN ") +
+                              (d.lane_kind[t] ? "stream" : "thread") + std::to_string(d.lane[t]) +
+                              " op" + std::to_string(d.op_class ? d.op_class[t] : 9);
+            by[key]++;
+          }
+        }
+        fprintf(stderr, "[slots] comp 0 peak %zu: fin %d start %d cov %d acc %d\n", peak.size(),
+                kinds[0], kinds[1], kinds[2], kinds[3]);
+        for (auto& [k, cnt] : by) fprintf(stderr, "[slots]   %s x%d\n", k.c_str(), cnt);
+      }
+      if (broken) {
+        err = "internal: compiled order reads a value before it is defined";
+        {
+              finish_rc = TS_E_UNSUPPORTED;
+              return -1;
+            }
+      }
+      if (n_slots > kMaxSlots) {
+        err = "unsupported graph: a component needs " + std::to_string(n_slots) +
+              " live values per scenario (limit " + std::to_string(kMaxSlots) + ")";
+        {
+              finish_rc = TS_E_UNSUPPORTED;
+              return -1;
+            }
+      }
+      // slot numbers -> byte offsets into the [slot][thread] table
+      {
+        auto off = [](uint16_t& s) {
+          if (s != kNoSlot) s = slot_off(s);
+        };
+        for (IrOp& o : ir) {
+          if (o.is_ext) {
+            OpExt x;
+            std::memcpy(&x, &o.op, sizeof(x));
+            for (int k = 0; k < kCertPerExt; ++k) {
+              off(x.fin[k]);
+              off(x.bs[k]);
+              off(x.next[k]);
+            }
+            std::memcpy(&o.op, &x, sizeof(x));
+          } else if (o.is_cov) {
+            OpCov x;
+            std::memcpy(&x, &o.op, sizeof(x));
+            for (int j = 0; j < kCovSets; ++j) {
+              off(x.dst[j]);
+              for (int k = 0; k < 4; ++k) off(x.src[j][k]);
+            }
+            std::memcpy(&o.op, &x, sizeof(x));
+          } else {
+            for (int k = 0; k < 4; ++k) off(o.op.pred[k]);
+            off(o.op.dst);
+            if (o.op.kind != OP_SYNC) off(o.op.x0);
+            if (o.op.kind != OP_POST && o.op.kind != OP_WAIT) off(o.op.x1);
+            off(o.op.x2);
+          }
+        }
+      }
+      // reset per-value state touched by this component (keeps arrays reusable)
+      for (const IrOp& o : ir) {
+        each_read(o, [&](int64_t v) {
+          last_use[v] = -1;
+          slot_of[v] = kNoSlot;
+        });
+        each_write(o, [&](int64_t v) {
+          if (v < static_cast<int64_t>(last_use.size())) {
+            last_use[v] = -1;
+            slot_of[v] = kNoSlot;
+          }
+        });
+      }
 
-    // ---- pad so that no op group straddles a kChunk boundary
-    {
-      std::vector<IrOp> padded;
-      padded.reserve(ir.size() + ir.size() / 16 + 8);
+      // ---- pad so that no op group straddles a kChunk boundary
+      {
+        std::vector<IrOp> padded;
+        padded.reserve(ir.size() + ir.size() / 16 + 8);
+        size_t i = 0;
+        while (i < ir.size()) {
+          size_t g = 1;
+          while (i + g < ir.size() && ir[i + g].aux()) ++g;
+          if (g > static_cast<size_t>(kChunk)) {
+            err = "unsupported graph: op group larger than a program chunk";
+            {
+              finish_rc = TS_E_UNSUPPORTED;
+              return -1;
+            }
+          }
+          size_t pos = padded.size() % kChunk;
+          if (pos + g > static_cast<size_t>(kChunk)) {
+            for (size_t k = pos; k < static_cast<size_t>(kChunk); ++k) {
+              IrOp nop;
+              nop.op.kind = OP_NOP;
+              nop.op.node = -1;
+              nop.op.flags = F_NO_OUT;
+              for (int q = 0; q < 4; ++q) nop.op.pred[q] = slot_off(kSlotOrigin);
+              nop.op.dst = slot_off(kSlotTrash);
+              nop.op.x0 = nop.op.x1 = nop.op.x2 = kNoSlot;
+              padded.push_back(nop);
+            }
+          }
+          for (size_t k = 0; k < g; ++k) padded.push_back(ir[i + k]);
+          i += g;
+        }
+        ir.swap(padded);
+      }
+
+      // ---- de-duplicate identical programs (TP / DP replicas of one stage)
+      uint64_t h = 1469598103934665603ull;
+      const unsigned char* bytes = reinterpret_cast<const unsigned char*>(ir.data());
+      (void)bytes;
+      for (const IrOp& o : ir) {
+        const unsigned char* p = reinterpret_cast<const unsigned char*>(&o.op);
+        for (size_t k = 0; k < sizeof(Op); ++k) h = (h ^ p[k]) * 1099511628211ull;
+      }
+      h ^= static_cast<uint64_t>(n_slots) * 0x9E3779B97F4A7C15ull;
+      int32_t prog = -1;
+      if (contiguous) {
+        for (int32_t cand : prog_by_hash[h]) {
+          const ProgramDesc& pd = out.programs[cand];
+          if (pd.n_ops != static_cast<int32_t>(ir.size()) || pd.n_slots != n_slots) continue;
+          bool same = true;
+          for (size_t k = 0; k < ir.size() && same; ++k)
+            same = std::memcmp(&out.ops[pd.op_offset + k], &ir[k].op, sizeof(Op)) == 0;
+          if (same) {
+            prog = cand;
+            break;
+          }
+        }
+      }
+      if (prog < 0) {
+        prog = static_cast<int32_t>(out.programs.size());
+        ProgramDesc pd;
+        pd.op_offset = static_cast<int64_t>(out.ops.size());
+        pd.n_ops = static_cast<int32_t>(ir.size());
+        pd.n_slots = n_slots;
+        out.programs.push_back(pd);
+        for (const IrOp& o : ir) out.ops.push_back(o.op);
+        if (contiguous) prog_by_hash[h].push_back(prog);
+      }
+      n_slots_out = n_slots;
+      return prog;
+    };
+
+    // ---- cooperative components (several ranks coupled by gates, estimate
+    // mode): one program per rank, in the component's order restricted to the
+    // rank; a value one rank produces and another reads travels through a
+    // shared-memory mailbox (OP_POST after its producer, OP_WAIT before its
+    // first reader in the other rank).  Restrictions of one topological order
+    // cannot wait on each other in a cycle, so the warps always progress.
+    std::vector<int32_t> rank_local;  // per op: index of its rank in the component
+    int32_t n_local = 1;
+    if (coop) {
+      std::vector<int32_t> comp_ranks;
+      for (int32_t t : comp_tasks) comp_ranks.push_back(d.rank[t]);
+      std::sort(comp_ranks.begin(), comp_ranks.end());
+      comp_ranks.erase(std::unique(comp_ranks.begin(), comp_ranks.end()), comp_ranks.end());
+      n_local = static_cast<int32_t>(comp_ranks.size());
+    }
+    std::vector<int32_t> progs_of_comp;
+    int32_t n_slots = 0;
+    if (!coop || n_local <= 1) {
+      const int32_t prog = finish_program(ir, n_slots);
+      if (prog < 0) return finish_rc;
+      progs_of_comp.push_back(prog);
+      out.max_slots = std::max(out.max_slots, n_slots);
+    } else {
+      std::vector<int32_t> comp_ranks;
+      for (int32_t t : comp_tasks) comp_ranks.push_back(d.rank[t]);
+      std::sort(comp_ranks.begin(), comp_ranks.end());
+      comp_ranks.erase(std::unique(comp_ranks.begin(), comp_ranks.end()), comp_ranks.end());
+      auto local_of = [&](int32_t rank) {
+        return static_cast<int32_t>(std::lower_bound(comp_ranks.begin(), comp_ranks.end(), rank) -
+                                    comp_ranks.begin());
+      };
+      // rank of every op: a task's rank; a fold (ACC) op takes its consumer's;
+      // auxiliary records their op's
+      rank_local.assign(ir.size(), -1);
+      for (size_t i = 0; i < ir.size(); ++i)
+        if (!ir[i].aux() && ir[i].op.kind != OP_ACC && ir[i].op.node >= 0)
+          rank_local[i] = local_of(d.rank[node_base + ir[i].op.node]);
+      for (size_t i = ir.size(); i-- > 0;)
+        if (rank_local[i] < 0 && !ir[i].aux())
+          rank_local[i] = i + 1 < ir.size() ? rank_local[i + 1] : 0;
+      for (size_t i = 0; i < ir.size(); ++i)
+        if (ir[i].aux()) rank_local[i] = rank_local[i - 1];
+      // producers, and the values other ranks read
+      std::unordered_map<int64_t, int32_t> producer;
+      auto writes_of = [&](const IrOp& o, auto&& f) {
+        if (o.is_ext) return;
+        if (o.is_cov) {
+          for (int j = 0; j < o.n_sets; ++j)
+            if (o.v_cov_dst[j] >= 0) f(o.v_cov_dst[j]);
+          return;
+        }
+        if (o.v_dst >= 0) f(o.v_dst);
+        if ((o.op.flags & F_STORE_START) && o.v_x2 >= 0) f(o.v_x2);
+        if (o.v_cov1_dst >= 0) f(o.v_cov1_dst);
+      };
+      auto reads_of = [&](IrOp& o, auto&& f) {  // f(int64_t& value)
+        if (o.is_ext) {
+          for (int k = 0; k < o.n_ent; ++k) {
+            if (o.v_fin[k] >= 0) f(o.v_fin[k]);
+            if (o.v_bs[k] >= 0) f(o.v_bs[k]);
+            if (o.v_next[k] >= 0) f(o.v_next[k]);
+          }
+          return;
+        }
+        if (o.is_cov) {
+          for (int j = 0; j < o.n_sets; ++j)
+            for (int k = 0; k < 4; ++k)
+              if (o.v_cov_src[j][k] >= 0) f(o.v_cov_src[j][k]);
+          return;
+        }
+        for (int k = 0; k < o.op.npred; ++k) f(o.v_pred[k]);
+        if (o.v_cov1_src >= 0) f(o.v_cov1_src);
+      };
+      for (size_t i = 0; i < ir.size(); ++i)
+        writes_of(ir[i], [&](int64_t v) { producer[v] = rank_local[i]; });
+      std::unordered_map<int64_t, int32_t> mailbox;  // value -> mailbox id
+      for (size_t i = 0; i < ir.size(); ++i)
+        reads_of(ir[i], [&](int64_t& v) {
+          auto it = producer.find(v);
+          if (it != producer.end() && it->second != rank_local[i] && !mailbox.count(v)) {
+            const int32_t m = static_cast<int32_t>(mailbox.size());
+            mailbox.emplace(v, m);
+          }
+        });
+      if (mailbox.size() > 0xFFFF) {
+        err = "unsupported graph: too many cross-rank values in one component";
+        return TS_E_UNSUPPORTED;
+      }
+      // per-rank streams: WAITs before a group's first cross read, the group,
+      // POSTs after a group's mailbox values
+      std::vector<std::vector<IrOp>> streams(n_local);
+      std::vector<std::unordered_map<int64_t, int64_t>> local_copy(n_local);
       size_t i = 0;
       while (i < ir.size()) {
         size_t g = 1;
         while (i + g < ir.size() && ir[i + g].aux()) ++g;
-        if (g > static_cast<size_t>(kChunk)) {
-          err = "unsupported graph: op group larger than a program chunk";
-          return TS_E_UNSUPPORTED;
-        }
-        size_t pos = padded.size() % kChunk;
-        if (pos + g > static_cast<size_t>(kChunk)) {
-          for (size_t k = pos; k < static_cast<size_t>(kChunk); ++k) {
-            IrOp nop;
-            nop.op.kind = OP_NOP;
-            nop.op.node = -1;
-            nop.op.flags = F_NO_OUT;
-            for (int q = 0; q < 4; ++q) nop.op.pred[q] = slot_off(kSlotOrigin);
-            nop.op.dst = slot_off(kSlotTrash);
-            nop.op.x0 = nop.op.x1 = nop.op.x2 = kNoSlot;
-            padded.push_back(nop);
-          }
-        }
-        for (size_t k = 0; k < g; ++k) padded.push_back(ir[i + k]);
+        const int32_t r = rank_local[i];
+        auto& st = streams[r];
+        for (size_t k = i; k < i + g; ++k)
+          reads_of(ir[k], [&](int64_t& v) {
+            auto mb = mailbox.find(v);
+            if (mb == mailbox.end() || producer[v] == r) return;
+            auto lc = local_copy[r].find(v);
+            if (lc == local_copy[r].end()) {
+              IrOp w;
+              w.op.kind = OP_WAIT;
+              w.op.node = -1;
+              w.op.flags = F_NO_OUT;
+              w.op.npred = 0;
+              w.op.x1 = static_cast<uint16_t>(mb->second);
+              w.v_dst = acc_next++;
+              w.v_x1 = mb->second;
+              st.push_back(w);
+              lc = local_copy[r].emplace(v, w.v_dst).first;
+            }
+            v = lc->second;
+          });
+        for (size_t k = i; k < i + g; ++k) st.push_back(ir[k]);
+        for (size_t k = i; k < i + g; ++k)
+          writes_of(ir[k], [&](int64_t v) {
+            auto mb = mailbox.find(v);
+            if (mb == mailbox.end()) return;
+            IrOp pst;
+            pst.op.kind = OP_POST;
+            pst.op.node = -1;
+            pst.op.flags = F_NO_OUT;
+            pst.op.npred = 1;
+            pst.v_pred[0] = v;
+            pst.v_x1 = mb->second;
+            st.push_back(pst);
+          });
         i += g;
       }
-      ir.swap(padded);
-    }
-
-    // ---- de-duplicate identical programs (TP / DP replicas of one stage)
-    uint64_t h = 1469598103934665603ull;
-    const unsigned char* bytes = reinterpret_cast<const unsigned char*>(ir.data());
-    (void)bytes;
-    for (const IrOp& o : ir) {
-      const unsigned char* p = reinterpret_cast<const unsigned char*>(&o.op);
-      for (size_t k = 0; k < sizeof(Op); ++k) h = (h ^ p[k]) * 1099511628211ull;
-    }
-    h ^= static_cast<uint64_t>(n_slots) * 0x9E3779B97F4A7C15ull;
-    int32_t prog = -1;
-    if (contiguous) {
-      for (int32_t cand : prog_by_hash[h]) {
-        const ProgramDesc& pd = out.programs[cand];
-        if (pd.n_ops != static_cast<int32_t>(ir.size()) || pd.n_slots != n_slots) continue;
-        bool same = true;
-        for (size_t k = 0; k < ir.size() && same; ++k)
-          same = std::memcmp(&out.ops[pd.op_offset + k], &ir[k].op, sizeof(Op)) == 0;
-        if (same) {
-          prog = cand;
-          break;
-        }
+      for (int32_t r = 0; r < n_local; ++r) {
+        int32_t ns = 0;
+        const int32_t prog = finish_program(streams[r], ns);
+        if (prog < 0) return finish_rc;
+        progs_of_comp.push_back(prog);
+        n_slots = std::max(n_slots, ns);
       }
+      out.max_slots = std::max(out.max_slots, n_slots);
+      out.max_coop_path = std::max(out.max_coop_path, comp_path[c]);
+      out.max_mailboxes = std::max(out.max_mailboxes, static_cast<int32_t>(mailbox.size()));
+      out.max_coop_ranks = std::max(out.max_coop_ranks, n_local);
     }
-    if (prog < 0) {
-      prog = static_cast<int32_t>(out.programs.size());
-      ProgramDesc pd;
-      pd.op_offset = static_cast<int64_t>(out.ops.size());
-      pd.n_ops = static_cast<int32_t>(ir.size());
-      pd.n_slots = n_slots;
-      out.programs.push_back(pd);
-      for (const IrOp& o : ir) out.ops.push_back(o.op);
-      if (contiguous) prog_by_hash[h].push_back(prog);
-    }
-    out.max_slots = std::max(out.max_slots, n_slots);
+    const int32_t prog = progs_of_comp[0];
+    out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
+    for (int32_t pg : progs_of_comp) out.coop_progs.push_back(pg);
     {
       int64_t sum = 0;
       for (int32_t t : comp_tasks) {
@@ -1063,6 +1245,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
   }
+  out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
 
   return TS_OK;
 }

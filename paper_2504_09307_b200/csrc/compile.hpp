@@ -34,6 +34,13 @@ struct CompiledGraph {
   std::vector<ProgramDesc> programs;
   std::vector<ComponentDesc> comps;
   int32_t max_slots = 0;
+  // cooperative components (program.hpp OP_POST / OP_WAIT): per component its
+  // rank programs coop_progs[coop_prog_off[c] .. coop_prog_off[c+1]) (one entry
+  // for a single-rank component)
+  std::vector<int32_t> coop_prog_off, coop_progs;
+  int32_t max_mailboxes = 0;
+  int32_t max_coop_ranks = 1;
+  int64_t max_coop_path = 0;  // nominal longest path of a cooperative component
   // largest per-component sum of base durations and task count: with the
   // scenario's worst-case duration factor they bound every time of a replay
   // (W + any path <= W + sum of the component's durations), which decides

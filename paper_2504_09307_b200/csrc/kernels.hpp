@@ -122,6 +122,23 @@ int walk_threads();
 int walk_width(int n_slots, bool rel32);  // walk CTA width for a slot count (0: too many)
 int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
+
+// Cooperative walk (components of several ranks coupled by gates): one CTA =
+// (component, 32 scenarios), one warp per rank program, cross-rank values
+// through shared-memory mailboxes (program.hpp OP_POST / OP_WAIT).  Uses the
+// WalkParams of the launch (outputs, scenarios, window) with comp_order /
+// n_comps naming the cooperative components.
+struct CoopParams {
+  const int32_t* prog_off;  // [n_all_comps + 1] into progs
+  const int32_t* progs;     // rank programs per component
+  int32_t max_ranks;        // warps per CTA
+  int32_t n_mail;           // mailboxes per CTA (max over components)
+  int32_t n_slots;          // slots per rank program (max)
+  int32_t rel32;            // uint32 offsets from W (additions checked, wraps -> fix-up)
+  int32_t fixup;            // re-run only chunks holding a scenario with status bit 0
+  int32_t pad;
+};
+cudaError_t launch_coop_walk(const WalkParams& p, const CoopParams& c, cudaStream_t stream);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
                              cudaStream_t stream);
 // compare_replay deltas of one tile: partial[chunk][count][3] then per column

@@ -66,6 +66,9 @@ enum OpKind : uint8_t {
   OP_FINISH = 4,  // start = slot[pred0]; fin = max(start, preds[1..)) + d
   OP_GATED = 5,   // start = max(W, preds[0..nfixed)); fin = max(start, preds[nfixed..)) + d
   OP_NOP = 6,     // padding to a chunk boundary
+  // cooperative multi-rank walks (one warp per rank of a component):
+  OP_POST = 7,    // mailbox[x1] = slot[pred0], then its ready flag
+  OP_WAIT = 8,    // wait for mailbox[x1]'s flag, slot[dst] = mailbox[x1]
 };
 
 enum OpFlags : uint8_t {

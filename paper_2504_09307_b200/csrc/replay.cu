@@ -347,6 +347,203 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   }
 }
 
+// ------------------------------------------------------------------- K1c
+// Cooperative walk: a CTA replays one component for 32 scenarios (lane =
+// scenario) with one warp per rank program; the programs are the component's
+// op order restricted to each rank, so a warp only ever waits for values
+// another warp produces earlier in that order (no cycles).  Records are read
+// straight from global memory (one-record lookahead), slots live in the warp's
+// own [slot][32] table, cross-rank values in [mailbox][32] with a ready flag.
+// A wait that spins ~1 s marks the scenario failed (status -2) rather than
+// hang; it cannot happen for a correctly compiled component.
+template <int kMode, typename V>
+__global__ void __launch_bounds__(1024) coop_walk_kernel(WalkParams P, CoopParams C) {
+  constexpr bool kRel = sizeof(V) == 4;
+  constexpr int kShiftC = kRel ? 0 : 1;  // record field s*128 -> s*32*sizeof(V)
+  constexpr V kInfV = kRel ? static_cast<V>(0xFFFFFFFFu) : static_cast<V>(kMaxI64);
+  extern __shared__ int4 smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int comp_i = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
+  const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
+  const int comp = P.comp_order[comp_i];
+  int* flags = reinterpret_cast<int*>(smem);
+  V* mail = reinterpret_cast<V*>(reinterpret_cast<char*>(smem) + ((C.n_mail * 4 + 15) / 16) * 16);
+  char* slots = reinterpret_cast<char*>(mail + static_cast<size_t>(C.n_mail) * 32);
+  for (int i = threadIdx.x; i < C.n_mail; i += blockDim.x) flags[i] = 0;
+  if (C.fixup) {  // int64 re-run of chunks where a uint32 addition wrapped
+    const int c = min(chunk * 32 + lane, P.sp.count - 1);
+    if (!__syncthreads_or((P.status[c] & 1) != 0)) return;
+  }
+  __syncthreads();
+  const int pfirst = C.prog_off[comp], nw = C.prog_off[comp + 1] - pfirst;
+  if (w >= nw) return;  // no block-wide barrier after this point
+  char* slot_base = slots + static_cast<size_t>(w) * C.n_slots * 32 * sizeof(V) + lane * sizeof(V);
+#define SLOTC(field) \
+  (*reinterpret_cast<V*>(slot_base + (static_cast<uint32_t>(field) << kShiftC)))
+  const ComponentDesc cd = P.comps[comp];
+  const ProgramDesc pd = P.progs[C.progs[pfirst + w]];
+  const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
+  const int n_ops = pd.n_ops;
+  const int last = P.sp.count - 1;
+  const int col = min(chunk * 32 + lane, last);
+  const int64_t W = P.window_start;
+  const V w0 = kRel ? V(0) : static_cast<V>(W);
+  auto absv = [&](V v) -> int64_t { return kRel ? W + static_cast<int64_t>(v) : static_cast<int64_t>(v); };
+  SLOTC(slot_off(kSlotOrigin)) = w0;
+  SLOTC(slot_off(kSlotInf)) = kInfV;
+  ThreadScen ts;
+  init_thread_scen(P.sp, col, ts);
+  int64_t hi = kMinI64;
+  bool fail = false, stalled = false;
+  int64_t* const start_c = P.out_start + col;
+  int64_t* const fin_c = P.out_fin + col;
+  const uint64_t ld = static_cast<uint64_t>(P.ld);
+  int4 ra = n_ops > 0 ? __ldg(gops) : int4{}, rb = n_ops > 0 ? __ldg(gops + 1) : int4{};
+  for (int i = 0; i < n_ops && !stalled; ++i) {
+    const int4 ca = ra, cb = rb;
+    if (i + 1 < n_ops) {  // lookahead
+      ra = __ldg(gops + 2 * (i + 1));
+      rb = __ldg(gops + 2 * (i + 1) + 1);
+    }
+    const uint32_t hdr = static_cast<uint32_t>(ca.w);
+    const uint32_t kind = hdr & 0xFFu, cls_b = (hdr >> 16) & 0xFFu, flags_op = hdr >> 24;
+    const uint32_t w0f = cb.x, w1f = cb.y, w2f = cb.z, w3f = cb.w;
+    if (kind == OP_NOP) continue;
+    const V p0 = SLOTC(lo16(w0f)), p1 = SLOTC(hi16(w0f));
+    const V p2 = SLOTC(lo16(w1f)), p3 = SLOTC(hi16(w1f));
+    if (kind == OP_POST || kind == OP_WAIT) {
+      const int m = static_cast<int>(lo16(w3f));  // x1: mailbox id
+      volatile V* box = mail + static_cast<size_t>(m) * 32 + lane;
+      if (kind == OP_POST) {
+        *box = p0;
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          atomicExch(flags + m, 1);
+        }
+      } else {
+        if (lane == 0) {
+          int spins = 0;
+          while (atomicAdd(flags + m, 0) == 0) {
+            __nanosleep(64);
+            if (++spins > (1 << 24)) {
+              stalled = true;
+              break;
+            }
+          }
+        }
+        stalled = __shfl_sync(0xFFFFFFFFu, stalled, 0);
+        __syncwarp();
+        __threadfence_block();
+        SLOTC(lo16(w2f)) = *box;
+      }
+      continue;
+    }
+    V st, fb;
+    if (kind <= OP_ACC) {
+      st = vmax(vmax(p0, p1), vmax(p2, p3));
+      fb = st;
+    } else if (kind == OP_FINISH) {
+      st = p0;
+      fb = vmax(vmax(p0, p1), vmax(p2, p3));
+    } else {  // OP_GATED
+      const int nfixed = static_cast<int>(cls_b >> 4);
+      st = w0;
+      V gate = w0;
+      if (nfixed > 0) st = vmax(st, p0); else gate = vmax(gate, p0);
+      if (nfixed > 1) st = vmax(st, p1); else gate = vmax(gate, p1);
+      if (nfixed > 2) st = vmax(st, p2); else gate = vmax(gate, p2);
+      gate = vmax(gate, p3);
+      fb = vmax(st, gate);
+    }
+    if (kind == OP_ACC) {
+      SLOTC(lo16(w2f)) = st;
+      continue;
+    }
+    if (kind == OP_SYNC) {
+      const V rs = st;
+      V S = rs;
+      const int n_ext = static_cast<int>(hi16(w2f));
+      for (int e = 0; e < n_ext; ++e) {
+        const int4 xa = __ldg(gops + 2 * (i + 1 + e));
+        const int n = __ldg(gops + 2 * (i + 1 + e) + 1).z & 0xFFFF;
+        const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
+        for (int k = 0; k < kCertPerExt; ++k)
+          if (k < n && f[k] != kNoSlot) S = vmax(S, SLOTC(f[k]));
+      }
+      bool cov = S == rs;
+      for (int e = 0; e < n_ext; ++e) {
+        const int4 xa = __ldg(gops + 2 * (i + 1 + e)), xb = __ldg(gops + 2 * (i + 1 + e) + 1);
+        const int n = xb.z & 0xFFFF;
+        const uint32_t f[4] = {lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)};
+        const uint32_t cv[4] = {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)};
+        const uint32_t nx[4] = {lo16(xb.x), hi16(xb.x), lo16(xb.y), hi16(xb.y)};
+        for (int k = 0; k < kCertPerExt; ++k) {
+          if (k >= n) continue;
+          if (f[k] != kNoSlot && cv[k] != kNoSlot)
+            cov = cov || (SLOTC(f[k]) == S && SLOTC(cv[k]) <= rs);
+          if (nx[k] != kNoSlot) fail = fail || SLOTC(nx[k]) <= S;
+        }
+      }
+      fail = fail || !cov;
+      st = S;
+      fb = S;
+      i += n_ext;
+      if (i + 1 < n_ops) {  // the lookahead skipped the certificate records
+        ra = __ldg(gops + 2 * (i + 1));
+        rb = __ldg(gops + 2 * (i + 1) + 1);
+      }
+    }
+    if (kind == OP_START) {
+      SLOTC(lo16(w2f)) = st;
+    } else {
+      const int64_t task = static_cast<int64_t>(cd.node_base) + ca.z;
+      const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ca.y)) << 32) |
+                           static_cast<uint32_t>(ca.x);
+      const int64_t d = scenario_duration<kMode>(P.sp, ts, task, base, static_cast<int>(cls_b & 15u));
+      const V fin = static_cast<V>(fb + static_cast<V>(d));
+      // uint32 windows are sized by the nominal path: an addition that wraps
+      // sends the scenario to the exact event-driven fix-up instead
+      if (kRel && (fin < fb || d > 0xFFFFFFFFll)) fail = true;
+      SLOTC(lo16(w2f)) = fin;
+      if (flags_op & F_STORE_START) SLOTC(hi16(w3f)) = st;
+      if (flags_op & F_SINK) hi = imax(hi, absv(fin));
+      const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
+      if (P.out_start) __stcs(start_c + at, absv(st));
+      if (P.out_fin) __stcs(fin_c + at, absv(fin));
+    }
+    if (flags_op & F_TRACK1) {
+      const V cs = SLOTC(hi16(w2f));
+      SLOTC(lo16(w3f)) = p0 >= st ? vmin(st, cs) : st;
+    } else if (flags_op & F_TRACK) {
+      const int4 xa = __ldg(gops + 2 * (i + 1)), xb = __ldg(gops + 2 * (i + 1) + 1);
+      const uint32_t src[2][4] = {{lo16(xa.x), hi16(xa.x), lo16(xa.y), hi16(xa.y)},
+                                  {lo16(xa.z), hi16(xa.z), lo16(xa.w), hi16(xa.w)}};
+      const uint32_t cdst[2] = {lo16(xb.x), hi16(xb.x)};
+      const int n_sets = xb.y & 0xFFFF;
+      const V pv[4] = {p0, p1, p2, p3};
+      for (int j = 0; j < kCovSets && j < n_sets; ++j) {
+        V cvj = st;
+        for (int k = 0; k < 4; ++k)
+          if (src[j][k] != kNoSlot && pv[k] >= st) cvj = vmin(cvj, SLOTC(src[j][k]));
+        SLOTC(cdst[j]) = cvj;
+      }
+      i += 1;
+      if (i + 1 < n_ops) {
+        ra = __ldg(gops + 2 * (i + 1));
+        rb = __ldg(gops + 2 * (i + 1) + 1);
+      }
+    }
+  }
+#undef SLOTC
+  if (hi != kMinI64) {
+    atomicMin(reinterpret_cast<long long*>(P.span_lo) + col, static_cast<long long>(W));
+    atomicMax(reinterpret_cast<long long*>(P.span_hi) + col, static_cast<long long>(hi));
+  }
+  if (stalled) atomicExch(P.status + col, -2);
+  else if (fail) atomicOr(P.status + col, 1);
+}
+
 __global__ void span_init_kernel(int64_t* lo, int64_t* hi, int32_t* status, int32_t count) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) {
@@ -1053,6 +1250,38 @@ cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t st
                : launch_walk_v<int64_t, 1>(p, n_slots, t, stream);
   return rel ? launch_walk_v<uint32_t, 2>(p, n_slots, t, stream)
              : launch_walk_v<int64_t, 2>(p, n_slots, t, stream);
+}
+
+template <typename V>
+static cudaError_t launch_coop_v(const WalkParams& p, const CoopParams& c, cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>((c.n_mail * 4 + 15) / 16) * 16 +
+                      static_cast<size_t>(c.n_mail) * 32 * sizeof(V) +
+                      static_cast<size_t>(c.max_ranks) * c.n_slots * 32 * sizeof(V);
+  const long long chunks = (p.sp.count + 31) / 32;
+  const long long blocks = chunks * p.n_comps;
+  if (blocks <= 0) return cudaSuccess;
+  const int threads = 32 * c.max_ranks;
+  auto go = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p, c);
+    return cudaGetLastError();
+  };
+  switch (p.sp.mode) {
+    case 0: return go(coop_walk_kernel<0, V>);
+    case kModeScale: return go(coop_walk_kernel<kModeScale, V>);
+    case kModeJitter: return go(coop_walk_kernel<kModeJitter, V>);
+    case kModeScale | kModeJitter: return go(coop_walk_kernel<kModeScale | kModeJitter, V>);
+    default: return go(coop_walk_kernel<kModeExplicit, V>);
+  }
+}
+
+cudaError_t launch_coop_walk(const WalkParams& p, const CoopParams& c, cudaStream_t stream) {
+  if (c.max_ranks < 1 || c.max_ranks > 32) return cudaErrorInvalidConfiguration;
+  return c.rel32 ? launch_coop_v<uint32_t>(p, c, stream) : launch_coop_v<int64_t>(p, c, stream);
 }
 
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,

@@ -62,3 +62,36 @@ def test_estimate_nominal_equals_generator_truth():
     sg = generate_graph(_spec(4, 2, 8, 4, estimate=True))
     res = simulate_batch(sg.graph, ScenarioSpec(count=2), breakdown=False)
     assert (res.makespan == sg.truth_makespan).all()
+
+
+def test_estimate_cooperative_and_single_walks_agree(monkeypatch):
+    # components coupling several ranks walk cooperatively (one warp per rank,
+    # cross-rank values through shared-memory mailboxes); LUMOS_COOP=0 compiles
+    # them as one program instead — both must equal build_pipeline
+    monkeypatch.setenv("LUMOS_COOP", "0")
+    _check((2, 2, 4, 4, 1024, 4096), S=16, seed=5, jitter=0.2)
+    monkeypatch.setenv("LUMOS_COOP", "1")
+    _check((2, 2, 4, 4, 1024, 4096), S=16, seed=5, jitter=0.2)
+
+
+def test_estimate_uint32_window_wrap_fixup(monkeypatch):
+    # a cooperative walk forced onto uint32 offsets for a timeline longer than
+    # 2^32 us (class scale x 30000): every wrapped addition must be caught and
+    # the chunk re-run in int64, still matching build_pipeline
+    monkeypatch.setenv("LUMOS_COOP_FORCE_U32", "1")
+    pp, dp, m, layers, d, f = (2, 2, 4, 4, 1024, 4096)
+    sg = generate_graph(_spec(pp, dp, m, layers, d, f, estimate=True))
+    g = sg.graph
+    S = 8
+    spec = ScenarioSpec(count=S, seed=3, jitter=0.1, scale_lo=30000, scale_hi=30000, scale_den=1)
+    res = simulate_batch(g, spec, breakdown=False)
+    assert int(res.makespan.max()) > 2 ** 32
+    og = _orc_graph(g)
+    sc = R.OrcScenarios(seed=3, jitter=0.1, scale_lo=30000, scale_hi=30000, scale_den=1)
+    spec_json = R.synth_spec(pp=pp, dp=dp, m=m, layers=layers, d_model=d, d_ffn=f)
+    for s in range(S):
+        dur = R.orc_durations(og, sc, s)
+        hook = np.zeros(sg.n_ops, np.int64)
+        hook[sg.op_index] = dur
+        ref, _ = _ref_pipeline(spec_json, hook)
+        assert _my_lane_sequences(og, res.start[:, s], res.fin[:, s]) == ref, f"scenario {s}"
