@@ -1103,12 +1103,8 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     std::vector<int32_t> progs_of_comp;
     int32_t n_slots = 0;
-    if (!coop || n_local <= 1) {
-      const int32_t prog = finish_program(ir, n_slots);
-      if (prog < 0) return finish_rc;
-      progs_of_comp.push_back(prog);
-      out.max_slots = std::max(out.max_slots, n_slots);
-    } else {
+    bool split = coop && n_local > 1 && n_local <= 32;
+    if (split) {
       std::vector<int32_t> comp_ranks;
       for (int32_t t : comp_tasks) comp_ranks.push_back(d.rank[t]);
       std::sort(comp_ranks.begin(), comp_ranks.end());
@@ -1184,8 +1180,9 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         while (i + g < ir.size() && ir[i + g].aux()) ++g;
         const int32_t r = rank_local[i];
         auto& st = streams[r];
-        for (size_t k = i; k < i + g; ++k)
-          reads_of(ir[k], [&](int64_t& v) {
+        std::vector<IrOp> grp(ir.begin() + static_cast<long>(i), ir.begin() + static_cast<long>(i + g));
+        for (IrOp& op : grp)
+          reads_of(op, [&](int64_t& v) {
             auto mb = mailbox.find(v);
             if (mb == mailbox.end() || producer[v] == r) return;
             auto lc = local_copy[r].find(v);
@@ -1203,7 +1200,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
             }
             v = lc->second;
           });
-        for (size_t k = i; k < i + g; ++k) st.push_back(ir[k]);
+        for (IrOp& op : grp) st.push_back(op);
         for (size_t k = i; k < i + g; ++k)
           writes_of(ir[k], [&](int64_t v) {
             auto mb = mailbox.find(v);
@@ -1226,10 +1223,26 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         progs_of_comp.push_back(prog);
         n_slots = std::max(n_slots, ns);
       }
+      // one CTA must hold the mailboxes and every rank's slot table (int64
+      // values, the wider case); otherwise walk the component as one program
+      const size_t smem64 = mailbox.size() * 4 + 16 + mailbox.size() * 32 * 8 +
+                            static_cast<size_t>(n_local) * n_slots * 32 * 8;
+      if (smem64 > 220 * 1024) {
+        split = false;  // the rank programs stay in the table, unused
+        progs_of_comp.clear();
+      } else {
+        out.max_slots = std::max(out.max_slots, n_slots);
+        out.max_coop_path = std::max(out.max_coop_path, comp_path[c]);
+        out.max_mailboxes = std::max(out.max_mailboxes, static_cast<int32_t>(mailbox.size()));
+        out.max_coop_ranks = std::max(out.max_coop_ranks, n_local);
+      }
+    }
+    if (!split) {
+      n_slots = 0;
+      const int32_t prog = finish_program(ir, n_slots);
+      if (prog < 0) return finish_rc;
+      progs_of_comp.push_back(prog);
       out.max_slots = std::max(out.max_slots, n_slots);
-      out.max_coop_path = std::max(out.max_coop_path, comp_path[c]);
-      out.max_mailboxes = std::max(out.max_mailboxes, static_cast<int32_t>(mailbox.size()));
-      out.max_coop_ranks = std::max(out.max_coop_ranks, n_local);
     }
     const int32_t prog = progs_of_comp[0];
     out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
