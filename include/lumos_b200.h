@@ -27,6 +27,10 @@
  * library detects which (cudaPointerGetAttributes) and stages host buffers
  * itself.  There is no CPU execution path: without a CUDA device every compute
  * call fails with TS_E_CUDA.
+ *
+ * Threading (the reference's contract): distinct ts_graph handles
+ * may be used concurrently from different host threads / CUDA streams; one
+ * handle serves one call at a time (it owns the call's staging buffers).
  */
 #ifndef LUMOS_B200_H
 #define LUMOS_B200_H

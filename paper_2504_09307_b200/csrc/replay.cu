@@ -1171,13 +1171,13 @@ int walk_threads() { return kThreads; }
 template <int kT, int kMode, bool kWS, bool kWF, typename V, int kS>
 static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
                                  cudaStream_t stream) {
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
+  // set per launch: the attribute is per device, and several host threads or
+  // devices may launch concurrently
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kWS, kWF, V, kS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   replay_walk_kernel<kT, kMode, kWS, kWF, V, kS><<<blocks, kT, smem, stream>>>(p);
   return cudaGetLastError();
