@@ -338,6 +338,12 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     gates_of[it->second].emplace_back(u, k);
     if (k == TS_GATE_START) split[v] = 1;
   }
+  if (d.n_gates > 0 && !sync_tasks.empty()) {
+    // a failed sync certificate is re-run by the event-driven replay, which
+    // has no gates: gated (estimate) graphs express their syncs as edges
+    err = "unsupported graph: Stream/DeviceSync rules in a graph with gates";
+    return TS_E_UNSUPPORTED;
+  }
   for (int32_t t : sync_tasks)
     if (split[t] || gate_slot.count(t)) {
       err = "unsupported graph: sync task " + std::to_string(t) + " carries gates";
