@@ -243,11 +243,11 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
                         static_cast<size_t>(c.max_mailboxes) * 32 * 4 +
                         static_cast<size_t>(c.max_coop_ranks) * c.max_slots * 32 * 4;
     if (c.max_coop_ranks > 32 || smem > 227 * 1024) {
+      const std::string msg = "a component couples " + std::to_string(c.max_coop_ranks) +
+                              " ranks through " + std::to_string(c.max_mailboxes) +
+                              " values: more than one CTA holds (compile with LUMOS_COOP=0)";
       delete g;
-      return fail(TS_E_UNSUPPORTED,
-                  "a component couples " + std::to_string(c.max_coop_ranks) + " ranks through " +
-                      std::to_string(c.max_mailboxes) +
-                      " values: more than one CTA holds (compile with LUMOS_COOP=0)");
+      return fail(TS_E_UNSUPPORTED, msg);
     }
   }
   cudaError_t e = cudaSuccess;
