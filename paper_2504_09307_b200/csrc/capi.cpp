@@ -7,10 +7,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -114,6 +116,13 @@ struct ts_graph {
   int32_t* d_rt_group = nullptr;
   int64_t* d_rt_mnk = nullptr;
   DevBuf retime_dur, retime_par;  // retimed durations tile, per-scenario parameters
+  // retime walk (kModeRetime) tables: per op record its dense F_RT index,
+  // per F_RT record {base, group, kind} and its task; per call the variant table
+  int32_t* d_rt_rec_of = nullptr;
+  RtRec* d_rt_rec = nullptr;
+  int32_t* d_rt_rec_task = nullptr;
+  int64_t n_rt_rec = 0;
+  DevBuf rt_vval, rt_var;
   uint8_t* d_cls = nullptr;
   uint8_t* d_is_comm = nullptr;
   int32_t* d_rank_stream_off = nullptr;
@@ -263,6 +272,17 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   if (e == cudaSuccess) e = upload(&g->d_rt_bytes, c.rt_bytes);
   if (e == cudaSuccess) e = upload(&g->d_rt_group, c.rt_group);
   if (e == cudaSuccess) e = upload(&g->d_rt_mnk, c.rt_mnk);
+  if (e == cudaSuccess && !c.rt_rec_task.empty()) {
+    std::vector<RtRec> rec(c.rt_rec_task.size());
+    for (size_t j = 0; j < rec.size(); ++j) {
+      const int32_t t = c.rt_rec_task[j];
+      rec[j] = RtRec{c.base[t], c.rt_group[t], static_cast<int32_t>(c.rt_kind[t])};
+    }
+    g->n_rt_rec = static_cast<int64_t>(rec.size());
+    e = upload(&g->d_rt_rec, rec);
+    if (e == cudaSuccess) e = upload(&g->d_rt_rec_of, c.rt_rec_of);
+    if (e == cudaSuccess) e = upload(&g->d_rt_rec_task, c.rt_rec_task);
+  }
   if (e == cudaSuccess) e = upload(&g->d_cls, c.scale_class);
   if (e == cudaSuccess) e = upload(&g->d_is_comm, c.is_comm);
   if (e == cudaSuccess) e = upload(&g->d_rank_stream_off, c.rank_stream_off);
@@ -344,6 +364,8 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_base), static_cast<void*>(g->d_cls),
                     static_cast<void*>(g->d_rt_kind), static_cast<void*>(g->d_rt_bytes),
                     static_cast<void*>(g->d_rt_group), static_cast<void*>(g->d_rt_mnk),
+                    static_cast<void*>(g->d_rt_rec_of), static_cast<void*>(g->d_rt_rec),
+                    static_cast<void*>(g->d_rt_rec_task),
                     static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
                     static_cast<void*>(g->d_stream_node_off),
                     static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists),
@@ -358,6 +380,8 @@ void ts_graph_destroy(ts_graph* g) {
     g->des_scratch.release();
     g->retime_dur.release();
     g->retime_par.release();
+    g->rt_vval.release();
+    g->rt_var.release();
     for (DevBuf* b : {&g->span_lo, &g->span_hi, &g->status, &g->scratch_ts, &g->delta_scratch})
       b->release();
     for (DevBuf& b : g->stage) b.release();
@@ -555,6 +579,85 @@ static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStr
   return TS_OK;
 }
 
+// Retime walk staging: the distinct target width triples of the scenarios
+// change_hidden applies to become variants (variant 0 = the source widths),
+// K4v fills vval[variant][F_RT record], and each scenario gets its variant and
+// cost-model terms.  Returns false (nothing staged) when the variant table
+// would not fit its memory budget; the caller then materialises durations.
+static bool retime_walk_stage(ts_graph* g, const ts_retime* rt, int32_t count,
+                              cudaStream_t stream, RetimeWalk& w, cudaError_t& err) {
+  err = cudaSuccess;
+  const int64_t* sm = rt->source_model;
+  std::vector<int64_t> targets = {sm[0], sm[1], sm[2]};
+  std::map<std::array<int64_t, 3>, int32_t> index;
+  std::vector<int32_t> var(static_cast<size_t>(count));
+  std::vector<RtScen> scen(static_cast<size_t>(count));
+  for (int32_t s = 0; s < count; ++s) {
+    RtScen& q = scen[s];
+    q.alpha = rt->alpha_us[s];
+    q.bpu = rt->bytes_per_us[s];
+    q.tdp = rt->target_dp ? rt->target_dp[s] : rt->source_dp;
+    q.flags = (rt->target_dp && q.tdp != rt->source_dp) ? kRtDp : 0;
+    int32_t v = 0;
+    if (rt->target_model) {
+      const int64_t* tm = rt->target_model + 3 * static_cast<size_t>(s);
+      if (tm[0] != sm[0] || tm[1] != sm[1]) {  // change_hidden applies (transform.cpp:282)
+        q.flags |= kRtHid;
+        const std::array<int64_t, 3> key = {tm[0], tm[1], tm[2]};
+        auto it = index.find(key);
+        if (it == index.end()) {
+          it = index.emplace(key, static_cast<int32_t>(targets.size() / 3)).first;
+          targets.insert(targets.end(), key.begin(), key.end());
+        }
+        v = it->second;
+      }
+    }
+    var[s] = v;
+  }
+  const int64_t n_var = static_cast<int64_t>(targets.size() / 3);
+  const size_t vbytes = static_cast<size_t>(n_var) * static_cast<size_t>(g->n_rt_rec) * 8;
+  if (vbytes > (size_t(2) << 30)) return false;
+  const size_t n = static_cast<size_t>(count);
+  const size_t pbytes = n * sizeof(RtScen) + targets.size() * 8 + n * 4 + 64;
+  if ((err = g->rt_vval.reserve(vbytes)) != cudaSuccess) return false;
+  if ((err = g->rt_var.reserve(pbytes)) != cudaSuccess) return false;
+  char* base = g->rt_var.as<char>();
+  RtScen* d_scen = reinterpret_cast<RtScen*>(base);
+  int64_t* d_targets = reinterpret_cast<int64_t*>(d_scen + n);
+  int32_t* d_var = reinterpret_cast<int32_t*>(d_targets + targets.size());
+  // pageable sources: each copy returns once its source has been staged
+  err = cudaMemcpyAsync(d_scen, scen.data(), n * sizeof(RtScen), cudaMemcpyHostToDevice, stream);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(d_targets, targets.data(), targets.size() * 8, cudaMemcpyHostToDevice,
+                          stream);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(d_var, var.data(), n * 4, cudaMemcpyHostToDevice, stream);
+  if (err != cudaSuccess) return false;
+  VariantParams vp{};
+  vp.rec = g->d_rt_rec;
+  vp.rec_task = g->d_rt_rec_task;
+  vp.bytes = g->d_rt_bytes;
+  vp.mnk = g->d_rt_mnk;
+  vp.targets = d_targets;
+  for (int k = 0; k < 3; ++k) vp.src_model[k] = sm[k];
+  vp.n_rec = g->n_rt_rec;
+  vp.n_var = static_cast<int32_t>(n_var);
+  vp.vval = g->rt_vval.as<int64_t>();
+  {
+    Timed tm(g, stream, 2);
+    if ((err = launch_retime_variants(vp, stream)) != cudaSuccess) return false;
+  }
+  g_launches++;
+  w.rec_of = g->d_rt_rec_of;
+  w.rec = g->d_rt_rec;
+  w.vval = vp.vval;
+  w.n_rec = g->n_rt_rec;
+  w.var = d_var;
+  w.scen = d_scen;
+  w.source_dp = rt->source_dp;
+  return true;
+}
+
 int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, void* stream_) {
   if (!g || !sc || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
   if (!g->has_device) return fail(TS_E_CUDA, "graph was compiled without a device");
@@ -689,8 +792,23 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   // per component, sum of the largest possible durations (class scale
   // mul_div <= d*num/den + 1, jitter <= d*(1+j) + 1, transform.cpp:38-43,
   // synth.cpp:150-155) bounds every start and finish
-  // retimed durations: materialised per tile (K4r), the walk reads them
+  // retimed durations: evaluated inside the walk (kModeRetime) when every
+  // component takes the single-program walk, else materialised per tile (K4r)
+  // and read back by an explicit-duration walk
+  RetimeWalk rtw{};
+  bool rt_fused = false;
   if (retime) {
+    const char* env = std::getenv("LUMOS_RT_FUSED");
+    if (!(env && env[0] == '0') && g->n_coop == 0 && !c.des_only && g->n_rt_rec > 0) {
+      cudaError_t e = cudaSuccess;
+      rt_fused = retime_walk_stage(g, sc->retime, count, stream, rtw, e);
+      if (e != cudaSuccess) {
+        cleanup();
+        return fail(TS_E_CUDA, cudaGetErrorString(e));
+      }
+    }
+  }
+  if (retime && !rt_fused) {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) cudaGetLastError();
     const size_t per_col = static_cast<size_t>(c.n_tasks) * 8 + 1;
@@ -741,7 +859,12 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.sp.count = bn;
     if (sp.scale_num) wp.sp.scale_num = sp.scale_num + static_cast<size_t>(b0) * sp.n_classes;
     if (sp.durations) wp.sp.durations = sp.durations + b0;
-    if (retime) {
+    if (rt_fused) {
+      wp.sp.mode |= kModeRetime;
+      wp.rt = rtw;
+      wp.rt.var = rtw.var + b0;
+      wp.rt.scen = rtw.scen + b0;
+    } else if (retime) {
       // what-if retime + class scale + jitter of this tile, then an explicit walk
       RetimeParams rp_ = rtp;
       rp_.sp = wp.sp;
@@ -843,6 +966,15 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       dp.span_hi = wp.span_hi;
       dp.status = wp.status;
       dp.fixup = c.des_only ? 0 : 1;
+      if (rt_fused) {  // the fix-up retimes its own durations
+        dp.has_rt = 1;
+        dp.rt = rtp;
+        dp.rt.sp = wp.sp;
+        dp.rt.alpha = rtp.alpha + b0;
+        dp.rt.bpu = rtp.bpu + b0;
+        if (rtp.target_dp) dp.rt.target_dp = rtp.target_dp + b0;
+        if (rtp.target_model) dp.rt.target_model = rtp.target_model + 3 * static_cast<size_t>(b0);
+      }
       if (c.des_only) {  // the walk's reductions are not valid here: DES does them
         dp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
         dp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;

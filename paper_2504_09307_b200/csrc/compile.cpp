@@ -97,6 +97,23 @@ struct IrOp {
   bool aux() const { return is_ext || is_cov; }
 };
 
+// retime kinds whose duration a retime walk recomputes (a receive keeps its
+// recorded duration, transform.cpp:342)
+bool rt_walk_kind(uint8_t k) {
+  return k == TS_RT_GEMM || k == TS_RT_OPT || k == TS_RT_ALLREDUCE || k == TS_RT_P2P_SEND;
+}
+
+bool same_rt_meta(const ts_graph_desc& d, int32_t a, int32_t b) {
+  if (d.rt_kind[a] != d.rt_kind[b]) return false;
+  if (d.rt_bytes && d.rt_bytes[a] != d.rt_bytes[b]) return false;
+  if (d.rt_group && d.rt_group[a] != d.rt_group[b]) return false;
+  if (d.rt_mnk)
+    for (int k = 0; k < 3; ++k)
+      if (d.rt_mnk[3 * static_cast<size_t>(a) + k] != d.rt_mnk[3 * static_cast<size_t>(b) + k])
+        return false;
+  return true;
+}
+
 struct CertEntry {
   int32_t kstar;  // -1: no kernel bound before the sync
   int32_t next;   // -1: none or a descendant of the sync
@@ -578,6 +595,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   for (int32_t c = 0; c < n_comp; ++c) comp_begin[c + 1] += comp_begin[c];
 
   std::unordered_map<uint64_t, std::vector<int32_t>> prog_by_hash;
+  std::vector<int32_t> prog_rep_base;  // node_base of the component that created each program
   std::vector<IrOp> ir;
   std::vector<int32_t> comp_tasks;
   out.comps.resize(n_comp);
@@ -715,6 +733,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       o.op.node = t - node_base;
       o.op.base = d.duration[t];
       o.op.flags = flags;
+      if (d.rt_kind && rt_walk_kind(d.rt_kind[t])) o.op.flags |= F_RT;
       o.v_dst = t;
       if (split[t]) {
         fold(gatev, 3);
@@ -1072,6 +1091,10 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
           bool same = true;
           for (size_t k = 0; k < ir.size() && same; ++k)
             same = std::memcmp(&out.ops[pd.op_offset + k], &ir[k].op, sizeof(Op)) == 0;
+          // a retime walk reads the creator's task metadata for a shared program
+          for (size_t k = 0; k < ir.size() && same; ++k)
+            if (!ir[k].aux() && (ir[k].op.flags & F_RT))
+              same = same_rt_meta(d, prog_rep_base[cand] + ir[k].op.node, node_base + ir[k].op.node);
           if (same) {
             prog = cand;
             break;
@@ -1085,6 +1108,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         pd.n_ops = static_cast<int32_t>(ir.size());
         pd.n_slots = n_slots;
         out.programs.push_back(pd);
+        prog_rep_base.push_back(node_base);
         for (const IrOp& o : ir) out.ops.push_back(o.op);
         if (contiguous) prog_by_hash[h].push_back(prog);
       }
@@ -1266,6 +1290,25 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   }
   out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
 
+  // retime walk tables: a dense index per F_RT record (programs are shared by
+  // replicas, so a record stands for the creator component's task)
+  out.rt_rec_of.clear();
+  out.rt_rec_task.clear();
+  if (d.rt_kind) {
+    out.rt_rec_of.assign(out.ops.size(), -1);
+    for (size_t p = 0; p < out.programs.size(); ++p) {
+      const ProgramDesc& pd = out.programs[p];
+      for (int32_t k = 0; k < pd.n_ops; ++k) {
+        const Op& o = out.ops[pd.op_offset + k];
+        const int32_t n_aux = o.kind == OP_SYNC ? o.x0 : ((o.flags & F_TRACK) ? 1 : 0);
+        if ((o.flags & F_RT) && o.kind != OP_NOP && o.kind != OP_START && o.kind != OP_ACC) {
+          out.rt_rec_of[pd.op_offset + k] = static_cast<int32_t>(out.rt_rec_task.size());
+          out.rt_rec_task.push_back(prog_rep_base[p] + o.node);
+        }
+        k += n_aux;  // OpExt / OpCov records carry no task
+      }
+    }
+  }
   return TS_OK;
 }
 

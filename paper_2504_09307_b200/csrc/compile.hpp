@@ -59,6 +59,10 @@ struct CompiledGraph {
   std::vector<int64_t> rt_bytes;
   std::vector<int32_t> rt_group;
   std::vector<int64_t> rt_mnk;  // [n][3]
+  // retime walk: per op record the dense index of its F_RT task (-1 for other
+  // records), and per dense index the task whose metadata it carries
+  std::vector<int32_t> rt_rec_of;
+  std::vector<int32_t> rt_rec_task;
 
   // reductions: ranks (sorted, = ranks_in(graph), build.cpp:582-590), their
   // CUDA-stream lanes and each stream's kernels in chain (= time) order

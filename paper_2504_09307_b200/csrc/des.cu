@@ -184,6 +184,8 @@ __global__ void des_kernel(DesParams P) {
     if (P.fixup && P.status[col] == 0) continue;
     ThreadScen ts;
     init_thread_scen(P.sp, col, ts);
+    RtCol rc{};
+    if (P.has_rt) rc = rt_col(P.rt, col);
     const int64_t W = P.W;
     for (int32_t l = 0; l < nl; ++l) {
       s.clock[l] = W;
@@ -213,7 +215,8 @@ __global__ void des_kernel(DesParams P) {
         }
         if (best < 0) break;
         E.ready_pop(best_lane);
-        const int64_t d = scenario_duration<-1>(P.sp, ts, best, P.base[best], P.cls[best]);
+        const int64_t b = P.has_rt ? rt_task(P.rt, rc, best) : P.base[best];
+        const int64_t d = scenario_duration<-1>(P.sp, ts, best, b, P.cls[best]);
         s.sim_start[best] = now;
         s.sim_end[best] = now + d;
         --unstarted;

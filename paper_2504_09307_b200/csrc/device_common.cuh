@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "kernels.hpp"
+#include "lumos_b200.h"
 #include "program.hpp"
 
 namespace lumos {
@@ -115,6 +116,77 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
     const int64_t r = __double2ll_rd(p >= 0x1.0p52 ? p : __dadd_rn(p, 0.5));
     return r < 1 ? 1 : r;
   }
+  return d;
+}
+
+// ---- what-if retime (transform.cpp:219-349 through apply_whatif :713-760):
+// change_hidden then scale_dp with the analytical collective cost
+// (cost.cpp:40-62), evaluated in double with explicitly rounded operations in
+// the reference's order, then llround (round half away from zero).
+__device__ __forceinline__ int64_t llround_exact(double t) {
+  if (t >= 0x1.0p52 || t <= -0x1.0p52) return static_cast<int64_t>(t);  // integral
+  const int64_t r = __double2ll_rz(t);
+  const double fr = __dadd_rn(t, -static_cast<double>(r));  // exact (Sterbenz)
+  return fr >= 0.5 ? r + 1 : (fr <= -0.5 ? r - 1 : r);
+}
+// collective_cost_us: max(0, llround(alpha + bytes * scale(c, g) / beta))
+__device__ __forceinline__ int64_t coll_cost(bool allreduce, int64_t bytes, int32_t g,
+                                             double alpha, double bpu) {
+  double scale = 1.0;  // SendRecv
+  if (allreduce) {
+    const double gd = static_cast<double>(g);
+    scale = __ddiv_rn(__dmul_rn(2.0, __dadd_rn(gd, -1.0)), gd);
+  }
+  const double t = __dadd_rn(alpha, __ddiv_rn(__dmul_rn(static_cast<double>(bytes), scale), bpu));
+  const int64_t r = llround_exact(t);
+  return r < 0 ? 0 : r;
+}
+
+// per-scenario retime inputs
+struct RtCol {
+  double alpha, bpu;
+  int32_t tdp;
+  bool dp, hid;
+  int64_t tm[3];
+};
+__device__ __forceinline__ RtCol rt_col(const RetimeParams& P, int col) {
+  RtCol c;
+  c.alpha = P.alpha[col];
+  c.bpu = P.bpu[col];
+  c.tdp = P.target_dp ? P.target_dp[col] : P.source_dp;
+  c.dp = P.target_dp && c.tdp != P.source_dp;
+  for (int k = 0; k < 3; ++k)
+    c.tm[k] = P.target_model ? P.target_model[3 * static_cast<int64_t>(col) + k] : P.src_model[k];
+  // change_hidden is a no-op unless d_model or d_ffn change (transform.cpp:282)
+  c.hid = P.target_model && (c.tm[0] != P.src_model[0] || c.tm[1] != P.src_model[1]);
+  return c;
+}
+// the retimed duration of task t before class scale and jitter
+__device__ __forceinline__ int64_t rt_task(const RetimeParams& P, const RtCol& c, int32_t t) {
+  int64_t d = P.base[t];
+  const uint8_t kd = P.kind[t];
+  if (kd == TS_RT_NONE || !(c.hid || c.dp)) return d;
+  int64_t bytes = P.bytes[t];
+  if (c.hid) {
+    if (kd == TS_RT_GEMM) {
+      const int64_t* mnk = P.mnk + 3 * static_cast<int64_t>(t);
+      int64_t nd[3];
+      for (int k = 0; k < 3; ++k)
+        nd[k] = mnk[k] == P.src_model[0] ? c.tm[0] : (mnk[k] == P.src_model[1] ? c.tm[1] : mnk[k]);
+      d = mul_div_nonneg(d, nd[0] * nd[1] * nd[2], mnk[0] * mnk[1] * mnk[2], -1);
+    } else if (kd == TS_RT_OPT) {
+      d = mul_div_nonneg(d, c.tm[2], P.src_model[2], -1);
+    } else if (kd == TS_RT_ALLREDUCE) {
+      bytes = mul_div_nonneg(bytes, c.tm[2], P.src_model[2], -1);
+      d = coll_cost(true, bytes, P.group[t], c.alpha, c.bpu);
+    } else if (kd == TS_RT_P2P_SEND || kd == TS_RT_P2P_RECV) {
+      bytes = mul_div_nonneg(bytes, c.tm[0], P.src_model[0], -1);
+      if (kd == TS_RT_P2P_SEND) d = coll_cost(false, bytes, 2, c.alpha, c.bpu);
+      // a receive keeps its recorded duration (arrival skew), transform.cpp:342
+    }
+  }
+  if (c.dp && kd == TS_RT_ALLREDUCE && P.group[t] == P.source_dp)
+    d = coll_cost(true, bytes, c.tdp, c.alpha, c.bpu);
   return d;
 }
 

@@ -9,7 +9,39 @@
 
 namespace lumos {
 
-enum : int32_t { kModeScale = 1, kModeJitter = 2, kModeExplicit = 4 };
+enum : int32_t { kModeScale = 1, kModeJitter = 2, kModeExplicit = 4, kModeRetime = 8 };
+
+// Per-scenario what-if retime parameters of a retime walk (ts_retime)
+struct RtScen {
+  double alpha;   // cost model alpha (us)
+  double bpu;     // bytes per us
+  int32_t tdp;    // target data-parallel size
+  int32_t flags;  // kRtHid: change_hidden applies; kRtDp: scale_dp applies
+};
+enum : int32_t { kRtHid = 1, kRtDp = 2 };
+
+// Retime walk (kModeRetime): the walk evaluates each F_RT task's retimed
+// duration itself.  Everything that depends only on the target model widths
+// (retimed GEMM / optimizer base durations, retimed collective byte counts)
+// is precomputed per distinct width triple ("variant") by K4v into
+// vval[variant][rec]; the cost-model terms (alpha, bytes/us, target dp) are
+// per scenario.
+struct RtRec {
+  int64_t base;   // recorded duration
+  int32_t group;  // meta group_size
+  int32_t kind;   // TS_RT_*
+};
+struct RetimeWalk {
+  const int32_t* rec_of;  // [op records] dense index of an F_RT record
+  const RtRec* rec;       // [n_rec]
+  const int64_t* vval;    // [n_var][n_rec]
+  int64_t n_rec;
+  const int32_t* var;     // [count] variant of each scenario (tile-relative)
+  const RtScen* scen;     // [count]
+  int32_t source_dp;
+  int32_t pad;
+};
+
 
 struct ScenarioParams {
   int64_t first;        // global id of column 0
@@ -50,6 +82,7 @@ struct WalkParams {
   int32_t* status;
   int32_t vec_store;   // 16-byte output stores allowed (ld, count even; aligned)
   int32_t rel32;       // slot values are uint32 offsets from W (bound proven on the host)
+  RetimeWalk rt;       // sp.mode & kModeRetime
 };
 
 struct ReduceParams {
@@ -77,6 +110,26 @@ struct ReduceParams {
   int32_t pad2;
 };
 
+// what-if retime of every (task, scenario) duration (ts_retime), then the
+// scenario's class scale and jitter; writes dur[task * ld + s]
+struct RetimeParams {
+  ScenarioParams sp;        // mode without kModeExplicit
+  const int64_t* base;
+  const uint8_t* cls;
+  const uint8_t* kind;      // TS_RT_*
+  const int64_t* bytes;
+  const int32_t* group;
+  const int64_t* mnk;       // [n][3]
+  const double* alpha;      // [count] (device)
+  const double* bpu;        // [count]
+  const int32_t* target_dp; // [count] or null
+  const int64_t* target_model;  // [count][3] or null
+  int64_t src_model[3];
+  int32_t source_dp;
+  int32_t n_tasks;
+  int64_t* dur;
+  int64_t ld;
+};
 struct DesParams {
   int32_t n, nl;
   const int64_t* ostart;
@@ -114,6 +167,9 @@ struct DesParams {
   int32_t n_slots;  // concurrent scenarios (scratch slots)
   char* scratch;
   int64_t scratch_bytes;  // per slot
+  RetimeParams rt;  // has_rt: retime each duration first (fix-up of a retime walk)
+  int32_t has_rt;
+  int32_t pad3;
 };
 size_t des_scratch_bytes(int32_t n, int32_t nl);
 cudaError_t launch_des(const DesParams& p, cudaStream_t stream);
@@ -161,27 +217,22 @@ cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, i
                               int64_t w, int32_t* n_bins, int32_t count, cudaStream_t stream);
 cudaError_t launch_span_finalize(const int64_t* lo, const int64_t* hi, int64_t W, int64_t* span,
                                  int64_t* makespan, int32_t count, cudaStream_t stream);
-// what-if retime of every (task, scenario) duration (ts_retime), then the
-// scenario's class scale and jitter; writes dur[task * ld + s]
-struct RetimeParams {
-  ScenarioParams sp;        // mode without kModeExplicit
-  const int64_t* base;
-  const uint8_t* cls;
-  const uint8_t* kind;      // TS_RT_*
-  const int64_t* bytes;
-  const int32_t* group;
-  const int64_t* mnk;       // [n][3]
-  const double* alpha;      // [count] (device)
-  const double* bpu;        // [count]
-  const int32_t* target_dp; // [count] or null
-  const int64_t* target_model;  // [count][3] or null
-  int64_t src_model[3];
-  int32_t source_dp;
-  int32_t n_tasks;
-  int64_t* dur;
-  int64_t ld;
-};
 cudaError_t launch_retime_durations(const RetimeParams& p, cudaStream_t stream);
+// K4v: vval[v][j] for the variant width triples targets[v] (v = 0: the source
+// widths, i.e. no change_hidden) of every F_RT record j
+struct VariantParams {
+  const RtRec* rec;
+  const int32_t* rec_task;  // [n_rec]
+  const int64_t* bytes;     // per task (ts_graph_desc.rt_bytes)
+  const int64_t* mnk;       // per task [n][3]
+  const int64_t* targets;   // [n_var][3]
+  int64_t src_model[3];
+  int64_t n_rec;
+  int32_t n_var;
+  int32_t pad;
+  int64_t* vval;
+};
+cudaError_t launch_retime_variants(const VariantParams& p, cudaStream_t stream);
 cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, const uint8_t* cls,
                              int32_t n_tasks, int64_t* dur, int64_t ld, cudaStream_t stream);
 // buckets 0..6: event merge by stream count (reduce_bucket); 7..10: the

@@ -79,6 +79,9 @@ enum OpFlags : uint8_t {
   F_NO_OUT = 16,      // helper op, produces no SimEntry
   F_TRACK1 = 32,      // compact coverage: cov = pred0 >= start ? min(start, slot x0) : start -> x1
   F_SINK = 64,        // finish read by no other op: candidate for the makespan
+  F_RT = 128,         // task carries what-if retime metadata (GEMM, optimizer,
+                      // allreduce, p2p send): a retime walk looks its duration up
+                      // through CompiledGraph::rt_rec_of
 };
 
 // 32-byte op record.  cls: low nibble = scenario class, high nibble = nfixed

@@ -73,10 +73,28 @@ __device__ __forceinline__ VPack<V, kS> splat(V x) {
 }
 constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
+// duration of a retimed allreduce / p2p send (v = its retimed byte count):
+// the cost model of change_hidden, then scale_dp (rt_task's order).  Rare ops:
+// kept out of line so the walk's registers stay those of the common path.
+__device__ __noinline__ int64_t rt_coll_base(const RtScen* scp, int32_t rk, int32_t grp,
+                                             int32_t source_dp, int64_t v, int64_t base) {
+  const RtScen sc = *scp;
+  int64_t d = base;
+  if (sc.flags & kRtHid)
+    d = coll_cost(rk == TS_RT_ALLREDUCE, v, rk == TS_RT_ALLREDUCE ? grp : 2, sc.alpha, sc.bpu);
+  if ((sc.flags & kRtDp) && rk == TS_RT_ALLREDUCE && grp == source_dp)
+    d = coll_cost(true, v, sc.tdp, sc.alpha, sc.bpu);
+  return d;
+}
+
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
 __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   using VP = VPack<V, kS>;
   constexpr bool kRel = sizeof(V) == 4;
+  // retime walk: F_RT tasks take their base duration from the variant tables
+  // (K4v) and the scenario's cost model; scale / jitter follow sp.mode
+  constexpr bool kRt = kMode >= 0 && (kMode & kModeRetime) != 0;
+  constexpr int kDurMode = kRt ? (kMode & (kModeScale | kModeJitter)) : kMode;
   constexpr int kRecPerThread = (kChunk + kT - 1) / kT;  // chunk refill: records per thread
   // record slot fields hold s * 128; a slot is kT packs of kS * sizeof(V) bytes
   constexpr int kShift = ilog2(kT) - 7 + ilog2(kS * static_cast<int>(sizeof(V)));
@@ -125,6 +143,10 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
   ThreadScen ts[kS];
 #pragma unroll
   for (int k = 0; k < kS; ++k) init_thread_scen(P.sp, col[k], ts[k]);
+  int64_t rt_vrow[kS];  // the scenario's row of the variant table
+#pragma unroll
+  for (int k = 0; k < kS; ++k)
+    rt_vrow[k] = kRt ? static_cast<int64_t>(__ldg(P.rt.var + col[k])) * P.rt.n_rec : 0;
 
   int64_t hi[kS];
   bool fail[kS];
@@ -259,10 +281,25 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
                              static_cast<uint32_t>(ra.x);
         const int cls = cls_b & 15u;
+        int64_t bs[kS];
+#pragma unroll
+        for (int s = 0; s < kS; ++s) bs[s] = base;
+        if (kRt && (flags & F_RT)) {
+          const int64_t j = __ldg(P.rt.rec_of + pd.op_offset + c * kChunk + i);
+          const int4 rw = __ldg(reinterpret_cast<const int4*>(P.rt.rec + j));
+          const int32_t rk = rw.w, grp = rw.z;
+#pragma unroll
+          for (int s = 0; s < kS; ++s) {
+            const int64_t v = __ldg(P.rt.vval + rt_vrow[s] + j);
+            bs[s] = (rk == TS_RT_GEMM || rk == TS_RT_OPT)
+                        ? v  // retimed base (change_hidden), or the base itself
+                        : rt_coll_base(P.rt.scen + col[s], rk, grp, P.rt.source_dp, v, base);
+          }
+        }
         VP fin;
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
-          const int64_t d = scenario_duration<kMode>(P.sp, ts[s], task, base, cls);
+          const int64_t d = scenario_duration<kDurMode>(P.sp, ts[s], task, bs[s], cls);
           fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
         }
         SLOTB(dst) = fin;
@@ -585,71 +622,48 @@ __global__ void durations_kernel(ScenarioParams sp, const int64_t* __restrict__ 
 }
 
 // ------------------------------------------------------------------- K4r
-// What-if retime (transform.cpp:219-349 through apply_whatif :713-760):
-// change_hidden then scale_dp with the analytical collective cost
-// (cost.cpp:40-62), evaluated in double with explicitly rounded operations in
-// the reference's order, then llround (round half away from zero).
-__device__ __forceinline__ int64_t llround_exact(double t) {
-  if (t >= 0x1.0p52 || t <= -0x1.0p52) return static_cast<int64_t>(t);  // integral
-  const int64_t r = __double2ll_rz(t);
-  const double fr = __dadd_rn(t, -static_cast<double>(r));  // exact (Sterbenz)
-  return fr >= 0.5 ? r + 1 : (fr <= -0.5 ? r - 1 : r);
-}
-// collective_cost_us: max(0, llround(alpha + bytes * scale(c, g) / beta))
-__device__ __forceinline__ int64_t coll_cost(bool allreduce, int64_t bytes, int32_t g,
-                                             double alpha, double bpu) {
-  double scale = 1.0;  // SendRecv
-  if (allreduce) {
-    const double gd = static_cast<double>(g);
-    scale = __ddiv_rn(__dmul_rn(2.0, __dadd_rn(gd, -1.0)), gd);
-  }
-  const double t = __dadd_rn(alpha, __ddiv_rn(__dmul_rn(static_cast<double>(bytes), scale), bpu));
-  const int64_t r = llround_exact(t);
-  return r < 0 ? 0 : r;
-}
-
+// What-if retime (transform.cpp:219-349 through apply_whatif :713-760) of every
+// (task, scenario): rt_task (device_common.cuh), then class scale and jitter.
 __global__ void retime_durations_kernel(RetimeParams P) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= P.sp.count) return;
   ThreadScen ts;
   init_thread_scen(P.sp, col, ts);
-  const double alpha = P.alpha[col], bpu = P.bpu[col];
-  const int32_t tdp = P.target_dp ? P.target_dp[col] : P.source_dp;
-  const bool dp = P.target_dp && tdp != P.source_dp;
-  int64_t tm[3] = {P.src_model[0], P.src_model[1], P.src_model[2]};
-  if (P.target_model)
-    for (int k = 0; k < 3; ++k) tm[k] = P.target_model[3 * static_cast<int64_t>(col) + k];
-  // change_hidden is a no-op unless d_model or d_ffn change (transform.cpp:282)
-  const bool hid = P.target_model && (tm[0] != P.src_model[0] || tm[1] != P.src_model[1]);
-  for (int32_t t = blockIdx.y; t < P.n_tasks; t += gridDim.y) {
-    int64_t d = P.base[t];
-    const uint8_t kd = P.kind[t];
-    if (kd != TS_RT_NONE && (hid || dp)) {
-      int64_t bytes = P.bytes[t];
-      if (hid) {
-        if (kd == TS_RT_GEMM) {
-          const int64_t* mnk = P.mnk + 3 * static_cast<int64_t>(t);
-          int64_t nd[3];
-          for (int k = 0; k < 3; ++k)
-            nd[k] = mnk[k] == P.src_model[0] ? tm[0] : (mnk[k] == P.src_model[1] ? tm[1] : mnk[k]);
-          d = mul_div_nonneg(d, nd[0] * nd[1] * nd[2], mnk[0] * mnk[1] * mnk[2], -1);
-        } else if (kd == TS_RT_OPT) {
-          d = mul_div_nonneg(d, tm[2], P.src_model[2], -1);
-        } else if (kd == TS_RT_ALLREDUCE) {
-          bytes = mul_div_nonneg(bytes, tm[2], P.src_model[2], -1);
-          d = coll_cost(true, bytes, P.group[t], alpha, bpu);
-        } else if (kd == TS_RT_P2P_SEND || kd == TS_RT_P2P_RECV) {
-          bytes = mul_div_nonneg(bytes, tm[0], P.src_model[0], -1);
-          if (kd == TS_RT_P2P_SEND) d = coll_cost(false, bytes, 2, alpha, bpu);
-          // a receive keeps its recorded duration (arrival skew), transform.cpp:342
-        }
-      }
-      if (dp && kd == TS_RT_ALLREDUCE && P.group[t] == P.source_dp)
-        d = coll_cost(true, bytes, tdp, alpha, bpu);
-    }
+  const RtCol rc = rt_col(P, col);
+  for (int32_t t = blockIdx.y; t < P.n_tasks; t += gridDim.y)
     P.dur[static_cast<int64_t>(t) * P.ld + col] =
-        scenario_duration<-1>(P.sp, ts, t, d, P.cls[t]);
+        scenario_duration<-1>(P.sp, ts, t, rt_task(P, rc, t), P.cls[t]);
+}
+
+// ------------------------------------------------------------------- K4v
+// The width-only part of the retime per (variant, F_RT record): retimed GEMM /
+// optimizer base durations, retimed collective byte counts (the same
+// mul_div calls rt_task makes).  Variant 0 is the source widths.
+__global__ void retime_variants_kernel(VariantParams P) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  if (j >= P.n_rec) return;
+  const RtRec r = P.rec[j];
+  const int32_t t = P.rec_task[j];
+  const int64_t* tm = P.targets + 3 * static_cast<int64_t>(v);
+  const bool hid = tm[0] != P.src_model[0] || tm[1] != P.src_model[1];
+  int64_t out = r.kind == TS_RT_GEMM || r.kind == TS_RT_OPT ? r.base : P.bytes[t];
+  if (hid) {
+    if (r.kind == TS_RT_GEMM) {
+      const int64_t* mnk = P.mnk + 3 * static_cast<int64_t>(t);
+      int64_t nd[3];
+      for (int k = 0; k < 3; ++k)
+        nd[k] = mnk[k] == P.src_model[0] ? tm[0] : (mnk[k] == P.src_model[1] ? tm[1] : mnk[k]);
+      out = mul_div_nonneg(r.base, nd[0] * nd[1] * nd[2], mnk[0] * mnk[1] * mnk[2], -1);
+    } else if (r.kind == TS_RT_OPT) {
+      out = mul_div_nonneg(r.base, tm[2], P.src_model[2], -1);
+    } else if (r.kind == TS_RT_ALLREDUCE) {
+      out = mul_div_nonneg(out, tm[2], P.src_model[2], -1);
+    } else {  // TS_RT_P2P_SEND
+      out = mul_div_nonneg(out, tm[0], P.src_model[0], -1);
+    }
   }
+  P.vval[static_cast<int64_t>(v) * P.n_rec + j] = out;
 }
 
 // ------------------------------------------------------------------- K5
@@ -1206,7 +1220,21 @@ static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStrea
     case kModeJitter: return launch_walk_mode<kT, kModeJitter, V, kS>(p, smem, nb, stream);
     case kModeScale | kModeJitter:
       return launch_walk_mode<kT, kModeScale | kModeJitter, V, kS>(p, smem, nb, stream);
-    default: return launch_walk_mode<kT, kModeExplicit, V, kS>(p, smem, nb, stream);
+    default:
+      if (p.sp.mode & kModeRetime) {
+        if constexpr (sizeof(V) == 8) {  // retime walks keep int64 slot values
+          constexpr int R = kModeRetime;
+          switch (p.sp.mode & (kModeScale | kModeJitter)) {
+            case 0: return launch_walk_mode<kT, R, V, kS>(p, smem, nb, stream);
+            case kModeScale: return launch_walk_mode<kT, R | kModeScale, V, kS>(p, smem, nb, stream);
+            case kModeJitter: return launch_walk_mode<kT, R | kModeJitter, V, kS>(p, smem, nb, stream);
+            default:
+              return launch_walk_mode<kT, R | kModeScale | kModeJitter, V, kS>(p, smem, nb, stream);
+          }
+        }
+        return cudaErrorInvalidValue;
+      }
+      return launch_walk_mode<kT, kModeExplicit, V, kS>(p, smem, nb, stream);
   }
 }
 
@@ -1302,6 +1330,13 @@ cudaError_t launch_retime_durations(const RetimeParams& p, cudaStream_t stream) 
   if (p.sp.count <= 0 || p.n_tasks <= 0) return cudaSuccess;
   dim3 grid((p.sp.count + 127) / 128, p.n_tasks < 4096 ? p.n_tasks : 4096);
   retime_durations_kernel<<<grid, 128, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_retime_variants(const VariantParams& p, cudaStream_t stream) {
+  if (p.n_rec <= 0 || p.n_var <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((p.n_rec + 255) / 256), static_cast<unsigned>(p.n_var));
+  retime_variants_kernel<<<grid, 256, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

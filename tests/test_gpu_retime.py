@@ -117,3 +117,83 @@ def test_retime_errors_follow_the_reference():
     with pytest.raises(Exception, match="no retime metadata"):
         simulate_batch(plain, ScenarioSpec(count=1, retime=Retime(**one, source_dp=2,
                                                                   target_dp=[4])))
+
+
+# ------------------------------------------- retime walk vs materialised path
+# The walk evaluates retimed durations itself (kModeRetime: K4v variant tables
+# + per-scenario cost model); LUMOS_RT_FUSED=0 takes the materialised path
+# (K4r writes every duration, an explicit-duration walk reads them back),
+# which the tests above pin to the reference.  Both must agree on everything.
+
+def _both_paths(monkeypatch, g, spec, **kw):
+    out = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("LUMOS_RT_FUSED", fused)
+        out.append(simulate_batch(g, spec, timestamps=True, breakdown=True, **kw))
+    monkeypatch.delenv("LUMOS_RT_FUSED")
+    return out
+
+
+def _assert_same(a, b):
+    for name in ("start", "fin", "span", "rank_breakdown", "stream_busy"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+def test_retime_walk_equals_materialised_on_replicated_graph(monkeypatch):
+    # TP and DP replicas share one program: the walk reads the creator
+    # component's metadata; many width variants, dp targets, cost models,
+    # class scale and jitter at once
+    h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4), tp=2)
+    g = _with_meta(h)
+    S = 200
+    rng = np.random.default_rng(5)
+    src = (1024, 4096, 350_000_000)
+    widths = np.array([(1024, 4096, 350_000_000), (1536, 6144, 780_000_000),
+                       (2048, 8192, 1_380_000_000), (1024, 8192, 600_000_000),
+                       (768, 3072, 200_000_000), (1024, 4096, 999)], np.int64)
+    tgt = widths[rng.integers(0, len(widths), S)]
+    tdp = rng.choice([2, 4, 8, 16], S).astype(np.int32)
+    alpha = rng.uniform(1.0, 40.0, S)
+    bpu = rng.uniform(5e3, 9e4, S)
+    rt = Retime(alpha_us=alpha, bytes_per_us=bpu, source_dp=2, target_dp=tdp, source_model=src,
+                target_model=tgt)
+    spec = ScenarioSpec(count=S, first=11, seed=3, jitter=0.07, scale_lo=900, scale_hi=1100,
+                        scale_den=1024, retime=rt)
+    a, b = _both_paths(monkeypatch, g, spec)
+    _assert_same(a, b)
+    # the first scenarios (no class scale: the reference has no such
+    # transform) against the reference transforms
+    res = _check(h, g, ScenarioSpec(count=8, first=11, seed=3, jitter=0.07,
+                                    retime=Retime(alpha_us=alpha[:8], bytes_per_us=bpu[:8],
+                                                  source_dp=2, target_dp=tdp[:8],
+                                                  source_model=src, target_model=tgt[:8])),
+                 lambda s: dict(src_model=src, tgt_model=tuple(int(x) for x in tgt[s]), src_dp=2,
+                                tgt_dp=int(tdp[s]), alpha=float(alpha[s]),
+                                bytes_per_us=float(bpu[s])),
+                 sc=R.OrcScenarios(seed=3, jitter=0.07))
+    assert res.span.shape == (8, 3)
+
+
+def test_retime_walk_fixup_retimes_its_durations(monkeypatch):
+    # a certificate failure sends the scenario to the event-driven kernel,
+    # which must apply the same retime (GEMM kernels rescaled by the widths)
+    from test_gpu_parity import _graph
+    g = _graph([(1, 7, 0, 100), (1, 7, 10, 10), (0, 1, 0, 2), (0, 1, 5, 4), (0, 1, 20, 5)],
+               edges=[(0, 1), (2, 3), (3, 4)], rules=[(0, 3, -1, [(0, 1, 7)])])
+    g.rt_kind = np.array([1, 1, 0, 0, 0], np.uint8)
+    g.rt_bytes = np.zeros(5, np.int64)
+    g.rt_group = np.zeros(5, np.int32)
+    g.rt_mnk = np.array([[64, 1024, 4096], [64, 4096, 1024], [0] * 3, [0] * 3, [0] * 3], np.int64)
+    src = (1024, 4096, 1000)
+    tgt = np.array([(1024, 4096, 1000), (2048, 8192, 4000), (512, 4096, 700)], np.int64)
+    rt = Retime(alpha_us=[5.0] * 3, bytes_per_us=[1e4] * 3, source_model=src, target_model=tgt)
+    spec = ScenarioSpec(count=3, retime=rt)
+    a, b = _both_paths(monkeypatch, g, spec)
+    _assert_same(a, b)
+    assert a.span[1, 2] > a.span[0, 2] > a.span[2, 2]
+    status = np.zeros(3, np.int32)
+    start = np.zeros((g.n, 3), np.int64)
+    fin = np.zeros((g.n, 3), np.int64)
+    DeviceGraph(g).replay_batch(spec, start=start, fin=fin, status=status)
+    assert (status == 1).all()  # every scenario went through the fix-up
+    assert np.array_equal(start, a.start) and np.array_equal(fin, a.fin)
