@@ -86,7 +86,10 @@ __device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t s
 
 // K4 semantics: the scenario's duration of one task (see lumos_b200.h).
 // kMode < 0: decided at run time from sp.mode.
-template <int kMode>
+// kSelectZero: no early return for a zero duration (the jitter is computed
+// and discarded), so per-scenario bases that differ do not split two
+// scenarios' Philox chains into separate branches
+template <int kMode, bool kSelectZero = false>
 __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
                                                      const ThreadScen& ts, int64_t task,
                                                      int64_t base, int cls) {
@@ -101,7 +104,7 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
     d = mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
   }
   if (mode & kModeJitter) {
-    if (d == 0) return 0;
+    if (!kSelectZero && d == 0) return 0;
     uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
     philox2x32_10_rk(x0, x1, sp.rk_jit);
     const uint64_t bits = (static_cast<uint64_t>(x0) << 32) | x1;
@@ -114,6 +117,7 @@ __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
     // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
     // already an integer
     const int64_t r = __double2ll_rd(p >= 0x1.0p52 ? p : __dadd_rn(p, 0.5));
+    if (kSelectZero) return d == 0 ? 0 : (r < 1 ? 1 : r);
     return r < 1 ? 1 : r;
   }
   return d;

@@ -88,7 +88,7 @@ __device__ __noinline__ int64_t rt_coll_base(const RtScen* scp, int32_t rk, int3
 }
 
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
-__global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
+__device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   using VP = VPack<V, kS>;
   constexpr bool kRel = sizeof(V) == 4;
   // retime walk: F_RT tasks take their base duration from the variant tables
@@ -281,10 +281,10 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
                              static_cast<uint32_t>(ra.x);
         const int cls = cls_b & 15u;
-        int64_t bs[kS];
+        int64_t bs[kS];  // retime walk: per-scenario base durations
 #pragma unroll
         for (int s = 0; s < kS; ++s) bs[s] = base;
-        if (kRt && (flags & F_RT)) {
+        if constexpr (kRt) if (flags & F_RT) {
           const int64_t j = __ldg(P.rt.rec_of + pd.op_offset + c * kChunk + i);
           const int4 rw = __ldg(reinterpret_cast<const int4*>(P.rt.rec + j));
           const int32_t rk = rw.w, grp = rw.z;
@@ -299,7 +299,10 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
         VP fin;
 #pragma unroll
         for (int s = 0; s < kS; ++s) {
-          const int64_t d = scenario_duration<kDurMode>(P.sp, ts[s], task, bs[s], cls);
+          // (non-retime walks pass the uniform base itself: both scenarios'
+          // Philox chains then interleave)
+          const int64_t d =
+              scenario_duration<kDurMode, kRt>(P.sp, ts[s], task, kRt ? bs[s] : base, cls);
           fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
         }
         SLOTB(dst) = fin;
@@ -382,6 +385,16 @@ __global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
     }
     if (fail[s]) atomicOr(P.status + col[s], 1);
   }
+}
+
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
+__global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
+  replay_walk_body<kT, kMode, kWriteStart, kWriteFin, V, kS>(P);
+}
+// retime walks: at least 6 CTAs of 128 threads per SM (<= 80 registers)
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
+__global__ void __launch_bounds__(kT, 6 * 128 / kT) replay_walk_rt_kernel(WalkParams P) {
+  replay_walk_body<kT, kMode, kWriteStart, kWriteFin, V, kS>(P);
 }
 
 // ------------------------------------------------------------------- K1c
@@ -1076,8 +1089,10 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
 }
 
 // rank_list entries: rank | compute-stream index << 24
+// (4 CTAs per SM: their rings already limit shared memory to that, so the
+// registers can go to 128 without costing occupancy)
 template <int NC, bool kUtil>
-__global__ void __launch_bounds__(kThreads) rank_reduce_fast_kernel(ReduceParams P) {
+__global__ void __launch_bounds__(kThreads, 4) rank_reduce_fast_kernel(ReduceParams P) {
   extern __shared__ int64_t ring[];
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int e = P.rank_list[blockIdx.y];
@@ -1187,14 +1202,19 @@ static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned bloc
                                  cudaStream_t stream) {
   // set per launch: the attribute is per device, and several host threads or
   // devices may launch concurrently
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(replay_walk_kernel<kT, kMode, kWS, kWF, V, kS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  replay_walk_kernel<kT, kMode, kWS, kWF, V, kS><<<blocks, kT, smem, stream>>>(p);
-  return cudaGetLastError();
+  auto go = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<blocks, kT, smem, stream>>>(p);
+    return cudaGetLastError();
+  };
+  if constexpr ((kMode & kModeRetime) != 0)
+    return go(replay_walk_rt_kernel<kT, kMode, kWS, kWF, V, kS>);
+  else
+    return go(replay_walk_kernel<kT, kMode, kWS, kWF, V, kS>);
 }
 
 template <int kT, int kMode, typename V, int kS>
