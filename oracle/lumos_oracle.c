@@ -412,10 +412,10 @@ int64_t orc_scenario_duration(const orc_scenarios* sc, int64_t scenario, int32_t
   if (sc->scale_den > 0) d = orc_mul_div(d, orc_class_num(sc, scenario, cls), sc->scale_den);
   if (sc->jitter > 0.0) {
     if (d == 0) return 0;
+    /* one Philox call per scenario pair (2p, 2p + 1): word (scenario & 1) */
     uint32_t r[2];
-    orc_philox2x32_10((uint32_t)task, (uint32_t)scenario, seed_key(sc->seed, 0u), r);
-    uint64_t bits = ((uint64_t)r[0] << 32) | (uint64_t)r[1];
-    double u01 = (double)(bits >> 11) * 0x1.0p-53;
+    orc_philox2x32_10((uint32_t)task, (uint32_t)(scenario >> 1), seed_key(sc->seed, 0u), r);
+    double u01 = (double)r[scenario & 1] * 0x1.0p-32;
     double u = (2.0 * sc->jitter) * u01 + (-sc->jitter); /* -ffp-contract=off: no FMA */
     double f = 1.0 + u;
     double p = (double)d * f;

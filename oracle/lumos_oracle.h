@@ -68,6 +68,8 @@ void orc_breakdown_rank(int32_t n, const int32_t* rank, const int32_t* lane_kind
  *      num = lo + floor(r * (hi - lo + 1) / 2^32), r = Philox2x32-10 word
  *   2. jitter       d = d == 0 ? 0 : max(1, llround(d * (1 + u)))
  *                   u = -j + 2j * U01              (src/synth.cpp:150-155)
+ *                   U01 = w * 2^-32, w = word (s & 1) of
+ *                   Philox2x32-10(ctr = (task, s >> 1), key(seed))
  * Philox2x32-10 (Salmon et al., SC'11, Random123 constants).               */
 typedef struct {
   uint64_t seed;

@@ -450,7 +450,7 @@ static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioPa
     sp.mode |= kModeJitter;
     sp.two_j = 2.0 * sc->jitter;
     sp.neg_j = -sc->jitter;
-    sp.two_j_ulp = std::ldexp(sp.two_j, -53);
+    sp.two_j_ulp = std::ldexp(sp.two_j, -32);
   }
   if (sc->scale_den > 0) {
     sp.mode |= kModeScale;

@@ -86,39 +86,58 @@ __device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t s
 
 // K4 semantics: the scenario's duration of one task (see lumos_b200.h).
 // kMode < 0: decided at run time from sp.mode.
-// kSelectZero: no early return for a zero duration (the jitter is computed
-// and discarded), so per-scenario bases that differ do not split two
-// scenarios' Philox chains into separate branches
-template <int kMode, bool kSelectZero = false>
+// Scenario durations (K4 semantics): class scale, then jitter
+//   d' = d == 0 ? 0 : max(1, llround(d * (1 + u))),  u = 2j * (w * 2^-32) - j
+// with w = word (s & 1) of Philox2x32-10(ctr = (task, s >> 1); seed), so one
+// Philox call serves the scenario pair (2p, 2p + 1).
+__device__ __forceinline__ int64_t class_scaled(const ScenarioParams& sp, const ThreadScen& ts,
+                                                int64_t d, int cls) {
+  int32_t num = ts.num[0];
+  if (cls == 1) num = ts.num[1];
+  if (cls == 2) num = ts.num[2];
+  if (cls == 3) num = ts.num[3];
+  return mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
+}
+__device__ __forceinline__ uint32_t jitter_word(const ScenarioParams& sp, int64_t task,
+                                                int64_t scen) {
+  uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(scen >> 1);
+  philox2x32_10_rk(x0, x1, sp.rk_jit);
+  return (scen & 1) ? x1 : x0;
+}
+// the words of two scenarios of one pair (s0 >> 1 == s1 >> 1): one Philox call
+__device__ __forceinline__ void jitter_words2(const ScenarioParams& sp, int64_t task,
+                                              int64_t s0, int64_t s1, uint32_t& w0,
+                                              uint32_t& w1) {
+  uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(s0 >> 1);
+  philox2x32_10_rk(x0, x1, sp.rk_jit);
+  w0 = (s0 & 1) ? x1 : x0;
+  w1 = (s1 & 1) ? x1 : x0;
+}
+// max(1, llround(d * (1 + u))) for d > 0; 0 for d == 0
+__device__ __forceinline__ int64_t jitter_apply(const ScenarioParams& sp, int64_t d, uint32_t w) {
+  // two_j * (w * 2^-32) == (two_j * 2^-32) * w exactly (power-of-two scaling
+  // commutes with rounding while nothing is subnormal)
+  const double u = __dadd_rn(__dmul_rn(sp.two_j_ulp, __uint2double_rn(w)), sp.neg_j);
+  const double f = __dadd_rn(1.0, u);
+  const double p = __dmul_rn(__ll2double_rn(d), f);
+  // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)
+  // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
+  // already an integer
+  const int64_t r = __double2ll_rd(p >= 0x1.0p52 ? p : __dadd_rn(p, 0.5));
+  return d == 0 ? 0 : (r < 1 ? 1 : r);
+}
+
+template <int kMode>
 __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
                                                      const ThreadScen& ts, int64_t task,
                                                      int64_t base, int cls) {
   const int mode = kMode >= 0 ? kMode : sp.mode;
   if (mode & kModeExplicit) return __ldcs(sp.durations + task * sp.durations_ld + ts.col);
   int64_t d = base;
-  if (mode & kModeScale) {
-    int32_t num = ts.num[0];
-    if (cls == 1) num = ts.num[1];
-    if (cls == 2) num = ts.num[2];
-    if (cls == 3) num = ts.num[3];
-    d = mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
-  }
+  if (mode & kModeScale) d = class_scaled(sp, ts, d, cls);
   if (mode & kModeJitter) {
-    if (!kSelectZero && d == 0) return 0;
-    uint32_t x0 = static_cast<uint32_t>(task), x1 = static_cast<uint32_t>(ts.scen);
-    philox2x32_10_rk(x0, x1, sp.rk_jit);
-    const uint64_t bits = (static_cast<uint64_t>(x0) << 32) | x1;
-    // two_j * (k * 2^-53) == (two_j * 2^-53) * k exactly (power-of-two
-    // scaling commutes with rounding while nothing is subnormal)
-    const double u = __dadd_rn(__dmul_rn(sp.two_j_ulp, __ull2double_rn(bits >> 11)), sp.neg_j);
-    const double f = __dadd_rn(1.0, u);
-    const double p = __dmul_rn(__ll2double_rn(d), f);
-    // max(1, llround(p)) for p >= 0: below 1.5 the answer is 1; on [1.5, 2^52)
-    // p + 0.5 is exact so floor(p + 0.5) is round-half-up; from 2^52 up p is
-    // already an integer
-    const int64_t r = __double2ll_rd(p >= 0x1.0p52 ? p : __dadd_rn(p, 0.5));
-    if (kSelectZero) return d == 0 ? 0 : (r < 1 ? 1 : r);
-    return r < 1 ? 1 : r;
+    if (d == 0) return 0;
+    return jitter_apply(sp, d, jitter_word(sp, task, ts.scen));
   }
   return d;
 }

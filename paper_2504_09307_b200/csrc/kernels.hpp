@@ -51,7 +51,7 @@ struct ScenarioParams {
   uint32_t key_cls;     // Philox key of the class-scale stream
   double two_j;         // 2 * jitter
   double neg_j;         // -jitter
-  double two_j_ulp;     // two_j * 2^-53 (exact for jitter >= 2^-60; below that f == 1 anyway)
+  double two_j_ulp;     // two_j * 2^-32 (exact: a power-of-two scaling)
   uint32_t rk_jit[10];  // Philox round keys of key_jit (key + r * 0x9E3779B9)
   int32_t scale_lo;
   uint32_t scale_span;  // hi - lo + 1

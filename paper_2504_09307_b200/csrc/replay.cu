@@ -297,13 +297,29 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
           }
         }
         VP fin;
+        constexpr bool kJit = kDurMode >= 0 && (kDurMode & kModeJitter) != 0;
+        if constexpr (kS == 2 && kJit) {
+          // one Philox call for the thread's scenario pair (columns c0, c0 + 1
+          // with c0 even, or a duplicated last column; the launch takes the
+          // one-scenario walk when the batch starts at an odd global id); the
+          // rounding is branch-free per scenario (a zero duration selects 0)
+          int64_t dsc[kS];
 #pragma unroll
-        for (int s = 0; s < kS; ++s) {
-          // (non-retime walks pass the uniform base itself: both scenarios'
-          // Philox chains then interleave)
-          const int64_t d =
-              scenario_duration<kDurMode, kRt>(P.sp, ts[s], task, kRt ? bs[s] : base, cls);
-          fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
+          for (int s = 0; s < kS; ++s)
+            dsc[s] = (kDurMode & kModeScale) ? class_scaled(P.sp, ts[s], kRt ? bs[s] : base, cls)
+                                             : (kRt ? bs[s] : base);
+          uint32_t w[kS] = {0u, 0u};
+          if (kRt || (kDurMode & kModeScale) || base != 0)
+            jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
+#pragma unroll
+          for (int s = 0; s < kS; ++s)
+            fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
+        } else {
+#pragma unroll
+          for (int s = 0; s < kS; ++s) {
+            const int64_t d = scenario_duration<kDurMode>(P.sp, ts[s], task, kRt ? bs[s] : base, cls);
+            fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
+          }
         }
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
@@ -1293,7 +1309,9 @@ static cudaError_t launch_walk_v(const WalkParams& p, int n_slots, int t, cudaSt
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
   const bool rel = p.rel32 != 0;
   const int t = walk_width(n_slots, rel);
-  if (single_scenario(p))
+  // two scenarios per thread share one Philox call per task, which needs the
+  // thread's columns to be one global pair: an even first id
+  if (single_scenario(p) || (p.sp.first & 1))
     return rel ? launch_walk_v<uint32_t, 1>(p, n_slots, t, stream)
                : launch_walk_v<int64_t, 1>(p, n_slots, t, stream);
   return rel ? launch_walk_v<uint32_t, 2>(p, n_slots, t, stream)

@@ -441,3 +441,16 @@ def test_walk_value_width_paths():
     g2.duration[t] = 5_000_000_000                  # > 2^32 us on its own
     h2 = R.from_graph(g2)
     _check_batch(h2, g2, spec, sc, every=4)         # int64 path
+
+
+@pytest.mark.parametrize("first,count", [(0, 37), (1000, 129), (7, 40), (3, 37)])
+def test_scenario_pairs_share_philox(first, count):
+    # two scenarios per thread draw their jitter from one Philox call (words 0
+    # and 1 of counter (task, s >> 1)); odd counts leave a duplicated last
+    # column, odd first ids take the one-scenario walk — all equal the oracle
+    h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h.export()
+    spec = ScenarioSpec(count=count, first=first, seed=21, jitter=0.25, scale_lo=800,
+                        scale_hi=1200, scale_den=1000)
+    _check_batch(h, g, spec, R.OrcScenarios(seed=21, jitter=0.25, scale_lo=800, scale_hi=1200,
+                                            scale_den=1000), every=3)

@@ -175,14 +175,15 @@ def test_mul_div_exact():
     assert R.orc().orc_mul_div(1200, 64, 1) == 76800
 
 
-def _jitter_exact(d, bits, j):
-    """max(1, llround(d * (1 + u))) with u = 2j*U01 - j evaluated in IEEE
-    double exactly as the restatement does (round-to-nearest at each op)."""
+def _jitter_exact(d, w, j):
+    """max(1, llround(d * (1 + u))) with u = 2j*U01 - j, U01 = w * 2^-32,
+    evaluated in IEEE double exactly as the restatement does (round-to-nearest
+    at each op)."""
     import struct
 
     def rn(x):  # round a Fraction to the nearest double
         return float(x)
-    u01 = float(bits >> 11) * 2.0 ** -53
+    u01 = float(w) * 2.0 ** -32
     t = rn(Fraction(2.0 * j) * Fraction(u01))
     u = rn(Fraction(t) + Fraction(-j))
     fct = rn(Fraction(1.0) + Fraction(u))
@@ -206,9 +207,9 @@ def test_jitter_formula_exact():
         if d == 0:
             assert got == 0
             continue
-        R.orc().orc_philox2x32_10(task, scen, key, out)
-        bits = (out[0] << 32) | out[1]
-        assert got == _jitter_exact(d, bits, 0.37)
+        # one Philox call per scenario pair: word (scen & 1) of (task, scen >> 1)
+        R.orc().orc_philox2x32_10(task, scen >> 1, key, out)
+        assert got == _jitter_exact(d, out[scen & 1], 0.37)
 
 
 def test_reference_metric_shims_golden():
