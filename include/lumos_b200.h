@@ -157,7 +157,8 @@ int ts_graph_streams(const ts_graph* g, int32_t* rank, int32_t* lane /* [n_strea
  *   class scale (transform.cpp:38-43): d = mul_div(d, num, scale_den), with
  *     num = scale_num[s][class] if given, else drawn in [scale_lo, scale_hi]
  *   jitter      (synth.cpp:150-155):   d = d == 0 ? 0 : max(1, llround(d*(1+u))),
- *     u ~ U[-jitter, jitter) from Philox2x32-10(task, scenario; seed)
+ *     u = jitter * (2 * w / 2^32 - 1), w = word (s & 1) of
+ *     Philox2x32-10(ctr = (task, s >> 1); seed): one call per scenario pair
  *   explicit: durations[task * durations_ld + s] replaces both.          */
 typedef struct {
   int64_t first;            /* global id of scenario 0 of this batch */
