@@ -46,6 +46,23 @@ CONFIGS = {
                 "8-rank GPT-3 15B (pp2 dp2 m4 x TP2 replicas)"),
 }
 METRIC = "scenario-node relaxations/sec (replays/sec) at 1/2/4/8 B200; % HBM roofline"
+# per-class kernel-duration scaling sweep of config4: each
+# scenario draws a rational factor num/1024, num in [768, 1536], per duration
+# class (d' = mul_div(d, num, 1024), transform.cpp:38-43); no jitter
+SCALE_SWEEP = dict(scale_lo=768, scale_hi=1536, scale_den=1024)
+
+
+def scenario_kwargs(args):
+    """ScenarioSpec / OrcScenarios fields of the workload's scenarios."""
+    if args.config == "config4":
+        return dict(jitter=0.0, **SCALE_SWEEP)
+    return dict(jitter=args.jitter)
+
+
+def workload_kind(args):
+    if args.config == "config4":
+        return "kernel-duration scaling sweep (per-class factors 768..1536 / 1024)"
+    return f"Monte Carlo (jitter {args.jitter})"
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -156,7 +173,7 @@ def cpu_threads():
 
 
 def run_cpu_sample(R, h, g, args, first, threads, per_thread=1):
-    sc = R.OrcScenarios(seed=250409307, jitter=args.jitter)
+    sc = R.OrcScenarios(seed=250409307, **scenario_kwargs(args))
     cls = g.default_scale_class()
     count = threads * per_thread
     secs, mk = h.bench_simulate(sc, first, count, cls, threads)
@@ -259,7 +276,8 @@ def main():
 
     def step():
         for t0_ in range(0, S_local, tile):
-            spec = ScenarioSpec(count=tile, first=first + t0_, seed=250409307, jitter=args.jitter)
+            spec = ScenarioSpec(count=tile, first=first + t0_, seed=250409307,
+                                **scenario_kwargs(args))
             dg.replay_batch(spec, start=start, fin=fin, ld=tile, span=span[t0_:t0_ + tile],
                             rank_breakdown=bd[t0_:t0_ + tile], stream_busy=busy[t0_:t0_ + tile],
                             stream=sptr)
@@ -327,7 +345,7 @@ def main():
             sc_bytes = 0
             for t0_ in range(0, S_local, tile):
                 spec = ScenarioSpec(count=tile, first=first + t0_, seed=250409307,
-                                    jitter=args.jitter)
+                                    **scenario_kwargs(args))
                 sc_bytes += 72  # the ts_scenarios descriptor read from host memory
                 dg.replay_batch(spec, start=start, fin=fin, ld=tile,
                                 span=h_span[t0_:t0_ + tile], rank_breakdown=h_bd[t0_:t0_ + tile],
@@ -375,10 +393,10 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (GPT-3 generator graph, random-free base durations from the "
-                    "reference cost formulas; Philox-jittered scenarios)",
+                    "reference cost formulas; Philox-drawn scenario durations)",
             "replays_per_s": S_total / (ms_per_step / 1e3),
-            "config": {"workload": f"{args.config}: {label}, {S_total}-scenario Monte Carlo "
-                                   f"(jitter {args.jitter})",
+            "config": {"workload": f"{args.config}: {label}, {S_total}-scenario "
+                                   f"{workload_kind(args)}",
                        "tasks": n, "edges": int(g.edge_from.shape[0]), "ranks": R_,
                        "scenarios": S_total, "tile": tile, "parallelism": f"scenario-shard x{world}",
                        "outputs": "start+finish of every task x scenario (HBM), span, per-rank "
