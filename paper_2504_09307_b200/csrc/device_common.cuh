@@ -90,13 +90,27 @@ __device__ __forceinline__ int32_t class_num(const ScenarioParams& sp, int64_t s
 //   d' = d == 0 ? 0 : max(1, llround(d * (1 + u))),  u = 2j * (w * 2^-32) - j
 // with w = word (s & 1) of Philox2x32-10(ctr = (task, s >> 1); seed), so one
 // Philox call serves the scenario pair (2p, 2p + 1).
+// out of line: keeps the general 128-bit path's registers off the walk loop
+__device__ __noinline__ int64_t mul_div_slow(int64_t a, int64_t num, int64_t den, int den_shift) {
+  return mul_div_nonneg(a, num, den, den_shift);
+}
+__device__ __forceinline__ int64_t class_scaled_num(const ScenarioParams& sp, int64_t d,
+                                                    int32_t num) {
+  // power-of-two denominator and a 32-bit duration (every duration of a
+  // uint32-window walk): one 32x32 -> 64 multiply, add, shift
+  if (sp.den_shift >= 0 && (static_cast<uint64_t>(d) >> 32) == 0 && num >= 0)
+    return static_cast<int64_t>(
+        (static_cast<uint64_t>(static_cast<uint32_t>(d)) * static_cast<uint32_t>(num) +
+         static_cast<uint64_t>(sp.scale_den / 2)) >> sp.den_shift);
+  return mul_div_slow(d, num, sp.scale_den, sp.den_shift);
+}
 __device__ __forceinline__ int64_t class_scaled(const ScenarioParams& sp, const ThreadScen& ts,
                                                 int64_t d, int cls) {
   int32_t num = ts.num[0];
   if (cls == 1) num = ts.num[1];
   if (cls == 2) num = ts.num[2];
   if (cls == 3) num = ts.num[3];
-  return mul_div_nonneg(d, num, sp.scale_den, sp.den_shift);
+  return class_scaled_num(sp, d, num);
 }
 __device__ __forceinline__ uint32_t jitter_word(const ScenarioParams& sp, int64_t task,
                                                 int64_t scen) {

@@ -106,8 +106,11 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   // (pred[4], dst, x0, x1, x2) widened to byte offsets by the loader, so the
   // walk adds one register per operand address
   int4* opbuf = smem;
-  char* slot_base =
-      reinterpret_cast<char*>(smem + 8 * kChunk) + threadIdx.x * static_cast<uint32_t>(sizeof(VP));
+  // [kMaxClasses][kT] class-scale numerators of the thread's two scenarios
+  // (shared memory instead of 8 registers), then the slot table
+  int2* numtab = reinterpret_cast<int2*>(smem + 8 * kChunk);
+  char* slot_base = reinterpret_cast<char*>(numtab + kMaxClasses * kT) +
+                    threadIdx.x * static_cast<uint32_t>(sizeof(VP));
   const int tid = threadIdx.x;
   const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
   const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
@@ -143,6 +146,11 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   ThreadScen ts[kS];
 #pragma unroll
   for (int k = 0; k < kS; ++k) init_thread_scen(P.sp, col[k], ts[k]);
+  constexpr bool kScaleTab = kS == 2 && kDurMode >= 0 && (kDurMode & kModeScale) != 0;
+  if constexpr (kScaleTab) {
+#pragma unroll
+    for (int c = 0; c < kMaxClasses; ++c) numtab[c * kT + tid] = make_int2(ts[0].num[c], ts[1].num[c]);
+  }
   int64_t rt_vrow[kS];  // the scenario's row of the variant table
 #pragma unroll
   for (int k = 0; k < kS; ++k)
@@ -298,22 +306,30 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         }
         VP fin;
         constexpr bool kJit = kDurMode >= 0 && (kDurMode & kModeJitter) != 0;
+        int64_t dsc[kS];  // class-scaled durations (kScaleTab)
+        if constexpr (kScaleTab) {
+          const int2 nm = numtab[cls * kT + tid];
+          dsc[0] = class_scaled_num(P.sp, kRt ? bs[0] : base, nm.x);
+          dsc[1] = class_scaled_num(P.sp, kRt ? bs[1] : base, nm.y);
+        }
         if constexpr (kS == 2 && kJit) {
           // one Philox call for the thread's scenario pair (columns c0, c0 + 1
           // with c0 even, or a duplicated last column; the launch takes the
           // one-scenario walk when the batch starts at an odd global id); the
           // rounding is branch-free per scenario (a zero duration selects 0)
-          int64_t dsc[kS];
+          if constexpr (!kScaleTab) {
 #pragma unroll
-          for (int s = 0; s < kS; ++s)
-            dsc[s] = (kDurMode & kModeScale) ? class_scaled(P.sp, ts[s], kRt ? bs[s] : base, cls)
-                                             : (kRt ? bs[s] : base);
+            for (int s = 0; s < kS; ++s) dsc[s] = kRt ? bs[s] : base;
+          }
           uint32_t w[kS] = {0u, 0u};
           if (kRt || (kDurMode & kModeScale) || base != 0)
             jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
 #pragma unroll
           for (int s = 0; s < kS; ++s)
             fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
+        } else if constexpr (kScaleTab) {  // class scale only
+#pragma unroll
+          for (int s = 0; s < kS; ++s) fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(dsc[s]));
         } else {
 #pragma unroll
           for (int s = 0; s < kS; ++s) {
@@ -1277,7 +1293,7 @@ static cudaError_t launch_walk_width(const WalkParams& p, size_t smem, cudaStrea
 // shared memory of a walk CTA of t threads with `vbytes` bytes of slot values
 // per thread and slot
 static size_t walk_smem(int n_slots, int t, int vbytes) {
-  return 8 * kChunk * sizeof(int4) +
+  return 8 * kChunk * sizeof(int4) + static_cast<size_t>(kMaxClasses) * t * sizeof(int2) +
          static_cast<size_t>(n_slots < kFirstSlot ? kFirstSlot : n_slots) * t * vbytes;
 }
 
