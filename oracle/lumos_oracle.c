@@ -88,6 +88,7 @@ static int32_t find_proc(const proc_t* lanes, int32_t nl, proc_t p) {
  * durations, bad edge endpoints / self loops, bad rule tasks, Kahn cycle. */
 static int validate(const orc_graph* g) {
   const int32_t n = g->n;
+  if (n < 0 || g->n_edges < 0 || g->n_rules < 0) return 0;
   for (int32_t i = 0; i < n; ++i)
     if (g->duration[i] < 0) return 0;
   for (int64_t e = 0; e < g->n_edges; ++e) {
@@ -133,7 +134,7 @@ static int validate(const orc_graph* g) {
 int orc_simulate(const orc_graph* g, int64_t* sim_start, int64_t* sim_end, int64_t span[3]) {
   if (!validate(g)) return ORC_INVALID;
   const int32_t n = g->n;
-  if (n == 0) {
+  if (n <= 0) {
     span[0] = span[1] = g->window_start;
     span[2] = 0;
     return ORC_OK;
