@@ -75,7 +75,7 @@ def parse():
     ap.add_argument("--config", default="config5", choices=sorted(CONFIGS))
     ap.add_argument("--scenarios", type=int, default=0, help="override the batch size")
     ap.add_argument("--tile", type=int, default=0,
-                    help="scenarios per replay call (default: 1024; 2048 for config4; the whole "
+                    help="scenarios per replay call (default: 1024; 2048 for config4/5; the whole "
                          "shard for config3, whose 4 components need wide launches)")
     ap.add_argument("--jitter", type=float, default=0.1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -240,9 +240,10 @@ def main():
     from paper_2504_09307_b200.shard import gather_rows, shard
     S_total = args.scenarios or scenarios
     first, S_local = shard(S_total, world, rank)
-    # config4: 2,048 scenarios per call (81 GB of timestamps, as config5 at 1,024) so the walk
-    # and K5 grids are not a fraction of a wave short (measured: 235 -> 251 G relaxations/s)
-    default_tile = {"config3": S_local, "config4": 2048}.get(args.config, 1024)
+    # configs 4/5: 2,048 scenarios per call (81 / 162 GB of timestamps in HBM): wider walk and
+    # K5 grids waste less of their last wave (measured: config4 235 -> 251, config5 225 -> 234
+    # G relaxations/s; 512 per call drops config5 to 205)
+    default_tile = {"config3": S_local, "config4": 2048, "config5": 2048}.get(args.config, 1024)
     tile = min(args.tile or default_tile, S_local)
     assert S_local % tile == 0, "scenarios per GPU must be a multiple of the tile"
 
