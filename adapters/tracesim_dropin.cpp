@@ -8,7 +8,9 @@
 // simulate() — CLI replay/whatif/analyze (cli.cpp:181, 224-225, 307), the
 // acceptance gate, the tests — then replays on the GPU.  Exceptions follow the
 // reference taxonomy (types.hpp:109-138): invalid graphs and deadlocks throw
-// SimulationError with the reference's message text.
+// SimulationError with the reference's message text ("invalid graph: ...";
+// "deadlock with N tasks blocked" — the witness id list of simulate.cpp:300 is
+// not reproduced).
 //
 // The batched entry point (not in the reference) is declared in
 // tracesim_b200.hpp: N duration scenarios of one graph in one call.
@@ -349,6 +351,13 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   ts_retime rt{};
   const bool retime = !spec.alpha_us.empty();
   if (retime) {
+    // the C ABI reads count (3 * count) entries of every per-scenario array
+    if (spec.alpha_us.size() != S || spec.bytes_per_us.size() != S)
+      throw std::invalid_argument("retime needs alpha_us and bytes_per_us per scenario (count entries)");
+    if (!spec.target_dp.empty() && spec.target_dp.size() != S)
+      throw std::invalid_argument("target_dp needs count entries (or none)");
+    if (!spec.target_model.empty() && spec.target_model.size() != 3 * S)
+      throw std::invalid_argument("target_model needs 3 * count entries (or none)");
     rt.alpha_us = spec.alpha_us.data();
     rt.bytes_per_us = spec.bytes_per_us.data();
     rt.source_dp = spec.source_dp;
@@ -417,6 +426,8 @@ ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, st
   rep.relative_error =
       relative_error(rep.reference_makespan, rep.simulated_makespan, &rep.zero_reference);
   const std::size_t n = graph.tasks.size();
+  if (s >= r.delta_abs_sum.size() || 3 * s + 2 >= r.delta_worst.size())
+    throw std::invalid_argument("replay_report needs a batch run with BatchOptions::deltas");
   rep.mean_abs_delta = n ? static_cast<double>(r.delta_abs_sum[s]) / static_cast<double>(n) : 0.0;
   rep.max_abs_delta = r.delta_worst[3 * s];
   const int64_t task = r.delta_worst[3 * s + 1];
@@ -467,7 +478,9 @@ std::vector<SimulatedTrace> replay_scenarios(const ExecutionGraph& graph, const 
     const bool retime = !spec.alpha_us.empty();
     if (retime) {  // per-scenario retime arrays are indexed from spec.first
       const std::size_t k = static_cast<std::size_t>(id - spec.first);
-      if (id < spec.first || k >= spec.alpha_us.size())
+      if (id < spec.first || k >= spec.alpha_us.size() || k >= spec.bytes_per_us.size() ||
+          (!spec.target_dp.empty() && k >= spec.target_dp.size()) ||
+          (!spec.target_model.empty() && 3 * k + 2 >= spec.target_model.size()))
         throw std::invalid_argument("scenario id outside the retime arrays");
       rt.alpha_us = &spec.alpha_us[k];
       rt.bytes_per_us = &spec.bytes_per_us[k];

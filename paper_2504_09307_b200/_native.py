@@ -108,6 +108,8 @@ def lib():
         L.ts_scenario_durations.restype = C.c_int
         L.ts_scenario_durations.argtypes = [C.c_void_p, C.POINTER(TsScenarios), i64p, C.c_int64,
                                             C.c_void_p]
+        L.ts_walk_counts.restype = C.c_int
+        L.ts_walk_counts.argtypes = [i64p]
         L.ts_profile_enable.restype = C.c_int
         L.ts_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.ts_profile_read.restype = C.c_int
@@ -118,13 +120,20 @@ def lib():
     return _lib
 
 
+def walk_counts() -> list:
+    """K1 walk launches per variant: [1/thread u32, 1/thread i64, 2/thread u32, 2/thread i64]."""
+    out = (C.c_int64 * 4)()
+    lib().ts_walk_counts(out)
+    return list(out)
+
+
 def last_error() -> str:
     return lib().ts_last_error().decode()
 
 
 EXPORTED = ["ts_abi_version", "ts_last_error", "ts_kernel_launches", "ts_graph_create",
             "ts_graph_destroy", "ts_graph_get_info", "ts_graph_ranks", "ts_graph_streams",
-            "ts_replay_batch", "ts_simulate", "ts_scenario_durations", "ts_profile_enable",
+            "ts_replay_batch", "ts_simulate", "ts_walk_counts", "ts_scenario_durations", "ts_profile_enable",
             "ts_profile_read", "ts_synth_defaults", "ts_synth_graph", "ts_host_graph_desc",
             "ts_host_graph_op_index", "ts_host_graph_n_ops", "ts_host_graph_name_ids",
             "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph",

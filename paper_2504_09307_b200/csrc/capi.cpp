@@ -189,6 +189,11 @@ extern "C" {
 int ts_abi_version(void) { return TS_ABI_VERSION; }
 const char* ts_last_error(void) { return g_err.c_str(); }
 int64_t ts_kernel_launches(void) { return g_launches.load(); }
+int ts_walk_counts(int64_t* out) {
+  if (!out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  walk_variant_counts(out);
+  return TS_OK;
+}
 
 int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   if (!desc || !out) return fail(TS_E_INVALID_ARGUMENT, "null argument");
@@ -219,19 +224,47 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   } else {
     cudaGetDevice(&g->device);
   }
-  const CompiledGraph& c = g->cg;
-  if (!c.des_only && walk_width(c.max_slots, false) == 0) {
-    const std::string msg = "a component needs " + std::to_string(c.max_slots) +
-                            " live values per scenario: more than shared memory holds";
-    delete g;
-    return fail(TS_E_UNSUPPORTED, msg);
-  }
-  for (size_t r = 0; r + 1 < c.rank_stream_off.size(); ++r)
-    if (c.rank_stream_off[r + 1] - c.rank_stream_off[r] > max_streams_per_rank()) {
+  // Graphs the walk cannot hold fall back instead of failing (the reference
+  // replays them): a component coupling more ranks than one CTA holds is
+  // compiled without the cooperative split; a component with more live values
+  // than shared memory holds, or a rank with more streams than the per-rank
+  // merge supports, takes the exact event-driven path (plain replay graphs;
+  // gated estimate graphs have no event-driven restatement and are rejected).
+  auto coop_fits = [](const CompiledGraph& cg) {
+    const size_t smem = static_cast<size_t>((cg.max_mailboxes * 4 + 15) / 16) * 16 +
+                        static_cast<size_t>(cg.max_mailboxes) * 32 * 4 +
+                        static_cast<size_t>(cg.max_coop_ranks) * cg.max_slots * 32 * 4;
+    return cg.max_coop_ranks <= 32 && smem <= 227 * 1024;
+  };
+  auto has_coop = [](const CompiledGraph& cg) {
+    for (size_t ci = 0; ci + 1 < cg.coop_prog_off.size(); ++ci)
+      if (cg.coop_prog_off[ci + 1] - cg.coop_prog_off[ci] > 1) return true;
+    return false;
+  };
+  if (!g->cg.des_only && has_coop(g->cg) && !coop_fits(g->cg)) {
+    g->cg = CompiledGraph{};
+    rc = compile_graph(*desc, g->cg, err, /*allow_coop=*/false);
+    if (rc != TS_OK) {
       delete g;
-      return fail(TS_E_UNSUPPORTED, "rank has more than " +
-                                        std::to_string(max_streams_per_rank()) + " streams");
+      return fail(rc, err);
     }
+  }
+  CompiledGraph& c = g->cg;
+  std::string fallback;
+  if (!c.des_only && walk_width(c.max_slots, false) == 0)
+    fallback = "a component needs " + std::to_string(c.max_slots) +
+               " live values per scenario: more than shared memory holds";
+  for (size_t r = 0; r + 1 < c.rank_stream_off.size() && fallback.empty() && !c.des_only; ++r)
+    if (c.rank_stream_off[r + 1] - c.rank_stream_off[r] > max_streams_per_rank())
+      fallback = "rank has more than " + std::to_string(max_streams_per_rank()) + " streams";
+  if (!fallback.empty()) {
+    if (desc->n_gates > 0) {
+      delete g;
+      return fail(TS_E_UNSUPPORTED, fallback);
+    }
+    c.des_only = true;
+    c.des_reason = fallback;
+  }
   // launch order: longest component first (smaller tail)
   std::vector<int32_t> order(c.comps.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int32_t>(i);
@@ -247,18 +280,6 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   }
   g->n_single = static_cast<int32_t>(single.size());
   g->n_coop = static_cast<int32_t>(coop.size());
-  if (g->n_coop > 0) {  // shared memory of a cooperative CTA with uint32 values
-    const size_t smem = static_cast<size_t>((c.max_mailboxes * 4 + 15) / 16) * 16 +
-                        static_cast<size_t>(c.max_mailboxes) * 32 * 4 +
-                        static_cast<size_t>(c.max_coop_ranks) * c.max_slots * 32 * 4;
-    if (c.max_coop_ranks > 32 || smem > 227 * 1024) {
-      const std::string msg = "a component couples " + std::to_string(c.max_coop_ranks) +
-                              " ranks through " + std::to_string(c.max_mailboxes) +
-                              " values: more than one CTA holds (compile with LUMOS_COOP=0)";
-      delete g;
-      return fail(TS_E_UNSUPPORTED, msg);
-    }
-  }
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&g->d_ops, c.ops);
   if (e == cudaSuccess) e = upload(&g->d_progs, c.programs);
@@ -494,8 +515,11 @@ static int retime_stage(ts_graph* g, const ts_retime* rt, int32_t count, cudaStr
   int32_t first_np = -1, first_nogroup = -1;
   for (int32_t t = 0; t < c.n_tasks && (first_np < 0 || first_nogroup < 0); ++t) {
     const uint8_t k = c.rt_kind[t];
-    if (first_np < 0 && (k == TS_RT_OPT || k == TS_RT_ALLREDUCE)) first_np = t;
-    if (first_nogroup < 0 && k == TS_RT_ALLREDUCE && c.rt_group[t] <= 0) first_nogroup = t;
+    // change_hidden touches an allreduce only when it carries a byte count
+    // (transform.cpp:313); scale_dp's missing-bytes error is checked below
+    const bool ar_bytes = k == TS_RT_ALLREDUCE && c.rt_bytes[t] >= 0;
+    if (first_np < 0 && (k == TS_RT_OPT || ar_bytes)) first_np = t;
+    if (first_nogroup < 0 && ar_bytes && c.rt_group[t] <= 0) first_nogroup = t;
   }
   bool any_dp_change = false;
   for (int32_t s = 0; s < count; ++s) {
@@ -840,6 +864,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     const char* force = std::getenv("LUMOS_COOP_FORCE_U32");  // tests: exercise the wrap fix-up
     if (force && force[0] == '1') coop_rel32 = true;
   }
+  // LUMOS_WALK_KS=1|2 pins the walk's scenarios per thread (tests run every
+  // parity case on both variants; an odd first id always takes one)
+  int32_t force_ks = 0;
+  if (const char* ks = std::getenv("LUMOS_WALK_KS")) force_ks = (ks[0] == '1') ? 1 : (ks[0] == '2') ? 2 : 0;
   {
     Timed tm(g, stream, 2);
     CUDA_TRY(launch_span_init(lo, hi, status, count, stream));
@@ -853,6 +881,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.comps = g->d_comps;
     wp.comp_order = g->d_comp_order;
     wp.n_comps = g->n_single;
+    wp.force_ks = force_ks;
     wp.window_start = c.window_start;
     wp.sp = sp;
     wp.sp.first = sp.first + b0;
@@ -1075,10 +1104,22 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   }
   if (prev_dev >= 0 && prev_dev != g->device) cudaSetDevice(prev_dev);
   int64_t n_dead = 0;
-  for (int32_t st : host_status) n_dead += st < 0;
-  if (c.des_only && n_dead > 0)
-    return fail(TS_E_SIMULATION, "deadlock: " + std::to_string(n_dead) +
-                                     " scenario(s) left tasks blocked");
+  int32_t first_dead = -1;
+  for (int32_t i = 0; i < static_cast<int32_t>(host_status.size()); ++i)
+    if (host_status[i] < 0 && n_dead++ == 0) first_dead = i;
+  if (c.des_only && n_dead > 0) {
+    // the reference's message (simulate.cpp:300) without the witness ids
+    int64_t blocked = 0;
+    if (cudaMemcpy(&blocked, hi + first_dead, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaGetLastError();
+      blocked = -1;
+    }
+    std::string msg = "deadlock with " + std::to_string(blocked) + " tasks blocked";
+    if (count > 1)
+      msg += " (scenario " + std::to_string(sc->first + first_dead) + "; " +
+             std::to_string(n_dead) + " of " + std::to_string(count) + " scenarios deadlocked)";
+    return fail(TS_E_SIMULATION, msg);
+  }
   return TS_OK;
 }
 

@@ -123,7 +123,8 @@ struct CertEntry {
 
 namespace {
 
-int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
+int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& err,
+                     bool allow_coop) {
   const int32_t n = d.n_tasks;
   if (n < 0) {
     err = "n_tasks must be non-negative";
@@ -623,7 +624,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
 
   // cooperative multi-rank walks (LUMOS_COOP=0 disables them)
   const char* coop_env = std::getenv("LUMOS_COOP");
-  const bool coop = !(coop_env && coop_env[0] == '0');
+  const bool coop = allow_coop && !(coop_env && coop_env[0] == '0');
   out.coop_prog_off.clear();
   out.coop_progs.clear();
   out.max_mailboxes = 0;
@@ -1453,8 +1454,9 @@ void build_common(const ts_graph_desc& d, CompiledGraph& out) {
 
 }  // namespace
 
-int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err) {
-  int rc = compile_programs(d, out, err);
+int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err,
+                  bool allow_coop) {
+  int rc = compile_programs(d, out, err, allow_coop);
   if (rc == TS_E_UNSUPPORTED && d.n_gates == 0) {
     // outside the chained class: every scenario takes the exact event-driven
     // path (a restatement of the reference Engine on the device)

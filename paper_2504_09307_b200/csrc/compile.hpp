@@ -80,6 +80,9 @@ struct CompiledGraph {
 };
 
 // Returns TS_OK or a TS_E_* code with `err` set to the reference-style message.
-int compile_graph(const ts_graph_desc& desc, CompiledGraph& out, std::string& err);
+// allow_coop = false compiles gated components as single programs (no
+// cooperative per-rank split), as LUMOS_COOP=0 does.
+int compile_graph(const ts_graph_desc& desc, CompiledGraph& out, std::string& err,
+                  bool allow_coop = true);
 
 }  // namespace lumos

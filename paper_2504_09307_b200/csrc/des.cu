@@ -239,8 +239,9 @@ __global__ void des_kernel(DesParams P) {
       }
       now = t2;
     }
-    if (dead) {
+    if (dead) {  // span_hi carries the blocked-task count for the error message
       P.status[col] = -1;
+      P.span_hi[col] = unstarted;
       continue;
     }
     int64_t lo = W, hi = W;

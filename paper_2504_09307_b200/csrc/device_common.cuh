@@ -213,7 +213,7 @@ __device__ __forceinline__ int64_t rt_task(const RetimeParams& P, const RtCol& c
       d = mul_div_nonneg(d, nd[0] * nd[1] * nd[2], mnk[0] * mnk[1] * mnk[2], -1);
     } else if (kd == TS_RT_OPT) {
       d = mul_div_nonneg(d, c.tm[2], P.src_model[2], -1);
-    } else if (kd == TS_RT_ALLREDUCE) {
+    } else if (kd == TS_RT_ALLREDUCE && bytes >= 0) {  // no byte count: left as is
       bytes = mul_div_nonneg(bytes, c.tm[2], P.src_model[2], -1);
       d = coll_cost(true, bytes, P.group[t], c.alpha, c.bpu);
     } else if (kd == TS_RT_P2P_SEND || kd == TS_RT_P2P_RECV) {

@@ -71,7 +71,7 @@ struct WalkParams {
   const ComponentDesc* comps;
   const int32_t* comp_order;  // optional launch order of components
   int32_t n_comps;
-  int32_t pad;
+  int32_t force_ks;  // 0: scenarios per thread chosen by occupancy; 1 / 2: forced (tests)
   int64_t window_start;
   ScenarioParams sp;
   int64_t* out_start;  // [n_tasks][ld] or null
@@ -178,6 +178,9 @@ int walk_threads();
 int walk_width(int n_slots, bool rel32);  // walk CTA width for a slot count (0: too many)
 int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
+// walk launches per variant since load: [0] one scenario per thread (uint32
+// slots), [1] one (int64), [2] two per thread (uint32), [3] two (int64)
+void walk_variant_counts(int64_t out[4]);
 
 // Cooperative walk (components of several ranks coupled by gates): one CTA =
 // (component, 32 scenarios), one warp per rank program, cross-rank values

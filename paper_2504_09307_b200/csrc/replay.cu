@@ -19,6 +19,7 @@
 // host restatement (compiled with -ffp-contract=off) bit for bit.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -80,7 +81,9 @@ __device__ __noinline__ int64_t rt_coll_base(const RtScen* scp, int32_t rk, int3
                                              int32_t source_dp, int64_t v, int64_t base) {
   const RtScen sc = *scp;
   int64_t d = base;
-  if (sc.flags & kRtHid)
+  // v < 0: an allreduce without a byte count, which change_hidden leaves as is
+  // (transform.cpp:313; scale_dp rejects it on the host)
+  if ((sc.flags & kRtHid) && v >= 0)
     d = coll_cost(rk == TS_RT_ALLREDUCE, v, rk == TS_RT_ALLREDUCE ? grp : 2, sc.alpha, sc.bpu);
   if ((sc.flags & kRtDp) && rk == TS_RT_ALLREDUCE && grp == source_dp)
     d = coll_cost(true, v, sc.tdp, sc.alpha, sc.bpu);
@@ -703,7 +706,7 @@ __global__ void retime_variants_kernel(VariantParams P) {
     } else if (r.kind == TS_RT_OPT) {
       out = mul_div_nonneg(r.base, tm[2], P.src_model[2], -1);
     } else if (r.kind == TS_RT_ALLREDUCE) {
-      out = mul_div_nonneg(out, tm[2], P.src_model[2], -1);
+      if (out >= 0) out = mul_div_nonneg(out, tm[2], P.src_model[2], -1);
     } else {  // TS_RT_P2P_SEND
       out = mul_div_nonneg(out, tm[0], P.src_model[0], -1);
     }
@@ -1322,12 +1325,22 @@ static cudaError_t launch_walk_v(const WalkParams& p, int n_slots, int t, cudaSt
   return cudaErrorInvalidConfiguration;
 }
 
+static std::atomic<int64_t> g_walk_variant[4];
+
+void walk_variant_counts(int64_t out[4]) {
+  for (int k = 0; k < 4; ++k) out[k] = g_walk_variant[k].load();
+}
+
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
   const bool rel = p.rel32 != 0;
   const int t = walk_width(n_slots, rel);
   // two scenarios per thread share one Philox call per task, which needs the
-  // thread's columns to be one global pair: an even first id
-  if (single_scenario(p) || (p.sp.first & 1))
+  // thread's columns to be one global pair: an even first id.  force_ks (tests)
+  // overrides the occupancy choice but never the pairing rule.
+  bool one = p.force_ks == 1 || (p.force_ks != 2 && single_scenario(p));
+  if (p.sp.first & 1) one = true;
+  g_walk_variant[(one ? 0 : 2) + (rel ? 0 : 1)]++;
+  if (one)
     return rel ? launch_walk_v<uint32_t, 1>(p, n_slots, t, stream)
                : launch_walk_v<int64_t, 1>(p, n_slots, t, stream);
   return rel ? launch_walk_v<uint32_t, 2>(p, n_slots, t, stream)

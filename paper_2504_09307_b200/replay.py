@@ -40,11 +40,24 @@ def _raise(rc: int):
     raise ValueError(msg)
 
 
+_ITEM = {N.i64p: ("int64", 8), N.i32p: ("int32", 4), N.u8p: ("uint8", 1)}
+
+
 def _ptr(a, t):
+    """Raw pointer of a buffer the C ABI reads or writes as a dense row-major
+    array of t's element type: strided views or other dtypes are rejected
+    (the library would silently use the wrong layout)."""
     if a is None:
         return None
+    name, size = _ITEM[t]
     if hasattr(a, "data_ptr"):  # torch tensor (device or host)
+        if str(a.dtype) != f"torch.{name}" or not a.is_contiguous():
+            raise ValueError(f"expected a contiguous torch.{name} tensor, got {a.dtype} "
+                             f"(contiguous={a.is_contiguous()})")
         return C.cast(C.c_void_p(a.data_ptr()), t)
+    if a.dtype != np.dtype(name) or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"expected a C-contiguous {name} array, got {a.dtype} "
+                         f"(C_CONTIGUOUS={a.flags['C_CONTIGUOUS']})")
     return a.ctypes.data_as(t)
 
 

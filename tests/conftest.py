@@ -30,3 +30,13 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(params=["1", "2"], ids=["ks1", "ks2"])
+def walk_ks(request, monkeypatch):
+    """Runs a GPU parity test once per K1 walk variant: one scenario per
+    thread and two per thread (the variant every benchmark launch takes).
+    LUMOS_WALK_KS pins the choice inside ts_replay_batch (capi.cpp); batches
+    starting at an odd global id always take one scenario per thread."""
+    monkeypatch.setenv("LUMOS_WALK_KS", request.param)
+    return int(request.param)

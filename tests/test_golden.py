@@ -54,7 +54,7 @@ def test_restatement_matches_golden(path):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", GOLDEN, ids=os.path.basename)
-def test_cuda_path_matches_golden(path):
+def test_cuda_path_matches_golden(path, walk_ks):
     from paper_2504_09307_b200 import ScenarioSpec, simulate_batch
     d, g, sc = _load(path)
     count = d["durations"].shape[0]

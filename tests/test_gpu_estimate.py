@@ -10,7 +10,7 @@ from paper_2504_09307_b200 import ScenarioSpec, simulate_batch
 from paper_2504_09307_b200.synth import generate_graph
 from test_synth_graph import FIELDS, _my_lane_sequences, _ref_pipeline, _spec
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("walk_ks")]
 
 
 def _orc_graph(g):

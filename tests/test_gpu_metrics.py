@@ -15,7 +15,7 @@ import refshim as R
 from paper_2504_09307_b200 import ScenarioSpec, SimulationError, simulate_batch
 from test_gpu_parity import _graph
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("walk_ks")]
 
 
 def _check_util(h, g, res, s, rs, rf, width):

@@ -14,7 +14,7 @@ from paper_2504_09307_b200 import (DeviceGraph, ScenarioSpec, SimulationError,
                                    UnsupportedGraphError, simulate, simulate_batch)
 from paper_2504_09307_b200.graph import ExecutionGraph
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("walk_ks")]
 
 
 def _graph(tasks, edges=(), rules=(), window=None):

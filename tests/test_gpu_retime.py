@@ -17,7 +17,7 @@ import refshim as R
 from paper_2504_09307_b200 import Retime, ScenarioSpec, DeviceGraph, simulate_batch
 from paper_2504_09307_b200.graph import ExecutionGraph, SimulationError
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("walk_ks")]
 
 
 def _with_meta(h):
@@ -197,3 +197,41 @@ def test_retime_walk_fixup_retimes_its_durations(monkeypatch):
     DeviceGraph(g).replay_batch(spec, start=start, fin=fin, status=status)
     assert (status == 1).all()  # every scenario went through the fix-up
     assert np.array_equal(start, a.start) and np.array_equal(fin, a.fin)
+
+
+def test_allreduce_without_bytes_is_left_alone(tmp_path):
+    # change_hidden retimes an allreduce only when it carries a byte count
+    # (transform.cpp:313): drop "bytes" from one gradient allreduce in the
+    # recorded trace; a width sweep must leave it as recorded (no n_params /
+    # group-size errors for it either), and a dp change must raise the
+    # reference's "carries no byte count" (transform.cpp:238-240)
+    import json
+    import os
+    R.write_rank_traces(R.synth_spec(pp=1, dp=2, m=4, layers=4), str(tmp_path))
+    path = os.path.join(tmp_path, "rank_0.json")
+    with open(path) as f:
+        tr = json.load(f)
+    evs = tr["traceEvents"] if isinstance(tr, dict) else tr
+    hit = [e for e in evs if e.get("cat") == "kernel" and
+           e.get("args", {}).get("collective") == "allreduce" and "bytes" in e.get("args", {})]
+    assert hit
+    del hit[0]["args"]["bytes"]
+    with open(path, "w") as f:
+        json.dump(tr, f)
+    h = R.ingest_traces([path])
+    g = _with_meta(h)
+    ar = np.flatnonzero(g.rt_kind == 3)
+    assert len(ar) and (g.rt_bytes[ar] < 0).any()
+    src = (1024, 4096, 350_000_000)
+    tgt = np.array([(1536, 6144, 780_000_000), (2048, 8192, 1_380_000_000)] * 2, np.int64)
+    rt = Retime(alpha_us=[10.0] * 4, bytes_per_us=[30000.0] * 4, source_model=src,
+                target_model=tgt)
+    spec = ScenarioSpec(count=4, first=2, seed=3, jitter=0.05, retime=rt)
+    _check(h, g, spec, lambda s: dict(src_model=src, tgt_model=tuple(int(x) for x in tgt[s]),
+                                      alpha=10.0, bytes_per_us=30000.0),
+           sc=R.OrcScenarios(seed=3, jitter=0.05))
+    with pytest.raises(Exception, match="carries no byte count"):
+        simulate_batch(g, ScenarioSpec(count=1, retime=Retime(alpha_us=[10.0],
+                                                              bytes_per_us=[30000.0],
+                                                              source_dp=2, target_dp=[4])),
+                       breakdown=False)
