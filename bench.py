@@ -80,6 +80,7 @@ def parse():
     ap.add_argument("--jitter", type=float, default=0.1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-audit", action="store_true", help="skip the parity audit")
     return ap.parse_args()
 
 
@@ -214,6 +215,87 @@ def reference_arm(args):
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------------- parity audit
+
+def audit(args, g, dg, replay_tile, first, S_local, tile, bd_all, span_all, busy_all):
+    """Bit-exact audit of the benchmarked path, outside the timed region: for
+    scenario ids spread over the whole batch (first, middle and last tile,
+    even and odd columns) every start / finish of every task of all TP
+    replicas, the span and every per-rank breakdown row are compared with the
+    unmodified reference simulate() / breakdown_by_rank() (oracle/_ref) on the
+    oracle's durations of the same global (task, scenario) ids.  The reference
+    replays one TP replica (the tp=1 generator graph, task-for-task identical
+    to each replica's ranks) at a time, so 8 replicas x K scenarios run as
+    independent CPU jobs on the host threads."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    R, h1, g1 = cpu_sample_graph(args)
+    _, _, tp, _, _ = CONFIGS[args.config]
+    n_tiles = S_local // tile
+    picks = sorted({(0, 0), (0, 1), (n_tiles // 2, tile // 2 - 1), (n_tiles // 2, tile // 2),
+                    (max(0, (2 * n_tiles) // 3), min(tile - 1, 777)), (n_tiles - 1, tile - 2),
+                    (n_tiles - 1, tile - 1), (max(0, n_tiles - 2), min(tile - 1, 1501))})
+    t0 = time.time()
+    nr1 = int(g1.rank.max()) + 1
+    of = np.searchsorted(g.rank, np.arange(nr1 * tp + 1))
+    replica_idx = [np.concatenate([np.arange(of[r * tp + t], of[r * tp + t + 1])
+                                   for r in range(nr1)]) for t in range(tp)]
+    cls = np.zeros(g.duration.shape[0], np.uint8)
+    cls[g.task_kind == 1] = 1
+    cls[(g.task_kind == 1) & (g.op_class == 1)] = 2
+    sc = R.OrcScenarios(seed=250409307, **scenario_kwargs(args))
+    cols = {}
+    for ti in sorted({p[0] for p in picks}):
+        start, fin = replay_tile(ti)  # the benchmark's own call for that tile
+        for t_, c in picks:
+            if t_ == ti:
+                cols[ti * tile + c] = (start[:, c].cpu().numpy(), fin[:, c].cpu().numpy())
+    jobs = []
+    for s_local, (st, fi) in cols.items():
+        s = first + s_local
+        dur = np.zeros(g.duration.shape[0], np.int64)
+        R.orc().orc_fill_durations(C.byref(sc), s, dur.shape[0],
+                                   g.duration.ctypes.data_as(R._i64p), cls.ctypes.data_as(R._u8p),
+                                   dur.ctypes.data_as(R._i64p))
+        for t in range(tp):
+            jobs.append((s_local, t, np.ascontiguousarray(dur[replica_idx[t]])))
+
+    def run(job):
+        s_local, t, d = job
+        rs, rf, rspan = h1.simulate(d)
+        return s_local, t, rs, rf, rspan
+
+    threads = max(1, min(len(jobs), os.cpu_count() or 1, 16))
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(run, jobs))
+    mism = {"start": 0, "fin": 0, "span": 0, "breakdown_rows": 0}
+    ends = {}
+    ranks_of = np.asarray(dg.ranks)
+    for s_local, t, rs, rf, rspan in res:
+        st, fi = cols[s_local]
+        mism["start"] += int(np.count_nonzero(st[replica_idx[t]] != rs))
+        mism["fin"] += int(np.count_nonzero(fi[replica_idx[t]] != rf))
+        ends[s_local] = max(ends.get(s_local, rspan[1]), rspan[1])
+    W = g.window_start
+    for s_local, end in ends.items():
+        want = np.array([W, end, end - W], np.int64)
+        mism["span"] += int(not np.array_equal(span_all[s_local], want))
+    for s_local, t, rs, rf, rspan in res:
+        wend = max(g.window_end, W + int(ends[s_local] - W))
+        ref = h1.breakdown_by_rank(rs, rf, W, wend)
+        for r1, row in ref.items():
+            rr = int(np.searchsorted(ranks_of, r1 * tp + t))
+            mism["breakdown_rows"] += int(tuple(bd_all[s_local, rr]) != row)
+    return {"scenarios": sorted(first + s for s in cols), "replicas": tp,
+            "tasks_checked": int(len(cols) * g.duration.shape[0]),
+            "breakdown_rows_checked": int(len(cols) * len(ranks_of)),
+            "mismatches": int(sum(mism.values())), "by_field": mism,
+            "reference": "oracle/_ref tracesim::simulate + breakdown_by_rank, one TP replica "
+                         "(tp=1 generator graph) per job",
+            "cpu_threads": threads, "seconds": round(time.time() - t0, 1)}
 
 
 # ------------------------------------------------------------------ our arm
@@ -375,6 +457,23 @@ def main():
                        "per-stream busy copied to pinned host memory every step; timestamps "
                        "stay in device memory"}
 
+    # parity audit of the benchmarked kernels (N = 1, outside the timed region)
+    audit_res = None
+    if rank == 0 and world == 1 and not args.no_audit and args.config in ("config5", "config4"):
+        def replay_tile(ti):
+            spec = ScenarioSpec(count=tile, first=first + ti * tile, seed=250409307,
+                                **scenario_kwargs(args))
+            dg.replay_batch(spec, start=start, fin=fin, ld=tile, span=span[ti * tile:(ti + 1) * tile],
+                            rank_breakdown=bd[ti * tile:(ti + 1) * tile],
+                            stream_busy=busy[ti * tile:(ti + 1) * tile], stream=sptr)
+            torch.cuda.synchronize()
+            return start, fin
+        try:
+            audit_res = audit(args, g, dg, replay_tile, first, S_local, tile,
+                              bd.cpu().numpy(), span.cpu().numpy(), busy.cpu().numpy())
+        except Exception as exc:  # the checker is test infrastructure
+            audit_res = {"error": repr(exc)}
+
     # CPU baseline (rank 0, N = 1 only): the reference on a bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -420,6 +519,7 @@ def main():
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "audit": audit_res,
             "wall_s": wall,
         }
         print(json.dumps(line), flush=True)

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 3
+#define TS_ABI_VERSION 4
 
 /* error codes (0 = success) */
 enum {
@@ -139,6 +139,10 @@ typedef struct {
   int32_t n_syncs;        /* Stream/DeviceSync rules resolved statically       */
   int32_t n_gpu_tasks;
   int64_t window_start, window_end;
+  int32_t n_fused_ranks;  /* ranks on the split breakdown accounting (|A| summed
+                             by the walk, only candidate kernels re-read)     */
+  int32_t des_only;       /* 1: every scenario takes the event-driven path */
+  int64_t n_candidates;   /* compute kernels the split accounting re-reads   */
 } ts_graph_info;
 
 /* validate_graph + compile to device programs (simulate.cpp:26-196).

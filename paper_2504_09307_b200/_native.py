@@ -44,7 +44,8 @@ class TsGraphInfo(C.Structure):
                 ("n_ranks", C.c_int32), ("n_streams", C.c_int32), ("max_slots", C.c_int32),
                 ("program_bytes", C.c_int64), ("n_ops", C.c_int64), ("n_syncs", C.c_int32),
                 ("n_gpu_tasks", C.c_int32), ("window_start", C.c_int64),
-                ("window_end", C.c_int64)]
+                ("window_end", C.c_int64), ("n_fused_ranks", C.c_int32), ("des_only", C.c_int32),
+                ("n_candidates", C.c_int64)]
 
 
 class TsScenarios(C.Structure):
@@ -75,7 +76,7 @@ class TsResult(C.Structure):
                 ("delta_abs_sum", i64p), ("delta_worst", i64p)]
 
 
-ABI_VERSION = 3  # TS_ABI_VERSION in include/lumos_b200.h
+ABI_VERSION = 4  # TS_ABI_VERSION in include/lumos_b200.h
 _lib = None
 
 

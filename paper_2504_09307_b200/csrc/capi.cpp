@@ -137,6 +137,15 @@ struct ts_graph {
   int32_t *d_rule_wl = nullptr, *d_lane_rank = nullptr, *d_lane_stream = nullptr;
   DevBuf des_scratch;
   int32_t bucket_off[kReduceBuckets + 1] = {0};
+  // in-walk accounting: per component descriptor, the fused rank rows, and the
+  // K5 rank lists restricted to the other ranks
+  FusedDesc* d_fused = nullptr;
+  int32_t n_fused_rows = 0;
+  int32_t* d_cand_off = nullptr;
+  int32_t* d_cand_nodes = nullptr;
+  int32_t* d_rank_lists_nf = nullptr;  // non-fused ranks by bucket, then fused ranks (lite)
+  int32_t bucket_off_nf[kReduceAllBuckets + 1] = {0};
+  DevBuf acct_a;  // [tile][n_ranks] |A| sums of the walk
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[12];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur,
                      // util, util bins, delta sum, delta worst
@@ -345,6 +354,35 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     }
     g->bucket_off[kReduceBuckets] = static_cast<int32_t>(lists.size());
     if (e == cudaSuccess) e = upload(&g->d_rank_lists, lists);
+    // split accounting: fused ranks go to the lite buckets (by comm stream
+    // count), the others keep their bucket
+    std::vector<int> fused_bucket(n_ranks, -1);
+    std::vector<int32_t> fused_entry(n_ranks, 0);
+    if (!c.des_only)
+      for (const FusedDesc& fd : c.fused) {
+        if (fd.row < 0 || fused_bucket[fd.row] >= 0) continue;
+        const int s0 = c.rank_stream_off[fd.row], ns = c.rank_stream_off[fd.row + 1] - s0;
+        const int ci = fd.stream_a >= 0 ? fd.stream_a - s0 : 0xFF;
+        fused_bucket[fd.row] = kReduceLiteBucket + ns - (fd.stream_a >= 0 ? 1 : 0);
+        fused_entry[fd.row] = static_cast<int32_t>(static_cast<uint32_t>(fd.row) |
+                                                   (static_cast<uint32_t>(ci) << 24));
+        g->n_fused_rows++;
+      }
+    std::vector<int32_t> lists_nf;
+    for (int b = 0; b < kReduceAllBuckets; ++b) {
+      g->bucket_off_nf[b] = static_cast<int32_t>(lists_nf.size());
+      for (size_t r = 0; r < n_ranks; ++r) {
+        if (fused_bucket[r] < 0 && bucket[r] == b) lists_nf.push_back(entry[r]);
+        if (fused_bucket[r] == b) lists_nf.push_back(fused_entry[r]);
+      }
+    }
+    g->bucket_off_nf[kReduceAllBuckets] = static_cast<int32_t>(lists_nf.size());
+    if (e == cudaSuccess) e = upload(&g->d_rank_lists_nf, lists_nf);
+    if (g->n_fused_rows > 0) {
+      if (e == cudaSuccess) e = upload(&g->d_fused, c.fused);
+      if (e == cudaSuccess) e = upload(&g->d_cand_off, c.cand_off);
+      if (e == cudaSuccess) e = upload(&g->d_cand_nodes, c.cand_nodes);
+    }
   }
   {
     const DesTables& T = c.des;
@@ -390,6 +428,8 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_is_comm), static_cast<void*>(g->d_rank_stream_off),
                     static_cast<void*>(g->d_stream_node_off),
                     static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists),
+                    static_cast<void*>(g->d_fused), static_cast<void*>(g->d_cand_off),
+                    static_cast<void*>(g->d_cand_nodes), static_cast<void*>(g->d_rank_lists_nf),
                     static_cast<void*>(g->d_ostart), static_cast<void*>(g->d_lane_of),
                     static_cast<void*>(g->d_lane_off), static_cast<void*>(g->d_lane_tasks),
                     static_cast<void*>(g->d_succ_off), static_cast<void*>(g->d_succ),
@@ -399,6 +439,7 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_lane_rank), static_cast<void*>(g->d_lane_stream)})
       if (p) cudaFree(p);
     g->des_scratch.release();
+    g->acct_a.release();
     g->retime_dur.release();
     g->retime_par.release();
     g->rt_vval.release();
@@ -431,6 +472,9 @@ int ts_graph_get_info(const ts_graph* g, ts_graph_info* out) {
   out->n_gpu_tasks = c.n_gpu_tasks;
   out->window_start = c.window_start;
   out->window_end = c.window_end;
+  out->n_fused_ranks = g->has_device ? g->n_fused_rows : (c.des_only ? 0 : c.n_fused);
+  out->des_only = c.des_only ? 1 : 0;
+  out->n_candidates = c.cand_nodes.size();
   return TS_OK;
 }
 
@@ -780,6 +824,14 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   int64_t* hi = g->span_hi.as<int64_t>();
   int32_t* status = g->status.as<int32_t>();
 
+  // in-walk accounting (program.hpp FusedDesc): fused ranks get their
+  // breakdown and stream busy from the walk itself; K5 reduces the others.
+  // Utilization bins need the sweep, so they keep K5 for every rank.
+  const char* acct_env = std::getenv("LUMOS_FUSED_REDUCE");
+  const bool acct = want_red && !d_util && g->n_fused_rows > 0 && !c.des_only &&
+                    !(acct_env && acct_env[0] == '0');
+  const bool k5_needed = want_red && !c.des_only;
+
   // timestamps needed for the reductions but not requested: sub-batch through
   // an internal scratch tile
   int32_t sub = count;
@@ -788,7 +840,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   int64_t* s_fin = d_fin;
   int64_t s_ld = out->ld;
   // compare_replay deltas need the starts, the reductions both timestamps
-  const bool need_start = want_red || want_delta, need_fin = want_red;
+  const bool need_start = k5_needed || want_delta, need_fin = k5_needed;
   if ((need_start && !d_start) || (need_fin && !d_fin)) {
     if (!want_ts) {
       // none requested: sub-batch through an internal scratch tile of up to
@@ -925,6 +977,12 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.span_hi = hi + b0;
     wp.status = status + b0;
     wp.rel32 = rel32 ? 1 : 0;
+    if (acct) {
+      CUDA_TRY(g->acct_a.reserve(static_cast<size_t>(sub) * n_ranks * 8));
+      wp.fused = g->d_fused;
+      wp.acct_a = g->acct_a.as<int64_t>();
+      wp.n_ranks = n_ranks;
+    }
     {
       auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
       wp.vec_store = (wp.ld % 2 == 0) && (bn % 2 == 0) &&
@@ -1004,7 +1062,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
         if (rtp.target_dp) dp.rt.target_dp = rtp.target_dp + b0;
         if (rtp.target_model) dp.rt.target_model = rtp.target_model + 3 * static_cast<size_t>(b0);
       }
-      if (c.des_only) {  // the walk's reductions are not valid here: DES does them
+      if (c.des_only || acct) {  // DES reduces the scenarios it replays
         dp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
         dp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
         dp.util = d_util ? d_util + static_cast<size_t>(b0) * n_ranks * ubins : nullptr;
@@ -1022,7 +1080,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       CUDA_TRY(launch_des(dp, stream));
       g_launches++;
     }
-    if (want_red && !c.des_only) {
+    if (k5_needed) {
       ReduceParams rp{};
       rp.rank_stream_off = g->d_rank_stream_off;
       rp.stream_node_off = g->d_stream_node_off;
@@ -1043,10 +1101,18 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       rp.util = d_util ? d_util + static_cast<size_t>(b0) * n_ranks * ubins : nullptr;
       rp.util_bw = out->util_bin_width;
       rp.util_max_bins = ubins;
-      for (int b = 0; b < kReduceBuckets; ++b) {
-        const int nr = g->bucket_off[b + 1] - g->bucket_off[b];
+      if (acct) {
+        rp.cand_off = g->d_cand_off;
+        rp.cand_nodes = g->d_cand_nodes;
+        rp.acct_a = g->acct_a.as<int64_t>();
+        rp.status = status + b0;
+      }
+      const int32_t* boff = acct ? g->bucket_off_nf : g->bucket_off;
+      int32_t* lists = acct ? g->d_rank_lists_nf : g->d_rank_lists;
+      for (int b = 0; b < (acct ? kReduceAllBuckets : kReduceBuckets); ++b) {
+        const int nr = boff[b + 1] - boff[b];
         if (nr == 0) continue;
-        rp.rank_list = g->d_rank_lists + g->bucket_off[b];
+        rp.rank_list = lists + boff[b];
         Timed tm(g, stream, 1);
         CUDA_TRY(launch_rank_reduce(rp, b, nr, stream));
         g_launches++;

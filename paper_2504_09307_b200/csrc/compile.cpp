@@ -600,6 +600,119 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   std::vector<IrOp> ir;
   std::vector<int32_t> comp_tasks;
   out.comps.resize(n_comp);
+  out.fused.assign(n_comp, FusedDesc{-1, -1});
+  out.n_fused = 0;
+
+  // ---- split breakdown accounting (program.hpp FusedDesc).  Rank rows
+  // (ranks_in order, build.cpp:582-590) and stream slots (stream lanes in lane
+  // order) are numbered as build_common numbers them.
+  std::vector<int32_t> rank_ids(d.rank, d.rank + n);
+  std::vector<int32_t> rank_count;
+  std::sort(rank_ids.begin(), rank_ids.end());
+  {
+    std::vector<int32_t> u;
+    for (int32_t r : rank_ids) {
+      if (u.empty() || u.back() != r) {
+        u.push_back(r);
+        rank_count.push_back(0);
+      }
+      rank_count.back()++;
+    }
+    rank_ids.swap(u);
+  }
+  std::vector<int32_t> stream_slot(nl, -1);
+  std::vector<int8_t> lane_class(nl, -1);  // stream lanes: 0 compute-only, 1 comm-only, 2 mixed
+  {
+    int32_t k = 0;
+    for (int32_t l = 0; l < nl; ++l) {
+      if (lanes[l].kind != TS_LANE_CUDA_STREAM) continue;
+      stream_slot[l] = k++;
+      bool comm = false, comp = false;
+      for (int32_t q = lane_off[l]; q < lane_off[l + 1]; ++q)
+        (d.op_class && d.op_class[lane_tasks[q]] == TS_OP_COMMUNICATION ? comm : comp) = true;
+      lane_class[l] = comm && comp ? 2 : comm ? 1 : 0;
+    }
+  }
+  const char* fuse_env = std::getenv("LUMOS_FUSED_REDUCE");
+  const bool fuse_enabled = !(fuse_env && fuse_env[0] == '0');
+  std::vector<std::vector<int32_t>> cand_of_row(rank_ids.size());
+  std::vector<int32_t> fz_anc, fz_desc;  // per task: last compute ancestor / first descendant (A chain)
+  // Marks component c (one whole rank, single program) for split accounting:
+  // F_BUSY on its compute-stream kernels and the candidate list; false when it
+  // does not qualify (K5 sweeps all of its timestamps then).
+  auto fuse_accounting = [&](int32_t c, std::vector<IrOp>& ir) -> bool {
+    if (!fuse_enabled || comp_tasks.empty()) return false;
+    const int32_t r = d.rank[comp_tasks[0]];
+    for (int32_t t : comp_tasks)
+      if (d.rank[t] != r || split[t] || gate_slot.count(t)) return false;
+    const int32_t row = static_cast<int32_t>(
+        std::lower_bound(rank_ids.begin(), rank_ids.end(), r) - rank_ids.begin());
+    if (rank_count[row] != static_cast<int32_t>(comp_tasks.size())) return false;
+    int32_t lane_a = -1;
+    std::vector<int32_t> comm_lanes;
+    {
+      auto lo = std::lower_bound(lanes.begin(), lanes.end(), Proc{r, TS_LANE_CUDA_STREAM, INT32_MIN});
+      for (auto it = lo; it != lanes.end() && it->rank == r && it->kind == TS_LANE_CUDA_STREAM; ++it) {
+        const int32_t l = static_cast<int32_t>(it - lanes.begin());
+        if (lane_class[l] == 0 && lane_a < 0) lane_a = l;
+        else if (lane_class[l] == 1) comm_lanes.push_back(l);
+        else return false;
+      }
+    }
+    if (static_cast<int>(comm_lanes.size()) > kFusedMaxComm) return false;
+    // DAG comparability with the A chain over the timing edges (fixed edges,
+    // event-sync bound, static sync bindings — a failed sync certificate sends
+    // the whole scenario to the event-driven path, which reduces it itself).
+    // The component's op order is topological for these edges.
+    std::vector<int32_t> topo_tasks;
+    for (const IrOp& o : ir)
+      if (!o.aux() && o.v_dst >= 0 && o.v_dst < n &&
+          (o.op.kind == OP_NODE || o.op.kind == OP_SYNC))
+        topo_tasks.push_back(static_cast<int32_t>(o.v_dst));
+    if (topo_tasks.size() != comp_tasks.size()) return false;
+    auto each_pred = [&](int32_t t, auto&& f) {
+      for (int64_t k = pred.begin(t); k < pred.end(t); ++k) f(pred.idx[k]);
+      if (event_bound[t] >= 0) f(event_bound[t]);
+      if (sync_id[t] >= 0)
+        for (const auto& ce : sync_cert[sync_id[t]])
+          if (ce.kstar >= 0) f(ce.kstar);
+    };
+    const int32_t len_a = lane_a < 0 ? 0 : lane_off[lane_a + 1] - lane_off[lane_a];
+    auto apos = [&](int32_t t) { return lane_of[t] == lane_a ? chain_pos[t] : -1; };
+    if (fz_anc.empty()) {
+      fz_anc.assign(n, -1);
+      fz_desc.assign(n, INT32_MAX);
+    }
+    for (int32_t t : topo_tasks)
+      each_pred(t, [&](int32_t p) { fz_anc[t] = std::max({fz_anc[t], fz_anc[p], apos(p)}); });
+    for (size_t q = topo_tasks.size(); q-- > 0;) {
+      const int32_t t = topo_tasks[q];
+      const int32_t at = apos(t) < 0 ? INT32_MAX : apos(t);
+      each_pred(t, [&](int32_t p) { fz_desc[p] = std::min({fz_desc[p], fz_desc[t], at}); });
+    }
+    // candidates: A positions in (anc(c), desc(c)) for some comm kernel c
+    std::vector<char> cand(static_cast<size_t>(len_a), 0);
+    for (int32_t l : comm_lanes)
+      for (int32_t q = lane_off[l]; q < lane_off[l + 1]; ++q) {
+        const int32_t cm = lane_tasks[q];
+        for (int32_t k = fz_anc[cm] + 1; k < std::min(fz_desc[cm], len_a); ++k) cand[k] = 1;
+      }
+    for (int32_t t : comp_tasks) {
+      fz_anc[t] = -1;
+      fz_desc[t] = INT32_MAX;
+    }
+    auto& list = cand_of_row[row];
+    list.clear();
+    for (int32_t k = 0; k < len_a; ++k)
+      if (cand[k]) list.push_back(lane_tasks[lane_off[lane_a] + k]);
+    for (IrOp& o : ir)
+      if (!o.aux() && o.v_dst >= 0 && o.v_dst < n && lane_of[o.v_dst] == lane_a &&
+          o.op.kind == OP_NODE)
+        o.op.flags |= F_BUSY;
+    out.fused[c] = FusedDesc{row, lane_a >= 0 ? stream_slot[lane_a] : -1};
+    out.n_fused++;
+    return true;
+  };
 
   auto fold = [&](std::vector<int64_t>& vals, size_t room) {
     std::vector<int64_t> u;
@@ -658,8 +771,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         err = "scale_class must be < " + std::to_string(kMaxClasses);
         return TS_E_INVALID_ARGUMENT;
       }
-      uint8_t flags = (gpu ? F_GPU : 0) |
-                      (d.op_class && d.op_class[t] == TS_OP_COMMUNICATION ? F_COMM : 0);
+      uint8_t flags = d.op_class && d.op_class[t] == TS_OP_COMMUNICATION ? F_COMM : 0;
 
       // fixed predecessors (+ event-sync bound)
       std::vector<int64_t> fixedv;
@@ -1270,6 +1382,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     if (!split) {
       n_slots = 0;
+      fuse_accounting(c, ir);
       const int32_t prog = finish_program(ir, n_slots);
       if (prog < 0) return finish_rc;
       progs_of_comp.push_back(prog);
@@ -1290,6 +1403,12 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
   }
   out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
+  out.cand_off.assign(1, 0);
+  out.cand_nodes.clear();
+  for (const auto& list : cand_of_row) {
+    out.cand_nodes.insert(out.cand_nodes.end(), list.begin(), list.end());
+    out.cand_off.push_back(static_cast<int32_t>(out.cand_nodes.size()));
+  }
 
   // retime walk tables: a dense index per F_RT record (programs are shared by
   // replicas, so a record stands for the creator component's task)

@@ -38,6 +38,12 @@ struct CompiledGraph {
   // rank programs coop_progs[coop_prog_off[c] .. coop_prog_off[c+1]) (one entry
   // for a single-rank component)
   std::vector<int32_t> coop_prog_off, coop_progs;
+  // split breakdown accounting (program.hpp FusedDesc): per component its
+  // descriptor; per rank row the compute kernels that may overlap a comm kernel
+  // (chain order), CSR over rank rows
+  std::vector<FusedDesc> fused;
+  int32_t n_fused = 0;  // components with row >= 0
+  std::vector<int32_t> cand_off, cand_nodes;
   int32_t max_mailboxes = 0;
   int32_t max_coop_ranks = 1;
   int64_t max_coop_path = 0;  // nominal longest path of a cooperative component

@@ -83,7 +83,15 @@ struct WalkParams {
   int32_t vec_store;   // 16-byte output stores allowed (ld, count even; aligned)
   int32_t rel32;       // slot values are uint32 offsets from W (bound proven on the host)
   RetimeWalk rt;       // sp.mode & kModeRetime
+  // split accounting (program.hpp FusedDesc), or null: a fused component
+  // writes its compute-stream busy sum |A| to acct_a[col][row]
+  const FusedDesc* fused;  // [component]
+  int64_t* acct_a;         // [count][n_ranks]
+  int32_t n_ranks;
+  int32_t pad2;
 };
+
+
 
 struct ReduceParams {
   const int32_t* rank_list;  // ranks (indices into rank_stream_off) of this launch
@@ -108,6 +116,13 @@ struct ReduceParams {
   int64_t util_bw;
   int32_t util_max_bins;
   int32_t pad2;
+  // split accounting (fast-path buckets only): A is read through the rank's
+  // candidate list (cand_off / cand_nodes by rank row) and |A| comes from the
+  // walk (acct_a[col][row]) instead of the full compute-stream list
+  const int32_t* cand_off;
+  const int32_t* cand_nodes;
+  const int64_t* acct_a;  // [count][n_ranks]
+  const int32_t* status;  // lite: scenarios with a non-zero status were reduced by the fix-up
 };
 
 // what-if retime of every (task, scenario) duration (ts_retime), then the
@@ -243,7 +258,13 @@ cudaError_t launch_durations(const ScenarioParams& sp, const int64_t* base, cons
 // carry the compute stream's index in bits 24..31)
 constexpr int kReduceGenericBuckets = 7;
 constexpr int kReduceFastMaxComm = 3;
+static_assert(kReduceFastMaxComm == kFusedMaxComm, "fused ranks take the fast sweep");
 constexpr int kReduceBuckets = kReduceGenericBuckets + kReduceFastMaxComm + 1;
+// buckets kReduceLiteBucket + NC (NC = 0..3 comm streams): split accounting of
+// fused ranks (ReduceParams cand_* / acct_a); rank_list entries carry the
+// compute stream's index in bits 24..31, 0xFF when the rank has none
+constexpr int kReduceLiteBucket = kReduceBuckets;
+constexpr int kReduceAllBuckets = kReduceLiteBucket + kReduceFastMaxComm + 1;
 int reduce_bucket(int streams_in_rank);
 cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in_bucket,
                                cudaStream_t stream);

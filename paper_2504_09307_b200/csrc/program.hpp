@@ -74,7 +74,8 @@ enum OpKind : uint8_t {
 enum OpFlags : uint8_t {
   F_TRACK = 1,        // followed by an OpCov record: maintain coverage values
   F_STORE_START = 2,  // also store start into slot x2
-  F_GPU = 4,          // task runs on a CUDA stream lane
+  F_BUSY = 4,         // kernel on the compute stream of a fused component: the
+                      // walk adds finish - start to the rank's busy sum |A|
   F_COMM = 8,         // OpClass::Communication
   F_NO_OUT = 16,      // helper op, produces no SimEntry
   F_TRACK1 = 32,      // compact coverage: cov = pred0 >= start ? min(start, slot x0) : start -> x1
@@ -130,6 +131,25 @@ struct alignas(16) OpExt {
   uint16_t pad[3];
 };
 static_assert(sizeof(OpExt) == 32, "OpExt must stay 32 bytes");
+
+// Split breakdown accounting (breakdown_by_rank, metrics.cpp:43-103).  A
+// component that is exactly one rank whose GPU streams are at most one
+// compute-only stream A and at most three communication-only streams is
+// "fused": its breakdown follows from |A|, |U| (U = union of the comm
+// intervals) and |A n U|
+//   exposed_compute = |A| - |A n U|, exposed_comm = |U| - |A n U|,
+//   overlapped = |A n U|, other = window - |A| - |U| + |A n U|.
+// The walk sums |A| in a register over the F_BUSY kernels (no extra memory
+// traffic).  Intervals of two tasks ordered in the DAG are disjoint (finish <=
+// start along every edge), so a compute kernel that is comparable with every
+// comm kernel of its rank cannot meet U: the reduction reads the comm
+// intervals and only the compute kernels DAG-incomparable with some comm
+// kernel (the rank's "candidates", a few percent of A), instead of all of A.
+constexpr int kFusedMaxComm = 3;  // comm streams a fused rank may have
+struct FusedDesc {
+  int32_t row;       // breakdown row (rank index), -1: not fused
+  int32_t stream_a;  // stream slot of A, -1 none
+};
 
 struct ProgramDesc {
   int64_t op_offset;  // index into the op array (in 32-byte records)

@@ -132,7 +132,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   }
   const bool vec_store = kS == 2 && P.vec_store;  // ld even, count even, aligned buffers
 
-  const ComponentDesc cd = P.comps[P.comp_order ? P.comp_order[comp] : comp];
+  const int comp_id = P.comp_order ? P.comp_order[comp] : comp;
+  const ComponentDesc cd = P.comps[comp_id];
   const ProgramDesc pd = P.progs[cd.program];
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
@@ -173,6 +174,10 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   char* const sbase = reinterpret_cast<char*>(start_c0);
   char* const fbase = reinterpret_cast<char*>(fin_c0);
   const uint64_t ld8 = static_cast<uint64_t>(ld) * 8u;
+  // split accounting of a fused component (program.hpp FusedDesc): |A| summed
+  // in registers over the F_BUSY kernels
+  const int acct_row = P.fused ? P.fused[comp_id].row : -1;
+  VP busy_a = splat<V, kS>(V(0));
 
   auto stage = [&](int4* dstbuf, int r, int4 a, int4 b) {
     dstbuf[4 * r] = a;
@@ -342,6 +347,10 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         }
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
+        if (flags & F_BUSY) {
+#pragma unroll
+          for (int s = 0; s < kS; ++s) busy_a.v[s] = static_cast<V>(busy_a.v[s] + (fin.v[s] - st.v[s]));
+        }
         if (__builtin_expect((flags & F_SINK) != 0, 0)) {
 #pragma unroll
           for (int s = 0; s < kS; ++s) hi[s] = imax(hi[s], absv(fin.v[s]));
@@ -410,6 +419,13 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
     }
     __syncthreads();
   }
+  if (acct_row >= 0) {
+#pragma unroll
+    for (int s = 0; s < kS; ++s)
+      P.acct_a[static_cast<int64_t>(col[s]) * P.n_ranks + acct_row] =
+          kRel ? static_cast<int64_t>(static_cast<uint32_t>(busy_a.v[s]))
+               : static_cast<int64_t>(busy_a.v[s]);
+  }
 #undef SLOT2
 #undef SLOTB
 #pragma unroll
@@ -422,8 +438,15 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   }
 }
 
+// LUMOS_WALK_MINB > 0 caps uint32 walks at 64 registers (8 CTAs of 128 threads
+// per SM); measured slower than the unconstrained 71-register code (30.4 vs
+// 33.5 ms per config-5 tile of 2,048 scenarios), so it is off by default
+#ifndef LUMOS_WALK_MINB
+#define LUMOS_WALK_MINB 0
+#endif
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
-__global__ void __launch_bounds__(kT) replay_walk_kernel(WalkParams P) {
+__global__ void __launch_bounds__(kT, sizeof(V) == 4 && LUMOS_WALK_MINB > 0 ? LUMOS_WALK_MINB * 128 / kT : 1)
+    replay_walk_kernel(WalkParams P) {
   replay_walk_body<kT, kMode, kWriteStart, kWriteFin, V, kS>(P);
 }
 // retime walks: at least 6 CTAs of 128 threads per SM (<= 80 registers)
@@ -1003,7 +1026,11 @@ constexpr size_t fast_ring_words() {
   return static_cast<size_t>(2 * kFastHA * 2 + NC * 2 * kFastHC * 2);
 }
 
-template <int NC, typename T, bool kUtil>
+// kLite (split accounting, program.hpp FusedDesc): the A cursor walks only the
+// rank's candidate compute kernels and |A| is the walk's sum; ci == kNoA: the
+// rank has no compute stream
+constexpr int kNoA = 0xFF;
+template <int NC, typename T, bool kUtil, bool kLite>
 __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int col, int r,
                                                       int ci, int64_t* ring, int64_t W,
                                                       int64_t wend) {
@@ -1021,14 +1048,18 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
     return static_cast<T>(x);
   };
   Cursor<kFastHA, T> A;
-  A.init(P.stream_node_off[s0 + ci], P.stream_node_off[s0 + ci + 1], ring + tid, nodes, S, F,
-         ld, col);
+  if (kLite)
+    A.init(P.cand_off[r], P.cand_off[r + 1], ring + tid, P.cand_nodes, S, F, ld, col);
+  else
+    A.init(P.stream_node_off[s0 + ci], P.stream_node_off[s0 + ci + 1], ring + tid, nodes, S, F,
+           ld, col);
+  const int* __restrict__ anodes = kLite ? P.cand_nodes : nodes;
   Cursor<kFastHC, T> C[NC > 0 ? NC : 1];
   T cs[NC > 0 ? NC : 1], ce[NC > 0 ? NC : 1];
   int64_t cbusy[NC > 0 ? NC : 1];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
-    const int s = s0 + j + (j >= ci ? 1 : 0);
+    const int s = s0 + j + (ci != kNoA && j >= ci ? 1 : 0);
     C[j].init(P.stream_node_off[s], P.stream_node_off[s + 1],
               ring + (2 * kFastHA * 2 + j * 2 * kFastHC * 2) * kThreads + tid, nodes, S, F, ld,
               col);
@@ -1085,8 +1116,8 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
 
   int64_t busy_a = 0, ov = 0;
   T as, ae;
-  while (A.get(as, ae, nodes, S, F, ld, col, rel)) {
-    busy_a += static_cast<int64_t>(ae - as);
+  while (A.get(as, ae, anodes, S, F, ld, col, rel)) {
+    if (!kLite) busy_a += static_cast<int64_t>(ae - as);
     if (kUtil) ua.add(static_cast<int64_t>(as), static_cast<int64_t>(ae), 1);
     if (NC > 0) {
       while (ue <= as) next_union();
@@ -1101,6 +1132,7 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
   }
   if (NC > 0)
     while (us != kInf) next_union();
+  if (kLite) busy_a = P.acct_a[static_cast<int64_t>(col) * P.n_ranks + r];
   if (kUtil) {
     ua.flush();
     uu.flush();
@@ -1117,22 +1149,23 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
   }
   if (P.stream_busy) {
     int64_t* b = P.stream_busy + static_cast<int64_t>(col) * P.n_streams + s0;
-    b[ci] = busy_a;
+    if (ci != kNoA) b[ci] = busy_a;
 #pragma unroll
-    for (int j = 0; j < NC; ++j) b[j + (j >= ci ? 1 : 0)] = cbusy[j];
+    for (int j = 0; j < NC; ++j) b[j + (ci != kNoA && j >= ci ? 1 : 0)] = cbusy[j];
   }
 }
 
 // rank_list entries: rank | compute-stream index << 24
 // (4 CTAs per SM: their rings already limit shared memory to that, so the
 // registers can go to 128 without costing occupancy)
-template <int NC, bool kUtil>
+template <int NC, bool kUtil, bool kLite>
 __global__ void __launch_bounds__(kThreads, 4) rank_reduce_fast_kernel(ReduceParams P) {
   extern __shared__ int64_t ring[];
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int e = P.rank_list[blockIdx.y];
+  const uint32_t e = static_cast<uint32_t>(P.rank_list[blockIdx.y]);
   if (col >= P.count) return;
-  const int r = e & 0xFFFFFF, ci = e >> 24;
+  if (kLite && P.status && P.status[col] != 0) return;  // the event-driven fix-up reduced it
+  const int r = static_cast<int>(e & 0xFFFFFFu), ci = static_cast<int>(e >> 24);
   const int64_t W = P.window_start;
   int64_t wend = P.window_end;
   {
@@ -1142,9 +1175,9 @@ __global__ void __launch_bounds__(kThreads, 4) rank_reduce_fast_kernel(ReducePar
   }
   if (wend < W) wend = W;
   if (wend - W < 0xFFFFFFFFll)
-    rank_reduce_fast_body<NC, uint32_t, kUtil>(P, col, r, ci, ring, W, wend);
+    rank_reduce_fast_body<NC, uint32_t, kUtil, kLite>(P, col, r, ci, ring, W, wend);
   else
-    rank_reduce_fast_body<NC, int64_t, kUtil>(P, col, r, ci, ring, W, wend);
+    rank_reduce_fast_body<NC, int64_t, kUtil, kLite>(P, col, r, ci, ring, W, wend);
 }
 
 // ------------------------------------------------------------------- K6
@@ -1437,9 +1470,10 @@ cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in
   const bool u = p.util != nullptr;
   cudaError_t e;
 #define LUMOS_GEN(NS_) (u ? go(rank_reduce_kernel<NS_, true>, NS_) : go(rank_reduce_kernel<NS_, false>, NS_))
-#define LUMOS_FAST(NC_)                                                      \
-  (u ? fast(rank_reduce_fast_kernel<NC_, true>, fast_ring_words<NC_>()) \
-     : fast(rank_reduce_fast_kernel<NC_, false>, fast_ring_words<NC_>()))
+#define LUMOS_FAST(NC_)                                                             \
+  (u ? fast(rank_reduce_fast_kernel<NC_, true, false>, fast_ring_words<NC_>()) \
+     : fast(rank_reduce_fast_kernel<NC_, false, false>, fast_ring_words<NC_>()))
+#define LUMOS_LITE(NC_) fast(rank_reduce_fast_kernel<NC_, false, true>, fast_ring_words<NC_>())
   auto fast = [&](auto kern, size_t words) -> cudaError_t {
     const size_t smem = words * kThreads * sizeof(int64_t);
     if (smem > 48 * 1024) {
@@ -1461,10 +1495,15 @@ cudaError_t launch_rank_reduce(const ReduceParams& p, int bucket, int n_ranks_in
     case kReduceGenericBuckets + 0: e = LUMOS_FAST(0); break;
     case kReduceGenericBuckets + 1: e = LUMOS_FAST(1); break;
     case kReduceGenericBuckets + 2: e = LUMOS_FAST(2); break;
-    default: e = LUMOS_FAST(3); break;
+    case kReduceGenericBuckets + 3: e = LUMOS_FAST(3); break;
+    case kReduceLiteBucket + 0: e = LUMOS_LITE(0); break;
+    case kReduceLiteBucket + 1: e = LUMOS_LITE(1); break;
+    case kReduceLiteBucket + 2: e = LUMOS_LITE(2); break;
+    default: e = LUMOS_LITE(3); break;
   }
 #undef LUMOS_GEN
 #undef LUMOS_FAST
+#undef LUMOS_LITE
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

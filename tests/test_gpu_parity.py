@@ -201,10 +201,19 @@ def test_certificate_failure_is_resolved_exactly():
     start = np.zeros((g.n, 1), np.int64)
     fin = np.zeros((g.n, 1), np.int64)
     span = np.zeros((1, 3), np.int64)
-    dg.replay_batch(ScenarioSpec(count=1), start=start, fin=fin, span=span, status=status)
+    bd = np.zeros((1, dg.n_ranks, 5), np.int64)
+    busy = np.zeros((1, dg.n_streams), np.int64)
+    dg.replay_batch(ScenarioSpec(count=1), start=start, fin=fin, span=span, status=status,
+                    rank_breakdown=bd, stream_busy=busy)
     assert status[0] == 1  # resolved by the exact path
     assert np.array_equal(start[:, 0], rs) and np.array_equal(fin[:, 0], rf)
     assert np.array_equal(span[0], rspan)
+    # the rank is on the split accounting; the fix-up reduces the scenario itself
+    assert dg.info["n_fused_ranks"] == 1
+    wend = max(g.window_end, g.window_start + int(rspan[2]))
+    ref_bd = h.breakdown_by_rank(rs, rf, g.window_start, wend)
+    assert tuple(bd[0, 0]) == ref_bd[0]
+    assert np.array_equal(busy[0], _expected_stream_busy(g, dg, rs, rf, wend))
 
 
 # ----------------------------------------------------- generator graphs (C1)
@@ -454,3 +463,33 @@ def test_scenario_pairs_share_philox(first, count):
                         scale_hi=1200, scale_den=1000)
     _check_batch(h, g, spec, R.OrcScenarios(seed=21, jitter=0.25, scale_lo=800, scale_hi=1200,
                                             scale_den=1000), every=3)
+
+
+@pytest.mark.parametrize("shape", [(4, 2, 8, 4), (1, 2, 4, 4), (2, 1, 4, 4)])
+def test_split_accounting_equals_full_sweep(shape, monkeypatch):
+    # split accounting (program.hpp FusedDesc): |A| summed by the walk, only
+    # the compute kernels DAG-incomparable with a comm kernel re-read.  Same
+    # breakdown / stream busy as the full K5 sweep (LUMOS_FUSED_REDUCE=0) and
+    # as the reference breakdown_by_rank.
+    pp, dp, m, layers = shape
+    h, _ = R.generate(R.synth_spec(pp=pp, dp=dp, m=m, layers=layers))
+    g = h.export()
+    spec = ScenarioSpec(count=96, first=40, seed=5, jitter=0.3)
+    out = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("LUMOS_FUSED_REDUCE", env)
+        dg = DeviceGraph(g)
+        assert (dg.info["n_fused_ranks"] == dg.n_ranks) == (env == "1")
+        if env == "1":
+            assert 0 < dg.info["n_candidates"] < dg.info["n_gpu_tasks"] // 4 or pp == 1
+        res = simulate_batch(dg, spec, timestamps=True, breakdown=True)
+        out[env] = res
+    assert np.array_equal(out["1"].rank_breakdown, out["0"].rank_breakdown)
+    assert np.array_equal(out["1"].stream_busy, out["0"].stream_busy)
+    sc = R.OrcScenarios(seed=5, jitter=0.3)
+    for s_ in (0, 47, 95):
+        rs, rf, rspan = h.simulate(R.orc_durations(g, sc, spec.first + s_))
+        wend = max(g.window_end, g.window_start + int(rspan[2]))
+        ref = h.breakdown_by_rank(rs, rf, g.window_start, wend)
+        for i, r in enumerate(sorted(ref)):
+            assert tuple(out["1"].rank_breakdown[s_, i]) == ref[r]
