@@ -283,6 +283,52 @@ int ts_host_graph_name_ids(const ts_host_graph* g, int32_t* out);
 const char* ts_host_graph_name(const ts_host_graph* g, int32_t name_id);
 void ts_host_graph_free(ts_host_graph* g);
 
+/* Mode-B boundary: the reference's PipelineSpec (pipeline.hpp:27-90) as
+ * PODs, for graphs with the generator / estimate() semantics of
+ * build_pipeline(spec, DurationHook) (pipeline.cpp:474-477) — the spec
+ * rebuild_pipeline constructs for a structural what-if (transform.cpp:556-701)
+ * or any hand-written one.  A kernel's args (KernelSpec::args) travel onto its
+ * task's metadata with the builder's tags (pipeline.cpp:122-123, 229-297);
+ * kernels are classified by name as build_graph does (build.cpp:93-98), so
+ * op_class is informational (the reference's events do not carry it). */
+typedef struct {
+  const char* name;
+  int64_t duration;              /* KernelSpec::duration, us (negative -> 0) */
+  int32_t op_class;              /* KernelSpec::op_class (informational)     */
+  int32_t n_args;
+  const char* const* arg_keys;   /* KernelSpec::args                          */
+  const char* const* arg_values;
+} ts_kernel_spec;
+typedef struct {
+  const ts_kernel_spec* k;
+  int32_t n;
+  int32_t pad;
+} ts_kernel_list;
+typedef struct {                 /* StageSpec (pipeline.hpp:34-43) */
+  int32_t n_layers;
+  int32_t pad;
+  const ts_kernel_list* layers_fwd; /* [n_layers] */
+  const ts_kernel_list* layers_bwd; /* [n_layers], layer order (run back to front) */
+  ts_kernel_list pre_fwd, post_fwd, pre_bwd, post_bwd, reduce, optimizer;
+} ts_stage_spec;
+typedef struct {                 /* PipelineSpec (pipeline.hpp:52-70) */
+  int32_t pp, dp, num_microbatches, n_stages;
+  const ts_stage_spec* stages;   /* [n_stages], n_stages must equal pp */
+  int64_t launch_us, record_us, wait_us, sync_us;  /* HostCosts */
+  int64_t p2p_send_us, p2p_recv_base_us, activation_bytes, origin;
+  int32_t compute_stream, reduce_stream, p2p_stream, main_thread, helper_thread, pad;
+  int64_t first_event, first_correlation;
+} ts_pipeline_spec;
+/* PipelineSpec's defaults (HostCosts 5/2/2/5 us, streams 7/9/11, threads 100/200) */
+void ts_pipeline_defaults(ts_pipeline_spec* spec);
+/* build_pipeline(spec) as a graph: estimate = 1 the generator's dependency
+ * graph with gates (what estimate_batch replays), 0 the replay graph of its
+ * trace (build_graph + merge_ranks).  tp > 1 adds TP replicas r * tp + t.
+ * truth_makespan = BuiltPipeline end - origin at the base durations.  Errors
+ * follow build_pipeline's std::invalid_argument (TS_E_INVALID_ARGUMENT). */
+int ts_pipeline_graph(const ts_pipeline_spec* spec, int32_t estimate, int32_t tp,
+                      ts_host_graph** out, int64_t* truth_makespan);
+
 /* build_graph (build.cpp:338-510) over one rank's events, SoA.  cat is the
  * EventCategory (types.hpp:20-27); corr = -1, stream = -1 and
  * arg_event / arg_stream = INT64_MIN mean absent.  names is a '\n'-separated

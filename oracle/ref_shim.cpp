@@ -581,3 +581,138 @@ int64_t ref_pipeline_events(const char* spec_json, const int64_t* hook_dur, int6
 }
 
 }  // extern "C"
+
+// ------------------------------------------------ PipelineSpec as JSON (tests)
+// The Mode-B boundary takes a PipelineSpec (pipeline.hpp:27-90); tests build
+// one from the reference's pipeline_spec_for (synth.cpp:71-138), edit it in
+// Python and hand the same spec to both sides: JSON here, the ts_pipeline_spec
+// POD on the engine side.
+namespace {
+nlohmann::json kernel_json(const KernelSpec& k) {
+  return {{"name", k.name}, {"duration", k.duration}, {"op_class", static_cast<int>(k.op_class)},
+          {"args", k.args}};
+}
+KernelSpec kernel_of(const nlohmann::json& j) {
+  KernelSpec k;
+  k.name = j.at("name").get<std::string>();
+  k.duration = j.at("duration").get<Micros>();
+  k.op_class = static_cast<OpClass>(j.value("op_class", 0));
+  k.args = j.value("args", std::map<std::string, std::string>{});
+  return k;
+}
+std::vector<KernelSpec> kernels_of(const nlohmann::json& a) {
+  std::vector<KernelSpec> v;
+  for (const auto& k : a) v.push_back(kernel_of(k));
+  return v;
+}
+nlohmann::json list_json(const std::vector<KernelSpec>& v) {
+  nlohmann::json a = nlohmann::json::array();
+  for (const auto& k : v) a.push_back(kernel_json(k));
+  return a;
+}
+PipelineSpec pipeline_of(const nlohmann::json& j) {
+  PipelineSpec p;
+  p.pp = j.at("pp");
+  p.dp = j.at("dp");
+  p.num_microbatches = j.at("num_microbatches");
+  p.host.launch = j.at("launch");
+  p.host.record = j.at("record");
+  p.host.wait = j.at("wait");
+  p.host.sync = j.at("sync");
+  p.p2p_send = j.at("p2p_send");
+  p.p2p_recv_base = j.at("p2p_recv_base");
+  p.activation_bytes = j.at("activation_bytes");
+  p.origin = j.at("origin");
+  p.compute_stream = j.at("compute_stream");
+  p.reduce_stream = j.at("reduce_stream");
+  p.p2p_stream = j.at("p2p_stream");
+  p.main_thread = j.at("main_thread");
+  p.helper_thread = j.at("helper_thread");
+  p.first_event = j.at("first_event");
+  p.first_correlation = j.at("first_correlation");
+  for (const auto& s : j.at("stages")) {
+    StageSpec st;
+    for (const auto& l : s.at("layers_fwd")) st.layers_fwd.push_back(kernels_of(l));
+    for (const auto& l : s.at("layers_bwd")) st.layers_bwd.push_back(kernels_of(l));
+    st.pre_fwd = kernels_of(s.at("pre_fwd"));
+    st.post_fwd = kernels_of(s.at("post_fwd"));
+    st.pre_bwd = kernels_of(s.at("pre_bwd"));
+    st.post_bwd = kernels_of(s.at("post_bwd"));
+    st.reduce = kernels_of(s.at("reduce"));
+    st.optimizer = kernels_of(s.at("optimizer"));
+    p.stages.push_back(std::move(st));
+  }
+  return p;
+}
+std::string g_spec_json;
+}  // namespace
+
+extern "C" {
+
+// pipeline_spec_for(SynthSpec::from_json(spec_json)) as JSON (valid until the next call)
+const char* ref_pipeline_spec_json(const char* spec_json) {
+  try {
+    PipelineSpec p = pipeline_spec_for(SynthSpec::from_json(spec_json));
+    nlohmann::json j = {{"pp", p.pp}, {"dp", p.dp}, {"num_microbatches", p.num_microbatches},
+                        {"launch", p.host.launch}, {"record", p.host.record},
+                        {"wait", p.host.wait}, {"sync", p.host.sync},
+                        {"p2p_send", p.p2p_send}, {"p2p_recv_base", p.p2p_recv_base},
+                        {"activation_bytes", p.activation_bytes}, {"origin", p.origin},
+                        {"compute_stream", p.compute_stream}, {"reduce_stream", p.reduce_stream},
+                        {"p2p_stream", p.p2p_stream}, {"main_thread", p.main_thread},
+                        {"helper_thread", p.helper_thread}, {"first_event", p.first_event},
+                        {"first_correlation", p.first_correlation}};
+    nlohmann::json stages = nlohmann::json::array();
+    for (const auto& st : p.stages) {
+      nlohmann::json s;
+      s["layers_fwd"] = nlohmann::json::array();
+      for (const auto& l : st.layers_fwd) s["layers_fwd"].push_back(list_json(l));
+      s["layers_bwd"] = nlohmann::json::array();
+      for (const auto& l : st.layers_bwd) s["layers_bwd"].push_back(list_json(l));
+      s["pre_fwd"] = list_json(st.pre_fwd);
+      s["post_fwd"] = list_json(st.post_fwd);
+      s["pre_bwd"] = list_json(st.pre_bwd);
+      s["post_bwd"] = list_json(st.post_bwd);
+      s["reduce"] = list_json(st.reduce);
+      s["optimizer"] = list_json(st.optimizer);
+      stages.push_back(s);
+    }
+    j["stages"] = stages;
+    g_spec_json = j.dump();
+    return g_spec_json.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// build_pipeline(pipeline_of(json), hook) events, like ref_pipeline_events;
+// *end receives BuiltPipeline::end
+int64_t ref_pipeline_events_json(const char* pipeline_json, const int64_t* hook_dur,
+                                 int64_t n_hook, int32_t* pid, int32_t* tid, int64_t* ts,
+                                 int64_t* dur, int64_t cap, int64_t* n_ops, int64_t* end) {
+  int64_t count = -1;
+  guarded([&] {
+    PipelineSpec ps = pipeline_of(nlohmann::json::parse(pipeline_json));
+    int64_t calls = 0;
+    DurationHook hook = [&](std::size_t i, Micros base) -> Micros {
+      calls = std::max<int64_t>(calls, static_cast<int64_t>(i) + 1);
+      if (hook_dur && static_cast<int64_t>(i) < n_hook) return hook_dur[i];
+      return base;
+    };
+    BuiltPipeline b = build_pipeline(ps, hook);
+    if (n_ops) *n_ops = calls;
+    if (end) *end = b.end;
+    count = static_cast<int64_t>(b.events.size());
+    for (int64_t i = 0; i < count && i < cap; ++i) {
+      pid[i] = b.events[i].process_id;
+      tid[i] = b.events[i].thread_id;
+      ts[i] = b.events[i].timestamp;
+      dur[i] = b.events[i].duration;
+    }
+    return 0;
+  });
+  return count;
+}
+
+}  // extern "C"

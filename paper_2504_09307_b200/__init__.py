@@ -2,18 +2,21 @@
 
 Drop-in for the reference ``tracesim`` simulation path: the graph model
 (:mod:`.graph`), the replay API (:mod:`.replay`), the synthetic GPT trace
-generator and graph builder (:mod:`.synth`), all over the C ABI of
+generator and graph builder (:mod:`.synth`), the PipelineSpec / estimate()
+boundary (:mod:`.pipeline`), all over the C ABI of
 ``lib/liblumos_b200.so`` (include/lumos_b200.h).
 """
 from .graph import (COMMUNICATION, COMPUTE, CPU_THREAD, CUDA_STREAM, DEVICE_SYNC, EVENT_SYNC,
                     STREAM_SYNC, DeviceError, ExecutionGraph, GraphError, SimulatedTrace,
                     SimulationError, UnsupportedGraphError)
 from .replay import BatchResult, DeviceGraph, Retime, ScenarioSpec, simulate, simulate_batch
+from .pipeline import KernelSpec, PipelineSpec, StageSpec, estimate_batch, pipeline_graph
 
 __all__ = [
     "Retime",
     "ExecutionGraph", "SimulatedTrace", "SimulationError", "GraphError", "UnsupportedGraphError",
     "DeviceError", "DeviceGraph", "ScenarioSpec", "BatchResult", "simulate", "simulate_batch",
     "CPU_THREAD", "CUDA_STREAM", "STREAM_SYNC", "DEVICE_SYNC", "EVENT_SYNC", "COMPUTE",
-    "COMMUNICATION",
+    "COMMUNICATION", "KernelSpec", "StageSpec", "PipelineSpec", "pipeline_graph",
+    "estimate_batch",
 ]

@@ -901,7 +901,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     if (sp.mode & kModeJitter) f *= 1.0 + 0.5 * sp.two_j;
     const double bound = static_cast<double>(c.max_comp_dur_sum) * f +
                          3.0 * static_cast<double>(c.max_comp_tasks) + 16.0;
-    rel32 = f >= 0.0 && bound < 4.2e9 && walk_width(c.max_slots, true) > 0;
+    // offsets from O = W rounded down to a multiple of 2^32 (replay.cu):
+    // W - O + every time must stay below 2^32 - 1
+    const double w_lo = static_cast<double>(static_cast<uint32_t>(c.window_start));
+    rel32 = f >= 0.0 && w_lo + bound < 4.2e9 && walk_width(c.max_slots, true) > 0;
   }
   // cooperative walks size their uint32 window by the nominal longest path
   // and check every addition (a wrap sends the scenario to the fix-up)

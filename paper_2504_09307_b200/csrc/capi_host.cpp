@@ -40,6 +40,26 @@ int ts_synth_graph(const ts_synth_spec* spec, ts_host_graph** out, int64_t* trut
   return TS_OK;
 }
 
+void ts_pipeline_defaults(ts_pipeline_spec* spec) {
+  if (spec) pipeline_defaults(spec);
+}
+
+int ts_pipeline_graph(const ts_pipeline_spec* spec, int32_t estimate, int32_t tp,
+                      ts_host_graph** out, int64_t* truth_makespan) {
+  if (!spec || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  auto* h = new ts_host_graph;
+  std::string err;
+  int rc = pipeline_graph(*spec, estimate != 0, tp, h->s, err);
+  if (rc != TS_OK) {
+    delete h;
+    *out = nullptr;
+    return set_error(rc, err);
+  }
+  if (truth_makespan) *truth_makespan = h->s.truth_makespan;
+  *out = h;
+  return TS_OK;
+}
+
 int ts_host_graph_desc(const ts_host_graph* g, ts_graph_desc* out) {
   if (!g || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
   *out = g->s.graph.desc();

@@ -29,6 +29,8 @@ std::string lower(std::string s) {
   return s;
 }
 
+}  // namespace
+
 bool is_comm_name(const std::string& name) {
   static const char* kPat[] = {"nccl", "allreduce", "allgather", "reducescatter", "sendrecv",
                                "alltoall"};
@@ -37,6 +39,8 @@ bool is_comm_name(const std::string& name) {
     if (l.find(p) != std::string::npos) return true;
   return false;
 }
+
+namespace {
 
 // sync flavor of a host call: 0 none, 1 device, 2 stream, 3 event (build.hpp:27-31)
 int sync_flavor(const std::string& n) {

@@ -89,5 +89,7 @@ int build_rank_graph(const std::vector<Event>& events, const Names& names, int32
 
 // OpClass of an event under the default BuildPolicy (build.cpp:86-98).
 uint8_t classify_event(const Event& e, const Names& names);
+// BuildPolicy's communication-kernel name test (build.cpp:93-98)
+bool is_comm_name(const std::string& name);
 
 }  // namespace lumos

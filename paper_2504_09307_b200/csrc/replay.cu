@@ -102,6 +102,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   // record slot fields hold s * 128; a slot is kT packs of kS * sizeof(V) bytes
   constexpr int kShift = ilog2(kT) - 7 + ilog2(kS * static_cast<int>(sizeof(V)));
   constexpr V kInfV = kRel ? static_cast<V>(0xFFFFFFFFu) : static_cast<V>(kMaxI64);
+  constexpr uint32_t kFastMask =
+      0xFFu | (static_cast<uint32_t>(F_TRACK | F_TRACK1 | F_STORE_START | (kRt ? F_RT : 0)) << 24);
   static_assert(kT >= 32 && kShift >= 0, "");
   static_assert(kS == 1 || kS == 2, "");
   extern __shared__ int4 smem[];
@@ -138,8 +140,16 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
   const int64_t W = P.window_start;
-  const V w0 = kRel ? V(0) : static_cast<V>(W);  // the origin in V
-  auto absv = [&](V v) -> int64_t { return kRel ? W + static_cast<int64_t>(v) : static_cast<int64_t>(v); };
+  // uint32 values are offsets from O = W rounded down to a multiple of 2^32
+  // (the host proves W - O + every time < 2^32), so an absolute time is the
+  // offset with O's high word attached: no 64-bit add per stored value
+  const uint32_t o_hi = static_cast<uint32_t>(static_cast<uint64_t>(W) >> 32);
+  const V w0 = kRel ? static_cast<V>(static_cast<uint32_t>(W)) : static_cast<V>(W);  // W in V
+  auto absv = [&](V v) -> int64_t {
+    return kRel ? static_cast<int64_t>((static_cast<uint64_t>(o_hi) << 32) |
+                                       static_cast<uint32_t>(v))
+                : static_cast<int64_t>(v);
+  };
 #define SLOT2(off) \
   (*reinterpret_cast<VP*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
 #define SLOTB(boff) \
@@ -179,6 +189,97 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   const int acct_row = P.fused ? P.fused[comp_id].row : -1;
   VP busy_a = splat<V, kS>(V(0));
 
+  // A task's finish: its scenario durations (K4, fused), the busy / sink
+  // bookkeeping and the start / finish row stores.  rec = the op's record index
+  // in the program (retime walks look up their F_RT table through it).
+  auto finish_task = [&](const VP& st, const VP& fb, const int4& ra, uint32_t cls_b,
+                         uint32_t flags, int64_t rec) -> VP {
+    const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
+    const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
+                         static_cast<uint32_t>(ra.x);
+    const int cls = cls_b & 15u;
+    int64_t bs[kS];  // retime walk: per-scenario base durations
+#pragma unroll
+    for (int s = 0; s < kS; ++s) bs[s] = base;
+    if constexpr (kRt) if (flags & F_RT) {
+      const int64_t j = __ldg(P.rt.rec_of + rec);
+      const int4 rw = __ldg(reinterpret_cast<const int4*>(P.rt.rec + j));
+      const int32_t rk = rw.w, grp = rw.z;
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        const int64_t v = __ldg(P.rt.vval + rt_vrow[s] + j);
+        bs[s] = (rk == TS_RT_GEMM || rk == TS_RT_OPT)
+                    ? v  // retimed base (change_hidden), or the base itself
+                    : rt_coll_base(P.rt.scen + col[s], rk, grp, P.rt.source_dp, v, base);
+      }
+    }
+    VP fin;
+    constexpr bool kJit = kDurMode >= 0 && (kDurMode & kModeJitter) != 0;
+    int64_t dsc[kS];  // class-scaled durations (kScaleTab)
+    if constexpr (kScaleTab) {
+      const int2 nm = numtab[cls * kT + tid];
+      dsc[0] = class_scaled_num(P.sp, kRt ? bs[0] : base, nm.x);
+      dsc[1] = class_scaled_num(P.sp, kRt ? bs[1] : base, nm.y);
+    }
+    if constexpr (kS == 2 && kJit) {
+      // one Philox call for the thread's scenario pair (columns c0, c0 + 1
+      // with c0 even, or a duplicated last column; the launch takes the
+      // one-scenario walk when the batch starts at an odd global id); the
+      // rounding is branch-free per scenario (a zero duration selects 0)
+      if constexpr (!kScaleTab) {
+#pragma unroll
+        for (int s = 0; s < kS; ++s) dsc[s] = kRt ? bs[s] : base;
+      }
+      uint32_t w[kS] = {0u, 0u};
+      if (kRt || (kDurMode & kModeScale) || base != 0)
+        jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
+    } else if constexpr (kScaleTab) {  // class scale only
+#pragma unroll
+      for (int s = 0; s < kS; ++s) fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(dsc[s]));
+    } else {
+#pragma unroll
+      for (int s = 0; s < kS; ++s) {
+        const int64_t d = scenario_duration<kDurMode>(P.sp, ts[s], task, kRt ? bs[s] : base, cls);
+        fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
+      }
+    }
+#ifndef LUMOS_NO_BUSY  // perf experiments only: breaks split accounting
+    if (flags & F_BUSY)
+#else
+    if (false)
+#endif
+    {
+#pragma unroll
+      for (int s = 0; s < kS; ++s) busy_a.v[s] = static_cast<V>(busy_a.v[s] + (fin.v[s] - st.v[s]));
+    }
+    if (__builtin_expect((flags & F_SINK) != 0, 0)) {
+#pragma unroll
+      for (int s = 0; s < kS; ++s) hi[s] = imax(hi[s], absv(fin.v[s]));
+    }
+    const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
+    if (vec_store) {
+      const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
+      if (kWriteStart)
+        __stcs(reinterpret_cast<longlong2*>(sbase + at8),
+               make_longlong2(absv(st.v[0]), absv(st.v[kS - 1])));
+      if (kWriteFin)
+        __stcs(reinterpret_cast<longlong2*>(fbase + at8),
+               make_longlong2(absv(fin.v[0]), absv(fin.v[kS - 1])));
+    } else {
+      if (kWriteStart) {
+        __stcs(start_c0 + at, absv(st.v[0]));
+        if (kS == 2) __stcs(start_c0 + at + dcol, absv(st.v[kS - 1]));
+      }
+      if (kWriteFin) {
+        __stcs(fin_c0 + at, absv(fin.v[0]));
+        if (kS == 2) __stcs(fin_c0 + at + dcol, absv(fin.v[kS - 1]));
+      }
+    }
+    return fin;
+  };
   auto stage = [&](int4* dstbuf, int r, int4 a, int4 b) {
     dstbuf[4 * r] = a;
     dstbuf[4 * r + 1] = b;
@@ -209,9 +310,20 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
     const int4* buf = opbuf + (c & 1) * 4 * kChunk;
     const int cnt = min(kChunk, n_ops - c * kChunk);
     for (int i = 0; i < cnt; ++i) {
-      const int4 ra = buf[4 * i], rb = buf[4 * i + 1];
+      const int4 ra = buf[4 * i];
       const int4 oa = buf[4 * i + 2], ob = buf[4 * i + 3];
       const uint32_t hdr = static_cast<uint32_t>(ra.w);
+      // fast path: a plain node (start = max(W, preds), no coverage, no stored
+      // start, no retime lookup) — every compute kernel and launch of a replay
+      // graph — without the kind dispatch
+      if ((hdr & kFastMask) == OP_NODE) {
+        const VP q0 = SLOTB(oa.x), q1 = SLOTB(oa.y), q2 = SLOTB(oa.z), q3 = SLOTB(oa.w);
+        const VP st = maxp(maxp(q0, q1), maxp(q2, q3));
+        SLOTB(ob.x) = finish_task(st, st, ra, (hdr >> 16) & 0xFFu, hdr >> 24,
+                                  pd.op_offset + c * kChunk + i);
+        continue;
+      }
+      const int4 rb = buf[4 * i + 1];
       const uint32_t kind = hdr & 0xFFu;
       const uint32_t cls_b = (hdr >> 16) & 0xFFu;
       const uint32_t flags = hdr >> 24;
@@ -293,87 +405,9 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
       if (kind == OP_START) {
         SLOTB(dst) = st;
       } else {
-        const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
-        const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
-                             static_cast<uint32_t>(ra.x);
-        const int cls = cls_b & 15u;
-        int64_t bs[kS];  // retime walk: per-scenario base durations
-#pragma unroll
-        for (int s = 0; s < kS; ++s) bs[s] = base;
-        if constexpr (kRt) if (flags & F_RT) {
-          const int64_t j = __ldg(P.rt.rec_of + pd.op_offset + c * kChunk + i);
-          const int4 rw = __ldg(reinterpret_cast<const int4*>(P.rt.rec + j));
-          const int32_t rk = rw.w, grp = rw.z;
-#pragma unroll
-          for (int s = 0; s < kS; ++s) {
-            const int64_t v = __ldg(P.rt.vval + rt_vrow[s] + j);
-            bs[s] = (rk == TS_RT_GEMM || rk == TS_RT_OPT)
-                        ? v  // retimed base (change_hidden), or the base itself
-                        : rt_coll_base(P.rt.scen + col[s], rk, grp, P.rt.source_dp, v, base);
-          }
-        }
-        VP fin;
-        constexpr bool kJit = kDurMode >= 0 && (kDurMode & kModeJitter) != 0;
-        int64_t dsc[kS];  // class-scaled durations (kScaleTab)
-        if constexpr (kScaleTab) {
-          const int2 nm = numtab[cls * kT + tid];
-          dsc[0] = class_scaled_num(P.sp, kRt ? bs[0] : base, nm.x);
-          dsc[1] = class_scaled_num(P.sp, kRt ? bs[1] : base, nm.y);
-        }
-        if constexpr (kS == 2 && kJit) {
-          // one Philox call for the thread's scenario pair (columns c0, c0 + 1
-          // with c0 even, or a duplicated last column; the launch takes the
-          // one-scenario walk when the batch starts at an odd global id); the
-          // rounding is branch-free per scenario (a zero duration selects 0)
-          if constexpr (!kScaleTab) {
-#pragma unroll
-            for (int s = 0; s < kS; ++s) dsc[s] = kRt ? bs[s] : base;
-          }
-          uint32_t w[kS] = {0u, 0u};
-          if (kRt || (kDurMode & kModeScale) || base != 0)
-            jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
-#pragma unroll
-          for (int s = 0; s < kS; ++s)
-            fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
-        } else if constexpr (kScaleTab) {  // class scale only
-#pragma unroll
-          for (int s = 0; s < kS; ++s) fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(dsc[s]));
-        } else {
-#pragma unroll
-          for (int s = 0; s < kS; ++s) {
-            const int64_t d = scenario_duration<kDurMode>(P.sp, ts[s], task, kRt ? bs[s] : base, cls);
-            fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(d));
-          }
-        }
+        const VP fin = finish_task(st, fb, ra, cls_b, flags, pd.op_offset + c * kChunk + i);
         SLOTB(dst) = fin;
         if (flags & F_STORE_START) SLOTB(ob.w) = st;
-        if (flags & F_BUSY) {
-#pragma unroll
-          for (int s = 0; s < kS; ++s) busy_a.v[s] = static_cast<V>(busy_a.v[s] + (fin.v[s] - st.v[s]));
-        }
-        if (__builtin_expect((flags & F_SINK) != 0, 0)) {
-#pragma unroll
-          for (int s = 0; s < kS; ++s) hi[s] = imax(hi[s], absv(fin.v[s]));
-        }
-        const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
-        if (vec_store) {
-          const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
-          if (kWriteStart)
-            __stcs(reinterpret_cast<longlong2*>(sbase + at8),
-                   make_longlong2(absv(st.v[0]), absv(st.v[kS - 1])));
-          if (kWriteFin)
-            __stcs(reinterpret_cast<longlong2*>(fbase + at8),
-                   make_longlong2(absv(fin.v[0]), absv(fin.v[kS - 1])));
-        } else {
-          if (kWriteStart) {
-            __stcs(start_c0 + at, absv(st.v[0]));
-            if (kS == 2) __stcs(start_c0 + at + dcol, absv(st.v[kS - 1]));
-          }
-          if (kWriteFin) {
-            __stcs(fin_c0 + at, absv(fin.v[0]));
-            if (kS == 2) __stcs(fin_c0 + at + dcol, absv(fin.v[kS - 1]));
-          }
-        }
       }
       if (flags & F_TRACK1) {
         // the source slot outlives this op's results (compile.cpp), so it is

@@ -80,6 +80,7 @@ struct PSpec {
   int64_t origin = 0;
   int compute_stream = 7, reduce_stream = 9, p2p_stream = 11;
   int main_thread = 100, helper_thread = 200;
+  int64_t first_event = 1, first_correlation = 1;
 };
 
 // ------------------------------------------------------------------ keys
@@ -156,7 +157,7 @@ class Builder {
   std::unordered_map<uint64_t, std::pair<int64_t, int64_t>> published_;  // time, event
   std::unordered_map<uint64_t, std::map<int, int64_t>> barrier_starts_;
   std::unordered_map<uint64_t, std::vector<POp*>> barrier_members_;
-  int64_t next_event_ = 1, next_corr_ = 1, op_index_ = 0;
+  int64_t next_event_ = s_.first_event, next_corr_ = s_.first_correlation, op_index_ = 0;
 
   int64_t cost(int64_t base) {
     ++op_index_;
@@ -554,7 +555,153 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
   return ps;
 }
 
+
+// ------------------------------------------- a user PipelineSpec (Mode B)
+// strict integer of an args string (transform.cpp:19-30 meta_i64)
+bool strict_int(const std::string& v, int64_t& out) {
+  if (v.empty()) return false;
+  try {
+    size_t pos = 0;
+    const long long x = std::stoll(v, &pos);
+    if (pos != v.size()) return false;
+    out = x;
+    return true;
+  } catch (const std::exception&) {
+    return false;
+  }
+}
+
+// The retime metadata a kernel's task carries: its KernelSpec args with the
+// builder's role tag applied (tags override args, pipeline.cpp:122-123; role
+// regions embed / head / dp / opt, pipeline.cpp:229-297), classified the way
+// change_hidden / scale_dp read Task.meta (transform.cpp:219-349) on the op
+// class build_graph gives the kernel by name (build.cpp:93-98).
+KMeta kernel_meta(const ts_kernel_spec& k, const char* role_region) {
+  std::map<std::string, std::string> args;
+  for (int32_t a = 0; a < k.n_args; ++a)
+    if (k.arg_keys && k.arg_keys[a] && k.arg_values && k.arg_values[a])
+      args[k.arg_keys[a]] = k.arg_values[a];
+  if (role_region) args["region"] = role_region;
+  auto get = [&](const char* key) {
+    auto it = args.find(key);
+    return it == args.end() ? std::string() : it->second;
+  };
+  auto num = [&](const char* key, int64_t absent, bool* present = nullptr) {
+    int64_t v = absent;
+    auto it = args.find(key);
+    const bool ok = it != args.end() && strict_int(it->second, v);
+    if (!ok) v = absent;
+    if (present) *present = ok;
+    return v;
+  };
+  KMeta m;
+  bool has_bytes = false;
+  m.bytes = num("bytes", -1, &has_bytes);
+  m.group = static_cast<int32_t>(num("group_size", 0));
+  m.m = num("m", 0);
+  m.n = num("n", 0);
+  m.k = num("k", 0);
+  if (is_comm_name(k.name ? k.name : "")) {
+    if (get("collective") == "allreduce") m.kind = TS_RT_ALLREDUCE;
+    else if (get("region") == "p2p" && has_bytes)
+      m.kind = get("dir") != "recv" ? TS_RT_P2P_SEND : TS_RT_P2P_RECV;
+  } else if (m.m > 0 && m.n > 0 && m.k > 0) {
+    m.kind = TS_RT_GEMM;
+  } else if (get("region") == "opt" && has_bytes) {
+    m.kind = TS_RT_OPT;
+  }
+  return m;
+}
+
+int pspec_of(const ts_pipeline_spec& c, Names& names, PSpec& ps, std::string& err) {
+  // build_pipeline's checks (pipeline.cpp:62-68)
+  if (c.pp < 1 || c.dp < 1) {
+    err = "pipeline: pp and dp must be >= 1";
+    return TS_E_INVALID_ARGUMENT;
+  }
+  if (c.n_stages != c.pp || !c.stages) {
+    err = "pipeline: need one stage spec per pipeline stage";
+    return TS_E_INVALID_ARGUMENT;
+  }
+  if (c.num_microbatches < 1) {
+    err = "pipeline: need at least one microbatch";
+    return TS_E_INVALID_ARGUMENT;
+  }
+  ps = PSpec{};
+  ps.pp = c.pp;
+  ps.dp = c.dp;
+  ps.m = c.num_microbatches;
+  ps.launch = c.launch_us;
+  ps.record = c.record_us;
+  ps.wait = c.wait_us;
+  ps.sync = c.sync_us;
+  ps.p2p_send = c.p2p_send_us;
+  ps.p2p_recv_base = c.p2p_recv_base_us;
+  ps.act_bytes = c.activation_bytes;
+  ps.origin = c.origin;
+  ps.compute_stream = c.compute_stream;
+  ps.reduce_stream = c.reduce_stream;
+  ps.p2p_stream = c.p2p_stream;
+  ps.main_thread = c.main_thread;
+  ps.helper_thread = c.helper_thread;
+  ps.first_event = c.first_event;
+  ps.first_correlation = c.first_correlation;
+  auto list = [&](const ts_kernel_list& l, const char* role, std::vector<KSpec>& outl) {
+    outl.clear();
+    for (int32_t i = 0; i < l.n; ++i) {
+      const ts_kernel_spec& k = l.k[i];
+      outl.push_back({names.get(k.name ? k.name : ""), k.duration, kernel_meta(k, role)});
+    }
+  };
+  for (int32_t s = 0; s < c.pp; ++s) {
+    const ts_stage_spec& cs = c.stages[s];
+    StageSpec st;
+    st.fwd.resize(cs.n_layers);
+    st.bwd.resize(cs.n_layers);
+    for (int32_t l = 0; l < cs.n_layers; ++l) {
+      list(cs.layers_fwd[l], nullptr, st.fwd[l]);
+      list(cs.layers_bwd[l], nullptr, st.bwd[l]);
+    }
+    list(cs.pre_fwd, "embed", st.pre_fwd);
+    list(cs.post_bwd, "embed", st.post_bwd);
+    list(cs.post_fwd, "head", st.post_fwd);
+    list(cs.pre_bwd, "head", st.pre_bwd);
+    list(cs.reduce, "dp", st.reduce);
+    list(cs.optimizer, "opt", st.optimizer);
+    ps.stages.push_back(std::move(st));
+  }
+  return TS_OK;
+}
+
 }  // namespace
+
+int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, SynthOutput& out,
+                   std::string& err);
+
+void pipeline_defaults(ts_pipeline_spec* c) {
+  std::memset(c, 0, sizeof(*c));
+  // PipelineSpec / HostCosts defaults (pipeline.hpp:47-80)
+  c->pp = c->dp = c->num_microbatches = 1;
+  c->launch_us = 5;
+  c->record_us = 2;
+  c->wait_us = 2;
+  c->sync_us = 5;
+  c->compute_stream = 7;
+  c->reduce_stream = 9;
+  c->p2p_stream = 11;
+  c->main_thread = 100;
+  c->helper_thread = 200;
+  c->first_event = 1;
+  c->first_correlation = 1;
+}
+
+int pipeline_graph(const ts_pipeline_spec& c, bool estimate, int tp, SynthOutput& out,
+                   std::string& err) {
+  out = SynthOutput{};
+  PSpec ps;
+  if (int rc = pspec_of(c, out.names, ps, err)) return rc;
+  return graph_of_pspec(ps, estimate, tp, -1, out, err);
+}
 
 void synth_defaults(ts_synth_spec* s) {
   std::memset(s, 0, sizeof(*s));
@@ -610,7 +757,19 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
     return TS_E_INVALID_ARGUMENT;
   }
   out = SynthOutput{};
-  PSpec ps = pspec_for(sp, out.names);
+  const PSpec ps = pspec_for(sp, out.names);
+  return graph_of_pspec(ps, sp.estimate != 0, sp.tp, sp.slice_rank, out, err);
+}
+
+// The generated trace of a PipelineSpec as the replay graph (build_graph +
+// merge_ranks) or the estimate graph (generator dependencies + gates), with
+// tp replicas of every rank; out.names must hold the spec's name ids.
+int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, SynthOutput& out,
+                   std::string& err) {
+  if (tp < 1) {
+    err = "tp must be >= 1";
+    return TS_E_INVALID_ARGUMENT;
+  }
   Builder b(ps, out.names);
   try {
     b.run();
@@ -645,7 +804,7 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
   std::vector<HostGraph> rank_graphs(n_ranks);
   BuildPolicyLite pol;
   for (int r = 0; r < n_ranks; ++r) {
-    if (!sp.estimate) {
+    if (!estimate) {
       int rc = build_rank_graph(per_rank[r], out.names, r, pol, rank_graphs[r], err);
       if (rc != TS_OK) return rc;
       continue;
@@ -671,7 +830,7 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
     }
     g.duration.resize(n);
   }
-  if (sp.estimate) {
+  if (estimate) {
     for (int64_t i = 0; i < ne; ++i) {
       const GenEvent& ge = b.events[i];
       rank_graphs[ge.ev.pid].duration[local[i]] = ge.cost;
@@ -679,7 +838,6 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
   }
 
   // TP replicas in rank order r * tp + t (merge_ranks order)
-  const int tp = sp.tp;
   std::vector<int64_t> base(static_cast<size_t>(n_ranks) * tp + 1, 0);  // by new rank
   for (int r = 0; r < n_ranks; ++r)
     for (int t = 0; t < tp; ++t)
@@ -693,11 +851,11 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
   bool first = true;
   for (int r = 0; r < n_ranks; ++r)
     for (int t = 0; t < tp; ++t) {
-      if (sp.slice_rank >= 0 && r * tp + t != sp.slice_rank) continue;
+      if (slice_rank >= 0 && r * tp + t != slice_rank) continue;
       G.append_relabelled(rank_graphs[r], r * tp + t, first);
       first = false;
     }
-  if (sp.estimate && sp.slice_rank < 0) {
+  if (estimate && slice_rank < 0) {
     // cross-rank dependencies of the generator, per replica
     auto gid = [&](int64_t ev, int t) {
       const int r = b.events[ev].ev.pid;
@@ -721,7 +879,7 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
       G.edge_from.push_back(e.first);
       G.edge_to.push_back(e.second);
     }
-  } else if (sp.estimate) {
+  } else if (estimate) {
     err = "estimate graphs couple ranks; slice_rank is not supported";
     return TS_E_INVALID_ARGUMENT;
   }

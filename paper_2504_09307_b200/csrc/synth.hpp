@@ -18,5 +18,10 @@ struct SynthOutput {
 
 void synth_defaults(ts_synth_spec* s);
 int synth_graph(const ts_synth_spec& spec, SynthOutput& out, std::string& err);
+// A user PipelineSpec (ts_pipeline_spec): its build_pipeline trace as the
+// replay graph or the estimate graph (estimate = true), with tp replicas.
+void pipeline_defaults(ts_pipeline_spec* c);
+int pipeline_graph(const ts_pipeline_spec& c, bool estimate, int tp, SynthOutput& out,
+                   std::string& err);
 
 }  // namespace lumos

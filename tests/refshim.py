@@ -395,3 +395,40 @@ def orc_durations(g: Graph, sc: OrcScenarios, scenario: int, cls=None):
     orc().orc_fill_durations(C.byref(sc), scenario, g.n, _p(g.duration, _i64p), _p(cls, _u8p),
                              _p(out, _i64p))
     return out
+
+
+def pipeline_spec_json(spec_json: str) -> dict:
+    """The reference's pipeline_spec_for(SynthSpec::from_json(spec)) as JSON."""
+    import json as _json
+    lib = ref()
+    lib.ref_pipeline_spec_json.restype = C.c_char_p
+    lib.ref_pipeline_spec_json.argtypes = [C.c_char_p]
+    out = lib.ref_pipeline_spec_json(spec_json.encode())
+    if not out:
+        raise RefError(1, lib.ref_last_error().decode())
+    return _json.loads(out.decode())
+
+
+def pipeline_events_json(pipeline: dict, hook=None):
+    """build_pipeline(spec, hook) of a JSON PipelineSpec: (pid, tid, ts, dur, n_ops, end)."""
+    import json as _json
+    lib = ref()
+    lib.ref_pipeline_events_json.restype = C.c_int64
+    lib.ref_pipeline_events_json.argtypes = [C.c_char_p, _i64p, C.c_int64, _i32p, _i32p, _i64p,
+                                             _i64p, C.c_int64, _i64p, _i64p]
+    cap = 4_000_000
+    pid = np.zeros(cap, np.int32)
+    tid = np.zeros(cap, np.int32)
+    ts = np.zeros(cap, np.int64)
+    dur = np.zeros(cap, np.int64)
+    nops = C.c_int64(0)
+    end = C.c_int64(0)
+    h = None if hook is None else np.ascontiguousarray(hook, np.int64)
+    n = lib.ref_pipeline_events_json(_json.dumps(pipeline).encode(),
+                                     None if h is None else _p(h, _i64p),
+                                     0 if h is None else h.shape[0], _p(pid, _i32p),
+                                     _p(tid, _i32p), _p(ts, _i64p), _p(dur, _i64p), cap,
+                                     C.byref(nops), C.byref(end))
+    if n < 0:
+        raise RefError(1, lib.ref_last_error().decode())
+    return pid[:n], tid[:n], ts[:n], dur[:n], int(nops.value), int(end.value)

@@ -95,3 +95,37 @@ def test_estimate_uint32_window_wrap_fixup(monkeypatch):
         hook[sg.op_index] = dur
         ref, _ = _ref_pipeline(spec_json, hook)
         assert _my_lane_sequences(og, res.start[:, s], res.fin[:, s]) == ref, f"scenario {s}"
+
+
+@pytest.mark.parametrize("pp,dp,m,tp", [(3, 2, 5, 1), (2, 3, 7, 2), (4, 2, 9, 1)])
+def test_estimate_batch_from_pipeline_spec(pp, dp, m, tp):
+    # Mode-B boundary: a hand-edited reference PipelineSpec (non-generator
+    # kernels, odd microbatch counts, moved streams / costs) replayed by
+    # estimate_batch must equal build_pipeline(spec, hook) per scenario, hook
+    # slot op_index[t] carrying the oracle's duration of task t
+    from paper_2504_09307_b200 import estimate_batch
+    from test_pipeline_spec import hand_edited
+    from test_synth_graph import _lane_sequences
+    sp = hand_edited(pp, dp, m)
+    S = 24
+    spec = ScenarioSpec(count=S, first=6, seed=77, jitter=0.2)
+    res, sg = estimate_batch(sp, spec, tp=tp)
+    g = sg.graph
+    og = _orc_graph(g)
+    sc = R.OrcScenarios(seed=77, jitter=0.2)
+    js = sp.to_json()
+    for s in range(0, S, 5):
+        dur = R.orc_durations(og, sc, spec.first + s)
+        for t in range(tp):
+            sel = np.where(g.rank % tp == t)[0]
+            hook = np.zeros(sg.n_ops, np.int64)
+            hook[sg.op_index[sel]] = dur[sel]
+            pid, tid, ts, du, _, end = R.pipeline_events_json(js, hook)
+            sub = R.Graph(**{k: (getattr(g, k)[sel] if k in ("duration", "original_start",
+                                                              "rank", "lane_kind", "lane",
+                                                              "op_class", "task_kind")
+                                 else getattr(g, k)) for k in FIELDS},
+                          window_start=g.window_start, window_end=g.window_end)
+            sub.rank = sub.rank // tp
+            got = _my_lane_sequences(sub, res.start[sel, s], res.fin[sel, s])
+            assert got == _lane_sequences(pid, tid, ts, du), f"scenario {s} replica {t}"
