@@ -9,6 +9,7 @@
 
 #include "tracesim/build.hpp"
 #include "tracesim/metrics.hpp"
+#include "tracesim/pipeline.hpp"
 #include "tracesim/simulate.hpp"
 
 namespace tracesim::b200 {
@@ -37,8 +38,10 @@ struct ScenarioSpec {
 struct BatchOptions {
   bool timestamps = false;
   int64_t util_bin_width = 0;  // > 0: utilization_by_rank bins (metrics.cpp:105-155)
-  int32_t util_max_bins = 0;   // bins kept per rank
+  int32_t util_max_bins = 0;   // 0: every bin of every window; > 0: a cap (a window
+                               // needing more throws std::invalid_argument)
   bool deltas = false;         // compare_replay start deltas (metrics.cpp:189-221)
+  int32_t worst_n = 10;        // compare_replay's worst list length (metrics.hpp:82-83), <= 64
 };
 
 struct BatchResult {
@@ -51,7 +54,9 @@ struct BatchResult {
   std::vector<int64_t> util_covered;   // [scenario][rank][util_max_bins] covered us
   std::vector<int32_t> util_n_bins;    // [scenario] bins each window needs
   std::vector<int64_t> delta_abs_sum;  // [scenario] sum |sim_start - original_start|
-  std::vector<int64_t> delta_worst;    // [scenario][3] {max |delta|, task, delta}
+  std::vector<int64_t> delta_worst;    // [scenario][worst_n][3] {|delta|, task (-1: none), delta}
+  int32_t worst_n = 0;
+  int32_t n_fixups = 0;                // scenarios re-run by the exact event-driven path
 };
 
 BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
@@ -64,8 +69,28 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
 // (cli.cpp:303-316); bins past util_max_bins are not returned.
 std::map<int, UtilizationSeries> utilization_by_rank(const BatchResult& r, std::size_t s,
                                                      IterationWindow window);
-// compare_replay with the worst list cut to one task (the batch keeps one).
+// compare_replay of scenario s, worst list of BatchOptions::worst_n tasks.
 ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, std::size_t s);
+
+// Mode B: estimate() semantics.  The graph build_pipeline(spec, DurationHook)
+// lays out (pipeline.cpp:474-477) — generator dependencies plus the p2p
+// rendezvous and collective-barrier gates — replayed for every scenario on
+// the device, tp replicas of each rank.  Task t of the estimate graph is hook
+// slot op_index[t] (a launch takes two slots, pipeline.cpp:105-109); its base
+// duration is base[t].  Scenario durations follow ScenarioSpec (class scale,
+// jitter); retime fields are rejected (a structural what-if rebuilds the spec
+// instead, transform.cpp:556-701).  Errors: std::invalid_argument as
+// build_pipeline raises them.
+struct EstimateResult {
+  BatchResult batch;                 // timestamps / spans over the estimate graph's tasks
+  std::vector<int64_t> op_index;     // [task] DurationHook slot, -1 none
+  std::vector<int64_t> base;         // [task] intrinsic duration (the hook's base)
+  std::vector<int32_t> rank;         // [task] rank (stage + pp * dp, replica r * tp + t)
+  int64_t n_ops = 0;                 // hook slots of one replica
+  int64_t truth_makespan = 0;        // BuiltPipeline end - origin at the base durations
+};
+EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scenarios,
+                              const BatchOptions& options = {}, int tp = 1);
 
 // Scenario s of a batch run with timestamps as a SimulatedTrace (entries in
 // (sim_start, task_id) order, simulate.hpp:12-24) — e.g. for

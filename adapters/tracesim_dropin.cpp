@@ -18,6 +18,7 @@
 #include <limits>
 #include <stdexcept>
 #include <map>
+#include <memory>
 #include <optional>
 #include <queue>
 #include <sstream>
@@ -155,13 +156,43 @@ struct Soa {
   throw SimulationError("B200 replay engine: " + msg);
 }
 
+bool same_soa(const Soa& a, const Soa& b) {
+  return a.duration == b.duration && a.original_start == b.original_start && a.rank == b.rank &&
+         a.lane_kind == b.lane_kind && a.lane == b.lane && a.op_class == b.op_class &&
+         a.task_kind == b.task_kind && a.edge_from == b.edge_from && a.edge_to == b.edge_to &&
+         a.rule_kind == b.rule_kind && a.rule_task == b.rule_task &&
+         a.rule_bound == b.rule_bound && a.rule_watch_off == b.rule_watch_off &&
+         a.watch_rank == b.watch_rank && a.watch_kind == b.watch_kind &&
+         a.watch_lane == b.watch_lane && a.rt_kind == b.rt_kind && a.rt_bytes == b.rt_bytes &&
+         a.rt_group == b.rt_group && a.rt_mnk == b.rt_mnk &&
+         a.desc.window_start == b.desc.window_start && a.desc.window_end == b.desc.window_end;
+}
+
+// The last compiled graph of this thread: repeated replays of one graph (the
+// CLI's whatif / analyze flows, parameter sweeps) compile and upload it once.
+// A graph is reused only when every field the engine reads is identical.
+// Per thread, because one ts_graph serves one call at a time.
+struct GraphCache {
+  std::unique_ptr<Soa> soa;
+  ts_graph* g = nullptr;
+  ~GraphCache() { ts_graph_destroy(g); }
+};
+thread_local GraphCache t_cache;
+
 struct Handle {
   ts_graph* g = nullptr;
   explicit Handle(const ExecutionGraph& graph) {
-    Soa s(graph);
-    if (int rc = ts_graph_create(&s.desc, -1, &g)) rethrow(rc);
+    auto s = std::make_unique<Soa>(graph);
+    if (t_cache.g && t_cache.soa && same_soa(*s, *t_cache.soa)) {
+      g = t_cache.g;
+      return;
+    }
+    ts_graph* fresh = nullptr;
+    if (int rc = ts_graph_create(&s->desc, -1, &fresh)) rethrow(rc);
+    ts_graph_destroy(t_cache.g);
+    t_cache.g = g = fresh;
+    t_cache.soa = std::move(s);
   }
-  ~Handle() { ts_graph_destroy(g); }
 };
 
 }  // namespace
@@ -322,23 +353,23 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   return simulate_batch(graph, spec, o);
 }
 
-BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
-                           const BatchOptions& o) {
-  for (const ValidationIssue& issue : validate_graph(graph))
-    if (issue.error) throw SimulationError("invalid graph: " + issue.message);
-  Handle h(graph);
+namespace {
+
+// one batched replay of a compiled graph through the C ABI
+BatchResult run_batch(ts_graph* g, std::size_t n_tasks, const ScenarioSpec& spec,
+                      const BatchOptions& o, int32_t util_bins) {
   ts_graph_info info{};
-  ts_graph_get_info(h.g, &info);
+  ts_graph_get_info(g, &info);
   BatchResult r;
   const std::size_t S = static_cast<std::size_t>(spec.count);
   const std::size_t R = static_cast<std::size_t>(info.n_ranks);
   r.span.assign(S * 3, 0);
   r.rank_breakdown.assign(S * R * 5, 0);
   r.ranks.resize(R);
-  ts_graph_ranks(h.g, r.ranks.data());
+  ts_graph_ranks(g, r.ranks.data());
   if (o.timestamps) {
-    r.start.assign(graph.tasks.size() * S, 0);
-    r.fin.assign(graph.tasks.size() * S, 0);
+    r.start.assign(n_tasks * S, 0);
+    r.fin.assign(n_tasks * S, 0);
   }
   ts_scenarios sc{};
   sc.first = spec.first;
@@ -374,7 +405,7 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
   res.rank_breakdown = R ? r.rank_breakdown.data() : nullptr;
   if (o.util_bin_width > 0) {
     r.util_bin_width = o.util_bin_width;
-    r.util_max_bins = std::max<int32_t>(1, o.util_max_bins);
+    r.util_max_bins = std::max<int32_t>(1, util_bins);
     r.util_covered.assign(S * std::max<std::size_t>(1, R) * r.util_max_bins, 0);
     r.util_n_bins.assign(S, 0);
     res.util_bin_width = r.util_bin_width;
@@ -383,13 +414,46 @@ BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec
     res.util_n_bins = r.util_n_bins.data();
   }
   if (o.deltas) {
+    if (o.worst_n < 1) throw std::invalid_argument("worst_n must be >= 1");
+    r.worst_n = o.worst_n;
     r.delta_abs_sum.assign(S, 0);
-    r.delta_worst.assign(S * 3, 0);
+    r.delta_worst.assign(S * static_cast<std::size_t>(o.worst_n) * 3, 0);
     res.delta_abs_sum = r.delta_abs_sum.data();
     res.delta_worst = r.delta_worst.data();
+    res.delta_worst_n = o.worst_n;
   }
-  if (int rc = ts_replay_batch(h.g, &sc, &res, nullptr)) rethrow(rc, retime);
+  res.n_fixups = &r.n_fixups;
+  if (int rc = ts_replay_batch(g, &sc, &res, nullptr)) {
+    const std::string msg = ts_last_error();
+    if (rc == TS_E_INVALID_ARGUMENT && msg.rfind("utilization needs ", 0) == 0)
+      throw std::invalid_argument(msg);
+    rethrow(rc, retime);
+  }
   return r;
+}
+
+}  // namespace
+
+BatchResult simulate_batch(const ExecutionGraph& graph, const ScenarioSpec& spec,
+                           const BatchOptions& o) {
+  for (const ValidationIssue& issue : validate_graph(graph))
+    if (issue.error) throw SimulationError("invalid graph: " + issue.message);
+  Handle h(graph);
+  if (o.util_bin_width > 0 && o.util_max_bins <= 0) {
+    // every bin: try the recorded window, then the count the engine reports
+    const Micros span = graph.iteration_window.end - graph.iteration_window.start;
+    const int32_t guess =
+        static_cast<int32_t>(std::max<Micros>(1, (span + o.util_bin_width - 1) / o.util_bin_width));
+    try {
+      return run_batch(h.g, graph.tasks.size(), spec, o, guess);
+    } catch (const std::invalid_argument& e) {
+      const std::string m = e.what();
+      if (m.rfind("utilization needs ", 0) != 0) throw;
+      return run_batch(h.g, graph.tasks.size(), spec, o,
+                       static_cast<int32_t>(std::stol(m.substr(18))));
+    }
+  }
+  return run_batch(h.g, graph.tasks.size(), spec, o, o.util_max_bins);
 }
 
 std::map<int, UtilizationSeries> utilization_by_rank(const BatchResult& r, std::size_t s,
@@ -426,17 +490,147 @@ ReplayReport replay_report(const ExecutionGraph& graph, const BatchResult& r, st
   rep.relative_error =
       relative_error(rep.reference_makespan, rep.simulated_makespan, &rep.zero_reference);
   const std::size_t n = graph.tasks.size();
-  if (s >= r.delta_abs_sum.size() || 3 * s + 2 >= r.delta_worst.size())
+  if (r.worst_n < 1 || s >= r.delta_abs_sum.size() ||
+      (s + 1) * static_cast<std::size_t>(r.worst_n) * 3 > r.delta_worst.size())
     throw std::invalid_argument("replay_report needs a batch run with BatchOptions::deltas");
   rep.mean_abs_delta = n ? static_cast<double>(r.delta_abs_sum[s]) / static_cast<double>(n) : 0.0;
-  rep.max_abs_delta = r.delta_worst[3 * s];
-  const int64_t task = r.delta_worst[3 * s + 1];
-  if (task >= 0) {
+  const std::size_t wn = static_cast<std::size_t>(r.worst_n);
+  const int64_t* w = r.delta_worst.data() + s * wn * 3;
+  rep.max_abs_delta = w[0];
+  for (std::size_t k = 0; k < wn && w[3 * k + 1] >= 0; ++k) {
+    const TaskId task = static_cast<TaskId>(w[3 * k + 1]);
     const Micros rs = graph.tasks[static_cast<std::size_t>(task)].original_start;
-    rep.worst.push_back({static_cast<TaskId>(task), rs, rs + r.delta_worst[3 * s + 2],
-                         r.delta_worst[3 * s + 2]});
+    rep.worst.push_back({task, rs, rs + w[3 * k + 2], w[3 * k + 2]});
   }
   return rep;
+}
+
+namespace {
+
+// tracesim::PipelineSpec -> ts_pipeline_spec (pointers into `spec` and into
+// this object's arrays)
+struct PipelinePod {
+  std::vector<std::vector<const char*>> keys, values;
+  std::vector<std::vector<ts_kernel_spec>> kernels;
+  std::vector<std::vector<ts_kernel_list>> layer_lists;
+  std::vector<ts_stage_spec> stages;
+  ts_pipeline_spec c{};
+
+  ts_kernel_list list(const std::vector<KernelSpec>& ks) {
+    std::vector<ts_kernel_spec> v;
+    for (const KernelSpec& k : ks) {
+      keys.emplace_back();
+      values.emplace_back();
+      for (const auto& [a, b] : k.args) {
+        keys.back().push_back(a.c_str());
+        values.back().push_back(b.c_str());
+      }
+      ts_kernel_spec x{};
+      x.name = k.name.c_str();
+      x.duration = k.duration;
+      x.op_class = static_cast<int32_t>(k.op_class);
+      x.n_args = static_cast<int32_t>(k.args.size());
+      x.arg_keys = keys.back().data();
+      x.arg_values = values.back().data();
+      v.push_back(x);
+    }
+    kernels.push_back(std::move(v));
+    return ts_kernel_list{kernels.back().data(), static_cast<int32_t>(ks.size()), 0};
+  }
+
+  explicit PipelinePod(const PipelineSpec& p) {
+    std::size_t n_lists = 0, n_kernels = 0;
+    for (const StageSpec& st : p.stages) {
+      n_lists += st.layers_fwd.size() + st.layers_bwd.size() + 6;
+      for (const auto& l : st.layers_fwd) n_kernels += l.size();
+      for (const auto& l : st.layers_bwd) n_kernels += l.size();
+      n_kernels += st.pre_fwd.size() + st.post_fwd.size() + st.pre_bwd.size() +
+                   st.post_bwd.size() + st.reduce.size() + st.optimizer.size();
+    }
+    kernels.reserve(n_lists);  // no reallocation: lists point into these
+    keys.reserve(n_kernels);
+    values.reserve(n_kernels);
+    layer_lists.reserve(2 * p.stages.size());
+    for (const StageSpec& st : p.stages) {
+      if (st.layers_fwd.size() != st.layers_bwd.size())
+        throw std::invalid_argument("pipeline: layers_fwd and layers_bwd differ in length");
+      ts_stage_spec cs{};
+      cs.n_layers = static_cast<int32_t>(st.layers_fwd.size());
+      layer_lists.emplace_back();
+      for (const auto& l : st.layers_fwd) layer_lists.back().push_back(list(l));
+      cs.layers_fwd = layer_lists.back().data();
+      layer_lists.emplace_back();
+      for (const auto& l : st.layers_bwd) layer_lists.back().push_back(list(l));
+      cs.layers_bwd = layer_lists.back().data();
+      cs.pre_fwd = list(st.pre_fwd);
+      cs.post_fwd = list(st.post_fwd);
+      cs.pre_bwd = list(st.pre_bwd);
+      cs.post_bwd = list(st.post_bwd);
+      cs.reduce = list(st.reduce);
+      cs.optimizer = list(st.optimizer);
+      stages.push_back(cs);
+    }
+    c.pp = p.pp;
+    c.dp = p.dp;
+    c.num_microbatches = p.num_microbatches;
+    c.n_stages = static_cast<int32_t>(stages.size());
+    c.stages = stages.data();
+    c.launch_us = p.host.launch;
+    c.record_us = p.host.record;
+    c.wait_us = p.host.wait;
+    c.sync_us = p.host.sync;
+    c.p2p_send_us = p.p2p_send;
+    c.p2p_recv_base_us = p.p2p_recv_base;
+    c.activation_bytes = p.activation_bytes;
+    c.origin = p.origin;
+    c.compute_stream = p.compute_stream;
+    c.reduce_stream = p.reduce_stream;
+    c.p2p_stream = p.p2p_stream;
+    c.main_thread = p.main_thread;
+    c.helper_thread = p.helper_thread;
+    c.first_event = p.first_event;
+    c.first_correlation = p.first_correlation;
+  }
+};
+
+}  // namespace
+
+EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scenarios,
+                              const BatchOptions& options, int tp) {
+  if (!scenarios.alpha_us.empty())
+    throw std::invalid_argument(
+        "estimate_batch: retime the PipelineSpec itself (rebuild_pipeline) instead of per scenario");
+  PipelinePod pod(spec);
+  ts_host_graph* hg = nullptr;
+  EstimateResult out;
+  if (int rc = ts_pipeline_graph(&pod.c, 1, tp, &hg, &out.truth_makespan)) {
+    const std::string msg = ts_last_error();
+    if (rc == TS_E_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    rethrow(rc);
+  }
+  struct Free {
+    ts_host_graph* h;
+    ~Free() { ts_host_graph_free(h); }
+  } free_hg{hg};
+  ts_graph_desc desc{};
+  ts_host_graph_desc(hg, &desc);
+  const std::size_t n = static_cast<std::size_t>(desc.n_tasks);
+  out.op_index.resize(n);
+  ts_host_graph_op_index(hg, out.op_index.data());
+  out.n_ops = ts_host_graph_n_ops(hg);
+  out.base.assign(desc.duration, desc.duration + n);
+  out.rank.assign(desc.rank, desc.rank + n);
+  ts_graph* g = nullptr;
+  if (int rc = ts_graph_create(&desc, -1, &g)) rethrow(rc);
+  struct Destroy {
+    ts_graph* g;
+    ~Destroy() { ts_graph_destroy(g); }
+  } destroy{g};
+  BatchOptions o = options;
+  o.util_bin_width = 0;  // the reductions of an estimate graph are not defined here
+  o.deltas = false;
+  out.batch = run_batch(g, n, scenarios, o, 0);
+  return out;
 }
 
 SimulatedTrace scenario_trace(const ExecutionGraph& graph, const BatchResult& r, std::size_t s) {

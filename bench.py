@@ -81,6 +81,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-audit", action="store_true", help="skip the parity audit")
+    ap.add_argument("--no-cpu-full", action="store_true",
+                    help="skip the same-config (whole-graph) reference sample")
     return ap.parse_args()
 
 
@@ -168,12 +170,40 @@ def cpu_sample_graph(args):
     return R, h, g
 
 
-def cpu_threads():
-    n = os.cpu_count() or 1
-    return max(1, min(n, 16))
+def host_info():
+    """Host cores and CPU model of the box the reference arm runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        import psutil
+        mem_gb = psutil.virtual_memory().available / 2 ** 30
+    except Exception:
+        mem_gb = None
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model,
+            "mem_available_gb": None if mem_gb is None else round(mem_gb, 1)}
+
+
+def cpu_threads(gb_per_thread=1.0):
+    """Every host core, bounded by available memory (each thread replays on its
+    own copy of the reference graph)."""
+    info = host_info()
+    n = info["nproc"]
+    if info["mem_available_gb"]:
+        n = min(n, max(1, int(info["mem_available_gb"] * 0.6 / gb_per_thread)))
+    return max(1, n)
 
 
 def run_cpu_sample(R, h, g, args, first, threads, per_thread=1):
+    """Wall seconds of threads * per_thread reference simulate() calls (one
+    scenario per call, one thread per call at a time); scenario durations are
+    filled before the clock (their time is not counted)."""
     sc = R.OrcScenarios(seed=250409307, **scenario_kwargs(args))
     cls = g.default_scale_class()
     count = threads * per_thread
@@ -181,12 +211,35 @@ def run_cpu_sample(R, h, g, args, first, threads, per_thread=1):
     return secs, count
 
 
+def cpu_full_graph(args, threads):
+    """Same-config reference number: the unmodified reference simulate() on the
+    whole workload graph (all TP replicas), one scenario per thread."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refshim as R
+    model, par, tp, _, _ = CONFIGS[args.config]
+    spec = R.synth_spec(pp=par["pp"], dp=par["dp"], m=par["num_microbatches"],
+                        layers=model["n_layers"], d_model=model["d_model"], d_ffn=model["d_ffn"],
+                        heads=model["n_heads"])
+    t0 = time.time()
+    h, _ = R.generate(spec, tp=tp)
+    g = h.export()
+    build_s = time.time() - t0
+    sc = R.OrcScenarios(seed=250409307, **scenario_kwargs(args))
+    secs, mk, fill = h.bench_simulate(sc, 0, threads, g.default_scale_class(), threads,
+                                      with_fill=True)
+    return {"value": g.n * threads / secs, "unit": "relaxations/s", "cores": threads,
+            "kind": "reference", "tasks": g.n,
+            "sample": f"{threads} scenarios of the full {g.n}-task workload graph, one "
+                      f"tracesim::simulate() per thread, {secs:.1f} s wall (duration fill "
+                      f"{fill:.1f} s and graph build {build_s:.1f} s outside the clock)"}
+
+
 def reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     R, h, g = cpu_sample_graph(args)
-    threads = cpu_threads()
+    threads = cpu_threads(1.0)
     for w in range(args.warmup):
         run_cpu_sample(R, h, g, args, 10_000_000 + w * threads, threads)
     # each step's clock covers the parallel simulate() region only; the
@@ -207,10 +260,11 @@ def reference_arm(args):
             "config": {"workload": CONFIGS[args.config][4] + " — reference CPU replay on a "
                        "bounded sample", "sample_tasks": g.n},
             "cpu_baseline": {"value": relax, "unit": "relaxations/s", "cores": threads,
-                             "kind": "reference",
+                             "kind": "reference", "host": host_info(),
                              "sample": f"{threads} scenarios per step, one per host thread, each a "
                                        f"full tracesim::simulate() of one TP replica "
-                                       f"({g.n} tasks) of the workload"},
+                                       f"({g.n} tasks) of the workload (durations filled outside "
+                                       f"the clock)"},
             "e2e": {"value": relax, "unit": "relaxations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -479,13 +533,17 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             R, h, cg = cpu_sample_graph(args)
-            threads = cpu_threads()
+            threads = cpu_threads(1.0)
             secs, count = run_cpu_sample(R, h, cg, args, 0, threads, per_thread=1)
             cpu = {"value": cg.n * count / secs, "unit": "relaxations/s", "cores": threads,
-                   "kind": "reference",
+                   "kind": "reference", "host": host_info(),
                    "sample": f"{count} scenarios ({threads} threads x 1), each a full "
                              f"tracesim::simulate() of one TP replica ({cg.n} tasks) of the "
-                             f"workload, {secs:.1f} s wall"}
+                             f"workload, {secs:.1f} s wall (durations filled outside the clock)"}
+            del h
+            if not args.no_cpu_full and args.config in ("config5", "config4"):
+                # the whole 4.95 M-task graph: ~5 GB and ~50 s per replay per thread
+                cpu["same_config"] = cpu_full_graph(args, cpu_threads(7.0))
         except Exception as exc:  # the oracle library is test infrastructure
             cpu = {"value": None, "unit": "relaxations/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}

@@ -214,14 +214,24 @@ typedef struct {
    * = [W + b*w, min(W + (b+1)*w, end)) covered by >= 1 kernel on any of the
    * rank's streams (value = covered / bin span, computed by the caller). */
   int64_t util_bin_width;  /* w > 0 to produce util_covered */
-  int32_t util_max_bins;   /* bins stored per rank (later bins are dropped) */
+  int32_t util_max_bins;   /* bins stored per rank; a window needing more fails
+                              the call (TS_E_INVALID_ARGUMENT, message names the
+                              bins needed) after util_n_bins is written */
   int32_t util_pad;
   int64_t* util_covered;   /* [count][n_ranks][util_max_bins] */
   int32_t* util_n_bins;    /* [count] bins the window needs */
   /* compare_replay (metrics.cpp:189-221): delta = sim_start - original_start */
-  int64_t* delta_abs_sum;  /* [count] sum of |delta| over all tasks (exact) */
-  int64_t* delta_worst;    /* [count][3] {max |delta|, its task (smallest id on
-                              ties, the report's sort order), signed delta} */
+  int64_t* delta_abs_sum;  /* [count] sum of |delta| over all tasks (exact int64;
+                              the reference's double sum equals it below 2^53) */
+  int64_t* delta_worst;    /* [count][delta_worst_n][3] {|delta|, task, delta}:
+                              the report's worst list, largest |delta| first,
+                              ties by smaller task id (metrics.cpp:213-217);
+                              task -1 pads a graph with fewer tasks */
+  int32_t delta_worst_n;   /* entries per scenario, 1..64 (0 means 1); the
+                              reference's default is 10 (metrics.hpp:82-83) */
+  int32_t pad2;
+  int32_t* n_fixups;       /* [1] scenarios of this call re-run by the exact
+                              event-driven path (failed sync certificates), or NULL */
 } ts_result;
 
 /* Replays `sc->count` scenarios on `stream` (cudaStream_t, NULL = legacy
@@ -351,6 +361,24 @@ int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, con
  * TS_E_INVALID_ARGUMENT with the ParseError text, TS_E_GRAPH for cycles. */
 int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_threads,
                      int64_t gap_threshold_us, ts_host_graph** out);
+
+/* The full input options of the reference's build_from_inputs (cli.cpp:52-58,
+ * 118-137): a rank manifest (load_multirank_manifest, trace_parse.cpp:296-328),
+ * the iteration window ("full", "auto" = detect_iteration_window +
+ * filter_window, trace_parse.cpp:330-419, or "START:END"), a custom category
+ * table (CategoryTable::from_json, trace_parse.cpp:186-211) and a build policy
+ * (BuildPolicy::from_json, build.cpp:41-66), the last two as JSON file paths
+ * like the CLI's --categories / --policy.  NULL fields take the defaults. */
+typedef struct {
+  const char* const* paths;      /* --trace inputs */
+  int32_t n_paths;
+  int32_t n_threads;             /* <= 0: all cores */
+  const char* manifest;          /* --manifest JSON {rank: path} or NULL */
+  const char* window;            /* NULL = "full" */
+  const char* categories_path;   /* or NULL */
+  const char* policy_path;       /* or NULL */
+} ts_ingest_options;
+int ts_ingest_traces_ex(const ts_ingest_options* options, ts_host_graph** out);
 
 /* Device-time accounting: when enabled, CUDA events are recorded on the
  * caller's stream around every kernel the engine launches for this graph;

@@ -17,6 +17,7 @@
 #include "oracles.hpp"
 #include "tracesim/build.hpp"
 #include "tracesim/metrics.hpp"
+#include "tracesim/pipeline.hpp"
 #include "tracesim/simulate.hpp"
 #include "tracesim/synth.hpp"
 #include "tracesim/trace_parse.hpp"
@@ -43,8 +44,7 @@ int main() {
   spec.seed = 99;
   spec.jitter = 0.2;
   b200::BatchOptions opt;
-  opt.util_bin_width = 4000;
-  opt.util_max_bins = 1024;
+  opt.util_bin_width = 4000;  // util_max_bins 0: every bin of every window
   opt.deltas = true;
   const b200::BatchResult r = b200::simulate_batch(g, spec, opt);
 
@@ -73,14 +73,16 @@ int main() {
       for (std::size_t b = 0; b < ws.bins.size(); ++b)
         if (ws.bins[b].start != gs_.bins[b].start || ws.bins[b].value != gs_.bins[b].value) ++bad;
     }
-    const ReplayReport a = compare_replay(g, sim, 1), b = b200::replay_report(g, r, s);
+    const ReplayReport a = compare_replay(g, sim), b = b200::replay_report(g, r, s);  // worst 10
     if (a.reference_makespan != b.reference_makespan || a.simulated_makespan != b.simulated_makespan ||
         a.max_abs_delta != b.max_abs_delta || a.mean_abs_delta != b.mean_abs_delta ||
-        a.relative_error != b.relative_error || a.worst.size() != b.worst.size() ||
-        (!a.worst.empty() && (a.worst[0].task != b.worst[0].task ||
-                              a.worst[0].delta != b.worst[0].delta ||
-                              a.worst[0].simulated_start != b.worst[0].simulated_start)))
+        a.relative_error != b.relative_error || a.worst.size() != b.worst.size())
       ++bad;
+    for (std::size_t k = 0; k < a.worst.size() && k < b.worst.size(); ++k)
+      if (a.worst[k].task != b.worst[k].task || a.worst[k].delta != b.worst[k].delta ||
+          a.worst[k].simulated_start != b.worst[k].simulated_start ||
+          a.worst[k].reference_start != b.worst[k].reference_start)
+        ++bad;
   }
   // what-if retime through the C++ API vs the reference transforms
   // (change_hidden then scale_dp, transform.cpp:741-755) replayed by the tick oracle
@@ -153,7 +155,55 @@ int main() {
   }
   if (!threw) ++bad_rt;
   bad += bad_rt;
-  std::printf("%s: %d scenarios, %zu tasks, %d mismatches (retime: %d scenarios, %d)\n",
-              bad ? "FAIL" : "PASS", spec.count, g.tasks.size(), bad, rs.count, bad_rt);
+  // Mode B through the C++ API: estimate_batch(PipelineSpec) vs the
+  // reference build_pipeline(spec, hook) (pipeline.cpp:474-477), for the spec
+  // pipeline_spec_for builds and a hand-edited one; makespans of nominal and
+  // jittered scenarios (hook slot op_index[t] = the scenario duration of t)
+  int bad_est = 0;
+  {
+    nlohmann::json je;
+    je["parallelism"] = {{"pp", 3}, {"dp", 2}, {"num_microbatches", 5}};
+    je["model"] = {{"n_layers", 6}, {"d_model", 1024}, {"d_ffn", 4096}, {"n_heads", 16},
+                   {"d_head", 64}};
+    PipelineSpec base_spec = pipeline_spec_for(SynthSpec::from_json(je.dump()));
+    PipelineSpec edited = base_spec;
+    edited.num_microbatches = 7;
+    edited.host.launch = 9;
+    edited.stages[1].layers_fwd[0].push_back({"fused_dropout", 41, OpClass::Compute, {}});
+    edited.stages[1].layers_bwd[0].push_back({"fused_dropout_bwd", 57, OpClass::Compute, {}});
+    edited.stages[2].optimizer.push_back({"clip_grad", 33, OpClass::Compute, {{"bytes", "4096"}}});
+    for (const PipelineSpec* ps : {&base_spec, &edited}) {
+      b200::ScenarioSpec es;
+      es.first = 11;
+      es.count = 6;
+      es.seed = 5;
+      es.jitter = 0.15;
+      b200::BatchOptions eo;
+      eo.timestamps = true;
+      const b200::EstimateResult er = b200::estimate_batch(*ps, es, eo);
+      const BuiltPipeline nominal = build_pipeline(*ps);
+      if (er.truth_makespan != nominal.end - ps->origin) ++bad_est;
+      orc_scenarios esc{};
+      esc.seed = es.seed;
+      esc.jitter = es.jitter;
+      const std::size_t n = er.base.size();
+      std::vector<uint8_t> ecls(n, 0);
+      std::vector<int64_t> d(n);
+      for (int s = 0; s < es.count; ++s) {
+        orc_fill_durations(&esc, es.first + s, static_cast<int32_t>(n), er.base.data(),
+                           ecls.data(), d.data());
+        std::vector<Micros> hook(static_cast<std::size_t>(er.n_ops), 0);
+        for (std::size_t t = 0; t < n; ++t)
+          if (er.op_index[t] >= 0) hook[static_cast<std::size_t>(er.op_index[t])] = d[t];
+        const BuiltPipeline b = build_pipeline(
+            *ps, [&](std::size_t i, Micros base) { return i < hook.size() ? hook[i] : base; });
+        if (b.end - ps->origin != er.batch.span[3 * s + 2]) ++bad_est;
+      }
+    }
+  }
+  bad += bad_est;
+  std::printf("%s: %d scenarios, %zu tasks, %d mismatches (retime: %d scenarios, %d; "
+              "estimate_batch: %d)\n",
+              bad ? "FAIL" : "PASS", spec.count, g.tasks.size(), bad, rs.count, bad_rt, bad_est);
   return bad ? 1 : 0;
 }

@@ -373,26 +373,42 @@ int ref_compare_replay(void* h, const int64_t* start, const int64_t* fin, int32_
 
 // Times the reference simulate() over `count` scenarios whose durations come
 // from the oracle's scenario formula (lumos_oracle.c), one scenario per call,
-// on `threads` host threads (each with its own graph copy).  Returns wall
-// seconds of the parallel region (duration fill + simulate; graph copies are
-// made before the clock starts).  makespans[i] receives scenario i's makespan.
+// on `threads` host threads (each with its own graph copy).  The durations of
+// every scenario are materialised before the clock starts (their fill time is
+// returned in *fill_seconds), so the returned wall seconds cover the parallel
+// simulate() region only.  makespans[i] receives scenario i's
+// makespan.
 double ref_bench_simulate(void* h, const orc_scenarios* sc, int64_t first, int32_t count,
-                          const uint8_t* cls, int threads, int64_t* makespans) {
+                          const uint8_t* cls, int threads, int64_t* makespans,
+                          double* fill_seconds) {
   const ExecutionGraph& src = static_cast<RefGraph*>(h)->g;
   if (threads < 1) threads = 1;
+  const std::size_t n = src.tasks.size();
   std::vector<ExecutionGraph> copies(static_cast<std::size_t>(threads), src);
-  std::vector<int64_t> base(src.tasks.size());
-  for (std::size_t i = 0; i < src.tasks.size(); ++i) base[i] = src.tasks[i].duration;
+  std::vector<int64_t> base(n);
+  for (std::size_t i = 0; i < n; ++i) base[i] = src.tasks[i].duration;
+  std::vector<std::vector<int64_t>> dur(static_cast<std::size_t>(count), std::vector<int64_t>(n));
+  auto f0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+      pool.emplace_back([&, w] {
+        for (int32_t s = w; s < count; s += threads)
+          orc_fill_durations(sc, first + s, static_cast<int32_t>(n), base.data(), cls,
+                             dur[static_cast<std::size_t>(s)].data());
+      });
+    for (auto& t : pool) t.join();
+  }
+  if (fill_seconds)
+    *fill_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - f0).count();
   auto t0 = std::chrono::steady_clock::now();
   std::vector<std::thread> pool;
   for (int w = 0; w < threads; ++w) {
     pool.emplace_back([&, w] {
       ExecutionGraph& g = copies[static_cast<std::size_t>(w)];
-      std::vector<int64_t> dur(g.tasks.size());
       for (int32_t s = w; s < count; s += threads) {
-        orc_fill_durations(sc, first + s, static_cast<int32_t>(g.tasks.size()), base.data(),
-                           cls, dur.data());
-        for (std::size_t i = 0; i < g.tasks.size(); ++i) g.tasks[i].duration = dur[i];
+        const std::vector<int64_t>& d = dur[static_cast<std::size_t>(s)];
+        for (std::size_t i = 0; i < n; ++i) g.tasks[i].duration = d[i];
         try {
           makespans[s] = simulate(g).makespan;
         } catch (const std::exception&) {
@@ -453,6 +469,103 @@ void* ref_ingest_traces(const char* const* paths, int n) {
       ss << in.rdbuf();
       if (graphs.count(rank)) throw std::runtime_error("duplicate rank " + std::to_string(rank));
       graphs.emplace(rank, build_graph(parse_trace(ss.str(), cats), BuildPolicy(), rank));
+    }
+    auto* r = new RefGraph;
+    r->g = merge_ranks(graphs);
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// The reference's build_from_inputs (cli.cpp:118-137) with every option:
+// manifest (rank -> path, relative to the manifest's directory), window
+// ("full" | "auto" | START:END), custom category table and build policy (JSON
+// texts).  load_inputs (cli.cpp:93-116) is restated with the files read into
+// strings (see ref_ingest_traces); the rank files are the inputs whose file
+// name carries a rank_<N> marker.  Returns a handle or NULL.
+void* ref_ingest_traces_ex(const char* const* paths, int n, const char* manifest,
+                           const char* window, const char* categories_json,
+                           const char* policy_json) {
+  try {
+    const CategoryTable cats = categories_json ? CategoryTable::from_json(categories_json)
+                                               : CategoryTable();
+    const BuildPolicy policy = policy_json ? BuildPolicy::from_json(policy_json) : BuildPolicy();
+    auto slurp = [](const std::string& path) {
+      std::ifstream in(path, std::ios::binary);
+      if (!in) throw ParseError("cannot open trace file '" + path + "'");
+      std::stringstream ss;
+      ss << in.rdbuf();
+      return ss.str();
+    };
+    auto marker = [](const std::string& text, int& rank) {
+      bool found = false;
+      for (std::size_t p = text.find("rank"); p != std::string::npos; p = text.find("rank", p + 1)) {
+        std::size_t q = p + 4;
+        if (q < text.size() && text[q] == '_') ++q;
+        std::size_t e = q;
+        while (e < text.size() && std::isdigit(static_cast<unsigned char>(text[e]))) ++e;
+        if (e > q) {
+          rank = std::stoi(text.substr(q, e - q));
+          found = true;
+        }
+      }
+      return found;
+    };
+    std::map<int, std::vector<TraceEvent>> per_rank;
+    auto take = [&](int rank, std::vector<TraceEvent> evs) {
+      if (!per_rank.emplace(rank, std::move(evs)).second)
+        throw ParseError("rank " + std::to_string(rank) + " appears in more than one input");
+    };
+    if (manifest && *manifest) {
+      const std::string mp = manifest;
+      nlohmann::json root = nlohmann::json::parse(slurp(mp));
+      std::string dir;
+      if (auto slash = mp.find_last_of('/'); slash != std::string::npos) dir = mp.substr(0, slash + 1);
+      for (auto it = root.begin(); it != root.end(); ++it) {
+        std::string path = it.value().get<std::string>();
+        if (!path.empty() && path[0] != '/') path = dir + path;
+        take(std::stoi(it.key()), parse_trace(slurp(path), cats));
+      }
+    }
+    std::vector<std::pair<int, std::string>> marked;
+    for (int i = 0; i < n; ++i) {
+      const std::string path = paths[i];
+      const std::string fname = path.substr(path.find_last_of('/') == std::string::npos
+                                                ? 0 : path.find_last_of('/') + 1);
+      int rank = 0;
+      if (marker(fname, rank)) {
+        marker(path, rank);
+        marked.emplace_back(rank, path);
+        continue;
+      }
+      for (auto& [r, sub] : split_by_rank(parse_trace(slurp(path), cats))) take(r, std::move(sub));
+    }
+    {
+      std::map<int, std::vector<TraceEvent>> mr;
+      for (const auto& [rank, path] : marked) {
+        if (mr.count(rank))
+          throw ParseError("duplicate rank " + std::to_string(rank) + " from '" + path + "'");
+        mr.emplace(rank, parse_trace(slurp(path), cats));
+      }
+      for (auto& [rank, evs] : mr) take(rank, std::move(evs));
+    }
+    if (per_rank.empty()) throw ParseError("no input traces; pass --trace or --manifest");
+    const std::string win = window ? window : "full";
+    std::map<int, ExecutionGraph> graphs;
+    for (auto& [rank, events] : per_rank) {
+      std::vector<TraceEvent> scoped = std::move(events);
+      if (win == "auto") {
+        scoped = filter_window(scoped, detect_iteration_window(scoped));
+      } else if (win != "full") {  // parse_window_arg (cli.cpp:72-85)
+        const auto sep = win.find_first_of(":,");
+        IterationWindow w;
+        w.start = std::stoll(win.substr(0, sep));
+        w.end = std::stoll(win.substr(sep + 1));
+        scoped = filter_window(scoped, w);
+      }
+      graphs.emplace(rank, build_graph(scoped, policy, rank));
     }
     auto* r = new RefGraph;
     r->g = merge_ranks(graphs);

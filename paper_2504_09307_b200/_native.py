@@ -73,7 +73,8 @@ class TsResult(C.Structure):
                 ("rank_breakdown", i64p), ("stream_busy", i64p), ("status", i32p),
                 ("util_bin_width", C.c_int64), ("util_max_bins", C.c_int32),
                 ("util_pad", C.c_int32), ("util_covered", i64p), ("util_n_bins", i32p),
-                ("delta_abs_sum", i64p), ("delta_worst", i64p)]
+                ("delta_abs_sum", i64p), ("delta_worst", i64p), ("delta_worst_n", C.c_int32),
+                ("pad2", C.c_int32), ("n_fixups", i32p)]
 
 
 ABI_VERSION = 4  # TS_ABI_VERSION in include/lumos_b200.h

@@ -148,7 +148,7 @@ struct ts_graph {
   DevBuf acct_a;  // [tile][n_ranks] |A| sums of the walk
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[12];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur,
-                     // util, util bins, delta sum, delta worst
+                     // util, util bins, delta sum, delta worst, internal bin counts
   DevBuf delta_scratch;
   // device-time accounting
   bool profile = false;
@@ -806,8 +806,19 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       out_ptr(7, out->util_covered, static_cast<size_t>(count) * n_ranks * ubins * 8));
   int32_t* d_nbins = static_cast<int32_t*>(out_ptr(8, out->util_n_bins, static_cast<size_t>(count) * 4));
   int64_t* d_dsum = static_cast<int64_t*>(out_ptr(9, out->delta_abs_sum, static_cast<size_t>(count) * 8));
-  int64_t* d_dworst =
-      static_cast<int64_t*>(out_ptr(10, out->delta_worst, static_cast<size_t>(count) * 24));
+  const int32_t worst_n = out->delta_worst_n <= 0 ? 1 : out->delta_worst_n;
+  if (worst_n > kMaxWorst)
+    return fail(TS_E_INVALID_ARGUMENT,
+                "delta_worst_n must be <= " + std::to_string(kMaxWorst) + " on the device");
+  int64_t* d_dworst = static_cast<int64_t*>(
+      out_ptr(10, out->delta_worst, static_cast<size_t>(count) * worst_n * 24));
+  // utilization needs the per-scenario bin counts to check util_max_bins
+  int32_t* d_nbins_chk = d_nbins;
+  if (out->util_covered && !d_nbins_chk) {
+    if (g->stage[11].reserve(static_cast<size_t>(count) * 4) != cudaSuccess)
+      return fail(TS_E_NOMEM, "could not stage output buffers");
+    d_nbins_chk = g->stage[11].as<int32_t>();
+  }
   if ((out->start && ts_bytes && !d_start) || (out->fin && ts_bytes && !d_fin) ||
       (out->span && !d_span) || (out->rank_breakdown && n_ranks && !d_bd) ||
       (out->stream_busy && n_streams && !d_busy) || (out->util_covered && n_ranks && !d_util) ||
@@ -1132,19 +1143,22 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       const int64_t want = (4 * 148 * 8 + col_blocks - 1) / col_blocks;
       dl.n_chunks = static_cast<int32_t>(
           std::max<int64_t>(1, std::min<int64_t>(want, (c.n_tasks + 255) / 256)));
-      CUDA_TRY(g->delta_scratch.reserve(static_cast<size_t>(dl.n_chunks) * bn * 32));
-      dl.partial = g->delta_scratch.as<int64_t>();
+      dl.worst_n = worst_n;
+      const size_t cells = static_cast<size_t>(dl.n_chunks) * bn;
+      CUDA_TRY(g->delta_scratch.reserve(cells * 8 + cells * worst_n * 16));
+      dl.partial_sum = g->delta_scratch.as<int64_t>();
+      dl.partial = dl.partial_sum + cells;
       dl.abs_sum = d_dsum ? d_dsum + b0 : nullptr;
-      dl.worst = d_dworst ? d_dworst + static_cast<size_t>(b0) * 3 : nullptr;
+      dl.worst = d_dworst ? d_dworst + static_cast<size_t>(b0) * worst_n * 3 : nullptr;
       Timed tm(g, stream, 1);
       CUDA_TRY(launch_deltas(dl, stream));
       g_launches += 2;
     }
   }
-  if (d_nbins) {
+  if (d_nbins_chk) {
     Timed tm(g, stream, 2);
-    CUDA_TRY(launch_util_nbins(lo, hi, c.window_start, c.window_end, out->util_bin_width, d_nbins,
-                               count, stream));
+    CUDA_TRY(launch_util_nbins(lo, hi, c.window_start, c.window_end, out->util_bin_width,
+                               d_nbins_chk, count, stream));
     g_launches++;
   }
   if (d_span) {
@@ -1155,14 +1169,21 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
 
   // deadlock (only possible outside the chained class) -> SimulationError
   std::vector<int32_t> host_status;
-  if (c.des_only || (out->status && !is_device_ptr(out->status))) {
+  if (c.des_only || out->n_fixups || (out->status && !is_device_ptr(out->status))) {
     host_status.resize(count);
     CUDA_TRY(cudaMemcpyAsync(host_status.data(), status, static_cast<size_t>(count) * 4,
                              cudaMemcpyDeviceToHost, stream));
   }
+  std::vector<int32_t> host_nbins;
+  if (out->util_covered && d_nbins_chk) {
+    host_nbins.resize(count);
+    CUDA_TRY(cudaMemcpyAsync(host_nbins.data(), d_nbins_chk, static_cast<size_t>(count) * 4,
+                             cudaMemcpyDeviceToHost, stream));
+  }
   for (const OutBuf& b : copies)
     CUDA_TRY(cudaMemcpyAsync(b.user, b.dev, b.bytes, cudaMemcpyDeviceToHost, stream));
-  if (!copies.empty() || !host_status.empty()) CUDA_TRY(cudaStreamSynchronize(stream));
+  if (!copies.empty() || !host_status.empty() || !host_nbins.empty())
+    CUDA_TRY(cudaStreamSynchronize(stream));
   cleanup();
   if (out->status) {
     if (is_device_ptr(out->status))
@@ -1172,6 +1193,21 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       std::memcpy(out->status, host_status.data(), static_cast<size_t>(count) * 4);
   }
   if (prev_dev >= 0 && prev_dev != g->device) cudaSetDevice(prev_dev);
+  if (out->n_fixups) {
+    int32_t nf = 0;
+    for (int32_t st : host_status) nf += st > 0;
+    if (is_device_ptr(out->n_fixups))
+      CUDA_TRY(cudaMemcpy(out->n_fixups, &nf, 4, cudaMemcpyHostToDevice));
+    else
+      *out->n_fixups = nf;
+  }
+  if (!host_nbins.empty()) {
+    const int32_t need = *std::max_element(host_nbins.begin(), host_nbins.end());
+    if (need > out->util_max_bins)
+      return fail(TS_E_INVALID_ARGUMENT,
+                  "utilization needs " + std::to_string(need) + " bins per rank; util_max_bins is " +
+                      std::to_string(out->util_max_bins));
+  }
   int64_t n_dead = 0;
   int32_t first_dead = -1;
   for (int32_t i = 0; i < static_cast<int32_t>(host_status.size()); ++i)

@@ -1,6 +1,8 @@
 // capi_host.cpp — extern "C" entry points of the host-side graph sources
 // (synthetic generator, trace-event graph builder); see include/lumos_b200.h.
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -87,17 +89,11 @@ const char* ts_host_graph_name(const ts_host_graph* g, int32_t id) {
 
 void ts_host_graph_free(ts_host_graph* g) { delete g; }
 
-int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_threads,
-                     int64_t gap_threshold_us, ts_host_graph** out) {
-  if (!out || (n_paths > 0 && !paths)) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
-  std::vector<std::string> ps;
-  for (int32_t i = 0; i < n_paths; ++i) ps.emplace_back(paths[i] ? paths[i] : "");
+static int ingest(const IngestOptions& opts, ts_host_graph** out) {
   auto* h = new ts_host_graph;
-  BuildPolicyLite pol;
-  pol.gap_threshold_us = gap_threshold_us;
   std::vector<RtMeta> rt;
   std::string err;
-  const int rc = ingest_trace_files(ps, n_threads, pol, h->s.names, h->s.graph, rt, err);
+  const int rc = ingest_traces(opts, h->s.names, h->s.graph, rt, err);
   if (rc != TS_OK) {
     delete h;
     *out = nullptr;
@@ -106,6 +102,48 @@ int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_thread
   fill_retime_arrays(h->s.graph, rt);
   *out = h;
   return TS_OK;
+}
+
+static bool read_text(const char* path, std::string& text, std::string& err) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) {
+    err = std::string("cannot open '") + path + "'";
+    return false;
+  }
+  std::ostringstream os;
+  os << in.rdbuf();
+  text = os.str();
+  return true;
+}
+
+int ts_ingest_traces(const char* const* paths, int32_t n_paths, int32_t n_threads,
+                     int64_t gap_threshold_us, ts_host_graph** out) {
+  if (!out || (n_paths > 0 && !paths)) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  IngestOptions o;
+  for (int32_t i = 0; i < n_paths; ++i) o.paths.emplace_back(paths[i] ? paths[i] : "");
+  o.threads = n_threads;
+  o.policy.gap_threshold_us = gap_threshold_us;
+  return ingest(o, out);
+}
+
+int ts_ingest_traces_ex(const ts_ingest_options* opt, ts_host_graph** out) {
+  if (!opt || !out || (opt->n_paths > 0 && !opt->paths))
+    return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  IngestOptions o;
+  for (int32_t i = 0; i < opt->n_paths; ++i) o.paths.emplace_back(opt->paths[i] ? opt->paths[i] : "");
+  o.threads = opt->n_threads;
+  if (opt->manifest) o.manifest = opt->manifest;
+  if (opt->window) o.window = opt->window;
+  std::string err, text;
+  if (opt->categories_path) {
+    if (!read_text(opt->categories_path, text, err) || !categories_from_json(text, o.categories, err))
+      return set_error(TS_E_INVALID_ARGUMENT, err);
+  }
+  if (opt->policy_path) {
+    if (!read_text(opt->policy_path, text, err) || !policy_from_json(text, o.policy, err))
+      return set_error(TS_E_INVALID_ARGUMENT, err);
+  }
+  return ingest(o, out);
 }
 
 int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, const uint8_t* cat,

@@ -31,41 +31,46 @@ std::string lower(std::string s) {
 
 }  // namespace
 
-bool is_comm_name(const std::string& name) {
-  static const char* kPat[] = {"nccl", "allreduce", "allgather", "reducescatter", "sendrecv",
-                               "alltoall"};
-  const std::string l = lower(name);
-  for (const char* p : kPat)
+bool BuildPolicyLite::is_launch(const std::string& n) const {
+  return std::find(launch_names.begin(), launch_names.end(), n) != launch_names.end();
+}
+bool BuildPolicyLite::is_record(const std::string& n) const {
+  return std::find(record_names.begin(), record_names.end(), n) != record_names.end();
+}
+bool BuildPolicyLite::is_wait(const std::string& n) const {
+  return std::find(wait_names.begin(), wait_names.end(), n) != wait_names.end();
+}
+int BuildPolicyLite::sync_flavor(const std::string& n) const {
+  for (const auto& [name, f] : sync_names)
+    if (name == n) return f;
+  return 0;
+}
+bool BuildPolicyLite::is_comm(const std::string& n) const {
+  const std::string l = lower(n);
+  for (const std::string& p : comm_patterns)
     if (l.find(p) != std::string::npos) return true;
   return false;
 }
 
-namespace {
-
-// sync flavor of a host call: 0 none, 1 device, 2 stream, 3 event (build.hpp:27-31)
-int sync_flavor(const std::string& n) {
-  if (n == "cudaDeviceSynchronize") return 1;
-  if (n == "cudaStreamSynchronize") return 2;
-  if (n == "cudaEventSynchronize") return 3;
-  return 0;
+bool is_comm_name(const std::string& name) {
+  static const BuildPolicyLite kDefault;
+  return kDefault.is_comm(name);
 }
 
-bool is_launch_name(const std::string& n) {
-  return n == "cudaLaunchKernel" || n == "cudaLaunchKernelExC" || n == "cuLaunchKernel" ||
-         n == "cudaLaunchCooperativeKernel" || n == "cudaMemcpyAsync" || n == "cudaMemsetAsync";
-}
-
-}  // namespace
-
-uint8_t classify_event(const Event& e, const Names& names) {
+uint8_t classify_event(const Event& e, const Names& names, const BuildPolicyLite& policy) {
   const std::string& n = names.str[e.name];
   if (e.cat == CAT_MEMCPY) return TS_OP_COMMUNICATION;
-  if (is_gpu_cat(e.cat)) return is_comm_name(n) ? TS_OP_COMMUNICATION : TS_OP_COMPUTE;
-  if (is_launch_name(n)) return TS_OP_LAUNCH;
-  if (sync_flavor(n)) return TS_OP_SYNC;
-  if (n == "cudaEventRecord") return TS_OP_EVENT_RECORD;
-  if (n == "cudaStreamWaitEvent") return TS_OP_EVENT_WAIT;
+  if (is_gpu_cat(e.cat)) return policy.is_comm(n) ? TS_OP_COMMUNICATION : TS_OP_COMPUTE;
+  if (policy.is_launch(n)) return TS_OP_LAUNCH;
+  if (policy.sync_flavor(n)) return TS_OP_SYNC;
+  if (policy.is_record(n)) return TS_OP_EVENT_RECORD;
+  if (policy.is_wait(n)) return TS_OP_EVENT_WAIT;
   return TS_OP_OTHER;
+}
+
+uint8_t classify_event(const Event& e, const Names& names) {
+  static const BuildPolicyLite kDefault;
+  return classify_event(e, names, kDefault);
 }
 
 ts_graph_desc HostGraph::desc() const {
@@ -216,7 +221,7 @@ int build_rank_graph(const std::vector<Event>& events, const Names& names, int32
     const Event& e = events[kept[t]];
     const bool gpu = is_gpu_cat(e.cat);
     g.task_kind[t] = gpu ? 1 : 0;
-    g.op_class[t] = classify_event(e, names);
+    g.op_class[t] = classify_event(e, names, policy);
     g.duration[t] = e.dur;
     g.original_start[t] = e.ts;
     g.name[t] = e.name;
@@ -389,7 +394,7 @@ int build_rank_graph(const std::vector<Event>& events, const Names& names, int32
     if (proc.first == TS_LANE_CUDA_STREAM) stream_lanes.push_back(proc.second);
   for (int32_t t = 0; t < n; ++t) {
     if (g.task_kind[t] != 0 || g.op_class[t] != TS_OP_SYNC) continue;
-    const int flavor = sync_flavor(names.str[g.name[t]]);
+    const int flavor = policy.sync_flavor(names.str[g.name[t]]);
     if (!flavor) continue;
     int32_t bound = -1;
     if (flavor == 1) {

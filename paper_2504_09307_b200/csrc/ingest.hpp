@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "lumos_b200.h"
@@ -78,16 +79,36 @@ struct HostGraph {
   void append_relabelled(const HostGraph& src, int32_t new_rank, bool first);
 };
 
+// BuildPolicy (build.hpp:17-44): the host-call names and communication
+// patterns build_graph classifies by; defaults are the reference's.
 struct BuildPolicyLite {
   int64_t gap_threshold_us = 1000;  // build.hpp:18
+  std::vector<std::string> launch_names = {"cudaLaunchKernel", "cudaLaunchKernelExC",
+                                           "cuLaunchKernel", "cudaLaunchCooperativeKernel",
+                                           "cudaMemcpyAsync", "cudaMemsetAsync"};
+  // name -> sync flavor: 1 device, 2 stream, 3 event
+  std::vector<std::pair<std::string, int>> sync_names = {
+      {"cudaDeviceSynchronize", 1}, {"cudaStreamSynchronize", 2}, {"cudaEventSynchronize", 3}};
+  std::vector<std::string> record_names = {"cudaEventRecord"};
+  std::vector<std::string> wait_names = {"cudaStreamWaitEvent"};
+  std::vector<std::string> comm_patterns = {"nccl", "allreduce", "allgather", "reducescatter",
+                                            "sendrecv", "alltoall"};
+  bool is_launch(const std::string& n) const;
+  bool is_record(const std::string& n) const;
+  bool is_wait(const std::string& n) const;
+  int sync_flavor(const std::string& n) const;  // 0 none
+  bool is_comm(const std::string& n) const;     // case-insensitive substring
 };
+// BuildPolicy::from_json (build.cpp:41-66); false with `err` on a bad document
+bool policy_from_json(const std::string& text, BuildPolicyLite& out, std::string& err);
 
 // build_graph (build.cpp:338-510) over one rank's events.  Returns TS_OK or
 // TS_E_GRAPH (cycle / GPU event without stream) with `err` set.
 int build_rank_graph(const std::vector<Event>& events, const Names& names, int32_t rank,
                      const BuildPolicyLite& policy, HostGraph& out, std::string& err);
 
-// OpClass of an event under the default BuildPolicy (build.cpp:86-98).
+// OpClass of an event (build.cpp:93-103), under `policy` or the default.
+uint8_t classify_event(const Event& e, const Names& names, const BuildPolicyLite& policy);
 uint8_t classify_event(const Event& e, const Names& names);
 // BuildPolicy's communication-kernel name test (build.cpp:93-98)
 bool is_comm_name(const std::string& name);

@@ -217,6 +217,10 @@ cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t 
                              cudaStream_t stream);
 // compare_replay deltas of one tile: partial[chunk][count][3] then per column
 // {sum |d|, max |d|, worst task, signed delta} (see ts_result)
+// compare_replay's worst list (metrics.cpp:213-217): the worst_n tasks with
+// the largest |delta|, ties by smaller task id; kept per (chunk, scenario)
+// and merged per scenario
+constexpr int kMaxWorst = 64;
 struct DeltaParams {
   const int64_t* start;  // [n_tasks][ld]
   int64_t ld;
@@ -224,10 +228,11 @@ struct DeltaParams {
   int32_t n_tasks;
   int32_t count;
   int32_t n_chunks;
-  int32_t pad;
-  int64_t* partial;  // [n_chunks][count][4]
+  int32_t worst_n;   // 1..kMaxWorst
+  int64_t* partial_sum;  // [n_chunks][count]
+  int64_t* partial;      // [n_chunks][count][worst_n][2] {|d| (-1 empty), task}
   int64_t* abs_sum;  // [count] or null
-  int64_t* worst;    // [count][3] or null
+  int64_t* worst;    // [count][worst_n][3] {|d|, task (-1: none), d} or null
 };
 cudaError_t launch_deltas(const DeltaParams& p, cudaStream_t stream);
 // n_bins[i] = ceil(window span / w) for the utilization bins

@@ -1216,51 +1216,77 @@ __global__ void __launch_bounds__(kThreads, 4) rank_reduce_fast_kernel(ReducePar
 
 // ------------------------------------------------------------------- K6
 // compare_replay deltas (metrics.cpp:189-221).  Pass 1: thread = (scenario
-// column, task chunk), tasks ascending, strict '>' so the first maximum (the
-// smallest task id) wins; pass 2 folds the chunks in ascending order.
+// column, task chunk), tasks ascending; the chunk's worst_n largest |delta|
+// (ties: the smaller task id, i.e. the one seen first) kept sorted in local
+// memory.  Pass 2 merges the chunks per column with the same order.
+struct WorstEntry {
+  int64_t mag;
+  int64_t task;
+};
+__device__ __forceinline__ bool worse(int64_t ma, int64_t ta, const WorstEntry& b) {
+  return ma > b.mag || (ma == b.mag && ta < b.task);
+}
+// inserts (mag, task) into the sorted list w[0..n) of capacity cap
+__device__ __forceinline__ void worst_insert(WorstEntry* w, int& n, int cap, int64_t mag,
+                                             int64_t task) {
+  if (n == cap && !worse(mag, task, w[cap - 1])) return;
+  int k = n < cap ? n++ : cap - 1;
+  while (k > 0 && worse(mag, task, w[k - 1])) {
+    w[k] = w[k - 1];
+    --k;
+  }
+  w[k] = WorstEntry{mag, task};
+}
+
 __global__ void delta_partial_kernel(DeltaParams P) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = blockIdx.y;
   if (col >= P.count) return;
   const int32_t per = (P.n_tasks + P.n_chunks - 1) / P.n_chunks;
   const int32_t t0 = chunk * per, t1 = min(P.n_tasks, t0 + per);
-  int64_t sum = 0, best = -1, best_d = 0;
-  int32_t best_t = -1;
+  WorstEntry w[kMaxWorst];
+  int n = 0;
+  int64_t sum = 0;
   for (int32_t t = t0; t < t1; ++t) {
     const int64_t d = __ldcs(P.start + static_cast<int64_t>(t) * P.ld + col) - __ldg(P.ostart + t);
     const int64_t a = d < 0 ? -d : d;
     sum += a;
-    if (a > best) {
-      best = a;
-      best_t = t;
-      best_d = d;
-    }
+    worst_insert(w, n, P.worst_n, a, t);
   }
-  int64_t* o = P.partial + (static_cast<int64_t>(chunk) * P.count + col) * 4;
-  o[0] = sum;
-  o[1] = best;
-  o[2] = best_t;
-  o[3] = best_d;
+  P.partial_sum[static_cast<int64_t>(chunk) * P.count + col] = sum;
+  int64_t* o = P.partial + (static_cast<int64_t>(chunk) * P.count + col) * P.worst_n * 2;
+  for (int k = 0; k < P.worst_n; ++k) {
+    o[2 * k] = k < n ? w[k].mag : -1;
+    o[2 * k + 1] = k < n ? w[k].task : -1;
+  }
 }
 
 __global__ void delta_final_kernel(DeltaParams P) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= P.count) return;
-  int64_t sum = 0, best = -1, best_t = -1, best_d = 0;
+  WorstEntry w[kMaxWorst];
+  int n = 0;
+  int64_t sum = 0;
   for (int c = 0; c < P.n_chunks; ++c) {
-    const int64_t* o = P.partial + (static_cast<int64_t>(c) * P.count + col) * 4;
-    sum += o[0];
-    if (o[1] > best) {
-      best = o[1];
-      best_t = o[2];
-      best_d = o[3];
-    }
+    sum += P.partial_sum[static_cast<int64_t>(c) * P.count + col];
+    const int64_t* o = P.partial + (static_cast<int64_t>(c) * P.count + col) * P.worst_n * 2;
+    for (int k = 0; k < P.worst_n && o[2 * k] >= 0; ++k) worst_insert(w, n, P.worst_n, o[2 * k], o[2 * k + 1]);
   }
   if (P.abs_sum) P.abs_sum[col] = sum;
   if (P.worst) {
-    P.worst[3 * static_cast<int64_t>(col) + 0] = best < 0 ? 0 : best;
-    P.worst[3 * static_cast<int64_t>(col) + 1] = best_t;
-    P.worst[3 * static_cast<int64_t>(col) + 2] = best_d;
+    int64_t* out = P.worst + static_cast<int64_t>(col) * P.worst_n * 3;
+    for (int k = 0; k < P.worst_n; ++k) {
+      if (k < n) {
+        const int64_t t = w[k].task;
+        out[3 * k] = w[k].mag;
+        out[3 * k + 1] = t;
+        out[3 * k + 2] = __ldcs(P.start + t * P.ld + col) - __ldg(P.ostart + t);
+      } else {
+        out[3 * k] = 0;
+        out[3 * k + 1] = -1;
+        out[3 * k + 2] = 0;
+      }
+    }
   }
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <fstream>
+#include <map>
 #include <cctype>
 #include <sstream>
 #include <string>
@@ -85,8 +86,15 @@ bool arg_to_int(const json& args, const char* key, int64_t& out) {  // trace_par
   return false;
 }
 
-uint8_t lookup_category(const std::string& cat) {  // CategoryTable defaults, :156-184
-  auto map = [](const std::string& c, uint8_t& out) {
+using CatOverrides = std::vector<std::pair<std::string, uint8_t>>;
+
+uint8_t lookup_category(const std::string& cat, const CatOverrides& over) {  // :156-184
+  auto map = [&](const std::string& c, uint8_t& out) {
+    for (auto it = over.rbegin(); it != over.rend(); ++it)  // later entries win (set())
+      if (c == it->first) {
+        out = it->second;
+        return true;
+      }
     static const std::pair<const char*, uint8_t> kTable[] = {
         {"cpu_op", CAT_CPU_OP},       {"cpu_instant_event", CAT_METADATA},
         {"user_annotation", CAT_METADATA}, {"gpu_user_annotation", CAT_METADATA},
@@ -139,7 +147,8 @@ struct RawEvent {
   RtMeta rt;
 };
 
-void parse_dom(const json& root, std::vector<RawEvent>& out) {  // trace_parse.cpp:79-154
+void parse_dom(const json& root, std::vector<RawEvent>& out,
+               const CatOverrides& cats) {  // trace_parse.cpp:79-154
   const json* list = nullptr;
   if (root.is_array()) {
     list = &root;
@@ -160,7 +169,7 @@ void parse_dom(const json& root, std::vector<RawEvent>& out) {  // trace_parse.c
     RawEvent r;
     r.name = ev.value("name", "");
     Event& e = r.ev;
-    e.cat = lookup_category(ev.value("cat", ""));
+    e.cat = lookup_category(ev.value("cat", ""), cats);
     if (!ev.contains("ts")) throw ParseError{"record " + std::to_string(idx) + ": missing ts"};
     e.ts = to_micros(ev["ts"]);
     if (e.ts < 0) throw ParseError{"record " + std::to_string(idx) + ": negative ts"};
@@ -225,7 +234,9 @@ void parse_dom(const json& root, std::vector<RawEvent>& out) {  // trace_parse.c
 }
 
 // the last "rank_?(\\d+)" match of a path (trace_parse.cpp:260-270), scanned
-// by hand: matches of that pattern never overlap, so the last one wins
+// by hand: matches of that pattern never overlap, so the last one wins.  Which
+// inputs are rank files is decided on the file name alone (cli.cpp:87-91
+// has_rank_marker); their rank comes from the whole path.
 bool rank_marker(const std::string& path, int& rank) {
   bool found = false;
   for (std::size_t p = path.find("rank"); p != std::string::npos; p = path.find("rank", p + 1)) {
@@ -254,38 +265,253 @@ void parallel_for(int64_t n, int threads, F f) {
   for (auto& th : pool) th.join();
 }
 
+std::string file_name(const std::string& path) {
+  const std::size_t slash = path.find_last_of('/');
+  return slash == std::string::npos ? path : path.substr(slash + 1);
+}
+
+// detect_iteration_window (trace_parse.cpp:330-399) over one rank's events
+std::pair<int64_t, int64_t> detect_window(const std::vector<RawEvent>& evs) {
+  if (evs.empty()) return {0, 0};
+  int64_t lo = evs.front().ev.ts, hi = lo;
+  for (const RawEvent& r : evs) {
+    lo = std::min(lo, r.ev.ts);
+    hi = std::max(hi, r.ev.ts + r.ev.dur);
+  }
+  const std::pair<int64_t, int64_t> full{lo, hi};
+  auto host = [](const RawEvent& r) { return r.ev.cat == CAT_CPU_OP || r.ev.cat == CAT_RUNTIME; };
+  std::map<std::pair<int, int>, int> counts;
+  for (const RawEvent& r : evs)
+    if (host(r)) counts[{r.ev.pid, r.ev.tid}]++;
+  if (counts.empty()) return full;
+  auto best_thread = counts.begin();
+  for (auto it = counts.begin(); it != counts.end(); ++it)
+    if (it->second > best_thread->second) best_thread = it;  // ties: smaller (pid, tid)
+  std::vector<std::pair<int64_t, int64_t>> spans;
+  for (const RawEvent& r : evs)
+    if (host(r) && std::make_pair(r.ev.pid, r.ev.tid) == best_thread->first)
+      spans.emplace_back(r.ev.ts, r.ev.ts + r.ev.dur);
+  std::sort(spans.begin(), spans.end());
+  std::vector<int64_t> gaps;
+  for (std::size_t i = 1; i < spans.size(); ++i)
+    gaps.push_back(std::max<int64_t>(0, spans[i].first - spans[i - 1].second));
+  if (gaps.empty()) return full;
+  const int64_t max_gap = *std::max_element(gaps.begin(), gaps.end());
+  if (max_gap <= 0) return full;
+  std::vector<int64_t> sorted = gaps;
+  std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
+  if (max_gap < 8 * std::max<int64_t>(sorted[sorted.size() / 2], 1)) return full;
+  std::vector<std::size_t> seg = {0};
+  for (std::size_t i = 1; i < spans.size(); ++i)
+    if (spans[i].first - spans[i - 1].second >= (max_gap + 1) / 2) seg.push_back(i);
+  if (seg.size() == 1) return full;
+  std::size_t best = 0, best_n = 0;
+  for (std::size_t k = 0; k < seg.size(); ++k) {
+    const std::size_t end = k + 1 < seg.size() ? seg[k + 1] : spans.size();
+    if (end - seg[k] > best_n) {
+      best_n = end - seg[k];
+      best = k;
+    }
+  }
+  const std::size_t a = seg[best];
+  const std::size_t b = (best + 1 < seg.size() ? seg[best + 1] : spans.size()) - 1;
+  return {spans[a].first, spans[b].second};
+}
+
+// filter_window (trace_parse.cpp:401-419): events starting in [lo, hi), plus
+// GPU events whose correlation matches a retained runtime call
+void filter_window(std::vector<RawEvent>& evs, int64_t lo, int64_t hi) {
+  std::vector<int64_t> kept;
+  for (const RawEvent& r : evs)
+    if (r.ev.cat == CAT_RUNTIME && r.ev.corr >= 0 && r.ev.ts >= lo && r.ev.ts < hi)
+      kept.push_back(r.ev.corr);
+  std::sort(kept.begin(), kept.end());
+  std::vector<RawEvent> out;
+  for (RawEvent& r : evs) {
+    const bool inside = r.ev.ts >= lo && r.ev.ts < hi;
+    const bool gpu = r.ev.cat == CAT_KERNEL || r.ev.cat == CAT_MEMCPY || r.ev.cat == CAT_MEMSET;
+    if (inside || (gpu && r.ev.corr >= 0 && std::binary_search(kept.begin(), kept.end(), r.ev.corr)))
+      out.push_back(std::move(r));
+  }
+  evs.swap(out);
+}
+
+std::string read_file(const std::string& path, bool& ok) {
+  std::ifstream in(path, std::ios::binary);
+  ok = static_cast<bool>(in);
+  std::string text;
+  if (!ok) return text;
+  in.seekg(0, std::ios::end);
+  text.resize(static_cast<std::size_t>(std::max<std::streamoff>(0, in.tellg())));
+  in.seekg(0, std::ios::beg);
+  in.read(text.data(), static_cast<std::streamsize>(text.size()));
+  return text;
+}
+
 }  // namespace
 
-int ingest_trace_files(const std::vector<std::string>& paths, int threads,
-                       const BuildPolicyLite& policy, Names& names, HostGraph& out,
-                       std::vector<RtMeta>& task_rt, std::string& err) {
-  if (paths.empty()) {
-    err = "no input traces; pass --trace or --manifest";
-    return TS_E_INVALID_ARGUMENT;
+bool policy_from_json(const std::string& text, BuildPolicyLite& p, std::string& err) {
+  try {  // BuildPolicy::from_json (build.cpp:41-66)
+    const json root = json::parse(text);
+    p = BuildPolicyLite{};
+    if (root.contains("gap_threshold_us")) p.gap_threshold_us = root["gap_threshold_us"].get<int64_t>();
+    if (p.gap_threshold_us < 0) {
+      err = "build policy: gap_threshold_us must be >= 0";
+      return false;
+    }
+    if (root.contains("launch_names"))
+      p.launch_names = root["launch_names"].get<std::vector<std::string>>();
+    if (root.contains("sync_names")) {
+      p.sync_names.clear();
+      for (const auto& [name, flavor] : root["sync_names"].get<std::map<std::string, std::string>>()) {
+        const int f = flavor == "device" ? 1 : flavor == "stream" ? 2 : flavor == "event" ? 3 : 0;
+        if (!f) {
+          err = "build policy: sync flavor for '" + name + "' must be device|stream|event";
+          return false;
+        }
+        p.sync_names.emplace_back(name, f);
+      }
+    }
+    if (root.contains("record_names"))
+      p.record_names = root["record_names"].get<std::vector<std::string>>();
+    if (root.contains("wait_names")) p.wait_names = root["wait_names"].get<std::vector<std::string>>();
+    if (root.contains("comm_patterns"))
+      p.comm_patterns = root["comm_patterns"].get<std::vector<std::string>>();
+    return true;
+  } catch (const json::parse_error& e) {
+    err = std::string("build policy: ") + e.what();
+  } catch (const std::exception& e) {
+    err = std::string("build policy: ") + e.what();
   }
+  return false;
+}
+
+bool categories_from_json(const std::string& text, CatOverrides& out, std::string& err) {
+  json root;  // CategoryTable::from_json (trace_parse.cpp:186-211)
+  try {
+    root = json::parse(text);
+  } catch (const json::parse_error& e) {
+    err = std::string("category table: ") + e.what();
+    return false;
+  }
+  if (!root.is_object()) {
+    err = "category table must be a JSON object";
+    return false;
+  }
+  out.clear();
+  for (auto it = root.begin(); it != root.end(); ++it) {
+    const std::string v = it.value().is_string() ? it.value().get<std::string>() : it.value().dump();
+    uint8_t c;
+    if (v == "CpuOp") c = CAT_CPU_OP;
+    else if (v == "CudaRuntime") c = CAT_RUNTIME;
+    else if (v == "GpuKernel") c = CAT_KERNEL;
+    else if (v == "GpuMemcpy") c = CAT_MEMCPY;
+    else if (v == "GpuMemset") c = CAT_MEMSET;
+    else if (v == "Metadata") c = CAT_METADATA;
+    else {
+      err = "category table: unknown category '" + v + "'";
+      return false;
+    }
+    out.emplace_back(it.key(), c);
+  }
+  return true;
+}
+
+int ingest_traces(const IngestOptions& opts, Names& names, HostGraph& out,
+                  std::vector<RtMeta>& task_rt, std::string& err) {
+  int threads = opts.threads;
   if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  // window argument (cli.cpp:72-85 parse_window_arg)
+  bool win_auto = false, win_fixed = false;
+  int64_t win_lo = 0, win_hi = 0;
+  if (opts.window == "auto") {
+    win_auto = true;
+  } else if (opts.window != "full" && !opts.window.empty()) {
+    const std::size_t sep = opts.window.find_first_of(":,");
+    if (sep == std::string::npos) {
+      err = "window must be 'full', 'auto' or START:END, got '" + opts.window + "'";
+      return TS_E_INVALID_ARGUMENT;
+    }
+    try {
+      win_lo = std::stoll(opts.window.substr(0, sep));
+      win_hi = std::stoll(opts.window.substr(sep + 1));
+    } catch (const std::exception&) {
+      err = "window bounds must be integers, got '" + opts.window + "'";
+      return TS_E_INVALID_ARGUMENT;
+    }
+    if (win_hi <= win_lo) {
+      err = "window end must be after its start";
+      return TS_E_INVALID_ARGUMENT;
+    }
+    win_fixed = true;
+  }
+  // the files: manifest entries (rank -> path, relative to the manifest's
+  // directory; trace_parse.cpp:296-328) first, then the --trace inputs
+  struct Input {
+    std::string path;
+    int rank = -1;  // manifest rank
+    bool manifest = false;
+  };
+  std::vector<Input> inputs;
+  if (!opts.manifest.empty()) {
+    bool ok = false;
+    const std::string text = read_file(opts.manifest, ok);
+    if (!ok) {
+      err = "cannot open manifest '" + opts.manifest + "'";
+      return TS_E_INVALID_ARGUMENT;
+    }
+    json root;
+    try {
+      root = json::parse(text);
+    } catch (const json::parse_error& e) {
+      err = opts.manifest + ": " + e.what();
+      return TS_E_INVALID_ARGUMENT;
+    }
+    if (!root.is_object()) {
+      err = opts.manifest + ": manifest must map rank -> path";
+      return TS_E_INVALID_ARGUMENT;
+    }
+    const std::size_t slash = opts.manifest.find_last_of('/');
+    const std::string dir = slash == std::string::npos ? "" : opts.manifest.substr(0, slash + 1);
+    std::vector<int> seen;
+    for (auto it = root.begin(); it != root.end(); ++it) {
+      int rank;
+      try {
+        rank = std::stoi(it.key());
+      } catch (const std::exception&) {
+        err = opts.manifest + ": manifest key '" + it.key() + "' is not a rank";
+        return TS_E_INVALID_ARGUMENT;
+      }
+      if (std::find(seen.begin(), seen.end(), rank) != seen.end()) {
+        err = opts.manifest + ": duplicate rank " + std::to_string(rank);
+        return TS_E_INVALID_ARGUMENT;
+      }
+      seen.push_back(rank);
+      std::string path = it.value().is_string() ? it.value().get<std::string>() : "";
+      if (!path.empty() && path[0] != '/') path = dir + path;
+      inputs.push_back({path, rank, true});
+    }
+  }
+  for (const std::string& p : opts.paths) inputs.push_back({p, -1, false});
   // 1. parse every file (parallel)
-  std::vector<std::vector<RawEvent>> parsed(paths.size());
-  std::vector<std::string> errs(paths.size());
-  parallel_for(static_cast<int64_t>(paths.size()), threads, [&](int64_t i) {
-    std::ifstream in(paths[i], std::ios::binary);
-    if (!in) {
-      errs[i] = "cannot open trace file '" + paths[i] + "'";
+  std::vector<std::vector<RawEvent>> parsed(inputs.size());
+  std::vector<std::string> errs(inputs.size());
+  parallel_for(static_cast<int64_t>(inputs.size()), threads, [&](int64_t i) {
+    const std::string& path = inputs[i].path;
+    bool ok = false;
+    const std::string text = read_file(path, ok);
+    if (!ok) {
+      errs[i] = "cannot open trace file '" + path + "'";
       return;
     }
-    std::string text;
-    in.seekg(0, std::ios::end);
-    text.resize(static_cast<std::size_t>(std::max<std::streamoff>(0, in.tellg())));
-    in.seekg(0, std::ios::beg);
-    in.read(text.data(), static_cast<std::streamsize>(text.size()));
     try {
-      parse_dom(json::parse(text), parsed[i]);
+      parse_dom(json::parse(text), parsed[i], opts.categories);
     } catch (const ParseError& e) {
-      errs[i] = paths[i] + ": " + e.msg;
+      errs[i] = path + ": " + e.msg;
     } catch (const json::parse_error& e) {
-      errs[i] = paths[i] + ": malformed trace JSON: " + e.what();
+      errs[i] = path + ": malformed trace JSON: " + e.what();
     } catch (const std::exception& e) {
-      errs[i] = paths[i] + ": " + e.what();
+      errs[i] = path + ": " + e.what();
     }
   });
   for (const std::string& e : errs)
@@ -293,8 +519,8 @@ int ingest_trace_files(const std::vector<std::string>& paths, int threads,
       err = e;
       return TS_E_INVALID_ARGUMENT;
     }
-  // 2. ranks: a rank_<N> file is one rank; other files split by pid
-  //    (cli.cpp:93-116 load_inputs, trace_parse.cpp split_by_rank)
+  // 2. ranks (cli.cpp:93-116 load_inputs): manifest ranks; files without a
+  //    rank_<N> file name split by pid; rank files (load_multirank)
   std::vector<std::pair<int, std::vector<RawEvent>>> ranks;
   auto take = [&](int rank, std::vector<RawEvent>&& evs) -> bool {
     for (const auto& r : ranks)
@@ -305,24 +531,55 @@ int ingest_trace_files(const std::vector<std::string>& paths, int threads,
     ranks.emplace_back(rank, std::move(evs));
     return true;
   };
-  for (std::size_t i = 0; i < paths.size(); ++i) {
+  for (std::size_t i = 0; i < inputs.size(); ++i)
+    if (inputs[i].manifest && !take(inputs[i].rank, std::move(parsed[i]))) return TS_E_INVALID_ARGUMENT;
+  std::vector<std::size_t> marked;
+  for (std::size_t i = 0; i < inputs.size(); ++i) {
+    if (inputs[i].manifest) continue;
     int rank = 0;
-    if (rank_marker(paths[i], rank)) continue;
+    if (rank_marker(file_name(inputs[i].path), rank)) {
+      marked.push_back(i);
+      continue;
+    }
     std::vector<std::pair<int, std::vector<RawEvent>>> by_pid;
     for (RawEvent& r : parsed[i]) {
-      if (by_pid.empty() || by_pid.back().first != r.ev.pid) by_pid.emplace_back(r.ev.pid, std::vector<RawEvent>{});
+      if (by_pid.empty() || by_pid.back().first != r.ev.pid)
+        by_pid.emplace_back(r.ev.pid, std::vector<RawEvent>{});
       by_pid.back().second.push_back(std::move(r));
     }
     for (auto& [pid, evs] : by_pid)
       if (!take(pid, std::move(evs))) return TS_E_INVALID_ARGUMENT;
   }
-  for (std::size_t i = 0; i < paths.size(); ++i) {
-    int rank = 0;
-    if (!rank_marker(paths[i], rank)) continue;
-    if (!take(rank, std::move(parsed[i]))) return TS_E_INVALID_ARGUMENT;
+  {
+    std::vector<int> seen;
+    for (std::size_t i : marked) {
+      int rank = 0;
+      rank_marker(inputs[i].path, rank);
+      if (std::find(seen.begin(), seen.end(), rank) != seen.end()) {
+        err = "duplicate rank " + std::to_string(rank) + " from '" + inputs[i].path + "'";
+        return TS_E_INVALID_ARGUMENT;
+      }
+      seen.push_back(rank);
+    }
+    for (std::size_t i : marked) {
+      int rank = 0;
+      rank_marker(inputs[i].path, rank);
+      if (!take(rank, std::move(parsed[i]))) return TS_E_INVALID_ARGUMENT;
+    }
+  }
+  if (ranks.empty()) {
+    err = "no input traces; pass --trace or --manifest";
+    return TS_E_INVALID_ARGUMENT;
   }
   std::sort(ranks.begin(), ranks.end(),
             [](const auto& a, const auto& b) { return a.first < b.first; });
+  // the iteration window per rank (cli.cpp:128-133)
+  if (win_auto || win_fixed)
+    parallel_for(static_cast<int64_t>(ranks.size()), threads, [&](int64_t k) {
+      auto& evs = ranks[k].second;
+      const auto w = win_auto ? detect_window(evs) : std::make_pair(win_lo, win_hi);
+      filter_window(evs, w.first, w.second);
+    });
   // 3. names interned in rank order; events keep their source ordinal in
   //    op_index so the built tasks can find their metadata
   std::vector<std::vector<Event>> events(ranks.size());
@@ -342,7 +599,7 @@ int ingest_trace_files(const std::vector<std::string>& paths, int threads,
   std::vector<int> rcs(ranks.size(), TS_OK);
   std::vector<std::string> berr(ranks.size());
   parallel_for(static_cast<int64_t>(ranks.size()), threads, [&](int64_t k) {
-    rcs[k] = build_rank_graph(events[k], names, ranks[k].first, policy, graphs[k], berr[k]);
+    rcs[k] = build_rank_graph(events[k], names, ranks[k].first, opts.policy, graphs[k], berr[k]);
   });
   for (std::size_t k = 0; k < ranks.size(); ++k)
     if (rcs[k] != TS_OK) {

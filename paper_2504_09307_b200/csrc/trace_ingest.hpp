@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ingest.hpp"
@@ -17,12 +18,27 @@ struct RtMeta {
   bool allreduce = false, region_opt = false, region_p2p = false, dir_recv = false;
 };
 
-// parse_trace + rank assignment + build_graph per rank + merge_ranks over
-// `paths` (window "full"), on `threads` host threads (<= 0: all cores).
+// The reference's input options (cli.cpp:52-58 InputOptions)
+struct IngestOptions {
+  std::vector<std::string> paths;  // --trace
+  std::string manifest;            // --manifest: JSON {rank: path}
+  std::string window = "full";     // --window: full | auto | START:END
+  // CategoryTable overrides merged over the defaults (CategoryTable::from_json)
+  std::vector<std::pair<std::string, uint8_t>> categories;
+  BuildPolicyLite policy;          // --policy (BuildPolicy::from_json)
+  int threads = 0;                 // host threads (<= 0: all cores)
+};
+
+// build_from_inputs (cli.cpp:118-137): parse_trace of every input,
+// load_inputs' rank assignment (manifest, pid split, rank_<N> files), the
+// iteration window (detect_iteration_window / filter_window), build_graph per
+// rank and merge_ranks — files parsed and ranks built on host threads.
 // Returns TS_OK or a TS_E_* code with `err` set (ParseError / GraphError text).
-int ingest_trace_files(const std::vector<std::string>& paths, int threads,
-                       const BuildPolicyLite& policy, Names& names, HostGraph& out,
-                       std::vector<RtMeta>& task_rt, std::string& err);
+int ingest_traces(const IngestOptions& opts, Names& names, HostGraph& out,
+                  std::vector<RtMeta>& task_rt, std::string& err);
+// CategoryTable::from_json (trace_parse.cpp:186-211) overrides; false + err
+bool categories_from_json(const std::string& text,
+                          std::vector<std::pair<std::string, uint8_t>>& out, std::string& err);
 
 // the graph's ts_graph_desc.rt_* arrays from per-task metadata
 void fill_retime_arrays(HostGraph& g, const std::vector<RtMeta>& rt);

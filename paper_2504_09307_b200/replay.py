@@ -225,7 +225,7 @@ class DeviceGraph:
     def replay_batch(self, spec: ScenarioSpec, start=None, fin=None, ld: int = 0, span=None,
                      rank_breakdown=None, stream_busy=None, status=None, stream=None,
                      util_bin_width: int = 0, util_covered=None, util_n_bins=None,
-                     delta_abs_sum=None, delta_worst=None) -> None:
+                     delta_abs_sum=None, delta_worst=None, n_fixups=None) -> None:
         """Raw ts_replay_batch: outputs are caller-owned numpy (host) or torch
         (device or host) buffers; see include/lumos_b200.h for shapes."""
         sc = spec.to_c()
@@ -244,6 +244,10 @@ class DeviceGraph:
         r.util_n_bins = _ptr(util_n_bins, N.i32p)
         r.delta_abs_sum = _ptr(delta_abs_sum, N.i64p)
         r.delta_worst = _ptr(delta_worst, N.i64p)
+        # delta_worst: [count][worst_n][3] (a [count][3] buffer means worst_n = 1)
+        r.delta_worst_n = int(delta_worst.shape[1]) if (delta_worst is not None and
+                                                          len(delta_worst.shape) == 3) else 1
+        r.n_fixups = _ptr(n_fixups, N.i32p)
         s = C.c_void_p(stream) if isinstance(stream, int) else stream
         rc = N.lib().ts_replay_batch(self.h, C.byref(sc), C.byref(r), s)
         if rc != N.TS_OK:
@@ -285,7 +289,8 @@ class BatchResult:
     util_covered: Optional[np.ndarray] = None  # [count][n_ranks][max_bins] covered us
     util_n_bins: Optional[np.ndarray] = None   # [count] bins of each scenario's window
     delta_abs_sum: Optional[np.ndarray] = None  # [count] sum |sim_start - original_start|
-    delta_worst: Optional[np.ndarray] = None    # [count][3] {max |delta|, task, delta}
+    delta_worst: Optional[np.ndarray] = None    # [count][worst_n][3] {|delta|, task, delta}
+    n_fixups: int = 0                           # scenarios re-run by the event-driven path
 
     @property
     def makespan(self) -> np.ndarray:
@@ -297,8 +302,7 @@ class BatchResult:
         window = [window_start, max(window_end, window_start + makespan))."""
         w = self.util_bin_width
         end = max(window_end, window_start + int(self.span[s, 2]))
-        nb = int(self.util_n_bins[s])
-        nb_kept = min(nb, self.util_covered.shape[-1])
+        nb_kept = int(self.util_n_bins[s])
         spans = np.minimum(w, end - (window_start + w * np.arange(nb_kept, dtype=np.int64)))
         return self.util_covered[s, :, :nb_kept] / spans
 
@@ -333,17 +337,20 @@ class BatchResult:
         return "".join(out)
 
     def replay_report(self, s: int, n_tasks: int, reference_makespan: int) -> dict:
-        """compare_replay fields of scenario s (metrics.cpp:189-221), worst
-        list truncated to one entry."""
+        """compare_replay fields of scenario s (metrics.cpp:189-221); the worst
+        list has the batch's worst_n entries (largest |delta| first, ties by
+        task id)."""
+        if self.delta_abs_sum is None or self.delta_worst is None:
+            raise ValueError("replay_report needs a batch run with deltas=True")
         sim = int(self.span[s, 2])
         zero = reference_makespan == 0
+        w = self.delta_worst[s].reshape(-1, 3)
         return {"reference_makespan": reference_makespan, "simulated_makespan": sim,
                 "relative_error": 0.0 if zero else abs(sim - reference_makespan) / reference_makespan,
                 "zero_reference": zero,
                 "mean_abs_delta": 0.0 if n_tasks == 0 else float(self.delta_abs_sum[s]) / n_tasks,
-                "max_abs_delta": int(self.delta_worst[s, 0]),
-                "worst": [] if self.delta_worst[s, 1] < 0 else
-                [{"task": int(self.delta_worst[s, 1]), "delta": int(self.delta_worst[s, 2])}]}
+                "max_abs_delta": int(w[0, 0]),
+                "worst": [{"task": int(t), "delta": int(d)} for _, t, d in w.tolist() if t >= 0]}
 
 
 def simulate(graph, device: Optional[int] = None) -> SimulatedTrace:
@@ -354,11 +361,27 @@ def simulate(graph, device: Optional[int] = None) -> SimulatedTrace:
 
 def simulate_batch(graph, spec: ScenarioSpec, timestamps: bool = True, breakdown: bool = True,
                    device: Optional[int] = None, util_bin_width: int = 0,
-                   util_max_bins: int = 0, deltas: bool = False) -> BatchResult:
+                   util_max_bins: int = 0, deltas: bool = False,
+                   worst_n: int = 10) -> BatchResult:
     """Replay ``spec.count`` scenarios; results in host numpy arrays.
-    util_bin_width > 0 adds utilization_by_rank bins (util_max_bins per rank);
-    deltas adds the compare_replay start-delta statistics."""
+    util_bin_width > 0 adds utilization_by_rank bins (every bin of every
+    window; util_max_bins > 0 caps them and fails if a window needs more);
+    deltas adds the compare_replay statistics with a worst_n-entry worst list
+    (compare_replay's default 10, metrics.hpp:82-83)."""
     dg = graph if isinstance(graph, DeviceGraph) else DeviceGraph(graph, device)
+    if util_bin_width > 0 and util_max_bins <= 0:
+        # every bin: the graph's window, or the device tells how many it needs
+        w0 = max(1, -(-(dg.info["window_end"] - dg.info["window_start"]) // util_bin_width))
+        try:
+            return simulate_batch(dg, spec, timestamps, breakdown, device, util_bin_width, w0,
+                                  deltas, worst_n)
+        except ValueError as e:
+            import re
+            m = re.search(r"utilization needs (\d+) bins", str(e))
+            if not m:
+                raise
+            return simulate_batch(dg, spec, timestamps, breakdown, device, util_bin_width,
+                                  int(m.group(1)), deltas, worst_n)
     S = spec.count
     span = np.zeros((S, 3), np.int64)
     start = fin = bd = busy = util = nbins = dsum = dworst = None
@@ -373,10 +396,11 @@ def simulate_batch(graph, spec: ScenarioSpec, timestamps: bool = True, breakdown
         nbins = np.zeros(S, np.int32)
     if deltas:
         dsum = np.zeros(S, np.int64)
-        dworst = np.zeros((S, 3), np.int64)
+        dworst = np.zeros((S, max(1, worst_n), 3), np.int64)
+    nfix = np.zeros(1, np.int32)
     dg.replay_batch(spec, start=start, fin=fin, ld=S, span=span, rank_breakdown=bd,
                     stream_busy=busy, util_bin_width=util_bin_width, util_covered=util,
-                    util_n_bins=nbins, delta_abs_sum=dsum, delta_worst=dworst)
+                    util_n_bins=nbins, delta_abs_sum=dsum, delta_worst=dworst, n_fixups=nfix)
     return BatchResult(span=span, start=start, fin=fin, rank_breakdown=bd, stream_busy=busy,
                        util_bin_width=util_bin_width, util_covered=util, util_n_bins=nbins,
-                       delta_abs_sum=dsum, delta_worst=dworst)
+                       delta_abs_sum=dsum, delta_worst=dworst, n_fixups=int(nfix[0]))

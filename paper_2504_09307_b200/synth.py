@@ -253,6 +253,39 @@ def events_from_chrome(trace: dict, categories: Optional[dict] = None) -> dict:
     return out
 
 
+class TsIngestOptions(C.Structure):
+    _fields_ = [("paths", C.POINTER(C.c_char_p)), ("n_paths", C.c_int32),
+                ("n_threads", C.c_int32), ("manifest", C.c_char_p), ("window", C.c_char_p),
+                ("categories_path", C.c_char_p), ("policy_path", C.c_char_p)]
+
+
+def ingest_traces_ex(paths=(), manifest=None, window=None, categories_path=None,
+                     policy_path=None, threads: int = 0, names: bool = False) -> ExecutionGraph:
+    """ts_ingest_traces_ex: the reference's build_from_inputs with every input
+    option (cli.cpp:52-58, 118-137) — a rank manifest, the iteration window
+    ("full", "auto" or "START:END"), a custom category table and a build
+    policy (JSON file paths, like the CLI's --categories / --policy)."""
+    L = _lib()
+    if not getattr(L, "_ingest_ex_bound", False):
+        L.ts_ingest_traces_ex.restype = C.c_int
+        L.ts_ingest_traces_ex.argtypes = [C.POINTER(TsIngestOptions), C.POINTER(C.c_void_p)]
+        L._ingest_ex_bound = True
+    arr = (C.c_char_p * max(1, len(paths)))(*[str(p).encode() for p in paths])
+    enc = lambda x: None if x is None else str(x).encode()
+    o = TsIngestOptions(arr, len(paths), int(threads), enc(manifest), enc(window),
+                        enc(categories_path), enc(policy_path))
+    h = C.c_void_p()
+    rc = L.ts_ingest_traces_ex(C.byref(o), C.byref(h))
+    if rc != N.TS_OK:
+        from .replay import _raise
+        _raise(rc)
+    try:
+        g, _, _ = _from_host(h, names=names)
+    finally:
+        L.ts_host_graph_free(h)
+    return g
+
+
 def ingest_traces(paths, threads: int = 0, gap_threshold_us: int = 1000,
                   names: bool = False) -> ExecutionGraph:
     """Native parallel ingest of recorded Chrome traces (ts_ingest_traces): the

@@ -141,7 +141,8 @@ def ref():
         lib.ref_ingest_traces.argtypes = [C.POINTER(C.c_char_p), C.c_int]
         lib.ref_bench_simulate.restype = C.c_double
         lib.ref_bench_simulate.argtypes = [C.c_void_p, C.POINTER(OrcScenarios), C.c_int64,
-                                           C.c_int32, _u8p, C.c_int, _i64p]
+                                           C.c_int32, _u8p, C.c_int, _i64p,
+                                           C.POINTER(C.c_double)]
         _ref = lib
     return _ref
 
@@ -278,11 +279,16 @@ class RefGraphHandle:
             raise RefError(3, ref().ref_last_error().decode())
         return RefGraphHandle(p)
 
-    def bench_simulate(self, sc: OrcScenarios, first: int, count: int, cls, threads: int):
+    def bench_simulate(self, sc: OrcScenarios, first: int, count: int, cls, threads: int,
+                       with_fill: bool = False):
+        """Wall seconds of `count` reference simulate() calls on `threads` host
+        threads (durations pre-filled outside the clock) and the makespans;
+        with_fill adds the fill seconds."""
         mk = np.zeros(count, np.int64)
+        fill = C.c_double(0.0)
         secs = ref().ref_bench_simulate(self.h, C.byref(sc), first, count, _p(cls, _u8p), threads,
-                                        _p(mk, _i64p))
-        return secs, mk
+                                        _p(mk, _i64p), C.byref(fill))
+        return (secs, mk, fill.value) if with_fill else (secs, mk)
 
 
 class RefError(RuntimeError):
@@ -326,6 +332,22 @@ def ingest_traces(paths) -> "RefGraphHandle":
     h = ref().ref_ingest_traces(arr, len(paths))
     if not h:
         raise RefError(3, ref().ref_last_error().decode())
+    return RefGraphHandle(h)
+
+
+def ingest_traces_ex(paths, manifest=None, window=None, categories=None, policy=None):
+    """The reference's build_from_inputs (cli.cpp:118-137) with options; the
+    category table / policy are JSON texts."""
+    lib = ref()
+    lib.ref_ingest_traces_ex.restype = C.c_void_p
+    lib.ref_ingest_traces_ex.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_char_p,
+                                         C.c_char_p, C.c_char_p]
+    arr = (C.c_char_p * max(1, len(paths)))(*[p.encode() for p in paths])
+    enc = lambda x: None if x is None else x.encode()
+    h = lib.ref_ingest_traces_ex(arr, len(paths), enc(manifest), enc(window), enc(categories),
+                                 enc(policy))
+    if not h:
+        raise RefError(3, lib.ref_last_error().decode())
     return RefGraphHandle(h)
 
 

@@ -34,7 +34,7 @@ def _check_util(h, g, res, s, rs, rf, width):
 
 
 def _check_deltas(h, res, s, rs, rf, n):
-    rep = h.compare_replay(rs, rf, worst_n=1)
+    rep = h.compare_replay(rs, rf, worst_n=res.delta_worst.shape[1])
     mine = res.replay_report(s, n, rep["reference_makespan"])
     assert mine["max_abs_delta"] == rep["max_abs_delta"]
     assert mine["simulated_makespan"] == rep["simulated_makespan"]
@@ -73,13 +73,15 @@ def test_util_overlap_not_double_counted():
 def test_compare_replay_golden():
     # test_metrics.cpp:167-193: recorded t0 [0,10), t1 [30,40) lane A, t2 [5,25) lane B
     g = _graph([(0, 1, 0, 10), (0, 1, 30, 10), (0, 2, 5, 20)], edges=[(0, 1)], window=(0, 40))
-    res = simulate_batch(g, ScenarioSpec(count=1), deltas=True)
+    res = simulate_batch(g, ScenarioSpec(count=1), deltas=True, worst_n=2)
     rep = res.replay_report(0, g.n, 40)
     assert rep["simulated_makespan"] == 20
     assert rep["max_abs_delta"] == 20
     assert rep["mean_abs_delta"] == pytest.approx(25.0 / 3)
-    assert rep["worst"] == [{"task": 1, "delta": -20}]
+    assert rep["worst"] == [{"task": 1, "delta": -20}, {"task": 2, "delta": -5}]  # worst_n = 2
     assert rep["relative_error"] == pytest.approx(0.5)
+    full = simulate_batch(g, ScenarioSpec(count=1), deltas=True).replay_report(0, g.n, 40)
+    assert [w["task"] for w in full["worst"]] == [1, 2, 0]  # default 10: every task
 
 
 @pytest.mark.parametrize("width", [1_000, 7_777, 250_000])
@@ -98,9 +100,10 @@ def test_util_and_deltas_generator_jitter(width):
         _check_deltas(h, res, s, rs, rf, g.n)
 
 
-def test_util_generic_ranks_and_truncation():
-    # mixed streams send ranks 0/1 to the event merge; max_bins below the
-    # window's bin count keeps the first bins and reports the full count
+def test_util_generic_ranks_all_bins_or_loud_failure():
+    # mixed streams send ranks 0/1 to the event merge; a util_max_bins below a
+    # window's bin count fails loudly with the count it needs, and the default
+    # (util_max_bins=0) returns every bin of every window
     h0, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
     g = h0.export()
     kern = g.task_kind == 1
@@ -110,13 +113,34 @@ def test_util_generic_ranks_and_truncation():
     h = R.from_graph(g)
     S, width = 32, 3_000
     spec = ScenarioSpec(count=S, seed=8, jitter=0.25)
-    res = simulate_batch(g, spec, util_bin_width=width, util_max_bins=7, deltas=True)
+    with pytest.raises(ValueError, match=r"utilization needs \d+ bins per rank; util_max_bins is 7"):
+        simulate_batch(g, spec, util_bin_width=width, util_max_bins=7, deltas=True)
+    res = simulate_batch(g, spec, util_bin_width=width, deltas=True, worst_n=25)
+    assert res.util_covered.shape[-1] == res.util_n_bins.max() > 7
     sc = R.OrcScenarios(seed=8, jitter=0.25)
     for s in range(0, S, 5):
         rs, rf, _ = h.simulate(R.orc_durations(g, sc, s))
-        assert res.util_n_bins[s] > 7
         _check_util(h, g, res, s, rs, rf, width)
         _check_deltas(h, res, s, rs, rf, g.n)
+
+
+@pytest.mark.parametrize("worst_n", [1, 10, 64])
+def test_compare_replay_worst_list(worst_n):
+    # the device's worst list equals compare_replay's (metrics.cpp:213-217)
+    # for the reference default 10 and the bounds, ties broken by task id
+    # (a nominal replay of a generator graph has many equal |delta| = 0)
+    h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h.export()
+    spec = ScenarioSpec(count=12, first=3, seed=13, jitter=0.15)
+    res = simulate_batch(g, spec, deltas=True, worst_n=worst_n)
+    assert res.delta_worst.shape == (12, worst_n, 3)
+    sc = R.OrcScenarios(seed=13, jitter=0.15)
+    for s in range(0, 12, 4):
+        rs, rf, _ = h.simulate(R.orc_durations(g, sc, spec.first + s))
+        _check_deltas(h, res, s, rs, rf, g.n)
+    nominal = simulate_batch(g, ScenarioSpec(count=2), deltas=True, worst_n=worst_n)
+    rs, rf, _ = h.simulate()
+    _check_deltas(h, nominal, 0, rs, rf, g.n)
 
 
 def test_util_random_graphs_event_path():

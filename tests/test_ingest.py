@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import refshim as R
-from paper_2504_09307_b200.synth import ingest_traces
+from paper_2504_09307_b200.synth import ingest_traces, ingest_traces_ex
 
 FIELDS = ["duration", "original_start", "rank", "lane_kind", "lane", "op_class", "task_kind",
           "edge_from", "edge_to", "rule_kind", "rule_task", "rule_bound", "rule_watch_off",
@@ -97,5 +97,99 @@ def test_duplicate_rank_rejected(tmp_path):
     a = str(tmp_path / "rank_0.json")
     b = str(tmp_path / "copy_rank_0.json")
     os.link(a, b)
-    with pytest.raises(Exception, match="rank 0 appears in more than one input"):
+    # both files carry a rank_<N> marker: load_multirank's duplicate check
+    # (trace_parse.cpp:286-296) fires before load_inputs' take()
+    with pytest.raises(Exception, match="duplicate rank 0 from '.*copy_rank_0.json'"):
         ingest_traces([a, b])
+    with pytest.raises(Exception, match="duplicate rank 0 from"):
+        R.ingest_traces_ex([a, b])
+
+
+def _two_iterations(src, dst, shift):
+    """A rank trace holding two copies of its iteration `shift` us apart (new
+    correlation / event ids for the copy)."""
+    doc = json.load(open(src))
+    evs = doc["traceEvents"]
+    more = []
+    for e in evs:
+        c = dict(e)
+        c["ts"] = e["ts"] + shift
+        if "args" in e:
+            a = dict(e["args"])
+            for k in ("correlation", "event"):
+                if k in a:
+                    a[k] = int(a[k]) + 1_000_000
+            c["args"] = a
+        more.append(c)
+    # the second iteration gets a few extra host ops so it wins detect_iteration_window
+    main = [e for e in evs if e.get("cat") == "cpu_op" or e.get("cat") == "cuda_runtime"]
+    t_end = max(e["ts"] + e.get("dur", 0) for e in more)
+    for k in range(3):
+        more.append({"name": "extra_op", "cat": "cpu_op", "ph": "X", "ts": t_end + 10 * k + 1,
+                     "dur": 2, "pid": main[0]["pid"], "tid": main[0]["tid"]})
+    json.dump({"traceEvents": evs + more}, open(dst, "w"))
+
+
+@pytest.mark.parametrize("window", ["auto", "first", "second"])
+def test_ingest_window_options(tmp_path, window):
+    # --window auto picks the iteration with the most main-thread events
+    # (detect_iteration_window), START:END keeps events starting inside plus
+    # kernels of kept launches (filter_window)
+    src = tmp_path / "src"
+    src.mkdir()
+    R.write_rank_traces(R.synth_spec(pp=2, dp=1, m=4, layers=4), str(src))
+    paths = []
+    for p in sorted(glob.glob(str(src / "rank_*.json"))):
+        d = str(tmp_path / os.path.basename(p))
+        _two_iterations(p, d, 50_000_000)
+        paths.append(d)
+    w = {"auto": "auto", "first": "0:40000000", "second": "50000000:99000000"}[window]
+    h = R.ingest_traces_ex(paths, window=w)
+    g = ingest_traces_ex(paths, window=w, names=True)
+    _same(g, h)
+    full = ingest_traces_ex(paths, names=True)
+    assert g.n * 2 < full.n + 10
+
+
+def test_ingest_manifest_categories_policy(tmp_path):
+    # a manifest maps ranks to files without rank markers (relative paths), a
+    # custom category table renames the kernel category, a build policy moves
+    # the gap threshold and the communication patterns
+    src = tmp_path / "src"
+    src.mkdir()
+    R.write_rank_traces(R.synth_spec(pp=2, dp=2, m=4, layers=4), str(src))
+    man = {}
+    for p in sorted(glob.glob(str(src / "rank_*.json"))):
+        r = int(os.path.basename(p)[5:-5])
+        doc = json.load(open(p))
+        for e in doc["traceEvents"]:
+            if e.get("cat") == "kernel":
+                e["cat"] = "device_kernel"
+        name = f"trace_{r}.json"
+        json.dump(doc, open(tmp_path / name, "w"))
+        man[str(r)] = name
+    (tmp_path / "manifest.json").write_text(json.dumps(man))
+    cats = json.dumps({"device_kernel": "GpuKernel"})
+    policy = json.dumps({"gap_threshold_us": 20, "comm_patterns": ["nccl", "sendrecv"],
+                         "sync_names": {"cudaDeviceSynchronize": "device",
+                                        "cudaStreamSynchronize": "stream"}})
+    (tmp_path / "cats.json").write_text(cats)
+    (tmp_path / "policy.json").write_text(policy)
+    h = R.ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"), categories=cats,
+                           policy=policy)
+    g = ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"),
+                         categories_path=str(tmp_path / "cats.json"),
+                         policy_path=str(tmp_path / "policy.json"), threads=3, names=True)
+    _same(g, h)
+    assert (g.task_kind == 1).sum() > 0
+    # errors of the options follow the reference's ParseError texts
+    (tmp_path / "bad.json").write_text(json.dumps({"x": "Kernelish"}))
+    with pytest.raises(Exception, match="unknown category 'Kernelish'"):
+        ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"),
+                         categories_path=str(tmp_path / "bad.json"))
+    (tmp_path / "badp.json").write_text(json.dumps({"sync_names": {"a": "b"}}))
+    with pytest.raises(Exception, match="must be device.stream.event"):
+        ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"),
+                         policy_path=str(tmp_path / "badp.json"))
+    with pytest.raises(Exception, match="window must be 'full', 'auto' or START:END"):
+        ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"), window="last")
