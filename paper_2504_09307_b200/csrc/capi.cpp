@@ -289,6 +289,17 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   }
   g->n_single = static_cast<int32_t>(single.size());
   g->n_coop = static_cast<int32_t>(coop.size());
+#ifdef LUMOS_DEBUG_BOUNDS
+  // self-test of the bounds checks: LUMOS_DEBUG_CORRUPT=1 points one operand
+  // of the first plain node past the slot table; the next replay must fail
+  if (const char* bad = std::getenv("LUMOS_DEBUG_CORRUPT"))
+    if (bad[0] == '1')
+      for (Op& o : c.ops)
+        if (o.kind == OP_NODE && !(o.flags & (F_TRACK | F_TRACK1))) {
+          o.pred[0] = slot_off(kMaxSlots);
+          break;
+        }
+#endif
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&g->d_ops, c.ops);
   if (e == cudaSuccess) e = upload(&g->d_progs, c.programs);
@@ -948,6 +959,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     wp.comp_order = g->d_comp_order;
     wp.n_comps = g->n_single;
     wp.force_ks = force_ks;
+    wp.n_tasks = c.n_tasks;
     wp.window_start = c.window_start;
     wp.sp = sp;
     wp.sp.first = sp.first + b0;
@@ -1110,6 +1122,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       rp.count = bn;
       rp.n_ranks = n_ranks;
       rp.n_streams = n_streams;
+      rp.n_tasks_total = c.n_tasks;
       rp.breakdown = d_bd ? d_bd + static_cast<size_t>(b0) * n_ranks * 5 : nullptr;
       rp.stream_busy = d_busy ? d_busy + static_cast<size_t>(b0) * n_streams : nullptr;
       rp.util = d_util ? d_util + static_cast<size_t>(b0) * n_ranks * ubins : nullptr;
@@ -1193,6 +1206,13 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       std::memcpy(out->status, host_status.data(), static_cast<size_t>(count) * 4);
   }
   if (prev_dev >= 0 && prev_dev != g->device) cudaSetDevice(prev_dev);
+#ifdef LUMOS_DEBUG_BOUNDS
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (int line = debug_bounds_status())
+    return fail(TS_E_CUDA, "bounds check failed (replay.cu line " + std::to_string(line) + ")");
+  if (int line = debug_bounds_status_des())
+    return fail(TS_E_CUDA, "bounds check failed (des.cu line " + std::to_string(line) + ")");
+#endif
   if (out->n_fixups) {
     int32_t nf = 0;
     for (int32_t st : host_status) nf += st > 0;

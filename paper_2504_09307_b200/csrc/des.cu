@@ -145,7 +145,8 @@ struct Des {
   }
   __device__ void complete(int32_t t) {
     for (int32_t k = P.succ_off[t]; k < P.succ_off[t + 1]; ++k) {
-      const int32_t v = P.succ[k];
+      int32_t v = P.succ[k];
+      if (!LUMOS_OK(v >= 0 && v < P.n)) v = 0;
       if (--s.indeg[v] == 0) ready_push(P.lane_of[v], v);
     }
   }
@@ -279,6 +280,7 @@ __global__ void des_kernel(DesParams P) {
           if (a >= b) continue;
           busy += b - a;
           const int64_t c = P.is_comm[t] ? 2 : 0;  // 0 compute, 2 comm; +1 = end
+          if (!LUMOS_OK(ne + 2 <= 2 * n)) break;
           s.ev[ne++] = ((a - W) << 2) | c;
           s.ev[ne++] = ((b - W) << 2) | (c + 1);
         }
@@ -325,6 +327,17 @@ __global__ void des_kernel(DesParams P) {
 }
 
 }  // namespace
+
+#ifdef LUMOS_DEBUG_BOUNDS
+int debug_bounds_status_des() {
+  int v = 0, zero = 0;
+  if (cudaMemcpyFromSymbol(&v, lumos_bounds_fail, sizeof(int)) != cudaSuccess) return -1;
+  cudaMemcpyToSymbol(lumos_bounds_fail, &zero, sizeof(int));
+  return v;
+}
+#else
+int debug_bounds_status_des() { return 0; }
+#endif
 
 size_t des_scratch_bytes(int32_t n, int32_t nl) {
   const size_t b = (static_cast<size_t>(n) * 3 + nl + 2 * static_cast<size_t>(n)) * 8 +

@@ -5,12 +5,33 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "kernels.hpp"
 #include "lumos_b200.h"
 #include "program.hpp"
 
 namespace lumos {
+
+// Debug builds (-DLUMOS_DEBUG_BOUNDS, `make debug`) check every slot,
+// mailbox, ring and output index the kernels compute; a failed check records
+// the source line in lumos_bounds_fail (read and cleared by the C ABI after
+// each call, which then fails the call), prints once, and redirects the
+// access to a safe location instead of faulting.  compute-sanitizer is closed
+// on this pool; these checks are the memory-safety evidence.
+#ifdef LUMOS_DEBUG_BOUNDS
+static __device__ int lumos_bounds_fail = 0;  // one per translation unit
+#define LUMOS_OK(cond)                                                              \
+  ((cond) ? true                                                                    \
+          : (atomicCAS(&lumos_bounds_fail, 0, __LINE__) == 0                        \
+                 ? (printf("lumos bounds check failed: %s:%d (%s)\n", __FILE__, __LINE__, \
+                           #cond),                                                  \
+                    false)                                                          \
+                 : false))
+#else
+#define LUMOS_OK(cond) true
+#endif
+
 namespace {
 
 constexpr int64_t kMinI64 = INT64_MIN;

@@ -88,8 +88,12 @@ struct WalkParams {
   const FusedDesc* fused;  // [component]
   int64_t* acct_a;         // [count][n_ranks]
   int32_t n_ranks;
-  int32_t pad2;
+  int32_t n_tasks;         // rows of out_start / out_fin (bounds checks)
 };
+// debug builds: the source line of the first failed bounds check since the
+// last call (0 = none), cleared by the read; always 0 in release builds
+int debug_bounds_status();
+int debug_bounds_status_des();
 
 
 
@@ -109,7 +113,7 @@ struct ReduceParams {
   int32_t count;
   int32_t n_ranks;
   int32_t n_streams;
-  int32_t pad;
+  int32_t n_tasks_total;  // rows of start / fin (bounds checks)
   int64_t* breakdown;    // [count][n_ranks][5]
   int64_t* stream_busy;  // [count][n_streams]
   int64_t* util;         // [count][n_ranks][util_max_bins] (zeroed), or null

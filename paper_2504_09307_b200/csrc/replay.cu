@@ -150,10 +150,23 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
                                        static_cast<uint32_t>(v))
                 : static_cast<int64_t>(v);
   };
+#ifdef LUMOS_DEBUG_BOUNDS
+  // every slot offset must address one of the program's slots
+  const uint32_t slot_limit = static_cast<uint32_t>(pd.n_slots < kFirstSlot ? kFirstSlot : pd.n_slots) *
+                              kT * static_cast<uint32_t>(sizeof(VP));
+  auto slot_chk = [&](uint32_t boff) -> uint32_t {
+    return LUMOS_OK(boff < slot_limit && boff % (kT * sizeof(VP)) == 0) ? boff : 0u;
+  };
+#define SLOT2(off) \
+  (*reinterpret_cast<VP*>(slot_base + slot_chk(static_cast<uint32_t>(off) << kShift)))
+#define SLOTB(boff) \
+  (*static_cast<VP*>(__builtin_assume_aligned(slot_base + slot_chk(static_cast<uint32_t>(boff)), sizeof(VP))))
+#else
 #define SLOT2(off) \
   (*reinterpret_cast<VP*>(slot_base + (static_cast<uint32_t>(off) << kShift)))
 #define SLOTB(boff) \
   (*static_cast<VP*>(__builtin_assume_aligned(slot_base + static_cast<uint32_t>(boff), sizeof(VP))))
+#endif
   SLOT2(slot_off(kSlotOrigin)) = splat<V, kS>(w0);
   SLOT2(slot_off(kSlotInf)) = splat<V, kS>(kInfV);
 
@@ -260,6 +273,9 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
       for (int s = 0; s < kS; ++s) hi[s] = imax(hi[s], absv(fin.v[s]));
     }
     const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
+    if (!LUMOS_OK(task >= 0 && task < P.n_tasks && col[kS - 1] < static_cast<int>(ld) &&
+                  col[0] >= 0))
+      return fin;  // debug builds: an out-of-range row is not written
     if (vec_store) {
       const uint64_t at8 = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld8;
       if (kWriteStart)
@@ -520,8 +536,17 @@ __global__ void __launch_bounds__(1024) coop_walk_kernel(WalkParams P, CoopParam
   const int pfirst = C.prog_off[comp], nw = C.prog_off[comp + 1] - pfirst;
   if (w >= nw) return;  // no block-wide barrier after this point
   char* slot_base = slots + static_cast<size_t>(w) * C.n_slots * 32 * sizeof(V) + lane * sizeof(V);
+#ifdef LUMOS_DEBUG_BOUNDS
+  const uint32_t slotc_limit = static_cast<uint32_t>(C.n_slots) * 32u * sizeof(V);
+  auto slotc_chk = [&](uint32_t field) -> uint32_t {
+    const uint32_t b = field << kShiftC;
+    return LUMOS_OK(b < slotc_limit) ? b : 0u;
+  };
+#define SLOTC(field) (*reinterpret_cast<V*>(slot_base + slotc_chk(static_cast<uint32_t>(field))))
+#else
 #define SLOTC(field) \
   (*reinterpret_cast<V*>(slot_base + (static_cast<uint32_t>(field) << kShiftC)))
+#endif
   const ComponentDesc cd = P.comps[comp];
   const ProgramDesc pd = P.progs[C.progs[pfirst + w]];
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
@@ -554,7 +579,8 @@ __global__ void __launch_bounds__(1024) coop_walk_kernel(WalkParams P, CoopParam
     const V p0 = SLOTC(lo16(w0f)), p1 = SLOTC(hi16(w0f));
     const V p2 = SLOTC(lo16(w1f)), p3 = SLOTC(hi16(w1f));
     if (kind == OP_POST || kind == OP_WAIT) {
-      const int m = static_cast<int>(lo16(w3f));  // x1: mailbox id
+      int m = static_cast<int>(lo16(w3f));  // x1: mailbox id
+      if (!LUMOS_OK(m < C.n_mail)) m = 0;
       volatile V* box = mail + static_cast<size_t>(m) * 32 + lane;
       if (kind == OP_POST) {
         *box = p0;
@@ -651,8 +677,10 @@ __global__ void __launch_bounds__(1024) coop_walk_kernel(WalkParams P, CoopParam
       if (flags_op & F_STORE_START) SLOTC(hi16(w3f)) = st;
       if (flags_op & F_SINK) hi = imax(hi, absv(fin));
       const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
-      if (P.out_start) __stcs(start_c + at, absv(st));
-      if (P.out_fin) __stcs(fin_c + at, absv(fin));
+      if (LUMOS_OK(task >= 0 && task < P.n_tasks && col < static_cast<int>(ld))) {
+        if (P.out_start) __stcs(start_c + at, absv(st));
+        if (P.out_fin) __stcs(fin_c + at, absv(fin));
+      }
     }
     if (flags_op & F_TRACK1) {
       const V cs = SLOTC(hi16(w2f));
@@ -830,7 +858,8 @@ __device__ __forceinline__ void rank_reduce_merge(const ReduceParams& P, int col
     for (int q = 0; q < H; ++q)
       if (q < n) {
         const int e = nodes[base + q];
-        const int node = e & 0x7FFFFFFF;
+        int node = e & 0x7FFFFFFF;
+        if (!LUMOS_OK(node < P.n_tasks_total)) node = 0;
         bits |= static_cast<uint32_t>(e < 0) << q;
         const int64_t off = static_cast<int64_t>(node) * ld + col;
         cp_async8(&RING(j, h, q, 0), S + off);
@@ -993,6 +1022,7 @@ __global__ void __launch_bounds__(kThreads) rank_reduce_kernel(ReduceParams P) {
 template <int H, typename T>
 struct Cursor {
   int next, end, half, pos, avail, pend;
+  int n_tasks_total;  // bounds checks
   int64_t* ring;  // [2 halves][H][2][kThreads] + tid
   __device__ __forceinline__ int64_t& at(int h, int q, int k) {
     return ring[((h * H + q) * 2 + k) * kThreads];
@@ -1006,7 +1036,8 @@ struct Cursor {
 #pragma unroll
     for (int q = 0; q < H; ++q)
       if (q < n) {
-        const int node = nodes[base + q] & 0x7FFFFFFF;
+        int node = nodes[base + q] & 0x7FFFFFFF;
+        if (!LUMOS_OK(node < n_tasks_total)) node = 0;
         const int64_t off = static_cast<int64_t>(node) * ld + col;
         cp_async8(&at(h, q, 0), S + off);
         cp_async8(&at(h, q, 1), F + off);
@@ -1016,7 +1047,9 @@ struct Cursor {
     pend = n;
   }
   __device__ __forceinline__ void init(int b, int e, int64_t* rb, const int* nodes,
-                                       const int64_t* S, const int64_t* F, int64_t ld, int col) {
+                                       const int64_t* S, const int64_t* F, int64_t ld, int col,
+                                       int n_tasks = INT32_MAX) {
+    n_tasks_total = n_tasks;
     next = b;
     end = e;
     half = 1;
@@ -1083,10 +1116,11 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
   };
   Cursor<kFastHA, T> A;
   if (kLite)
-    A.init(P.cand_off[r], P.cand_off[r + 1], ring + tid, P.cand_nodes, S, F, ld, col);
+    A.init(P.cand_off[r], P.cand_off[r + 1], ring + tid, P.cand_nodes, S, F, ld, col,
+           P.n_tasks_total);
   else
     A.init(P.stream_node_off[s0 + ci], P.stream_node_off[s0 + ci + 1], ring + tid, nodes, S, F,
-           ld, col);
+           ld, col, P.n_tasks_total);
   const int* __restrict__ anodes = kLite ? P.cand_nodes : nodes;
   Cursor<kFastHC, T> C[NC > 0 ? NC : 1];
   T cs[NC > 0 ? NC : 1], ce[NC > 0 ? NC : 1];
@@ -1096,7 +1130,7 @@ __device__ __forceinline__ void rank_reduce_fast_body(const ReduceParams& P, int
     const int s = s0 + j + (ci != kNoA && j >= ci ? 1 : 0);
     C[j].init(P.stream_node_off[s], P.stream_node_off[s + 1],
               ring + (2 * kFastHA * 2 + j * 2 * kFastHC * 2) * kThreads + tid, nodes, S, F, ld,
-              col);
+              col, P.n_tasks_total);
     cbusy[j] = 0;
   }
 #pragma unroll
@@ -1324,6 +1358,18 @@ cudaError_t launch_util_nbins(const int64_t* lo, const int64_t* hi, int64_t W, i
   return cudaGetLastError();
 }
 int walk_threads() { return kThreads; }
+
+#ifdef LUMOS_DEBUG_BOUNDS
+int debug_bounds_status() {
+  int v = 0, zero = 0;
+  if (cudaMemcpyFromSymbol(&v, lumos_bounds_fail, sizeof(int)) != cudaSuccess) return -1;
+  cudaMemcpyToSymbol(lumos_bounds_fail, &zero, sizeof(int));
+  return v;
+}
+#else
+int debug_bounds_status() { return 0; }
+#endif
+// (des.cu keeps its own flag: debug_bounds_status_des)
 
 template <int kT, int kMode, bool kWS, bool kWF, typename V, int kS>
 static cudaError_t launch_walk_t(const WalkParams& p, size_t smem, unsigned blocks,
