@@ -1403,6 +1403,13 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     out.comps[c] = ComponentDesc{prog, node_base, static_cast<int32_t>(comp_tasks.size()), 0};
   }
   out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
+  if (std::getenv("LUMOS_DEBUG_OPS")) {  // op mix of the programs (debug only)
+    std::map<std::pair<int, int>, int64_t> mix;
+    for (const Op& o : out.ops) mix[{o.kind, o.flags & (F_TRACK | F_TRACK1 | F_STORE_START)}]++;
+    for (const auto& [k, v] : mix)
+      fprintf(stderr, "[ops] kind %d flags %02x: %lld\n", k.first, k.second,
+              static_cast<long long>(v));
+  }
   out.cand_off.assign(1, 0);
   out.cand_nodes.clear();
   for (const auto& list : cand_of_row) {
