@@ -205,10 +205,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   // A task's finish: its scenario durations (K4, fused), the busy / sink
   // bookkeeping and the start / finish row stores.  rec = the op's record index
   // in the program (retime walks look up their F_RT table through it).
-  // pre: the scenario pair's jitter words (pw0, pw1) were computed ahead
   auto finish_task = [&](const VP& st, const VP& fb, const int4& ra, uint32_t cls_b,
-                         uint32_t flags, int64_t rec, bool pre = false, uint32_t pw0 = 0,
-                         uint32_t pw1 = 0) -> VP {
+                         uint32_t flags, int64_t rec) -> VP {
     const int64_t task = static_cast<int64_t>(cd.node_base) + ra.z;
     const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ra.y)) << 32) |
                          static_cast<uint32_t>(ra.x);
@@ -245,8 +243,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
 #pragma unroll
         for (int s = 0; s < kS; ++s) dsc[s] = kRt ? bs[s] : base;
       }
-      uint32_t w[kS] = {pw0, pw1};
-      if (!pre && (kRt || (kDurMode & kModeScale) || base != 0))
+      uint32_t w[kS] = {0u, 0u};
+      if (kRt || (kDurMode & kModeScale) || base != 0)
         jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
 #pragma unroll
       for (int s = 0; s < kS; ++s)
@@ -327,17 +325,6 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
     }
     const int4* buf = opbuf + (c & 1) * 4 * kChunk;
     const int cnt = min(kChunk, n_ops - c * kChunk);
-    // jitter words of the pair for record `pw_rec` of this chunk, computed one
-    // record ahead inside the fast path: Philox depends only on (task,
-    // scenario pair), so its 20-instruction dependent chain overlaps the
-    // current op's max / rounding / stores instead of following them
-#ifdef LUMOS_NO_PREPHILOX
-    constexpr bool kPrePhilox = false;
-#else
-    constexpr bool kPrePhilox = kS == 2 && !kRt && kDurMode >= 0 && (kDurMode & kModeJitter) != 0;
-#endif
-    int pw_rec = -1;
-    uint32_t pw0 = 0, pw1 = 0;
     for (int i = 0; i < cnt; ++i) {
       const int4 ra = buf[4 * i];
       const int4 oa = buf[4 * i + 2], ob = buf[4 * i + 3];
@@ -348,21 +335,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
       if ((hdr & kFastMask) == OP_NODE) {
         const VP q0 = SLOTB(oa.x), q1 = SLOTB(oa.y), q2 = SLOTB(oa.z), q3 = SLOTB(oa.w);
         const VP st = maxp(maxp(q0, q1), maxp(q2, q3));
-        uint32_t nw0 = 0, nw1 = 0;
-        if constexpr (kPrePhilox) {
-          if (i + 1 < cnt) {
-            const int64_t ntask = static_cast<int64_t>(cd.node_base) + buf[4 * (i + 1)].z;
-            jitter_words2(P.sp, ntask, ts[0].scen, ts[kS - 1].scen, nw0, nw1);
-          }
-        }
         SLOTB(ob.x) = finish_task(st, st, ra, (hdr >> 16) & 0xFFu, hdr >> 24,
-                                  pd.op_offset + c * kChunk + i, kPrePhilox && pw_rec == i, pw0,
-                                  pw1);
-        if constexpr (kPrePhilox) {
-          pw0 = nw0;
-          pw1 = nw1;
-          pw_rec = i + 1;
-        }
+                                  pd.op_offset + c * kChunk + i);
         if (hdr & (static_cast<uint32_t>(F_TRACK1) << 24)) {
           // compact coverage (every kernel on a stream a sync watches): the
           // source slot outlives this op's results (compile.cpp)
