@@ -1409,6 +1409,8 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     for (const auto& [k, v] : mix)
       fprintf(stderr, "[ops] kind %d flags %02x: %lld\n", k.first, k.second,
               static_cast<long long>(v));
+    fprintf(stderr, "[ops] max_slots %d max_mailboxes %d max_coop_ranks %d\n", out.max_slots,
+            out.max_mailboxes, out.max_coop_ranks);
   }
   out.cand_off.assign(1, 0);
   out.cand_nodes.clear();

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <type_traits>
 #include <cstdint>
 
 #include "device_common.cuh"
@@ -524,8 +525,15 @@ __global__ void __launch_bounds__(kT, 6 * 128 / kT) replay_walk_rt_kernel(WalkPa
 // own [slot][32] table, cross-rank values in [mailbox][32] with a ready flag.
 // A wait that spins ~1 s marks the scenario failed (status -2) rather than
 // hang; it cannot happen for a correctly compiled component.
-template <int kMode, typename V>
-__global__ void __launch_bounds__(1024) coop_walk_kernel(WalkParams P, CoopParams C) {
+// kMaxW: warps per CTA the instantiation allows; components of <= 16 ranks
+// take the 512-thread variant, whose register cap fits LUMOS_COOP_MINB CTAs
+// per SM (the mailbox / slot shared memory of config 3 fits three)
+#ifndef LUMOS_COOP_MINB
+#define LUMOS_COOP_MINB 3
+#endif
+template <int kMode, typename V, int kMaxW>
+__global__ void __launch_bounds__(32 * kMaxW, kMaxW <= 16 ? LUMOS_COOP_MINB : 1)
+    coop_walk_kernel(WalkParams P, CoopParams C) {
   constexpr bool kRel = sizeof(V) == 4;
   constexpr int kShiftC = kRel ? 0 : 1;  // record field s*128 -> s*32*sizeof(V)
   constexpr V kInfV = kRel ? static_cast<V>(0xFFFFFFFFu) : static_cast<V>(kMaxI64);
@@ -1514,13 +1522,18 @@ static cudaError_t launch_coop_v(const WalkParams& p, const CoopParams& c, cudaS
     kern<<<static_cast<unsigned>(blocks), threads, smem, stream>>>(p, c);
     return cudaGetLastError();
   };
-  switch (p.sp.mode) {
-    case 0: return go(coop_walk_kernel<0, V>);
-    case kModeScale: return go(coop_walk_kernel<kModeScale, V>);
-    case kModeJitter: return go(coop_walk_kernel<kModeJitter, V>);
-    case kModeScale | kModeJitter: return go(coop_walk_kernel<kModeScale | kModeJitter, V>);
-    default: return go(coop_walk_kernel<kModeExplicit, V>);
-  }
+  auto by_mode = [&](auto tag) -> cudaError_t {
+    constexpr int W = decltype(tag)::value;
+    switch (p.sp.mode) {
+      case 0: return go(coop_walk_kernel<0, V, W>);
+      case kModeScale: return go(coop_walk_kernel<kModeScale, V, W>);
+      case kModeJitter: return go(coop_walk_kernel<kModeJitter, V, W>);
+      case kModeScale | kModeJitter: return go(coop_walk_kernel<kModeScale | kModeJitter, V, W>);
+      default: return go(coop_walk_kernel<kModeExplicit, V, W>);
+    }
+  };
+  if (c.max_ranks <= 16) return by_mode(std::integral_constant<int, 16>{});
+  return by_mode(std::integral_constant<int, 32>{});
 }
 
 cudaError_t launch_coop_walk(const WalkParams& p, const CoopParams& c, cudaStream_t stream) {
