@@ -141,6 +141,7 @@ struct ts_graph {
   // K5 rank lists restricted to the other ranks
   FusedDesc* d_fused = nullptr;
   int32_t n_fused_rows = 0;
+  int32_t* d_coop_rows = nullptr;  // per cooperative rank program: its fused row or -1
   int32_t* d_cand_off = nullptr;
   int32_t* d_cand_nodes = nullptr;
   int32_t* d_rank_lists_nf = nullptr;  // non-fused ranks by bucket, then fused ranks (lite)
@@ -370,7 +371,7 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     std::vector<int> fused_bucket(n_ranks, -1);
     std::vector<int32_t> fused_entry(n_ranks, 0);
     if (!c.des_only)
-      for (const FusedDesc& fd : c.fused) {
+      for (const FusedDesc& fd : c.fused_rows) {
         if (fd.row < 0 || fused_bucket[fd.row] >= 0) continue;
         const int s0 = c.rank_stream_off[fd.row], ns = c.rank_stream_off[fd.row + 1] - s0;
         const int ci = fd.stream_a >= 0 ? fd.stream_a - s0 : 0xFF;
@@ -391,6 +392,7 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
     if (e == cudaSuccess) e = upload(&g->d_rank_lists_nf, lists_nf);
     if (g->n_fused_rows > 0) {
       if (e == cudaSuccess) e = upload(&g->d_fused, c.fused);
+      if (e == cudaSuccess) e = upload(&g->d_coop_rows, c.coop_rows);
       if (e == cudaSuccess) e = upload(&g->d_cand_off, c.cand_off);
       if (e == cudaSuccess) e = upload(&g->d_cand_nodes, c.cand_nodes);
     }
@@ -440,6 +442,7 @@ void ts_graph_destroy(ts_graph* g) {
                     static_cast<void*>(g->d_stream_node_off),
                     static_cast<void*>(g->d_stream_nodes), static_cast<void*>(g->d_rank_lists),
                     static_cast<void*>(g->d_fused), static_cast<void*>(g->d_cand_off),
+                    static_cast<void*>(g->d_coop_rows),
                     static_cast<void*>(g->d_cand_nodes), static_cast<void*>(g->d_rank_lists_nf),
                     static_cast<void*>(g->d_ostart), static_cast<void*>(g->d_lane_of),
                     static_cast<void*>(g->d_lane_off), static_cast<void*>(g->d_lane_tasks),
@@ -483,7 +486,8 @@ int ts_graph_get_info(const ts_graph* g, ts_graph_info* out) {
   out->n_gpu_tasks = c.n_gpu_tasks;
   out->window_start = c.window_start;
   out->window_end = c.window_end;
-  out->n_fused_ranks = g->has_device ? g->n_fused_rows : (c.des_only ? 0 : c.n_fused);
+  out->n_fused_ranks = g->has_device ? g->n_fused_rows
+                                     : (c.des_only ? 0 : static_cast<int32_t>(c.fused_rows.size()));
   out->des_only = c.des_only ? 1 : 0;
   out->n_candidates = c.cand_nodes.size();
   return TS_OK;
@@ -1030,6 +1034,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       cp.n_mail = c.max_mailboxes;
       cp.n_slots = c.max_slots;
       cp.rel32 = coop_rel32 ? 1 : 0;
+      cp.rows = acct ? g->d_coop_rows : nullptr;
       {
         Timed tm(g, stream, 0);
         CUDA_TRY(launch_coop_walk(cw, cp, stream));
@@ -1132,7 +1137,9 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
         rp.cand_off = g->d_cand_off;
         rp.cand_nodes = g->d_cand_nodes;
         rp.acct_a = g->acct_a.as<int64_t>();
-        rp.status = status + b0;
+        // scenarios the event-driven fix-up replayed were reduced by it; a
+        // cooperative walk's int64 re-run (no syncs: no fix-up) rewrote |A|
+        rp.status = c.n_syncs > 0 ? status + b0 : nullptr;
       }
       const int32_t* boff = acct ? g->bucket_off_nf : g->bucket_off;
       int32_t* lists = acct ? g->d_rank_lists_nf : g->d_rank_lists;

@@ -602,6 +602,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   out.comps.resize(n_comp);
   out.fused.assign(n_comp, FusedDesc{-1, -1});
   out.n_fused = 0;
+  out.fused_rows.clear();
 
   // ---- split breakdown accounting (program.hpp FusedDesc).  Rank rows
   // (ranks_in order, build.cpp:582-590) and stream slots (stream lanes in lane
@@ -637,39 +638,45 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   const bool fuse_enabled = !(fuse_env && fuse_env[0] == '0');
   std::vector<std::vector<int32_t>> cand_of_row(rank_ids.size());
   std::vector<int32_t> fz_anc, fz_desc;  // per task: last compute ancestor / first descendant (A chain)
-  // Marks component c (one whole rank, single program) for split accounting:
-  // F_BUSY on its compute-stream kernels and the candidate list; false when it
-  // does not qualify (K5 sweeps all of its timestamps then).
-  auto fuse_accounting = [&](int32_t c, std::vector<IrOp>& ir) -> bool {
-    if (!fuse_enabled || comp_tasks.empty()) return false;
-    const int32_t r = d.rank[comp_tasks[0]];
-    for (int32_t t : comp_tasks)
-      if (d.rank[t] != r || split[t] || gate_slot.count(t)) return false;
-    const int32_t row = static_cast<int32_t>(
-        std::lower_bound(rank_ids.begin(), rank_ids.end(), r) - rank_ids.begin());
-    if (rank_count[row] != static_cast<int32_t>(comp_tasks.size())) return false;
-    int32_t lane_a = -1;
-    std::vector<int32_t> comm_lanes;
-    {
-      auto lo = std::lower_bound(lanes.begin(), lanes.end(), Proc{r, TS_LANE_CUDA_STREAM, INT32_MIN});
-      for (auto it = lo; it != lanes.end() && it->rank == r && it->kind == TS_LANE_CUDA_STREAM; ++it) {
-        const int32_t l = static_cast<int32_t>(it - lanes.begin());
-        if (lane_class[l] == 0 && lane_a < 0) lane_a = l;
-        else if (lane_class[l] == 1) comm_lanes.push_back(l);
-        else return false;
-      }
-    }
-    if (static_cast<int>(comm_lanes.size()) > kFusedMaxComm) return false;
-    // DAG comparability with the A chain over the timing edges (fixed edges,
-    // event-sync bound, static sync bindings — a failed sync certificate sends
-    // the whole scenario to the event-driven path, which reduces it itself).
-    // The component's op order is topological for these edges.
+  std::vector<char> fz_pos;              // scratch: task seen
+  // Split accounting of component c: for every rank of the component whose
+  // tasks all lie in it and whose GPU streams are <= 1 compute-only and <= 3
+  // comm-only streams, F_BUSY on its compute-stream kernels and its candidate
+  // list.  Returns the descriptor per rank of the component (ascending rank;
+  // row -1: not fused, K5 sweeps all of its timestamps).  A single-program
+  // walk holds one |A| register, so it fuses only one-rank components
+  // (multi = false); the cooperative walk holds one per warp = rank.
+  auto fuse_accounting = [&](std::vector<IrOp>& ir, bool multi) -> std::vector<FusedDesc> {
+    std::vector<int32_t> ranks_here;
+    for (int32_t t : comp_tasks) ranks_here.push_back(d.rank[t]);
+    std::sort(ranks_here.begin(), ranks_here.end());
+    ranks_here.erase(std::unique(ranks_here.begin(), ranks_here.end()), ranks_here.end());
+    std::vector<FusedDesc> res(ranks_here.size(), FusedDesc{-1, -1});
+    if (!fuse_enabled || comp_tasks.empty() || (!multi && ranks_here.size() != 1)) return res;
+    // tasks in op order (topological for every timing edge); a split task
+    // (OP_START ... OP_FINISH) is placed at its start
     std::vector<int32_t> topo_tasks;
-    for (const IrOp& o : ir)
-      if (!o.aux() && o.v_dst >= 0 && o.v_dst < n &&
-          (o.op.kind == OP_NODE || o.op.kind == OP_SYNC))
-        topo_tasks.push_back(static_cast<int32_t>(o.v_dst));
-    if (topo_tasks.size() != comp_tasks.size()) return false;
+    std::vector<char> seen_t;
+    for (const IrOp& o : ir) {
+      if (o.aux() || o.v_dst < 0) continue;
+      int64_t t = -1;
+      if (o.v_dst < n && (o.op.kind == OP_NODE || o.op.kind == OP_SYNC ||
+                          o.op.kind == OP_GATED || o.op.kind == OP_FINISH))
+        t = o.v_dst;
+      else if (o.op.kind == OP_START && o.v_dst >= V_START && o.v_dst < V_START + n)
+        t = o.v_dst - V_START;
+      if (t < 0) continue;
+      if (fz_pos.size() != static_cast<size_t>(n)) fz_pos.assign(n, 0);
+      if (fz_pos[t]) continue;
+      fz_pos[t] = 1;
+      topo_tasks.push_back(static_cast<int32_t>(t));
+    }
+    for (int32_t t : topo_tasks) fz_pos[t] = 0;
+    if (topo_tasks.size() != comp_tasks.size()) return res;
+    // timing predecessors: fixed edges, event-sync bound, static sync bindings
+    // (a failed sync certificate sends the scenario to the event-driven path,
+    // which reduces it itself).  Gates relate finishes only, so they are left
+    // out: fewer comparabilities, more candidates, never a missed overlap.
     auto each_pred = [&](int32_t t, auto&& f) {
       for (int64_t k = pred.begin(t); k < pred.end(t); ++k) f(pred.idx[k]);
       if (event_bound[t] >= 0) f(event_bound[t]);
@@ -677,41 +684,60 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         for (const auto& ce : sync_cert[sync_id[t]])
           if (ce.kstar >= 0) f(ce.kstar);
     };
-    const int32_t len_a = lane_a < 0 ? 0 : lane_off[lane_a + 1] - lane_off[lane_a];
-    auto apos = [&](int32_t t) { return lane_of[t] == lane_a ? chain_pos[t] : -1; };
     if (fz_anc.empty()) {
       fz_anc.assign(n, -1);
       fz_desc.assign(n, INT32_MAX);
     }
-    for (int32_t t : topo_tasks)
-      each_pred(t, [&](int32_t p) { fz_anc[t] = std::max({fz_anc[t], fz_anc[p], apos(p)}); });
-    for (size_t q = topo_tasks.size(); q-- > 0;) {
-      const int32_t t = topo_tasks[q];
-      const int32_t at = apos(t) < 0 ? INT32_MAX : apos(t);
-      each_pred(t, [&](int32_t p) { fz_desc[p] = std::min({fz_desc[p], fz_desc[t], at}); });
-    }
-    // candidates: A positions in (anc(c), desc(c)) for some comm kernel c
-    std::vector<char> cand(static_cast<size_t>(len_a), 0);
-    for (int32_t l : comm_lanes)
-      for (int32_t q = lane_off[l]; q < lane_off[l + 1]; ++q) {
-        const int32_t cm = lane_tasks[q];
-        for (int32_t k = fz_anc[cm] + 1; k < std::min(fz_desc[cm], len_a); ++k) cand[k] = 1;
+    for (size_t k = 0; k < ranks_here.size(); ++k) {
+      const int32_t r = ranks_here[k];
+      const int32_t row = static_cast<int32_t>(
+          std::lower_bound(rank_ids.begin(), rank_ids.end(), r) - rank_ids.begin());
+      int32_t in_comp = 0;
+      for (int32_t t : comp_tasks) in_comp += d.rank[t] == r;
+      if (rank_count[row] != in_comp) continue;
+      int32_t lane_a = -1;
+      std::vector<int32_t> comm_lanes;
+      bool ok = true;
+      auto lo = std::lower_bound(lanes.begin(), lanes.end(), Proc{r, TS_LANE_CUDA_STREAM, INT32_MIN});
+      for (auto it = lo; it != lanes.end() && it->rank == r && it->kind == TS_LANE_CUDA_STREAM; ++it) {
+        const int32_t l = static_cast<int32_t>(it - lanes.begin());
+        if (lane_class[l] == 0 && lane_a < 0) lane_a = l;
+        else if (lane_class[l] == 1) comm_lanes.push_back(l);
+        else ok = false;
       }
-    for (int32_t t : comp_tasks) {
-      fz_anc[t] = -1;
-      fz_desc[t] = INT32_MAX;
+      if (!ok || static_cast<int>(comm_lanes.size()) > kFusedMaxComm) continue;
+      const int32_t len_a = lane_a < 0 ? 0 : lane_off[lane_a + 1] - lane_off[lane_a];
+      auto apos = [&](int32_t t) { return lane_of[t] == lane_a ? chain_pos[t] : -1; };
+      for (int32_t t : topo_tasks)
+        each_pred(t, [&](int32_t p) { fz_anc[t] = std::max({fz_anc[t], fz_anc[p], apos(p)}); });
+      for (size_t q = topo_tasks.size(); q-- > 0;) {
+        const int32_t t = topo_tasks[q];
+        const int32_t at = apos(t) < 0 ? INT32_MAX : apos(t);
+        each_pred(t, [&](int32_t p) { fz_desc[p] = std::min({fz_desc[p], fz_desc[t], at}); });
+      }
+      // candidates: A positions in (anc(c), desc(c)) for some comm kernel c
+      std::vector<char> cand(static_cast<size_t>(len_a), 0);
+      for (int32_t l : comm_lanes)
+        for (int32_t q = lane_off[l]; q < lane_off[l + 1]; ++q) {
+          const int32_t cm = lane_tasks[q];
+          for (int32_t j = fz_anc[cm] + 1; j < std::min(fz_desc[cm], len_a); ++j) cand[j] = 1;
+        }
+      for (int32_t t : comp_tasks) {
+        fz_anc[t] = -1;
+        fz_desc[t] = INT32_MAX;
+      }
+      auto& list = cand_of_row[row];
+      list.clear();
+      for (int32_t j = 0; j < len_a; ++j)
+        if (cand[j]) list.push_back(lane_tasks[lane_off[lane_a] + j]);
+      for (IrOp& o : ir)
+        if (!o.aux() && o.v_dst >= 0 && o.v_dst < n && lane_of[o.v_dst] == lane_a &&
+            (o.op.kind == OP_NODE || o.op.kind == OP_GATED || o.op.kind == OP_FINISH))
+          o.op.flags |= F_BUSY;
+      res[k] = FusedDesc{row, lane_a >= 0 ? stream_slot[lane_a] : -1};
+      out.fused_rows.push_back(res[k]);
     }
-    auto& list = cand_of_row[row];
-    list.clear();
-    for (int32_t k = 0; k < len_a; ++k)
-      if (cand[k]) list.push_back(lane_tasks[lane_off[lane_a] + k]);
-    for (IrOp& o : ir)
-      if (!o.aux() && o.v_dst >= 0 && o.v_dst < n && lane_of[o.v_dst] == lane_a &&
-          o.op.kind == OP_NODE)
-        o.op.flags |= F_BUSY;
-    out.fused[c] = FusedDesc{row, lane_a >= 0 ? stream_slot[lane_a] : -1};
-    out.n_fused++;
-    return true;
+    return res;
   };
 
   auto fold = [&](std::vector<int64_t>& vals, size_t room) {
@@ -740,6 +766,8 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
   const bool coop = allow_coop && !(coop_env && coop_env[0] == '0');
   out.coop_prog_off.clear();
   out.coop_progs.clear();
+  out.coop_rows.clear();
+  out.fused_rows.clear();
   out.max_mailboxes = 0;
   out.max_coop_ranks = 1;
   out.max_coop_path = 0;
@@ -1246,6 +1274,8 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     std::vector<int32_t> progs_of_comp;
     int32_t n_slots = 0;
+    std::vector<FusedDesc> coop_fd;  // per rank program of a split component
+    size_t coop_mark = 0;
     bool split = coop && n_local > 1 && n_local <= 32;
     if (split) {
       std::vector<int32_t> comp_ranks;
@@ -1256,6 +1286,10 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
         return static_cast<int32_t>(std::lower_bound(comp_ranks.begin(), comp_ranks.end(), rank) -
                                     comp_ranks.begin());
       };
+      // split accounting per rank (one |A| register per warp); rolled back if
+      // the component ends up walked as one program
+      coop_mark = out.fused_rows.size();
+      coop_fd = fuse_accounting(ir, true);
       // rank of every op: a task's rank; a fold (ACC) op takes its consumer's;
       // auxiliary records their op's
       rank_local.assign(ir.size(), -1);
@@ -1373,6 +1407,11 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
       if (smem64 > 220 * 1024) {
         split = false;  // the rank programs stay in the table, unused
         progs_of_comp.clear();
+        for (size_t q = coop_mark; q < out.fused_rows.size(); ++q)
+          cand_of_row[out.fused_rows[q].row].clear();
+        out.fused_rows.resize(coop_mark);
+        coop_fd.clear();
+        for (IrOp& o : ir) o.op.flags &= static_cast<uint8_t>(~F_BUSY);
       } else {
         out.max_slots = std::max(out.max_slots, n_slots);
         out.max_coop_path = std::max(out.max_coop_path, comp_path[c]);
@@ -1382,7 +1421,11 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     if (!split) {
       n_slots = 0;
-      fuse_accounting(c, ir);
+      const std::vector<FusedDesc> fd = fuse_accounting(ir, false);
+      if (fd.size() == 1 && fd[0].row >= 0) {
+        out.fused[c] = fd[0];
+        out.n_fused++;
+      }
       const int32_t prog = finish_program(ir, n_slots);
       if (prog < 0) return finish_rc;
       progs_of_comp.push_back(prog);
@@ -1390,7 +1433,10 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     }
     const int32_t prog = progs_of_comp[0];
     out.coop_prog_off.push_back(static_cast<int32_t>(out.coop_progs.size()));
-    for (int32_t pg : progs_of_comp) out.coop_progs.push_back(pg);
+    for (size_t k = 0; k < progs_of_comp.size(); ++k) {
+      out.coop_progs.push_back(progs_of_comp[k]);
+      out.coop_rows.push_back(split && k < coop_fd.size() ? coop_fd[k].row : -1);
+    }
     {
       int64_t sum = 0;
       for (int32_t t : comp_tasks) {

@@ -44,6 +44,8 @@ struct CompiledGraph {
   std::vector<FusedDesc> fused;
   int32_t n_fused = 0;  // components with row >= 0
   std::vector<int32_t> cand_off, cand_nodes;
+  std::vector<FusedDesc> fused_rows;  // every fused rank (single-program and cooperative)
+  std::vector<int32_t> coop_rows;     // parallel to coop_progs: the rank row a warp accounts, -1
   int32_t max_mailboxes = 0;
   int32_t max_coop_ranks = 1;
   int64_t max_coop_path = 0;  // nominal longest path of a cooperative component

@@ -215,6 +215,8 @@ struct CoopParams {
   int32_t rel32;            // uint32 offsets from W (additions checked, wraps -> fix-up)
   int32_t fixup;            // re-run only chunks holding a scenario with status bit 0
   int32_t pad;
+  const int32_t* rows;      // [progs] split accounting: the rank row a warp's |A| goes to
+                            // (acct_a of the WalkParams), -1 none; null: off
 };
 cudaError_t launch_coop_walk(const WalkParams& p, const CoopParams& c, cudaStream_t stream);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,

@@ -129,3 +129,36 @@ def test_estimate_batch_from_pipeline_spec(pp, dp, m, tp):
             sub.rank = sub.rank // tp
             got = _my_lane_sequences(sub, res.start[sel, s], res.fin[sel, s])
             assert got == _lane_sequences(pid, tid, ts, du), f"scenario {s} replica {t}"
+
+
+@pytest.mark.parametrize("force_u32", ["0", "1"])
+def test_estimate_split_accounting(force_u32, monkeypatch):
+    # cooperative walks sum |A| per warp (= rank); the split accounting's
+    # breakdown and stream busy equal the full sweep (LUMOS_FUSED_REDUCE=0) and
+    # the C restatement of breakdown_by_rank on the same timestamps — also
+    # after the uint32-wrap int64 re-run (force_u32 with a > 2^32 us timeline)
+    monkeypatch.setenv("LUMOS_COOP_FORCE_U32", force_u32)
+    sg = generate_graph(_spec(4, 2, 8, 4, estimate=True))
+    g = sg.graph
+    kw = (dict(jitter=0.1, scale_lo=30000, scale_hi=30000, scale_den=1) if force_u32 == "1"
+          else dict(jitter=0.25))
+    spec = ScenarioSpec(count=48, first=4, seed=12, **kw)
+    out = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("LUMOS_FUSED_REDUCE", env)
+        from paper_2504_09307_b200 import DeviceGraph
+        dg = DeviceGraph(g)
+        assert (dg.info["n_fused_ranks"] == dg.n_ranks) == (env == "1")
+        out[env] = simulate_batch(dg, spec, timestamps=True, breakdown=True)
+    a, b = out["1"], out["0"]
+    if force_u32 == "1":
+        assert int(a.makespan.max()) > 2 ** 32
+    assert np.array_equal(a.rank_breakdown, b.rank_breakdown)
+    assert np.array_equal(a.stream_busy, b.stream_busy)
+    og = _orc_graph(g)
+    ranks = sorted(set(int(r) for r in g.rank))
+    for s in (0, 23, 47):
+        wend = max(g.window_end, g.window_start + int(a.span[s, 2]))
+        for i, r in enumerate(ranks):
+            want = R.orc_breakdown_rank(og, a.start[:, s], a.fin[:, s], r, g.window_start, wend)
+            assert tuple(a.rank_breakdown[s, i]) == want, (s, r)
