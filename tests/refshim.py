@@ -26,7 +26,11 @@ _u8p = C.POINTER(C.c_uint8)
 
 
 def _p(a, t):
-    return a.ctypes.data_as(t) if a is not None else None
+    if a is None:
+        return None
+    if not a.flags["C_CONTIGUOUS"]:  # a strided view would be read (or written) wrongly
+        raise ValueError("refshim: arrays passed to the C side must be C-contiguous")
+    return a.ctypes.data_as(t)
 
 
 class OrcScenarios(C.Structure):
@@ -404,6 +408,8 @@ def orc_simulate(g: Graph, durations=None):
 
 
 def orc_breakdown_rank(g: Graph, start, fin, rank, wstart, wend):
+    start = np.ascontiguousarray(start, np.int64)  # the C side reads dense arrays
+    fin = np.ascontiguousarray(fin, np.int64)
     out = np.zeros(5, np.int64)
     orc().orc_breakdown_rank(g.n, _p(g.rank, _i32p), _p(g.lane_kind, _i32p),
                              _p(np.ascontiguousarray(g.is_comm()), _u8p), _p(start, _i64p),

@@ -159,6 +159,8 @@ def test_estimate_split_accounting(force_u32, monkeypatch):
     ranks = sorted(set(int(r) for r in g.rank))
     for s in (0, 23, 47):
         wend = max(g.window_end, g.window_start + int(a.span[s, 2]))
+        st = np.ascontiguousarray(a.start[:, s])
+        fi = np.ascontiguousarray(a.fin[:, s])
         for i, r in enumerate(ranks):
-            want = R.orc_breakdown_rank(og, a.start[:, s], a.fin[:, s], r, g.window_start, wend)
+            want = R.orc_breakdown_rank(og, st, fi, r, g.window_start, wend)
             assert tuple(a.rank_breakdown[s, i]) == want, (s, r)
