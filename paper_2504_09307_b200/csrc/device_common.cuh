@@ -162,6 +162,19 @@ __device__ __forceinline__ int64_t jitter_apply(const ScenarioParams& sp, int64_
   return d == 0 ? 0 : (r < 1 ? 1 : r);
 }
 
+// jitter_apply for a uint32 walk, where the host has proven every jittered
+// duration < 2^32 (capi.cpp rel32 bound): p < 2^32 < 2^52, so p + 0.5 is
+// exact and floor fits an unsigned 32-bit conversion — the same value as
+// jitter_apply with 32-bit compares and no 2^52 guard
+__device__ __forceinline__ uint32_t jitter_apply_u32(const ScenarioParams& sp, double dd, bool dz,
+                                                     uint32_t w) {
+  const double u = __dadd_rn(__dmul_rn(sp.two_j_ulp, __uint2double_rn(w)), sp.neg_j);
+  const double f = __dadd_rn(1.0, u);
+  const double p = __dmul_rn(dd, f);
+  const uint32_t r = __double2uint_rd(__dadd_rn(p, 0.5));
+  return dz ? 0u : (r < 1u ? 1u : r);
+}
+
 template <int kMode>
 __device__ __forceinline__ int64_t scenario_duration(const ScenarioParams& sp,
                                                      const ThreadScen& ts, int64_t task,

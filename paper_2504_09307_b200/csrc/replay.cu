@@ -247,9 +247,16 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
       uint32_t w[kS] = {0u, 0u};
       if (kRt || (kDurMode & kModeScale) || base != 0)
         jitter_words2(P.sp, task, ts[0].scen, ts[1].scen, w[0], w[1]);
+      if constexpr (kRel) {
 #pragma unroll
-      for (int s = 0; s < kS; ++s)
-        fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
+        for (int s = 0; s < kS; ++s)
+          fin.v[s] = static_cast<V>(
+              fb.v[s] + jitter_apply_u32(P.sp, __ll2double_rn(dsc[s]), dsc[s] == 0, w[s]));
+      } else {
+#pragma unroll
+        for (int s = 0; s < kS; ++s)
+          fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(jitter_apply(P.sp, dsc[s], w[s])));
+      }
     } else if constexpr (kScaleTab) {  // class scale only
 #pragma unroll
       for (int s = 0; s < kS; ++s) fin.v[s] = static_cast<V>(fb.v[s] + static_cast<V>(dsc[s]));
