@@ -505,7 +505,7 @@ def main():
             e2e_s = float(t.item())
         d2h = (h_span.numel() + h_bd.numel() + h_busy.numel()) * 8
         e2e = {"value": relax_per_step / e2e_s, "unit": "relaxations/s",
-               "h2d_bytes_per_step": sc_bytes, "d2h_bytes_per_step": d2h * world,
+               "h2d_bytes_per_step": sc_bytes * world, "d2h_bytes_per_step": d2h * world,
                "ms_per_step": e2e_s * 1e3,
                "note": "host scenario descriptors in, per-scenario span + per-rank breakdown + "
                        "per-stream busy copied to pinned host memory every step; timestamps "
