@@ -1100,8 +1100,12 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
         dp.util_bw = out->util_bin_width;
         dp.util_max_bins = ubins;
       }
+      // one thread per concurrently replayed scenario, each with its own
+      // scratch: at least 1 GB, up to a quarter of the free device memory
       const size_t per = des_scratch_bytes(c.n_tasks, T.n_lanes);
-      const size_t budget = size_t(1) << 30;
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) cudaGetLastError();
+      const size_t budget = std::max<size_t>(size_t(1) << 30, (free_b + g->des_scratch.bytes) / 4);
       dp.n_slots = static_cast<int32_t>(
           std::max<size_t>(1, std::min<size_t>(static_cast<size_t>(bn), budget / per)));
       CUDA_TRY(g->des_scratch.reserve(per * dp.n_slots));

@@ -1631,6 +1631,13 @@ void build_common(const ts_graph_desc& d, CompiledGraph& out) {
 int compile_graph(const ts_graph_desc& d, CompiledGraph& out, std::string& err,
                   bool allow_coop) {
   int rc = compile_programs(d, out, err, allow_coop);
+  // LUMOS_FORCE_DES=1: every scenario on the event-driven kernel (measurement
+  // of that path; tests use it to compare both paths)
+  const char* force_des = std::getenv("LUMOS_FORCE_DES");
+  if (rc == TS_OK && d.n_gates == 0 && force_des && force_des[0] == '1') {
+    rc = TS_E_UNSUPPORTED;
+    err = "LUMOS_FORCE_DES=1";
+  }
   if (rc == TS_E_UNSUPPORTED && d.n_gates == 0) {
     // outside the chained class: every scenario takes the exact event-driven
     // path (a restatement of the reference Engine on the device)

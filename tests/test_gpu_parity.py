@@ -493,3 +493,19 @@ def test_split_accounting_equals_full_sweep(shape, monkeypatch):
         ref = h.breakdown_by_rank(rs, rf, g.window_start, wend)
         for i, r in enumerate(sorted(ref)):
             assert tuple(out["1"].rank_breakdown[s_, i]) == ref[r]
+
+
+def test_event_driven_path_equals_walk(monkeypatch):
+    # two independent device restatements of simulate(): the straight-line
+    # walk and the event-driven kernel (LUMOS_FORCE_DES=1 sends every scenario
+    # to it) agree on every timestamp, span, breakdown and stream busy value
+    h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
+    g = h.export()
+    spec = ScenarioSpec(count=40, first=6, seed=31, jitter=0.2)
+    walk = simulate_batch(g, spec)
+    monkeypatch.setenv("LUMOS_FORCE_DES", "1")
+    dg = DeviceGraph(g)
+    assert dg.info["des_only"] == 1
+    des = simulate_batch(dg, spec)
+    for k in ("start", "fin", "span", "rank_breakdown", "stream_busy"):
+        assert np.array_equal(getattr(walk, k), getattr(des, k)), k

@@ -61,6 +61,7 @@ def main():
     p = dg.profile_read()
     walk = p["walk_ms"] / max(1, p["walk_launches"])
     out = {"label": label, "config": cfg, "tile": tile, "metrics_only": metrics_only,
+           "des_only": dg.info["des_only"], "des_ms_per_call": p["other_ms"] / calls,
            "walk_ms": walk, "reduce_ms_per_call": p["reduce_ms"] / calls,
            "other_ms_per_call": p["other_ms"] / calls, "wall_ms_per_call": wall * 1e3,
            "walk_tb_s": n * tile * 16 / (walk / 1e3) / 1e12,
