@@ -64,7 +64,7 @@ def main():
            "des_only": dg.info["des_only"], "des_ms_per_call": p["other_ms"] / calls,
            "walk_ms": walk, "reduce_ms_per_call": p["reduce_ms"] / calls,
            "other_ms_per_call": p["other_ms"] / calls, "wall_ms_per_call": wall * 1e3,
-           "walk_tb_s": n * tile * 16 / (walk / 1e3) / 1e12,
+           "walk_tb_s": n * tile * 16 / (walk / 1e3) / 1e12 if walk > 0 else None,
            "g_relax_per_s": n * tile / wall / 1e9,
            "info": {k: dg.info[k] for k in ("max_slots", "n_fused_ranks", "n_candidates")}}
     print(json.dumps(out), flush=True)
