@@ -589,6 +589,10 @@ __global__ void __launch_bounds__(32 * kMaxW, kMaxW <= 16 ? LUMOS_COOP_MINB : 1)
   bool fail = false, stalled = false;
   const int acct_row = C.rows ? C.rows[pfirst + w] : -1;  // split accounting of this rank
   V busy_a = V(0);
+  constexpr uint32_t kCoopFastMask = 0xFFu | (static_cast<uint32_t>(F_TRACK | F_STORE_START) << 24);
+  auto coop_duration = [&](int64_t task, int64_t base, int cls) -> int64_t {
+    return scenario_duration<kMode>(P.sp, ts, task, base, cls);
+  };
   int64_t* const start_c = P.out_start + col;
   int64_t* const fin_c = P.out_fin + col;
   const uint64_t ld = static_cast<uint64_t>(P.ld);
@@ -602,6 +606,32 @@ __global__ void __launch_bounds__(32 * kMaxW, kMaxW <= 16 ? LUMOS_COOP_MINB : 1)
     const uint32_t hdr = static_cast<uint32_t>(ca.w);
     const uint32_t kind = hdr & 0xFFu, cls_b = (hdr >> 16) & 0xFFu, flags_op = hdr >> 24;
     const uint32_t w0f = cb.x, w1f = cb.y, w2f = cb.z, w3f = cb.w;
+    // fast path: a plain node (no coverage, no stored start) — most ops of a
+    // rank program — without the kind dispatch
+    if ((hdr & kCoopFastMask) == OP_NODE) {
+      const V q0 = SLOTC(lo16(w0f)), q1 = SLOTC(hi16(w0f));
+      const V q2 = SLOTC(lo16(w1f)), q3 = SLOTC(hi16(w1f));
+      const V st = vmax(vmax(q0, q1), vmax(q2, q3));
+      const int64_t task = static_cast<int64_t>(cd.node_base) + ca.z;
+      const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ca.y)) << 32) |
+                           static_cast<uint32_t>(ca.x);
+      const int64_t d = coop_duration(task, base, static_cast<int>(cls_b & 15u));
+      const V fin = static_cast<V>(st + static_cast<V>(d));
+      if (kRel && (fin < st || d > 0xFFFFFFFFll)) fail = true;
+      SLOTC(lo16(w2f)) = fin;
+      if (flags_op & F_BUSY) busy_a = static_cast<V>(busy_a + (fin - st));
+      if (flags_op & F_SINK) hi = imax(hi, absv(fin));
+      const uint64_t at = static_cast<uint64_t>(static_cast<uint32_t>(task)) * ld;
+      if (LUMOS_OK(task >= 0 && task < P.n_tasks && col < static_cast<int>(ld))) {
+        if (P.out_start) __stcs(start_c + at, absv(st));
+        if (P.out_fin) __stcs(fin_c + at, absv(fin));
+      }
+      if (flags_op & F_TRACK1) {
+        const V cs = SLOTC(hi16(w2f));
+        SLOTC(lo16(w3f)) = q0 >= st ? vmin(st, cs) : st;
+      }
+      continue;
+    }
     if (kind == OP_NOP) continue;
     const V p0 = SLOTC(lo16(w0f)), p1 = SLOTC(hi16(w0f));
     const V p2 = SLOTC(lo16(w1f)), p3 = SLOTC(hi16(w1f));
@@ -695,7 +725,7 @@ __global__ void __launch_bounds__(32 * kMaxW, kMaxW <= 16 ? LUMOS_COOP_MINB : 1)
       const int64_t task = static_cast<int64_t>(cd.node_base) + ca.z;
       const int64_t base = (static_cast<int64_t>(static_cast<uint32_t>(ca.y)) << 32) |
                            static_cast<uint32_t>(ca.x);
-      const int64_t d = scenario_duration<kMode>(P.sp, ts, task, base, static_cast<int>(cls_b & 15u));
+      const int64_t d = coop_duration(task, base, static_cast<int>(cls_b & 15u));
       const V fin = static_cast<V>(fb + static_cast<V>(d));
       // uint32 windows are sized by the nominal path: an addition that wraps
       // sends the scenario to the exact event-driven fix-up instead

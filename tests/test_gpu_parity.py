@@ -509,3 +509,32 @@ def test_event_driven_path_equals_walk(monkeypatch):
     des = simulate_batch(dg, spec)
     for k in ("start", "fin", "span", "rank_breakdown", "stream_busy"):
         assert np.array_equal(getattr(walk, k), getattr(des, k)), k
+
+
+def test_edge_cases_match_reference():
+    # reference edge cases (test_simulator.cpp, oracles.cpp fuzz): an empty
+    # graph, a single task, all-zero durations, and durations near 2^40 us
+    # (int64 walk), each on both walk variants via the module fixture
+    empty = _graph([])
+    res = simulate_batch(empty, ScenarioSpec(count=3, jitter=0.1))
+    assert res.span.tolist() == [[0, 0, 0]] * 3
+    one = _graph([(1, 7, 5, 40)])
+    res = simulate_batch(one, ScenarioSpec(count=5, first=2, seed=4, jitter=0.3))
+    h = R.from_graph(one)
+    sc = R.OrcScenarios(seed=4, jitter=0.3)
+    for s in range(5):
+        rs, rf, rspan = h.simulate(R.orc_durations(one, sc, 2 + s))
+        assert res.start[0, s] == rs[0] and res.fin[0, s] == rf[0]
+        assert np.array_equal(res.span[s], rspan)
+    h0, _ = R.generate(R.synth_spec(pp=2, dp=1, m=2, layers=2))
+    for scale in (0, 1 << 28):
+        g = h0.export()
+        g.duration = np.where(g.duration > 0, g.duration * scale + (scale > 0), 0).astype(np.int64)
+        hg = R.from_graph(g)
+        spec = ScenarioSpec(count=9, first=10, seed=8, jitter=0.2)
+        res = simulate_batch(g, spec)
+        sc = R.OrcScenarios(seed=8, jitter=0.2)
+        for s in (0, 4, 8):
+            rs, rf, rspan = hg.simulate(R.orc_durations(g, sc, 10 + s))
+            assert np.array_equal(res.start[:, s], rs) and np.array_equal(res.fin[:, s], rf)
+            assert np.array_equal(res.span[s], rspan)
