@@ -399,10 +399,12 @@ int ts_profile_read(ts_graph* g, ts_profile_stats* out);
 int64_t ts_kernel_launches(void);
 /* K1 walk launches per variant since load: out[0] one scenario per thread with
  * uint32 slot values, out[1] one with int64, out[2] two per thread uint32,
- * out[3] two per thread int64.  The environment variable LUMOS_WALK_KS=1|2
+ * out[3] two per thread int64, out[4] cluster walks of estimate-mode
+ * components (K1x; LUMOS_CLUSTER=0 takes the cooperative walk instead).
+ * The environment variable LUMOS_WALK_KS=1|2
  * pins the scenarios per thread (parity tests run both; a batch starting at an
  * odd global id always takes one, so Philox pairs never straddle threads). */
-int ts_walk_counts(int64_t* out /* [4] */);
+int ts_walk_counts(int64_t* out /* [5] */);
 const char* ts_last_error(void);
 int ts_abi_version(void);
 

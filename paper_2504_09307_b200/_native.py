@@ -123,8 +123,9 @@ def lib():
 
 
 def walk_counts() -> list:
-    """K1 walk launches per variant: [1/thread u32, 1/thread i64, 2/thread u32, 2/thread i64]."""
-    out = (C.c_int64 * 4)()
+    """K1 walk launches per variant: [1/thread u32, 1/thread i64, 2/thread u32,
+    2/thread i64, cluster walk (estimate mode)]."""
+    out = (C.c_int64 * 5)()
     lib().ts_walk_counts(out)
     return list(out)
 

@@ -147,6 +147,12 @@ struct ts_graph {
   int32_t* d_rank_lists_nf = nullptr;  // non-fused ranks by bucket, then fused ranks (lite)
   int32_t bucket_off_nf[kReduceAllBuckets + 1] = {0};
   DevBuf acct_a;  // [tile][n_ranks] |A| sums of the walk
+  DevBuf cl_mail;  // cluster walk mailboxes
+  int cluster_state = -1;  // -1 unknown, 0 unsupported, 1 supported
+  bool cluster_ok(int size, int n_slots) {
+    if (cluster_state < 0) cluster_state = cluster_walk_supported(size, n_slots) ? 1 : 0;
+    return cluster_state == 1;
+  }
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[12];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur,
                      // util, util bins, delta sum, delta worst, internal bin counts
@@ -454,6 +460,7 @@ void ts_graph_destroy(ts_graph* g) {
       if (p) cudaFree(p);
     g->des_scratch.release();
     g->acct_a.release();
+    g->cl_mail.release();
     g->retime_dur.release();
     g->retime_par.release();
     g->rt_vval.release();
@@ -934,7 +941,7 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   }
   // cooperative walks size their uint32 window by the nominal longest path
   // and check every addition (a wrap sends the scenario to the fix-up)
-  bool coop_rel32 = false;
+  bool coop_rel32 = false, use_cluster = false;
   if (!retime && !(sp.mode & kModeExplicit) && !sp.scale_num && g->n_coop > 0) {
     double f = 1.0;
     if (sp.mode & kModeScale)
@@ -944,6 +951,13 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     coop_rel32 = static_cast<double>(c.max_coop_path) * f * 1.25 + 1e6 < 4.0e9;
     const char* force = std::getenv("LUMOS_COOP_FORCE_U32");  // tests: exercise the wrap fix-up
     if (force && force[0] == '1') coop_rel32 = true;
+    // the cluster walk's offsets start at W rounded down to 2^32 (as K1's)
+    const double w_lo = static_cast<double>(static_cast<uint32_t>(c.window_start));
+    const char* cl = std::getenv("LUMOS_CLUSTER");
+    use_cluster = coop_rel32 && !(cl && cl[0] == '0') &&
+                  (w_lo + static_cast<double>(c.max_coop_path) * f * 1.25 + 1e6 < 4.0e9 ||
+                   (force && force[0] == '1')) &&
+                  g->cluster_ok(c.max_coop_ranks, c.max_slots);
   }
   // LUMOS_WALK_KS=1|2 pins the walk's scenarios per thread (tests run every
   // parity case on both variants; an odd first id always takes one)
@@ -1035,7 +1049,33 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       cp.n_slots = c.max_slots;
       cp.rel32 = coop_rel32 ? 1 : 0;
       cp.rows = acct ? g->d_coop_rows : nullptr;
-      {
+      // K1x cluster walk: one 128-thread CTA per rank program (two scenarios
+      // per thread, the K1 fast path), the component's ranks one cluster,
+      // cross-rank values through an L2-resident mailbox table; uint32 windows
+      // only (wraps re-run below in int64 by the cooperative kernel)
+      bool clustered = false;
+      if (use_cluster) {
+        const int64_t units = static_cast<int64_t>(g->n_coop) * ((bn + 255) / 256);
+        const size_t mail = static_cast<size_t>(units) * c.max_mailboxes * 128 * 8;
+        CUDA_TRY(g->cl_mail.reserve(mail + 8));
+        CUDA_TRY(cudaMemsetAsync(g->cl_mail.p, 0xFF, mail, stream));
+        cw.cl_prog_off = g->d_coop_prog_off;
+        cw.cl_progs = g->d_coop_progs;
+        cw.cl_rows = acct ? g->d_coop_rows : nullptr;
+        cw.cl_mail = g->cl_mail.as<uint64_t>();
+        cw.cl_size = c.max_coop_ranks;
+        cw.cl_n_mail = c.max_mailboxes;
+        Timed tm(g, stream, 0);
+        const cudaError_t ce = launch_cluster_walk(cw, c.max_slots, stream);
+        if (ce == cudaSuccess) {
+          clustered = true;
+        } else if (ce != cudaErrorNotSupported) {
+          CUDA_TRY(ce);
+        } else {
+          cudaGetLastError();
+        }
+      }
+      if (!clustered) {
         Timed tm(g, stream, 0);
         CUDA_TRY(launch_coop_walk(cw, cp, stream));
       }
@@ -1193,7 +1233,8 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
 
   // deadlock (only possible outside the chained class) -> SimulationError
   std::vector<int32_t> host_status;
-  if (c.des_only || out->n_fixups || (out->status && !is_device_ptr(out->status))) {
+  if (c.des_only || g->n_coop > 0 || out->n_fixups ||
+      (out->status && !is_device_ptr(out->status))) {
     host_status.resize(count);
     CUDA_TRY(cudaMemcpyAsync(host_status.data(), status, static_cast<size_t>(count) * 4,
                              cudaMemcpyDeviceToHost, stream));
@@ -1239,6 +1280,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
                   "utilization needs " + std::to_string(need) + " bins per rank; util_max_bins is " +
                       std::to_string(out->util_max_bins));
   }
+  if (g->n_coop > 0)
+    for (int32_t st : host_status)
+      if (st == -2)
+        return fail(TS_E_CUDA, "cooperative replay stalled waiting for a cross-rank value");
   int64_t n_dead = 0;
   int32_t first_dead = -1;
   for (int32_t i = 0; i < static_cast<int32_t>(host_status.size()); ++i)

@@ -89,6 +89,16 @@ struct WalkParams {
   int64_t* acct_a;         // [count][n_ranks]
   int32_t n_ranks;
   int32_t n_tasks;         // rows of out_start / out_fin (bounds checks)
+  // cluster walk (K1x, estimate-mode components): one CTA per rank program,
+  // the component's rank CTAs one thread-block cluster; cross-rank values
+  // through a global (L2-resident) mailbox table [cluster][mailbox][thread]
+  // of uint32 pairs, all-ones = not yet posted
+  const int32_t* cl_prog_off;  // [components + 1] into cl_progs
+  const int32_t* cl_progs;     // rank programs per component
+  const int32_t* cl_rows;      // split accounting row per rank program, or null
+  uint64_t* cl_mail;
+  int32_t cl_size;             // CTAs per cluster (ranks of the widest component)
+  int32_t cl_n_mail;           // mailboxes per cluster
 };
 // debug builds: the source line of the first failed bounds check since the
 // last call (0 = none), cleared by the read; always 0 in release builds
@@ -198,8 +208,9 @@ int walk_width(int n_slots, bool rel32);  // walk CTA width for a slot count (0:
 int max_streams_per_rank();
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
 // walk launches per variant since load: [0] one scenario per thread (uint32
-// slots), [1] one (int64), [2] two per thread (uint32), [3] two (int64)
-void walk_variant_counts(int64_t out[4]);
+// slots), [1] one (int64), [2] two per thread (uint32), [3] two (int64),
+// [4] cluster walks (K1x)
+void walk_variant_counts(int64_t out[5]);
 
 // Cooperative walk (components of several ranks coupled by gates): one CTA =
 // (component, 32 scenarios), one warp per rank program, cross-rank values
@@ -219,6 +230,10 @@ struct CoopParams {
                             // (acct_a of the WalkParams), -1 none; null: off
 };
 cudaError_t launch_coop_walk(const WalkParams& p, const CoopParams& c, cudaStream_t stream);
+// K1x: returns cudaErrorNotSupported when the device cannot co-schedule a
+// cluster of p.cl_size CTAs (the caller then takes the cooperative walk)
+cudaError_t launch_cluster_walk(const WalkParams& p, int n_slots, cudaStream_t stream);
+bool cluster_walk_supported(int cl_size, int n_slots);
 cudaError_t launch_span_init(int64_t* lo, int64_t* hi, int32_t* status, int32_t count,
                              cudaStream_t stream);
 // compare_replay deltas of one tile: partial[chunk][count][3] then per column

@@ -91,10 +91,12 @@ __device__ __noinline__ int64_t rt_coll_base(const RtScen* scp, int32_t rk, int3
   return d;
 }
 
-template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
+template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS,
+          bool kCl = false>
 __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   using VP = VPack<V, kS>;
   constexpr bool kRel = sizeof(V) == 4;
+  static_assert(!kCl || (kRel && kS == 2), "cluster walks keep uint32 pairs");
   // retime walk: F_RT tasks take their base duration from the variant tables
   // (K4v) and the scenario's cost model; scale / jitter follow sp.mode
   constexpr bool kRt = kMode >= 0 && (kMode & kModeRetime) != 0;
@@ -118,8 +120,13 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   char* slot_base = reinterpret_cast<char*>(numtab + kMaxClasses * kT) +
                     threadIdx.x * static_cast<uint32_t>(sizeof(VP));
   const int tid = threadIdx.x;
-  const int comp = static_cast<int>(blockIdx.x % static_cast<unsigned>(P.n_comps));
-  const int chunk = static_cast<int>(blockIdx.x / static_cast<unsigned>(P.n_comps));
+  // a cluster walk CTA is (component, chunk, rank program r_loc); the
+  // component's rank CTAs form one cluster, so they are co-scheduled
+  const int unit = kCl ? static_cast<int>(blockIdx.x / static_cast<unsigned>(P.cl_size))
+                       : static_cast<int>(blockIdx.x);
+  const int r_loc = kCl ? static_cast<int>(blockIdx.x % static_cast<unsigned>(P.cl_size)) : 0;
+  const int comp = static_cast<int>(unit % static_cast<unsigned>(P.n_comps));
+  const int chunk = static_cast<int>(unit / static_cast<unsigned>(P.n_comps));
   // lanes past the last scenario replay the last scenario again: identical
   // values, so their (duplicate) stores and atomics need no predication
   const int last = P.sp.count - 1;
@@ -137,7 +144,13 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
 
   const int comp_id = P.comp_order ? P.comp_order[comp] : comp;
   const ComponentDesc cd = P.comps[comp_id];
-  const ProgramDesc pd = P.progs[cd.program];
+  int prog_id = cd.program;
+  if constexpr (kCl) {
+    const int pf = P.cl_prog_off[comp_id], nw = P.cl_prog_off[comp_id + 1] - pf;
+    if (r_loc >= nw) return;  // a narrower component: no barrier is shared across CTAs
+    prog_id = P.cl_progs[pf + r_loc];
+  }
+  const ProgramDesc pd = P.progs[prog_id];
   const int4* __restrict__ gops = reinterpret_cast<const int4*>(P.ops + pd.op_offset);
   const int n_ops = pd.n_ops;
   const int64_t W = P.window_start;
@@ -200,7 +213,11 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   const uint64_t ld8 = static_cast<uint64_t>(ld) * 8u;
   // split accounting of a fused component (program.hpp FusedDesc): |A| summed
   // in registers over the F_BUSY kernels
-  const int acct_row = P.fused ? P.fused[comp_id].row : -1;
+  int acct_row = P.fused ? P.fused[comp_id].row : -1;
+  if constexpr (kCl) acct_row = P.cl_rows ? P.cl_rows[P.cl_prog_off[comp_id] + r_loc] : -1;
+  uint64_t* const mail_base =
+      kCl ? P.cl_mail + static_cast<int64_t>(unit) * P.cl_n_mail * kT + tid : nullptr;
+  bool stalled = false;
   VP busy_a = splat<V, kS>(V(0));
 
   // A task's finish: its scenario durations (K4, fused), the busy / sink
@@ -302,6 +319,14 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         if (kS == 2) __stcs(fin_c0 + at + dcol, absv(fin.v[kS - 1]));
       }
     }
+    if constexpr (kCl) {
+      // the cluster walk's uint32 window is sized by the nominal path (like
+      // the cooperative walk): a wrapped addition sends the scenario to the
+      // int64 re-run
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        fail[s] = fail[s] || fin.v[s] < fb.v[s] || fin.v[s] == static_cast<V>(0xFFFFFFFFu);
+    }
     return fin;
   };
   auto stage = [&](int4* dstbuf, int r, int4 a, int4 b) {
@@ -385,6 +410,33 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         if (nfixed > 2) st = maxp(st, p2); else gate = maxp(gate, p2);
         gate = maxp(gate, p3);
         fb = maxp(st, gate);
+      } else if (kCl && (kind == OP_POST || kind == OP_WAIT)) {
+        if constexpr (kCl) {
+          int m = static_cast<int>(ob.z >> kShift);  // x1: the mailbox id (widened)
+          if (!LUMOS_OK(m < P.cl_n_mail)) m = 0;
+          volatile uint64_t* box = mail_base + static_cast<int64_t>(m) * kT;
+          if (kind == OP_POST) {
+            uint64_t v = static_cast<uint64_t>(p0.v[0]) | (static_cast<uint64_t>(p0.v[1]) << 32);
+            if (v == ~0ull) v = ~1ull;  // only a wrapped (failed) value can look unposted
+            *box = v;
+          } else {
+            uint64_t v = *box;
+            for (int spins = 0; v == ~0ull; ++spins) {
+              if (spins > (1 << 22)) {  // ~seconds: a compiler bug, not a schedule
+                stalled = true;
+                v = 0;
+                break;
+              }
+              __nanosleep(32);
+              v = *box;
+            }
+            VP q;
+            q.v[0] = static_cast<V>(static_cast<uint32_t>(v));
+            q.v[1] = static_cast<V>(static_cast<uint32_t>(v >> 32));
+            SLOTB(ob.x) = q;
+          }
+        }
+        continue;
       } else {
         continue;  // OP_NOP
       }
@@ -502,7 +554,8 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
       atomicMin(reinterpret_cast<long long*>(P.span_lo) + col[s], static_cast<long long>(W));
       atomicMax(reinterpret_cast<long long*>(P.span_hi) + col[s], static_cast<long long>(hi[s]));
     }
-    if (fail[s]) atomicOr(P.status + col[s], 1);
+    if (kCl && stalled) atomicExch(P.status + col[s], -2);
+    else if (fail[s]) atomicOr(P.status + col[s], 1);
   }
 }
 
@@ -516,6 +569,11 @@ template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int k
 __global__ void __launch_bounds__(kT, sizeof(V) == 4 && LUMOS_WALK_MINB > 0 ? LUMOS_WALK_MINB * 128 / kT : 1)
     replay_walk_kernel(WalkParams P) {
   replay_walk_body<kT, kMode, kWriteStart, kWriteFin, V, kS>(P);
+}
+// K1x cluster walk (estimate-mode components): 128 threads, uint32 pairs
+template <int kMode, bool kWriteStart, bool kWriteFin>
+__global__ void __launch_bounds__(128) cluster_walk_kernel(WalkParams P) {
+  replay_walk_body<128, kMode, kWriteStart, kWriteFin, uint32_t, 2, true>(P);
 }
 // retime walks: at least 6 CTAs of 128 threads per SM (<= 80 registers)
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
@@ -1525,10 +1583,10 @@ static cudaError_t launch_walk_v(const WalkParams& p, int n_slots, int t, cudaSt
   return cudaErrorInvalidConfiguration;
 }
 
-static std::atomic<int64_t> g_walk_variant[4];
+static std::atomic<int64_t> g_walk_variant[5];
 
-void walk_variant_counts(int64_t out[4]) {
-  for (int k = 0; k < 4; ++k) out[k] = g_walk_variant[k].load();
+void walk_variant_counts(int64_t out[5]) {
+  for (int k = 0; k < 5; ++k) out[k] = g_walk_variant[k].load();
 }
 
 cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
@@ -1545,6 +1603,88 @@ cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t st
                : launch_walk_v<int64_t, 1>(p, n_slots, t, stream);
   return rel ? launch_walk_v<uint32_t, 2>(p, n_slots, t, stream)
              : launch_walk_v<int64_t, 2>(p, n_slots, t, stream);
+}
+
+template <int kMode, bool kWS, bool kWF>
+static cudaError_t launch_cluster_t(const WalkParams& p, size_t smem, unsigned blocks,
+                                    cudaStream_t stream) {
+  auto kern = cluster_walk_kernel<kMode, kWS, kWF>;
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+  if (e == cudaSuccess && p.cl_size > 8)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl_size);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int kMode>
+static cudaError_t launch_cluster_mode(const WalkParams& p, size_t smem, unsigned blocks,
+                                       cudaStream_t stream) {
+  const bool s = p.out_start != nullptr, f = p.out_fin != nullptr;
+  if (s && f) return launch_cluster_t<kMode, true, true>(p, smem, blocks, stream);
+  if (f) return launch_cluster_t<kMode, false, true>(p, smem, blocks, stream);
+  if (s) return launch_cluster_t<kMode, true, false>(p, smem, blocks, stream);
+  return launch_cluster_t<kMode, false, false>(p, smem, blocks, stream);
+}
+
+bool cluster_walk_supported(int cl_size, int n_slots) {
+  if (cl_size < 1 || cl_size > 16 || walk_width(n_slots, true) != 128) return false;
+  auto kern = cluster_walk_kernel<kModeJitter, true, true>;
+  const size_t smem = walk_smem(n_slots, 128, 8);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return cudaGetLastError(), false;
+  if (cl_size > 8 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return cudaGetLastError(), false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(cl_size));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cl_size);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return cudaGetLastError(), false;
+  return n > 0;
+}
+
+cudaError_t launch_cluster_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
+  if (p.cl_size < 1 || p.cl_size > 16) return cudaErrorNotSupported;
+  const long long units = static_cast<long long>(p.n_comps) * ((p.sp.count + 255) / 256);
+  if (units <= 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(units * p.cl_size);
+  const size_t smem = walk_smem(n_slots, 128, 8);
+  if (p.sp.mode == 0 || p.sp.mode == kModeScale || p.sp.mode == kModeJitter ||
+      p.sp.mode == (kModeScale | kModeJitter))
+    g_walk_variant[4]++;
+  switch (p.sp.mode) {
+    case 0: return launch_cluster_mode<0>(p, smem, blocks, stream);
+    case kModeScale: return launch_cluster_mode<kModeScale>(p, smem, blocks, stream);
+    case kModeJitter: return launch_cluster_mode<kModeJitter>(p, smem, blocks, stream);
+    case kModeScale | kModeJitter:
+      return launch_cluster_mode<kModeScale | kModeJitter>(p, smem, blocks, stream);
+    default: return cudaErrorNotSupported;  // explicit durations / retime: cooperative walk
+  }
 }
 
 template <typename V>

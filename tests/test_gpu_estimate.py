@@ -164,3 +164,27 @@ def test_estimate_split_accounting(force_u32, monkeypatch):
         for i, r in enumerate(ranks):
             want = R.orc_breakdown_rank(og, st, fi, r, g.window_start, wend)
             assert tuple(a.rank_breakdown[s, i]) == want, (s, r)
+
+
+@pytest.mark.parametrize("shape", [(4, 2, 8, 4, 1024, 4096), (2, 4, 4, 4, 1024, 4096)])
+def test_cluster_walk_equals_cooperative_walk(shape, monkeypatch):
+    # K1x (one CTA per rank program in a thread-block cluster, two scenarios
+    # per thread, L2 mailboxes) and the cooperative walk (LUMOS_CLUSTER=0)
+    # give identical timestamps, spans and breakdowns; both equal
+    # build_pipeline per scenario (_check); the launch counters prove which ran
+    from paper_2504_09307_b200 import DeviceGraph
+    from paper_2504_09307_b200 import _native as N
+    pp, dp, m, layers, d, f = shape
+    sg = generate_graph(_spec(pp, dp, m, layers, d, f, estimate=True))
+    spec = ScenarioSpec(count=600, first=8, seed=17, jitter=0.2)
+    out = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("LUMOS_CLUSTER", env)
+        before = N.walk_counts()
+        out[env] = simulate_batch(DeviceGraph(sg.graph), spec, timestamps=True, breakdown=True)
+        ran = N.walk_counts()[4] - before[4]
+        assert (ran > 0) == (env == "1"), ran
+    for k in ("start", "fin", "span", "rank_breakdown", "stream_busy"):
+        assert np.array_equal(getattr(out["1"], k), getattr(out["0"], k)), k
+    monkeypatch.setenv("LUMOS_CLUSTER", "1")
+    _check(shape, S=40, seed=17, jitter=0.2, every=7)
