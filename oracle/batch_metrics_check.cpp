@@ -197,7 +197,13 @@ int main() {
           if (er.op_index[t] >= 0) hook[static_cast<std::size_t>(er.op_index[t])] = d[t];
         const BuiltPipeline b = build_pipeline(
             *ps, [&](std::size_t i, Micros base) { return i < hook.size() ? hook[i] : base; });
-        if (b.end - ps->origin != er.batch.span[3 * s + 2]) ++bad_est;
+        if (b.end - ps->origin != er.batch.span[3 * s + 2]) {
+          ++bad_est;
+          std::printf("estimate_batch mismatch: spec %s scenario %d makespan %lld vs %lld\n",
+                      ps == &base_spec ? "pipeline_spec_for" : "edited", s,
+                      static_cast<long long>(er.batch.span[3 * s + 2]),
+                      static_cast<long long>(b.end - ps->origin));
+        }
       }
     }
   }

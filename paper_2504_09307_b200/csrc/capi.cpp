@@ -1054,7 +1054,8 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       // cross-rank values through an L2-resident mailbox table; uint32 windows
       // only (wraps re-run below in int64 by the cooperative kernel)
       bool clustered = false;
-      if (use_cluster) {
+      // a thread's two scenarios share one Philox call: an even first id
+      if (use_cluster && (wp.sp.first & 1) == 0) {
         const int64_t units = static_cast<int64_t>(g->n_coop) * ((bn + 255) / 256);
         const size_t mail = static_cast<size_t>(units) * c.max_mailboxes * 128 * 8;
         CUDA_TRY(g->cl_mail.reserve(mail + 8));

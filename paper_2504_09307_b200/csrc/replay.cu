@@ -571,8 +571,11 @@ __global__ void __launch_bounds__(kT, sizeof(V) == 4 && LUMOS_WALK_MINB > 0 ? LU
   replay_walk_body<kT, kMode, kWriteStart, kWriteFin, V, kS>(P);
 }
 // K1x cluster walk (estimate-mode components): 128 threads, uint32 pairs
+#ifndef LUMOS_CLUSTER_MINB
+#define LUMOS_CLUSTER_MINB 1
+#endif
 template <int kMode, bool kWriteStart, bool kWriteFin>
-__global__ void __launch_bounds__(128) cluster_walk_kernel(WalkParams P) {
+__global__ void __launch_bounds__(128, LUMOS_CLUSTER_MINB) cluster_walk_kernel(WalkParams P) {
   replay_walk_body<128, kMode, kWriteStart, kWriteFin, uint32_t, 2, true>(P);
 }
 // retime walks: at least 6 CTAs of 128 threads per SM (<= 80 registers)
@@ -1669,7 +1672,8 @@ bool cluster_walk_supported(int cl_size, int n_slots) {
 }
 
 cudaError_t launch_cluster_walk(const WalkParams& p, int n_slots, cudaStream_t stream) {
-  if (p.cl_size < 1 || p.cl_size > 16) return cudaErrorNotSupported;
+  // scenario pairs share a Philox call (needs an even first id)
+  if (p.cl_size < 1 || p.cl_size > 16 || (p.sp.first & 1)) return cudaErrorNotSupported;
   const long long units = static_cast<long long>(p.n_comps) * ((p.sp.count + 255) / 256);
   if (units <= 0) return cudaSuccess;
   const unsigned blocks = static_cast<unsigned>(units * p.cl_size);

@@ -177,6 +177,10 @@ def test_cluster_walk_equals_cooperative_walk(shape, monkeypatch):
     pp, dp, m, layers, d, f = shape
     sg = generate_graph(_spec(pp, dp, m, layers, d, f, estimate=True))
     spec = ScenarioSpec(count=600, first=8, seed=17, jitter=0.2)
+    # an odd first id keeps the cooperative walk (scenario pairs share Philox)
+    before = N.walk_counts()
+    simulate_batch(sg.graph, ScenarioSpec(count=64, first=9, seed=17, jitter=0.2))
+    assert N.walk_counts()[4] == before[4]
     out = {}
     for env in ("1", "0"):
         monkeypatch.setenv("LUMOS_CLUSTER", env)
