@@ -10,6 +10,20 @@
 // a completion heap keyed (end, id); each iteration starts the smallest-key
 // startable lane head (drain_startable) and then pops every completion at the
 // next end time.  Deadlock -> status -1 (SimulationError in the reference).
+//
+// drain_startable scans every lane per start in the reference (O(V·L)).  Here
+// the free lanes with a non-empty ready set sit in an indexed min-heap keyed
+// by their head task, so a start costs O(log L):
+//   * the smallest head is popped; if its rule fails the lane is parked (the
+//     reference skips it in that scan and rescans it after the next start);
+//   * a start with duration > 0 cannot unblock a parked head (its lane becomes
+//     busy, and an event sync bound to it needs sim_end <= now), so parked
+//     lanes stay parked; a zero-duration start (which also completes, and may
+//     change heads) and every time advance return all parked lanes to the heap;
+//   * a lane leaves the heap while busy and re-enters when its completion pops
+//     (one positive-duration task per lane is in flight, so lane clock == the
+//     end of that completion).
+// The start order therefore equals the reference's scan order exactly.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,7 +46,12 @@ struct DesScratch {
   int32_t* heap;       // [n]  per-lane ready heaps (lane_off regions)
   int32_t* comp_id;    // [n]
   int32_t* hsize;      // [nl]
+  int32_t* lheap;      // [nl] free lanes with a non-empty ready set, min by head key
+  int32_t* lpos;       // [nl] position in lheap; kOut / kParked
+  int32_t* parked;     // [nl]
 };
+
+constexpr int32_t kOut = -1, kParked = -2;
 
 __device__ DesScratch carve(char* base, int32_t n, int32_t nl) {
   DesScratch s;
@@ -47,18 +66,73 @@ __device__ DesScratch carve(char* base, int32_t n, int32_t nl) {
   s.heap = p32 + n;
   s.comp_id = p32 + 2 * static_cast<int64_t>(n);
   s.hsize = p32 + 3 * static_cast<int64_t>(n);
+  s.lheap = s.hsize + nl;
+  s.lpos = s.lheap + nl;
+  s.parked = s.lpos + nl;
   return s;
 }
 
 struct Des {
   const DesParams& P;
   DesScratch s;
+  int64_t now = 0;
+  int32_t lsize = 0, nparked = 0;
 
   __device__ bool key_less(int32_t a, int32_t b) const {
     const int64_t ka = P.ostart[a], kb = P.ostart[b];
     return ka < kb || (ka == kb && a < b);
   }
-  // ready heap of lane l (min by (original_start, id))
+  __device__ int32_t head(int32_t l) const { return s.heap[P.lane_off[l]]; }
+  // lane heap: free lanes (clock <= now) with a non-empty ready set
+  __device__ void lh_set(int32_t i, int32_t l) {
+    s.lheap[i] = l;
+    s.lpos[l] = i;
+  }
+  __device__ void lh_up(int32_t i) {
+    const int32_t l = s.lheap[i];
+    const int32_t hl = head(l);
+    while (i > 0) {
+      const int32_t p = (i - 1) >> 1;
+      if (!key_less(hl, head(s.lheap[p]))) break;
+      lh_set(i, s.lheap[p]);
+      i = p;
+    }
+    lh_set(i, l);
+  }
+  __device__ void lh_push(int32_t l) {
+    lh_set(lsize, l);
+    lh_up(lsize++);
+  }
+  __device__ int32_t lh_pop() {
+    const int32_t top = s.lheap[0];
+    s.lpos[top] = kOut;
+    const int32_t n = --lsize;
+    if (n > 0) {
+      const int32_t l = s.lheap[n];
+      const int32_t hl = head(l);
+      int32_t i = 0;
+      for (;;) {
+        const int32_t a = 2 * i + 1, b = a + 1;
+        int32_t m = -1, hm = hl;
+        if (a < n && key_less(head(s.lheap[a]), hm)) {
+          m = a;
+          hm = head(s.lheap[a]);
+        }
+        if (b < n && key_less(head(s.lheap[b]), hm)) m = b;
+        if (m < 0) break;
+        lh_set(i, s.lheap[m]);
+        i = m;
+      }
+      lh_set(i, l);
+    }
+    return top;
+  }
+  __device__ void unpark_all() {
+    for (int32_t k = 0; k < nparked; ++k) lh_push(s.parked[k]);
+    nparked = 0;
+  }
+  // ready heap of lane l (min by (original_start, id)); a new head of a lane
+  // in the lane heap moves it up, a free idle lane enters it
   __device__ void ready_push(int32_t l, int32_t t) {
     int32_t* h = s.heap + P.lane_off[l];
     int32_t i = s.hsize[l]++;
@@ -70,6 +144,12 @@ struct Des {
       h[i] = h[p];
       h[p] = x;
       i = p;
+    }
+    const int32_t pos = s.lpos[l];
+    if (pos >= 0) {
+      if (i == 0) lh_up(pos);
+    } else if (pos == kOut && s.clock[l] <= now) {
+      lh_push(l);
     }
   }
   __device__ void ready_pop(int32_t l) {
@@ -188,9 +268,13 @@ __global__ void des_kernel(DesParams P) {
     RtCol rc{};
     if (P.has_rt) rc = rt_col(P.rt, col);
     const int64_t W = P.W;
+    E.now = W;
+    E.lsize = 0;
+    E.nparked = 0;
     for (int32_t l = 0; l < nl; ++l) {
       s.clock[l] = W;
       s.hsize[l] = 0;
+      s.lpos[l] = kOut;
     }
     for (int32_t t = 0; t < n; ++t) {
       s.indeg[t] = P.indeg0[t];
@@ -198,24 +282,20 @@ __global__ void des_kernel(DesParams P) {
     }
     for (int32_t t = 0; t < n; ++t)
       if (s.indeg[t] == 0) E.ready_push(P.lane_of[t], t);
-    int64_t now = W;
     int32_t unstarted = n, comp = 0;
     bool dead = false;
     for (;;) {
-      // drain_startable (simulate.cpp:239-255)
-      for (;;) {
-        int32_t best = -1, best_lane = -1;
-        for (int32_t l = 0; l < nl; ++l) {
-          if (s.clock[l] > now || s.hsize[l] == 0) continue;
-          const int32_t head = s.heap[P.lane_off[l]];
-          if (!E.rule_ok(head, l, now)) continue;
-          if (best < 0 || E.key_less(head, best)) {
-            best = head;
-            best_lane = l;
-          }
+      // drain_startable (simulate.cpp:239-255): smallest startable head first
+      const int64_t now = E.now;
+      while (E.lsize > 0) {
+        const int32_t lane = E.lh_pop();
+        const int32_t best = E.head(lane);
+        if (!E.rule_ok(best, lane, now)) {  // the lane stalls behind its sync
+          s.lpos[lane] = kParked;
+          s.parked[E.nparked++] = lane;
+          continue;
         }
-        if (best < 0) break;
-        E.ready_pop(best_lane);
+        E.ready_pop(lane);
         const int64_t b = P.has_rt ? rt_task(P.rt, rc, best) : P.base[best];
         const int64_t d = scenario_duration<-1>(P.sp, ts, best, b, P.cls[best]);
         s.sim_start[best] = now;
@@ -223,8 +303,10 @@ __global__ void des_kernel(DesParams P) {
         --unstarted;
         if (d == 0) {
           E.complete(best);
+          if (s.lpos[lane] == kOut && s.hsize[lane] > 0) E.lh_push(lane);
+          E.unpark_all();
         } else {
-          s.clock[best_lane] = now + d;
+          s.clock[lane] = now + d;
           E.comp_push(comp, now + d, best);
         }
       }
@@ -232,13 +314,17 @@ __global__ void des_kernel(DesParams P) {
         dead = unstarted != 0;
         break;
       }
+      // advance to the next completion time (completing does not read now)
       const int64_t t2 = s.comp_t[0];
+      E.now = t2;
       while (comp > 0 && s.comp_t[0] == t2) {
         const int32_t done = s.comp_id[0];
         E.comp_pop(comp);
         E.complete(done);
+        const int32_t l = P.lane_of[done];
+        if (s.lpos[l] == kOut && s.hsize[l] > 0) E.lh_push(l);
       }
-      now = t2;
+      E.unpark_all();
     }
     if (dead) {  // span_hi carries the blocked-task count for the error message
       P.status[col] = -1;
@@ -341,7 +427,7 @@ int debug_bounds_status_des() { return 0; }
 
 size_t des_scratch_bytes(int32_t n, int32_t nl) {
   const size_t b = (static_cast<size_t>(n) * 3 + nl + 2 * static_cast<size_t>(n)) * 8 +
-                   (static_cast<size_t>(n) * 3 + nl) * 4;
+                   (static_cast<size_t>(n) * 3 + 4 * static_cast<size_t>(nl)) * 4;
   return (b + 255) / 256 * 256;
 }
 
