@@ -35,12 +35,14 @@ CONFIGS = {
     "config4": (dict(n_layers=96, d_model=12288, d_ffn=49152, n_heads=96, d_head=128),
                 dict(pp=4, dp=8, num_microbatches=32), 8, 16384,
                 "256-rank GPT-3 175B (pp4 dp8 m32 x TP8 replicas)"),
-    # estimate() semantics (build_pipeline + DurationHook): the generator's own
-    # dependency graph with p2p rendezvous / collective barrier gates
-    "config3": (dict(n_layers=48, d_model=12288, d_ffn=24576, n_heads=96, d_head=128,
-                     estimate=True),
+    # estimate() of a structural what-if: a measured pp2 dp2 trace of the 44B
+    # model is rebuilt for pp4 dp4 (rebuild_pipeline, transform.cpp:556-701)
+    # and the target pipeline's estimate graph (build_pipeline + DurationHook
+    # semantics: p2p rendezvous / collective barrier gates) is replayed
+    "config3": (dict(n_layers=48, d_model=12288, d_ffn=24576, n_heads=96, d_head=128),
                 dict(pp=4, dp=4, num_microbatches=16), 4, 4096,
-                "64-rank 44B estimate() pipeline (48L d12288 f24576, pp4 dp4 m16 x TP4 replicas)"),
+                "64-rank 44B estimate(): pipeline rebuilt for pp4 dp4 m16 from a measured "
+                "pp2 dp2 trace (48L d12288 f24576, x TP4 replicas)"),
     "config2": (dict(n_layers=48, d_model=6144, d_ffn=12288, n_heads=48, d_head=128),
                 dict(pp=2, dp=2, num_microbatches=4), 2, 1024,
                 "8-rank GPT-3 15B (pp2 dp2 m4 x TP2 replicas)"),
@@ -152,6 +154,21 @@ def walk_traffic(config, tile):
         return e
     except (OSError, ValueError):
         return None
+
+
+def config3_graph(model, par, tp):
+    """BASELINE config 3: the estimate graph of the pipeline rebuild_pipeline
+    lays out for the target parallelism from a measured source trace (the
+    generator's pp2 dp2 trace of the same model, Task.meta kept)."""
+    from paper_2504_09307_b200 import (ModelConfig, ParallelismConfig, WhatIfConfig,
+                                       pipeline_graph, rebuild_pipeline)
+    from paper_2504_09307_b200.synth import SynthSpec
+    src = dict(pp=2, dp=2, num_microbatches=par["num_microbatches"])
+    mc = ModelConfig(model["n_layers"], model["d_model"], model["d_ffn"], model["n_heads"],
+                     model["d_head"])
+    w = WhatIfConfig(mc, mc, ParallelismConfig(1, **src), ParallelismConfig(1, **par))
+    spec = rebuild_pipeline(SynthSpec(**model, **src), w)
+    return pipeline_graph(spec, estimate=True, tp=tp)
 
 
 # ------------------------------------------------------------ reference arm
@@ -384,7 +401,10 @@ def main():
     assert S_local % tile == 0, "scenarios per GPU must be a multiple of the tile"
 
     t0 = time.time()
-    sg = generate_graph(SynthSpec(tp=tp, **model, **par))
+    if args.config == "config3":
+        sg = config3_graph(model, par, tp)
+    else:
+        sg = generate_graph(SynthSpec(tp=tp, **model, **par))
     g = sg.graph
     t_gen = time.time() - t0
     t0 = time.time()

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 4
+#define TS_ABI_VERSION 5
 
 /* error codes (0 = success) */
 enum {
@@ -276,6 +276,9 @@ typedef struct {
   int64_t origin;
   int32_t estimate;   /* 0 replay graph, 1 estimate graph */
   int32_t slice_rank; /* -1 all ranks; else slice_rank (build.cpp:544-580) */
+  int32_t keep_meta;  /* replay graph: keep Task.meta + correlation ids (the
+                         source of a structural what-if, ts_rebuild_pipeline) */
+  int32_t pad;
 } ts_synth_spec;
 
 typedef struct ts_host_graph ts_host_graph;
@@ -339,6 +342,37 @@ void ts_pipeline_defaults(ts_pipeline_spec* spec);
 int ts_pipeline_graph(const ts_pipeline_spec* spec, int32_t estimate, int32_t tp,
                       ts_host_graph** out, int64_t* truth_makespan);
 
+/* Structural what-if (estimate()'s host step): the PipelineSpec the
+ * reference's rebuild_pipeline (transform.cpp:556-701) constructs from a
+ * measured source graph — tag_tasks (:71-162), measure_pipeline (:378-502),
+ * derive_vocab_bytes (:504-530), target stages with an AnalyticalCostModel —
+ * for scale_pp / change_layers / apply_whatif's structural branch
+ * (transform.hpp:56-72).  The source must keep its Task.meta (ts_synth_spec /
+ * ts_ingest_options keep_meta).  *out = NULL with TS_OK when the target
+ * differs in nothing the rebuild cares about (the reference returns the
+ * source graph).  Replay the result with ts_pipeline_graph (estimate = 1 for
+ * batched estimate(), 0 for the replay graph build_pipeline + graph_from_events
+ * yields).  Errors: TS_E_INVALID_ARGUMENT with the TransformError text. */
+typedef struct {                 /* ModelConfig (types.hpp:89-96) */
+  int64_t n_params;
+  int32_t n_layers, d_model, d_ffn, n_heads, d_head, pad;
+} ts_model_config;
+typedef struct {                 /* ParallelismConfig (types.hpp:98-103) */
+  int32_t tp, pp, dp, num_microbatches;
+} ts_par_config;
+typedef struct {                 /* WhatIfConfig (transform.hpp:28-41) */
+  ts_model_config source_model, target_model;
+  ts_par_config source_par, target_par;
+  double alpha_us, bytes_per_us; /* AnalyticalCostModel(alpha_us, bytes_per_us) */
+  int64_t activation_bytes;      /* activation_bytes_per_microbatch */
+  const char* tag_policy_json;   /* TagPolicy::from_json text, NULL = defaults */
+} ts_whatif;
+typedef struct ts_pipeline ts_pipeline;
+int ts_rebuild_pipeline(const ts_host_graph* source, const ts_whatif* whatif, ts_pipeline** out);
+/* the rebuilt spec; valid while the ts_pipeline lives */
+const ts_pipeline_spec* ts_pipeline_spec_get(const ts_pipeline* p);
+void ts_pipeline_free(ts_pipeline* p);
+
 /* build_graph (build.cpp:338-510) over one rank's events, SoA.  cat is the
  * EventCategory (types.hpp:20-27); corr = -1, stream = -1 and
  * arg_event / arg_stream = INT64_MIN mean absent.  names is a '\n'-separated
@@ -377,6 +411,8 @@ typedef struct {
   const char* window;            /* NULL = "full" */
   const char* categories_path;   /* or NULL */
   const char* policy_path;       /* or NULL */
+  int32_t keep_meta;             /* keep Task.meta + correlation ids (ts_rebuild_pipeline) */
+  int32_t pad;
 } ts_ingest_options;
 int ts_ingest_traces_ex(const ts_ingest_options* options, ts_host_graph** out);
 

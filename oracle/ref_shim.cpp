@@ -20,6 +20,8 @@
 #include <chrono>
 #include <limits>
 #include <cstdint>
+#include <cstdio>
+#include <memory>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -649,6 +651,55 @@ void* ref_apply_retime(void* h, const int64_t* src_model, const int64_t* tgt_mod
     if (src_dp != tgt_dp) out = scale_dp(out, src_dp, tgt_dp, model);
     auto* r = new RefGraph;
     r->g = std::move(out);
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// apply_whatif (transform.cpp:713-760) with AnalyticalCostModel(alpha,
+// bytes_per_us).  model = {n_params, n_layers, d_model, d_ffn, n_heads,
+// d_head}, par = {tp, pp, dp, num_microbatches}.  Returns a new handle (the
+// transformed graph) or NULL (message in ref_last_error()); notes gets the
+// TransformResult notes joined by '\n' (truncated to cap).
+void* ref_apply_whatif(void* h, const int64_t* src_model, const int64_t* tgt_model,
+                       const int32_t* src_par, const int32_t* tgt_par, double alpha,
+                       double bytes_per_us, int64_t activation_bytes, char* notes, int64_t cap) {
+  try {
+    auto model = [](const int64_t* m) {
+      ModelConfig c;
+      c.n_params = m[0];
+      c.n_layers = static_cast<int>(m[1]);
+      c.d_model = static_cast<int>(m[2]);
+      c.d_ffn = static_cast<int>(m[3]);
+      c.n_heads = static_cast<int>(m[4]);
+      c.d_head = static_cast<int>(m[5]);
+      return c;
+    };
+    auto par = [](const int32_t* p) {
+      ParallelismConfig c;
+      c.tp = p[0];
+      c.pp = p[1];
+      c.dp = p[2];
+      c.num_microbatches = p[3];
+      return c;
+    };
+    WhatIfConfig cfg;
+    cfg.source_model = model(src_model);
+    cfg.target_model = model(tgt_model);
+    cfg.source_par = par(src_par);
+    cfg.target_par = par(tgt_par);
+    cfg.activation_bytes = activation_bytes;
+    cfg.cost_model = std::make_shared<AnalyticalCostModel>(alpha, bytes_per_us);
+    TransformResult res = apply_whatif(static_cast<RefGraph*>(h)->g, cfg);
+    if (notes && cap > 0) {
+      std::string all;
+      for (const auto& n : res.notes) all += n + "\n";
+      std::snprintf(notes, static_cast<size_t>(cap), "%s", all.c_str());
+    }
+    auto* r = new RefGraph;
+    r->g = std::move(res.graph);
     return r;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -10,7 +10,9 @@ from .graph import (COMMUNICATION, COMPUTE, CPU_THREAD, CUDA_STREAM, DEVICE_SYNC
                     STREAM_SYNC, DeviceError, ExecutionGraph, GraphError, SimulatedTrace,
                     SimulationError, UnsupportedGraphError)
 from .replay import BatchResult, DeviceGraph, Retime, ScenarioSpec, simulate, simulate_batch
-from .pipeline import KernelSpec, PipelineSpec, StageSpec, estimate_batch, pipeline_graph
+from .pipeline import (KernelSpec, ModelConfig, ParallelismConfig, PipelineSpec, StageSpec,
+                       WhatIfConfig, estimate_batch, estimate_whatif, pipeline_graph,
+                       rebuild_pipeline)
 
 __all__ = [
     "Retime",
@@ -18,5 +20,6 @@ __all__ = [
     "DeviceError", "DeviceGraph", "ScenarioSpec", "BatchResult", "simulate", "simulate_batch",
     "CPU_THREAD", "CUDA_STREAM", "STREAM_SYNC", "DEVICE_SYNC", "EVENT_SYNC", "COMPUTE",
     "COMMUNICATION", "KernelSpec", "StageSpec", "PipelineSpec", "pipeline_graph",
-    "estimate_batch",
+    "estimate_batch", "ModelConfig", "ParallelismConfig", "WhatIfConfig", "rebuild_pipeline",
+    "estimate_whatif",
 ]

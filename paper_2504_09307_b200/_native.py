@@ -77,7 +77,7 @@ class TsResult(C.Structure):
                 ("pad2", C.c_int32), ("n_fixups", i32p)]
 
 
-ABI_VERSION = 4  # TS_ABI_VERSION in include/lumos_b200.h
+ABI_VERSION = 5  # TS_ABI_VERSION in include/lumos_b200.h
 _lib = None
 
 
@@ -140,4 +140,5 @@ EXPORTED = ["ts_abi_version", "ts_last_error", "ts_kernel_launches", "ts_graph_c
             "ts_profile_read", "ts_synth_defaults", "ts_synth_graph", "ts_host_graph_desc",
             "ts_host_graph_op_index", "ts_host_graph_n_ops", "ts_host_graph_name_ids",
             "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph",
-            "ts_ingest_traces"]
+            "ts_ingest_traces", "ts_ingest_traces_ex", "ts_pipeline_defaults", "ts_pipeline_graph",
+            "ts_rebuild_pipeline", "ts_pipeline_spec_get", "ts_pipeline_free"]

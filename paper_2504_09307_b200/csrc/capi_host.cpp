@@ -1,6 +1,7 @@
 // capi_host.cpp — extern "C" entry points of the host-side graph sources
 // (synthetic generator, trace-event graph builder); see include/lumos_b200.h.
 #include <cstring>
+#include <deque>
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -8,6 +9,7 @@
 
 #include "ingest.hpp"
 #include "lumos_b200.h"
+#include "rebuild.hpp"
 #include "synth.hpp"
 #include "trace_ingest.hpp"
 
@@ -15,6 +17,16 @@ using namespace lumos;
 
 struct ts_host_graph {
   SynthOutput s;
+};
+
+// a rebuilt PipelineSpec and the POD view of it (pointers into `p`)
+struct ts_pipeline {
+  lumos::PipelineStr p;
+  ts_pipeline_spec spec{};
+  std::vector<ts_stage_spec> stages;
+  std::deque<std::vector<ts_kernel_spec>> kernels;
+  std::deque<std::vector<ts_kernel_list>> layers;
+  std::deque<std::vector<const char*>> strs;
 };
 
 namespace lumos {
@@ -134,6 +146,7 @@ int ts_ingest_traces_ex(const ts_ingest_options* opt, ts_host_graph** out) {
   o.threads = opt->n_threads;
   if (opt->manifest) o.manifest = opt->manifest;
   if (opt->window) o.window = opt->window;
+  o.keep_meta = opt->keep_meta != 0;
   std::string err, text;
   if (opt->categories_path) {
     if (!read_text(opt->categories_path, text, err) || !categories_from_json(text, o.categories, err))
@@ -145,6 +158,87 @@ int ts_ingest_traces_ex(const ts_ingest_options* opt, ts_host_graph** out) {
   }
   return ingest(o, out);
 }
+
+static void build_pod(ts_pipeline& h) {
+  auto list = [&](const std::vector<KernelStr>& ks) {
+    h.kernels.emplace_back();
+    std::vector<ts_kernel_spec>& v = h.kernels.back();
+    for (const KernelStr& k : ks) {
+      h.strs.emplace_back();
+      std::vector<const char*>& kv = h.strs.back();
+      for (const auto& a : k.args) kv.push_back(a.first.c_str());
+      for (const auto& a : k.args) kv.push_back(a.second.c_str());
+      const int32_t na = static_cast<int32_t>(k.args.size());
+      v.push_back({k.name.c_str(), k.duration, k.op_class, na, kv.data(), kv.data() + na});
+    }
+    return ts_kernel_list{v.data(), static_cast<int32_t>(v.size()), 0};
+  };
+  const PipelineStr& p = h.p;
+  pipeline_defaults(&h.spec);
+  h.stages.resize(p.stages.size());
+  for (size_t s = 0; s < p.stages.size(); ++s) {
+    const StageStr& st = p.stages[s];
+    ts_stage_spec& c = h.stages[s];
+    c.n_layers = static_cast<int32_t>(st.layers_fwd.size());
+    h.layers.emplace_back();
+    std::vector<ts_kernel_list>& lf = h.layers.back();
+    for (const auto& l : st.layers_fwd) lf.push_back(list(l));
+    h.layers.emplace_back();
+    std::vector<ts_kernel_list>& lb = h.layers.back();
+    for (const auto& l : st.layers_bwd) lb.push_back(list(l));
+    c.layers_fwd = lf.data();
+    c.layers_bwd = lb.data();
+    c.pre_fwd = list(st.pre_fwd);
+    c.post_fwd = list(st.post_fwd);
+    c.pre_bwd = list(st.pre_bwd);
+    c.post_bwd = list(st.post_bwd);
+    c.reduce = list(st.reduce);
+    c.optimizer = list(st.optimizer);
+  }
+  h.spec.pp = p.pp;
+  h.spec.dp = p.dp;
+  h.spec.num_microbatches = p.num_microbatches;
+  h.spec.n_stages = static_cast<int32_t>(h.stages.size());
+  h.spec.stages = h.stages.data();
+  h.spec.launch_us = p.launch;
+  h.spec.record_us = p.record;
+  h.spec.wait_us = p.wait;
+  h.spec.sync_us = p.sync;
+  h.spec.p2p_send_us = p.p2p_send;
+  h.spec.p2p_recv_base_us = p.p2p_recv_base;
+  h.spec.activation_bytes = p.activation_bytes;
+  h.spec.origin = p.origin;
+}
+
+int ts_rebuild_pipeline(const ts_host_graph* source, const ts_whatif* w, ts_pipeline** out) {
+  if (!source || !w || !out) return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  WhatIfLite wl;
+  wl.source_model = w->source_model;
+  wl.target_model = w->target_model;
+  wl.source_par = w->source_par;
+  wl.target_par = w->target_par;
+  wl.alpha_us = w->alpha_us;
+  wl.bytes_per_us = w->bytes_per_us;
+  wl.activation_bytes = w->activation_bytes;
+  std::string err;
+  if (w->tag_policy_json && !tag_policy_from_json(w->tag_policy_json, wl.policy, err))
+    return set_error(TS_E_INVALID_ARGUMENT, err);
+  auto* h = new ts_pipeline;
+  bool unchanged = false;
+  const int rc = rebuild_pipeline(source->s.graph, source->s.names, wl, h->p, unchanged, err);
+  if (rc != TS_OK || unchanged) {
+    delete h;
+    return rc == TS_OK ? TS_OK : set_error(rc, err);
+  }
+  build_pod(*h);
+  *out = h;
+  return TS_OK;
+}
+
+const ts_pipeline_spec* ts_pipeline_spec_get(const ts_pipeline* p) { return p ? &p->spec : nullptr; }
+
+void ts_pipeline_free(ts_pipeline* p) { delete p; }
 
 int ts_build_rank_graph(int32_t rank, int64_t n_events, const int32_t* name, const uint8_t* cat,
                         const int64_t* ts, const int64_t* dur, const int32_t* tid,

@@ -126,6 +126,8 @@ void HostGraph::append_relabelled(const HostGraph& src, int32_t new_rank, bool f
   cat(task_kind, src.task_kind);
   cat(name, src.name);
   cat(op_index, src.op_index);
+  cat(corr, src.corr);
+  cat(meta, src.meta);
   for (size_t e = 0; e < src.edge_from.size(); ++e) {
     edge_from.push_back(src.edge_from[e] + base);
     edge_to.push_back(src.edge_to[e] + base);
@@ -162,7 +164,8 @@ void HostGraph::append_relabelled(const HostGraph& src, int32_t new_rank, bool f
 void HostGraph::append(const HostGraph& src, bool first) { append_relabelled(src, INT32_MIN, first); }
 
 int build_rank_graph(const std::vector<Event>& events, const Names& names, int32_t rank,
-                     const BuildPolicyLite& policy, HostGraph& g, std::string& err) {
+                     const BuildPolicyLite& policy, HostGraph& g, std::string& err,
+                     const std::vector<MetaList>* meta) {
   g = HostGraph{};
   if (events.empty()) return TS_OK;
 
@@ -240,6 +243,11 @@ int build_rank_graph(const std::vector<Event>& events, const Names& names, int32
       g.lane_kind[t] = TS_LANE_CPU_THREAD;
       g.lane[t] = e.tid;
     }
+  }
+  if (meta) {
+    g.corr = corr;
+    g.meta.resize(n);
+    for (int32_t t = 0; t < n; ++t) g.meta[t] = (*meta)[kept[t]];
   }
   g.window_start = g.original_start[0];
   g.window_end = g.window_start;

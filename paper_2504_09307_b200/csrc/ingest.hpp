@@ -38,6 +38,9 @@ struct Event {
   int64_t op_index = -1;       // generator cost index (estimate mode), -1 = none
 };
 
+// TraceEvent::args / Task.meta as (key, value) strings in key order
+using MetaList = std::vector<std::pair<std::string, std::string>>;
+
 struct Names {
   std::vector<std::string> str;
   std::unordered_map<std::string, int32_t> idx;
@@ -69,6 +72,10 @@ struct HostGraph {
   std::vector<int64_t> rt_bytes;
   std::vector<int32_t> rt_group;
   std::vector<int64_t> rt_mnk;
+  // Task.correlation_id (-1 = none) and Task.meta (build.cpp:355, 363), kept
+  // on request for the structural what-if rebuild (rebuild.cpp); empty otherwise
+  std::vector<int64_t> corr;
+  std::vector<MetaList> meta;
   int32_t n_diagnostics = 0;
 
   int32_t n() const { return static_cast<int32_t>(duration.size()); }
@@ -104,8 +111,11 @@ bool policy_from_json(const std::string& text, BuildPolicyLite& out, std::string
 
 // build_graph (build.cpp:338-510) over one rank's events.  Returns TS_OK or
 // TS_E_GRAPH (cycle / GPU event without stream) with `err` set.
+// With `meta` (parallel to events), the tasks keep their event's args and
+// correlation id (HostGraph::meta / corr).
 int build_rank_graph(const std::vector<Event>& events, const Names& names, int32_t rank,
-                     const BuildPolicyLite& policy, HostGraph& out, std::string& err);
+                     const BuildPolicyLite& policy, HostGraph& out, std::string& err,
+                     const std::vector<MetaList>* meta = nullptr);
 
 // OpClass of an event (build.cpp:93-103), under `policy` or the default.
 uint8_t classify_event(const Event& e, const Names& names, const BuildPolicyLite& policy);

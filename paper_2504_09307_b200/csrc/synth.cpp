@@ -64,6 +64,7 @@ struct KSpec {
   int32_t name;
   int64_t dur;
   KMeta meta{};
+  MetaList args{};  // KernelSpec::args (kept for traces that carry Task.meta)
 };
 
 struct StageSpec {
@@ -98,6 +99,7 @@ struct POp {
   int64_t cpu_dur = 0, kernel_dur = 0;
   int64_t cpu_index = -1, kernel_index = -1;  // cost indices
   int32_t kname = 0;
+  int32_t kargs = -1;                         // kernel event args (keep_meta)
   int stream = -1;
   int64_t event_id = -1, corr = -1;
   uint64_t recv_key = 0, send_key = 0, barrier_key = 0, pub_key = 0;
@@ -123,11 +125,20 @@ struct RankState {
 struct GenEvent {
   Event ev;
   int64_t cost = 0;  // intrinsic duration (estimate graph)
+  int32_t args = -1; // TraceEvent::args (Builder::arg_lists), keep_meta only
 };
+
+// args with tags applied over them, key order (launch_op, pipeline.cpp:119-127)
+MetaList with_tags(const MetaList& args, const MetaList& tags) {
+  std::map<std::string, std::string> m(args.begin(), args.end());
+  for (const auto& [k, v] : tags) m[k] = v;
+  return MetaList(m.begin(), m.end());
+}
 
 class Builder {
  public:
-  Builder(const PSpec& s, Names& names) : s_(s), names_(names) {
+  Builder(const PSpec& s, Names& names, bool keep_meta = false)
+      : s_(s), names_(names), keep_meta_(keep_meta) {
     n_launch_ = names.get("cudaLaunchKernel");
     n_record_ = names.get("cudaEventRecord");
     n_wait_ = names.get("cudaStreamWaitEvent");
@@ -143,6 +154,7 @@ class Builder {
   }
 
   std::vector<GenEvent> events;
+  std::vector<MetaList> arg_lists;  // keep_meta: the events' args
   std::vector<KMeta> kmeta;  // by kernel cost index (op_index)
   std::vector<std::pair<int64_t, int64_t>> edges;             // estimate graph, event ids
   std::vector<std::tuple<int64_t, int64_t, uint8_t>> gates;  // (from, to, kind)
@@ -151,6 +163,7 @@ class Builder {
  private:
   const PSpec& s_;
   Names& names_;
+  bool keep_meta_ = false;
   int32_t n_launch_, n_record_, n_wait_, n_ssync_, n_dsync_, n_sendrecv_;
   std::vector<ThreadOps> threads_;
   std::map<int, RankState> state_;
@@ -165,9 +178,17 @@ class Builder {
   }
   int rank_of(int stage, int dp) const { return stage + s_.pp * dp; }
 
-  POp launch(const KSpec& k) {
+  int32_t add_args(MetaList a) {
+    arg_lists.push_back(std::move(a));
+    return static_cast<int32_t>(arg_lists.size()) - 1;
+  }
+  static MetaList slot_tags(bool fwd, int mb) {  // pipeline.cpp:206-216
+    return {{"mb", std::to_string(mb)}, {"phase", fwd ? "fwd" : "bwd"}};
+  }
+  POp launch(const KSpec& k, const MetaList& tags = {}) {
     POp op;
     op.type = P_LAUNCH;
+    if (keep_meta_) op.kargs = add_args(with_tags(k.args, tags));
     op.cpu_index = op_index_;
     op.cpu_dur = cost(s_.launch);
     op.kernel_index = op_index_;
@@ -208,12 +229,20 @@ class Builder {
     return op;
   }
 
+  // p2p_kernel's args (pipeline.cpp:157-169)
+  MetaList p2p_args(bool send, bool fwd, int peer) const {
+    if (!keep_meta_) return {};
+    return {{"bytes", std::to_string(s_.act_bytes)}, {"collective", "sendrecv"},
+            {"dir", send ? "send" : "recv"}, {"peer_stage", std::to_string(peer)},
+            {"phase", fwd ? "fwd" : "bwd"}, {"region", "p2p"}};
+  }
   void emit_recv(std::vector<POp>& ops, bool fwd, int stage, int dp, int mb) {
     int from = fwd ? stage - 1 : stage + 1;
     KMeta rm;
     rm.kind = TS_RT_P2P_RECV;
     rm.bytes = s_.act_bytes;
-    POp r = launch({n_sendrecv_, s_.p2p_recv_base, rm});
+    POp r = launch({n_sendrecv_, s_.p2p_recv_base, rm, p2p_args(false, fwd, from)},
+                   {{"mb", std::to_string(mb)}});
     r.stream = s_.p2p_stream;
     r.recv_key = key(1, fwd, from, dp, mb);
     ops.push_back(r);
@@ -230,32 +259,53 @@ class Builder {
     KMeta sm;
     sm.kind = TS_RT_P2P_SEND;
     sm.bytes = s_.act_bytes;
-    POp snd = launch({n_sendrecv_, s_.p2p_send, sm});
+    const int to = fwd ? stage + 1 : stage - 1;
+    POp snd = launch({n_sendrecv_, s_.p2p_send, sm, p2p_args(true, fwd, to)},
+                     {{"mb", std::to_string(mb)}});
     snd.stream = s_.p2p_stream;
     snd.send_key = key(1, fwd, stage, dp, mb);
     ops.push_back(snd);
   }
-  void emit_compute(std::vector<POp>& ops, const std::vector<KSpec>& ks) {
+  void emit_compute(std::vector<POp>& ops, const std::vector<KSpec>& ks,
+                    const MetaList& tags = {}) {
     for (const KSpec& k : ks) {
-      POp op = launch(k);
+      POp op = launch(k, tags);
       op.stream = s_.compute_stream;
       ops.push_back(op);
     }
   }
+  // tags of a slot's compute (pipeline.cpp:206-216, 224-272); built only
+  // when the trace keeps its args
+  MetaList tags(bool fwd, int mb, const char* region, int layer = -1) const {
+    if (!keep_meta_) return {};
+    MetaList t = slot_tags(fwd, mb);
+    if (layer >= 0) t.emplace_back("layer", std::to_string(layer));
+    if (region) t.emplace_back("region", region);
+    return t;
+  }
+  int first_layer(int stage) const {
+    int acc = 0;
+    for (int q = 0; q < stage; ++q) acc += static_cast<int>(s_.stages[q].fwd.size());
+    return acc;
+  }
   void emit_fwd(std::vector<POp>& ops, int stage, int dp, int mb) {
     const StageSpec& st = s_.stages[stage];
     if (stage > 0) emit_recv(ops, true, stage, dp, mb);
-    if (stage == 0) emit_compute(ops, st.pre_fwd);
-    for (const auto& layer : st.fwd) emit_compute(ops, layer);
-    if (stage == s_.pp - 1) emit_compute(ops, st.post_fwd);
+    if (stage == 0) emit_compute(ops, st.pre_fwd, tags(true, mb, "embed"));
+    const int base = first_layer(stage);
+    for (size_t l = 0; l < st.fwd.size(); ++l)
+      emit_compute(ops, st.fwd[l], tags(true, mb, nullptr, base + static_cast<int>(l)));
+    if (stage == s_.pp - 1) emit_compute(ops, st.post_fwd, tags(true, mb, "head"));
     if (stage < s_.pp - 1) emit_send(ops, true, stage, dp, mb);
   }
   void emit_bwd(std::vector<POp>& ops, int stage, int dp, int mb) {
     const StageSpec& st = s_.stages[stage];
     if (stage < s_.pp - 1) emit_recv(ops, false, stage, dp, mb);
-    if (stage == s_.pp - 1) emit_compute(ops, st.pre_bwd);
-    for (int l = static_cast<int>(st.bwd.size()) - 1; l >= 0; --l) emit_compute(ops, st.bwd[l]);
-    if (stage == 0) emit_compute(ops, st.post_bwd);
+    if (stage == s_.pp - 1) emit_compute(ops, st.pre_bwd, tags(false, mb, "head"));
+    const int base = first_layer(stage);
+    for (int l = static_cast<int>(st.bwd.size()) - 1; l >= 0; --l)
+      emit_compute(ops, st.bwd[l], tags(false, mb, nullptr, base + l));
+    if (stage == 0) emit_compute(ops, st.post_bwd, tags(false, mb, "embed"));
     if (stage > 0) emit_send(ops, false, stage, dp, mb);
   }
   void emit_tail(std::vector<POp>& ops, int stage, uint64_t gate_key) {
@@ -275,7 +325,7 @@ class Builder {
       ops.push_back(wait(s_.reduce_stream, ev));
       int seq = 0;
       for (const KSpec& k : st.reduce) {
-        POp op = launch(k);
+        POp op = launch(k, {{"region", "dp"}});
         op.stream = s_.reduce_stream;
         op.barrier_key = key(3, false, stage, 0, seq++);
         op.barrier_size = s_.dp;
@@ -287,7 +337,7 @@ class Builder {
       ops.push_back(wait(s_.compute_stream, ev2));
     }
     for (const KSpec& k : st.optimizer) {
-      POp op = launch(k);
+      POp op = launch(k, {{"region", "opt"}});
       op.stream = s_.compute_stream;
       gate(op);
     }
@@ -339,8 +389,9 @@ class Builder {
 
   int64_t emit(const ThreadOps& to, int32_t name, uint8_t cat, int64_t ts, int64_t dur,
                int tid, int stream, int64_t corr, int64_t arg_ev, int64_t arg_stream,
-               int64_t op_index, int64_t cost_dur) {
+               int64_t op_index, int64_t cost_dur, int32_t args = -1) {
     GenEvent g;
+    g.args = args;
     g.ev.name = name;
     g.ev.cat = cat;
     g.ev.ts = ts;
@@ -355,6 +406,15 @@ class Builder {
     g.cost = cost_dur;
     events.push_back(g);
     return static_cast<int64_t>(events.size()) - 1;
+  }
+
+  // a runtime call's args (pipeline.cpp:404-423)
+  int32_t event_args(int64_t event_id, int stream) {
+    if (!keep_meta_) return -1;
+    MetaList a;
+    if (event_id != kNoArg) a.emplace_back("event", std::to_string(event_id));
+    a.emplace_back("stream", std::to_string(stream));
+    return add_args(std::move(a));
   }
 
   // host op: thread-order edge + hand-off edges
@@ -403,7 +463,7 @@ class Builder {
         cpu_edges(st, to, op, evc);
         const int64_t evk = emit(to, op.kname, CAT_KERNEL, kstart, kend - kstart, op.stream,
                                  op.stream, op.corr, kNoArg, kNoArg, op.kernel_index,
-                                 op.kernel_dur);
+                                 op.kernel_dur, op.kargs);
         op.ev_cpu = evc;
         op.ev_kernel = evk;
         edges.emplace_back(evc, evk);
@@ -423,7 +483,8 @@ class Builder {
         auto lk = st.last_kernel_ev.find(op.stream);
         st.bind_ev[op.event_id] = lk == st.last_kernel_ev.end() ? -1 : lk->second;
         const int64_t ev = emit(to, n_record_, CAT_RUNTIME, cpu, op.cpu_dur, to.thread, -1, -1,
-                                op.event_id, op.stream, op.cpu_index, op.cpu_dur);
+                                op.event_id, op.stream, op.cpu_index, op.cpu_dur,
+                                event_args(op.event_id, op.stream));
         cpu_edges(st, to, op, ev);
         st.cpu_clock[to.thread] = cpu + op.cpu_dur;
         break;
@@ -434,7 +495,8 @@ class Builder {
         auto b = st.bind_ev.find(op.event_id);
         if (b != st.bind_ev.end() && b->second >= 0) st.pending[op.stream].push_back(b->second);
         const int64_t ev = emit(to, n_wait_, CAT_RUNTIME, cpu, op.cpu_dur, to.thread, -1, -1,
-                                op.event_id, op.stream, op.cpu_index, op.cpu_dur);
+                                op.event_id, op.stream, op.cpu_index, op.cpu_dur,
+                                event_args(op.event_id, op.stream));
         cpu_edges(st, to, op, ev);
         st.cpu_clock[to.thread] = cpu + op.cpu_dur;
         break;
@@ -442,7 +504,8 @@ class Builder {
       case P_SSYNC: {
         const int64_t wake = std::max(cpu, st.stream_clock[op.stream]);
         const int64_t ev = emit(to, n_ssync_, CAT_RUNTIME, wake, op.cpu_dur, to.thread, -1, -1,
-                                kNoArg, op.stream, op.cpu_index, op.cpu_dur);
+                                kNoArg, op.stream, op.cpu_index, op.cpu_dur,
+                                event_args(kNoArg, op.stream));
         cpu_edges(st, to, op, ev);
         auto lk = st.last_kernel_ev.find(op.stream);
         if (lk != st.last_kernel_ev.end()) edges.emplace_back(lk->second, ev);
@@ -507,7 +570,8 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
     g.m = m;
     g.n = n;
     g.k = k;
-    return KSpec{names.get(name), llr(static_cast<double>(base) * factor), g};
+    return KSpec{names.get(name), llr(static_cast<double>(base) * factor), g,
+                 {{"k", std::to_string(k)}, {"m", std::to_string(m)}, {"n", std::to_string(n)}}};
   };
   std::vector<KSpec> lf{gemm("gemm_qkv", t, d, d, 1.0), {names.get("attn_core"), sp.attn_misc_us},
                         gemm("gemm_mlp", t, f, d, 1.0)};
@@ -541,7 +605,10 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
       st.reduce.push_back({names.get("ncclDevKernel_AllReduce_Sum_f16"),
                            collective_cost_us(ALLREDUCE, rbytes, sp.dp, sp.alpha_us,
                                               sp.bytes_per_us),
-                           ar});
+                           ar,
+                           {{"bytes", std::to_string(rbytes)},
+                            {"collective", "allreduce"},
+                            {"group_size", std::to_string(sp.dp)}}});
     KMeta om;
     om.kind = TS_RT_OPT;
     om.bytes = rbytes;
@@ -549,7 +616,8 @@ PSpec pspec_for(const ts_synth_spec& sp, Names& names) {
         {names.get("adam_step"),
          llr(static_cast<double>(sp.optimizer_ref_us) * static_cast<double>(rbytes) /
              static_cast<double>(sp.optimizer_ref_bytes)),
-         om});
+         om,
+         {{"bytes", std::to_string(rbytes)}}});
     ps.stages.push_back(std::move(st));
   }
   return ps;
@@ -650,7 +718,12 @@ int pspec_of(const ts_pipeline_spec& c, Names& names, PSpec& ps, std::string& er
     outl.clear();
     for (int32_t i = 0; i < l.n; ++i) {
       const ts_kernel_spec& k = l.k[i];
-      outl.push_back({names.get(k.name ? k.name : ""), k.duration, kernel_meta(k, role)});
+      std::map<std::string, std::string> args;
+      for (int32_t a = 0; a < k.n_args; ++a)
+        if (k.arg_keys && k.arg_keys[a] && k.arg_values && k.arg_values[a])
+          args[k.arg_keys[a]] = k.arg_values[a];
+      outl.push_back({names.get(k.name ? k.name : ""), k.duration, kernel_meta(k, role),
+                      MetaList(args.begin(), args.end())});
     }
   };
   for (int32_t s = 0; s < c.pp; ++s) {
@@ -676,7 +749,7 @@ int pspec_of(const ts_pipeline_spec& c, Names& names, PSpec& ps, std::string& er
 }  // namespace
 
 int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, SynthOutput& out,
-                   std::string& err);
+                   std::string& err, bool keep_meta = false);
 
 void pipeline_defaults(ts_pipeline_spec* c) {
   std::memset(c, 0, sizeof(*c));
@@ -758,19 +831,20 @@ int synth_graph(const ts_synth_spec& sp, SynthOutput& out, std::string& err) {
   }
   out = SynthOutput{};
   const PSpec ps = pspec_for(sp, out.names);
-  return graph_of_pspec(ps, sp.estimate != 0, sp.tp, sp.slice_rank, out, err);
+  return graph_of_pspec(ps, sp.estimate != 0, sp.tp, sp.slice_rank, out, err,
+                        sp.keep_meta != 0 && sp.estimate == 0);
 }
 
 // The generated trace of a PipelineSpec as the replay graph (build_graph +
 // merge_ranks) or the estimate graph (generator dependencies + gates), with
 // tp replicas of every rank; out.names must hold the spec's name ids.
 int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, SynthOutput& out,
-                   std::string& err) {
+                   std::string& err, bool keep_meta) {
   if (tp < 1) {
     err = "tp must be >= 1";
     return TS_E_INVALID_ARGUMENT;
   }
-  Builder b(ps, out.names);
+  Builder b(ps, out.names, keep_meta);
   try {
     b.run();
   } catch (const std::exception& e) {
@@ -794,10 +868,15 @@ int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, Synth
   for (int r = 0; r < n_ranks; ++r) rank_begin[r + 1] += rank_begin[r];
   std::vector<int32_t> local(ne);  // event -> position within its rank
   std::vector<std::vector<Event>> per_rank(n_ranks);
+  std::vector<std::vector<MetaList>> per_rank_args(keep_meta ? n_ranks : 0);
   for (int64_t i : order) {
     const Event& e = b.events[i].ev;
     local[i] = static_cast<int32_t>(per_rank[e.pid].size());
     per_rank[e.pid].push_back(e);
+    if (keep_meta) {
+      const int32_t a = b.events[i].args;
+      per_rank_args[e.pid].push_back(a >= 0 ? b.arg_lists[a] : MetaList{});
+    }
   }
 
   // one graph per source rank
@@ -805,7 +884,8 @@ int graph_of_pspec(const PSpec& ps, bool estimate, int tp, int slice_rank, Synth
   BuildPolicyLite pol;
   for (int r = 0; r < n_ranks; ++r) {
     if (!estimate) {
-      int rc = build_rank_graph(per_rank[r], out.names, r, pol, rank_graphs[r], err);
+      int rc = build_rank_graph(per_rank[r], out.names, r, pol, rank_graphs[r], err,
+                                keep_meta ? &per_rank_args[r] : nullptr);
       if (rc != TS_OK) return rc;
       continue;
     }

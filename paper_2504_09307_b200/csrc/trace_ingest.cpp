@@ -145,10 +145,11 @@ struct RawEvent {
   std::string name;
   Event ev;
   RtMeta rt;
+  MetaList args;  // TraceEvent::args, only with IngestOptions::keep_meta
 };
 
-void parse_dom(const json& root, std::vector<RawEvent>& out,
-               const CatOverrides& cats) {  // trace_parse.cpp:79-154
+void parse_dom(const json& root, std::vector<RawEvent>& out, const CatOverrides& cats,
+               bool keep_args) {  // trace_parse.cpp:79-154
   const json* list = nullptr;
   if (root.is_array()) {
     list = &root;
@@ -197,6 +198,7 @@ void parse_dom(const json& root, std::vector<RawEvent>& out,
       for (auto it = args.begin(); it != args.end(); ++it) {
         const std::string& k = it.key();
         const std::string v = arg_to_string(it.value());
+        if (keep_args) r.args.emplace_back(k, v);
         int64_t x = 0;
         if (k == "event") {
           if (prefix_i64(v, x)) e.arg_event = x;
@@ -505,7 +507,7 @@ int ingest_traces(const IngestOptions& opts, Names& names, HostGraph& out,
       return;
     }
     try {
-      parse_dom(json::parse(text), parsed[i], opts.categories);
+      parse_dom(json::parse(text), parsed[i], opts.categories, opts.keep_meta);
     } catch (const ParseError& e) {
       errs[i] = path + ": " + e.msg;
     } catch (const json::parse_error& e) {
@@ -609,12 +611,21 @@ int ingest_traces(const IngestOptions& opts, Names& names, HostGraph& out,
   out = HostGraph{};
   for (std::size_t k = 0; k < graphs.size(); ++k) out.append(graphs[k], k == 0);
   task_rt.assign(out.n(), RtMeta{});
+  if (opts.keep_meta) {
+    out.corr.assign(out.n(), -1);
+    out.meta.assign(out.n(), MetaList{});
+  }
   for (int32_t t = 0; t < out.n(); ++t) {
     const int64_t o = out.op_index[t];
     if (o < 0) continue;
     const auto k = static_cast<std::size_t>(
         std::upper_bound(ord_base.begin(), ord_base.end(), o) - ord_base.begin() - 1);
-    task_rt[t] = ranks[k].second[static_cast<std::size_t>(o - ord_base[k])].rt;
+    RawEvent& r = ranks[k].second[static_cast<std::size_t>(o - ord_base[k])];
+    task_rt[t] = r.rt;
+    if (opts.keep_meta) {
+      out.corr[t] = r.ev.corr;
+      out.meta[t] = std::move(r.args);  // Task.meta = ev.args (build.cpp:363)
+    }
     out.op_index[t] = -1;  // a recorded trace has no generator cost index
   }
   return TS_OK;

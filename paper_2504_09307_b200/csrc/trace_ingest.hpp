@@ -27,6 +27,7 @@ struct IngestOptions {
   std::vector<std::pair<std::string, uint8_t>> categories;
   BuildPolicyLite policy;          // --policy (BuildPolicy::from_json)
   int threads = 0;                 // host threads (<= 0: all cores)
+  bool keep_meta = false;          // keep Task.meta / correlation ids (what-if rebuild)
 };
 
 // build_from_inputs (cli.cpp:118-137): parse_trace of every input,

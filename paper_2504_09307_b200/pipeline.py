@@ -168,14 +168,173 @@ class PipelineSpec:
         return c
 
 
+    @staticmethod
+    def from_c(c: TsPipelineSpec) -> "PipelineSpec":
+        """From the ts_pipeline_spec POD (e.g. ts_rebuild_pipeline's result)."""
+        def kl(lst):
+            out = []
+            for i in range(lst.n):
+                k = lst.k[i]
+                args = {k.arg_keys[a].decode(): k.arg_values[a].decode() for a in range(k.n_args)}
+                out.append(KernelSpec(k.name.decode(), int(k.duration), int(k.op_class), args))
+            return out
+        stages = []
+        for s in range(c.n_stages):
+            st = c.stages[s]
+            stages.append(StageSpec(layers_fwd=[kl(st.layers_fwd[l]) for l in range(st.n_layers)],
+                                    layers_bwd=[kl(st.layers_bwd[l]) for l in range(st.n_layers)],
+                                    pre_fwd=kl(st.pre_fwd), post_fwd=kl(st.post_fwd),
+                                    pre_bwd=kl(st.pre_bwd), post_bwd=kl(st.post_bwd),
+                                    reduce=kl(st.reduce), optimizer=kl(st.optimizer)))
+        return PipelineSpec(pp=c.pp, dp=c.dp, num_microbatches=c.num_microbatches, stages=stages,
+                            launch=c.launch_us, record=c.record_us, wait=c.wait_us,
+                            sync=c.sync_us, p2p_send=c.p2p_send_us,
+                            p2p_recv_base=c.p2p_recv_base_us,
+                            activation_bytes=c.activation_bytes, origin=c.origin,
+                            compute_stream=c.compute_stream, reduce_stream=c.reduce_stream,
+                            p2p_stream=c.p2p_stream, main_thread=c.main_thread,
+                            helper_thread=c.helper_thread, first_event=c.first_event,
+                            first_correlation=c.first_correlation)
+
+
+# ------------------------------------------------------ structural what-if
+class TsModelConfig(C.Structure):
+    _fields_ = [("n_params", C.c_int64), ("n_layers", C.c_int32), ("d_model", C.c_int32),
+                ("d_ffn", C.c_int32), ("n_heads", C.c_int32), ("d_head", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class TsParConfig(C.Structure):
+    _fields_ = [("tp", C.c_int32), ("pp", C.c_int32), ("dp", C.c_int32),
+                ("num_microbatches", C.c_int32)]
+
+
+class TsWhatIf(C.Structure):
+    _fields_ = [("source_model", TsModelConfig), ("target_model", TsModelConfig),
+                ("source_par", TsParConfig), ("target_par", TsParConfig),
+                ("alpha_us", C.c_double), ("bytes_per_us", C.c_double),
+                ("activation_bytes", C.c_int64), ("tag_policy_json", C.c_char_p)]
+
+
+@dataclass
+class ModelConfig:
+    """ModelConfig (types.hpp:89-96)."""
+    n_layers: int
+    d_model: int
+    d_ffn: int
+    n_heads: int
+    d_head: int
+    n_params: int = 0
+
+    def to_c(self) -> TsModelConfig:
+        return TsModelConfig(self.n_params, self.n_layers, self.d_model, self.d_ffn,
+                             self.n_heads, self.d_head, 0)
+
+
+@dataclass
+class ParallelismConfig:
+    """ParallelismConfig (types.hpp:98-103)."""
+    tp: int = 1
+    pp: int = 1
+    dp: int = 1
+    num_microbatches: int = 1
+
+    def to_c(self) -> TsParConfig:
+        return TsParConfig(self.tp, self.pp, self.dp, self.num_microbatches)
+
+
+@dataclass
+class WhatIfConfig:
+    """WhatIfConfig (transform.hpp:28-41) with an AnalyticalCostModel."""
+    source_model: ModelConfig
+    target_model: ModelConfig
+    source_par: ParallelismConfig
+    target_par: ParallelismConfig
+    alpha_us: float = 10.0
+    bytes_per_us: float = 50000.0
+    activation_bytes: int = 0
+    tag_policy: Optional[dict] = None       # TagPolicy::from_json document
+
+    def to_c(self) -> TsWhatIf:
+        import json
+        pol = None if self.tag_policy is None else json.dumps(self.tag_policy).encode()
+        c = TsWhatIf(self.source_model.to_c(), self.target_model.to_c(), self.source_par.to_c(),
+                     self.target_par.to_c(), float(self.alpha_us), float(self.bytes_per_us),
+                     int(self.activation_bytes), pol)
+        c._keep = pol
+        return c
+
+
 def _bind():
     L = _lib()
     if not getattr(L, "_pipeline_bound", False):
         L.ts_pipeline_graph.restype = C.c_int
         L.ts_pipeline_graph.argtypes = [C.POINTER(TsPipelineSpec), C.c_int32, C.c_int32,
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
+        L.ts_rebuild_pipeline.restype = C.c_int
+        L.ts_rebuild_pipeline.argtypes = [C.c_void_p, C.POINTER(TsWhatIf),
+                                          C.POINTER(C.c_void_p)]
+        L.ts_pipeline_spec_get.restype = C.POINTER(TsPipelineSpec)
+        L.ts_pipeline_spec_get.argtypes = [C.c_void_p]
+        L.ts_pipeline_free.argtypes = [C.c_void_p]
         L._pipeline_bound = True
     return L
+
+
+def _source_handle(source):
+    """A ts_host_graph that keeps Task.meta: from a SynthSpec (its replay
+    graph, generated with keep_meta) or recorded traces (a list of paths, or a
+    dict of ingest_traces_ex options)."""
+    from dataclasses import replace
+    from .synth import SynthSpec, TsIngestOptions
+    L = _bind()
+    h = C.c_void_p()
+    if isinstance(source, SynthSpec):
+        cs = replace(source, estimate=False, keep_meta=True, tp=1, slice_rank=-1).to_c()
+        rc = L.ts_synth_graph(C.byref(cs), C.byref(h), None)
+    else:
+        opts = dict(source) if isinstance(source, dict) else {"paths": list(source)}
+        paths = [str(p).encode() for p in opts.get("paths", ())]
+        arr = (C.c_char_p * max(1, len(paths)))(*paths)
+        enc = lambda x: None if x is None else str(x).encode()
+        if not getattr(L, "_ingest_ex_bound", False):
+            L.ts_ingest_traces_ex.restype = C.c_int
+            L.ts_ingest_traces_ex.argtypes = [C.POINTER(TsIngestOptions), C.POINTER(C.c_void_p)]
+            L._ingest_ex_bound = True
+        o = TsIngestOptions(arr, len(paths), int(opts.get("threads", 0)),
+                            enc(opts.get("manifest")), enc(opts.get("window")),
+                            enc(opts.get("categories_path")), enc(opts.get("policy_path")), 1, 0)
+        rc = L.ts_ingest_traces_ex(C.byref(o), C.byref(h))
+    if rc != N.TS_OK:
+        from .replay import _raise
+        _raise(rc)
+    return h
+
+
+def rebuild_pipeline(source, whatif: WhatIfConfig) -> Optional[PipelineSpec]:
+    """The PipelineSpec the reference's rebuild_pipeline (transform.cpp:556-701)
+    builds for a structural what-if — scale_pp / change_layers / apply_whatif's
+    rebuild branch — from a measured source (a SynthSpec or recorded traces,
+    see _source_handle).  None when the target differs in nothing the rebuild
+    cares about (the reference returns the source graph).  Raises ValueError
+    with the TransformError text."""
+    L = _bind()
+    h = _source_handle(source)
+    try:
+        w = whatif.to_c()
+        p = C.c_void_p()
+        rc = L.ts_rebuild_pipeline(h, C.byref(w), C.byref(p))
+        if rc != N.TS_OK:
+            from .replay import _raise
+            _raise(rc)
+        if not p.value:
+            return None
+        try:
+            return PipelineSpec.from_c(L.ts_pipeline_spec_get(p).contents)
+        finally:
+            L.ts_pipeline_free(p)
+    finally:
+        L.ts_host_graph_free(h)
 
 
 def pipeline_graph(spec: PipelineSpec, estimate: bool = True, tp: int = 1,
@@ -208,3 +367,16 @@ def estimate_batch(spec: PipelineSpec, scenarios, tp: int = 1, device: Optional[
     sg = pipeline_graph(spec, estimate=True, tp=tp)
     return simulate_batch(sg.graph, scenarios, timestamps=timestamps, breakdown=False,
                           device=device), sg
+
+
+def estimate_whatif(source, whatif: WhatIfConfig, scenarios, tp: int = 1,
+                    device: Optional[int] = None, timestamps: bool = True):
+    """estimate() for a structural what-if, batched: rebuild_pipeline on the
+    host, then the target pipeline's estimate graph replayed for ``scenarios``
+    on the GPU.  Returns (BatchResult, SynthGraph, PipelineSpec)."""
+    spec = rebuild_pipeline(source, whatif)
+    if spec is None:
+        raise ValueError("what-if changes nothing the pipeline rebuild models; replay the "
+                         "source graph (or use a Retime sweep for pure dp / width changes)")
+    res, sg = estimate_batch(spec, scenarios, tp=tp, device=device, timestamps=timestamps)
+    return res, sg, spec

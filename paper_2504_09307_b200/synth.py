@@ -31,7 +31,7 @@ class TsSynthSpec(C.Structure):
                 ("optimizer_ref_us", C.c_int64), ("optimizer_ref_bytes", C.c_int64),
                 ("alpha_us", C.c_double), ("bytes_per_us", C.c_double),
                 ("p2p_recv_base_us", C.c_int64), ("origin", C.c_int64), ("estimate", C.c_int32),
-                ("slice_rank", C.c_int32)]
+                ("slice_rank", C.c_int32), ("keep_meta", C.c_int32), ("pad", C.c_int32)]
 
 
 def _lib():
@@ -80,6 +80,7 @@ class SynthSpec:
     estimate: bool = False
     slice_rank: int = -1
     origin: int = 1000000
+    keep_meta: bool = False  # replay graph keeps Task.meta (the source of a what-if rebuild)
 
     def to_c(self) -> TsSynthSpec:
         s = TsSynthSpec()
@@ -256,7 +257,8 @@ def events_from_chrome(trace: dict, categories: Optional[dict] = None) -> dict:
 class TsIngestOptions(C.Structure):
     _fields_ = [("paths", C.POINTER(C.c_char_p)), ("n_paths", C.c_int32),
                 ("n_threads", C.c_int32), ("manifest", C.c_char_p), ("window", C.c_char_p),
-                ("categories_path", C.c_char_p), ("policy_path", C.c_char_p)]
+                ("categories_path", C.c_char_p), ("policy_path", C.c_char_p),
+                ("keep_meta", C.c_int32), ("pad", C.c_int32)]
 
 
 def ingest_traces_ex(paths=(), manifest=None, window=None, categories_path=None,
@@ -273,7 +275,7 @@ def ingest_traces_ex(paths=(), manifest=None, window=None, categories_path=None,
     arr = (C.c_char_p * max(1, len(paths)))(*[str(p).encode() for p in paths])
     enc = lambda x: None if x is None else str(x).encode()
     o = TsIngestOptions(arr, len(paths), int(threads), enc(manifest), enc(window),
-                        enc(categories_path), enc(policy_path))
+                        enc(categories_path), enc(policy_path), 0, 0)
     h = C.c_void_p()
     rc = L.ts_ingest_traces_ex(C.byref(o), C.byref(h))
     if rc != N.TS_OK:

@@ -88,6 +88,10 @@ class Graph:
 def _load(path):
     if not os.path.exists(path):
         raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+    # the reference library (-std=c++20) must resolve libstdc++'s locale facet
+    # ids globally: with numpy's runtime libraries loaded first, its std::regex
+    # (tag_tasks) otherwise picks up a mismatched collate facet and crashes
+    C.CDLL("libstdc++.so.6", mode=C.RTLD_GLOBAL)
     return C.CDLL(path)
 
 
@@ -139,6 +143,9 @@ def ref():
         lib.ref_apply_retime.restype = C.c_void_p
         lib.ref_apply_retime.argtypes = [C.c_void_p, _i64p, _i64p, C.c_int, C.c_int, C.c_double,
                                          C.c_double]
+        lib.ref_apply_whatif.restype = C.c_void_p
+        lib.ref_apply_whatif.argtypes = [C.c_void_p, _i64p, _i64p, _i32p, _i32p, C.c_double,
+                                         C.c_double, C.c_int64, C.c_char_p, C.c_int64]
         lib.ref_write_rank_traces.restype = C.c_int
         lib.ref_write_rank_traces.argtypes = [C.c_char_p, C.c_char_p]
         lib.ref_ingest_traces.restype = C.c_void_p
@@ -282,6 +289,23 @@ class RefGraphHandle:
         if not p:
             raise RefError(3, ref().ref_last_error().decode())
         return RefGraphHandle(p)
+
+    def apply_whatif(self, src_model, tgt_model, src_par, tgt_par, alpha=10.0,
+                     bytes_per_us=50000.0, activation_bytes=0):
+        """The reference apply_whatif (transform.cpp:713-760): (handle, notes).
+        model = (n_params, n_layers, d_model, d_ffn, n_heads, d_head),
+        par = (tp, pp, dp, num_microbatches)."""
+        sm = np.ascontiguousarray(src_model, np.int64)
+        tm = np.ascontiguousarray(tgt_model, np.int64)
+        sp = np.ascontiguousarray(src_par, np.int32)
+        tp = np.ascontiguousarray(tgt_par, np.int32)
+        buf = C.create_string_buffer(4096)
+        p = ref().ref_apply_whatif(self.h, _p(sm, _i64p), _p(tm, _i64p), _p(sp, _i32p),
+                                   _p(tp, _i32p), alpha, bytes_per_us, int(activation_bytes),
+                                   buf, 4096)
+        if not p:
+            raise RefError(3, ref().ref_last_error().decode())
+        return RefGraphHandle(p), buf.value.decode()
 
     def bench_simulate(self, sc: OrcScenarios, first: int, count: int, cls, threads: int,
                        with_fill: bool = False):

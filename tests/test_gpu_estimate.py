@@ -105,14 +105,35 @@ def test_estimate_batch_from_pipeline_spec(pp, dp, m, tp):
     # slot op_index[t] carrying the oracle's duration of task t
     from paper_2504_09307_b200 import estimate_batch
     from test_pipeline_spec import hand_edited
-    from test_synth_graph import _lane_sequences
     sp = hand_edited(pp, dp, m)
-    S = 24
-    spec = ScenarioSpec(count=S, first=6, seed=77, jitter=0.2)
+    spec = ScenarioSpec(count=24, first=6, seed=77, jitter=0.2)
     res, sg = estimate_batch(sp, spec, tp=tp)
+    _check_spec_batch(sp, spec, res, sg, tp)
+
+
+@pytest.mark.parametrize("tp", [1, 2])
+def test_estimate_whatif_matches_build_pipeline(tp):
+    # estimate() for a structural what-if: rebuild_pipeline measures the
+    # source (pp2 dp2 m8, 4 layers) and lays out pp4 dp4 m8 with 8 layers;
+    # the batched replay of the rebuilt spec's estimate graph equals
+    # build_pipeline(rebuilt spec, hook) scenario by scenario
+    from paper_2504_09307_b200 import (ModelConfig, ParallelismConfig, WhatIfConfig,
+                                       estimate_whatif)
+    src = _spec(2, 2, 8, 4, 1024, 4096)
+    w = WhatIfConfig(ModelConfig(4, 1024, 4096, 16, 64), ModelConfig(8, 1024, 4096, 16, 64),
+                     ParallelismConfig(1, 2, 2, 8), ParallelismConfig(1, 4, 4, 8))
+    spec = ScenarioSpec(count=20, first=3, seed=41, jitter=0.25)
+    res, sg, sp = estimate_whatif(src, w, spec, tp=tp)
+    assert sp.pp == 4 and sp.dp == 4 and len(sp.stages[0].layers_fwd) == 2
+    _check_spec_batch(sp, spec, res, sg, tp)
+
+
+def _check_spec_batch(sp, spec, res, sg, tp):
+    from test_synth_graph import _lane_sequences
+    S = spec.count
     g = sg.graph
     og = _orc_graph(g)
-    sc = R.OrcScenarios(seed=77, jitter=0.2)
+    sc = R.OrcScenarios(seed=spec.seed, jitter=spec.jitter)
     js = sp.to_json()
     for s in range(0, S, 5):
         dur = R.orc_durations(og, sc, spec.first + s)

@@ -34,7 +34,10 @@ def main():
         config = cfg
         jitter = 0.1
     sk = bench.scenario_kwargs(A)
-    g = generate_graph(SynthSpec(tp=tp, **model, **par)).graph
+    if cfg == "config3":
+        g = bench.config3_graph(model, par, tp).graph
+    else:
+        g = generate_graph(SynthSpec(tp=tp, **model, **par)).graph
     dg = DeviceGraph(g, device=0)
     n = dg.n_tasks
     dev = torch.device("cuda", 0)
