@@ -607,7 +607,8 @@ def main():
                                    "sum": step_ms_dev},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "replay_walk (K1)", "bytes_per_launch": walk_bytes,
+                         "kernel": ("cluster_walk (K1x)" if args.config == "config3"
+                                    else "replay_walk (K1)"), "bytes_per_launch": walk_bytes,
                          "launch_ms": walk_avg_ms, "peak_source": peak_src},
             "clocks": clocks,
             "e2e": e2e,
