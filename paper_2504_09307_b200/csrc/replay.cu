@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <type_traits>
 #include <cstdint>
 
@@ -89,6 +90,20 @@ __device__ __noinline__ int64_t rt_coll_base(const RtScen* scp, int32_t rk, int3
   if ((sc.flags & kRtDp) && rk == TS_RT_ALLREDUCE && grp == source_dp)
     d = coll_cost(true, v, sc.tdp, sc.alpha, sc.bpu);
   return d;
+}
+
+// mailbox words: the value is the whole message (one aligned 64-bit word),
+// so relaxed device-scope accesses suffice (no system-scope volatile)
+#ifndef LUMOS_MAIL_SLEEP
+#define LUMOS_MAIL_SLEEP 32
+#endif
+__device__ __forceinline__ uint64_t mail_load(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mail_store(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS,
@@ -414,21 +429,21 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         if constexpr (kCl) {
           int m = static_cast<int>(ob.z >> kShift);  // x1: the mailbox id (widened)
           if (!LUMOS_OK(m < P.cl_n_mail)) m = 0;
-          volatile uint64_t* box = mail_base + static_cast<int64_t>(m) * kT;
+          uint64_t* box = mail_base + static_cast<int64_t>(m) * kT;
           if (kind == OP_POST) {
             uint64_t v = static_cast<uint64_t>(p0.v[0]) | (static_cast<uint64_t>(p0.v[1]) << 32);
             if (v == ~0ull) v = ~1ull;  // only a wrapped (failed) value can look unposted
-            *box = v;
+            mail_store(box, v);
           } else {
-            uint64_t v = *box;
+            uint64_t v = mail_load(box);
             for (int spins = 0; v == ~0ull; ++spins) {
               if (spins > (1 << 22)) {  // ~seconds: a compiler bug, not a schedule
                 stalled = true;
                 v = 0;
                 break;
               }
-              __nanosleep(32);
-              v = *box;
+              if (LUMOS_MAIL_SLEEP > 0) __nanosleep(LUMOS_MAIL_SLEEP);
+              v = mail_load(box);
             }
             VP q;
             q.v[0] = static_cast<V>(static_cast<uint32_t>(v));
@@ -573,6 +588,9 @@ __global__ void __launch_bounds__(kT, sizeof(V) == 4 && LUMOS_WALK_MINB > 0 ? LU
 // K1x cluster walk (estimate-mode components): 128 threads, uint32 pairs
 #ifndef LUMOS_CLUSTER_MINB
 #define LUMOS_CLUSTER_MINB 1
+#endif
+#ifndef LUMOS_CLUSTER_CARVEOUT_DEFAULT
+#define LUMOS_CLUSTER_CARVEOUT_DEFAULT -1
 #endif
 template <int kMode, bool kWriteStart, bool kWriteFin>
 __global__ void __launch_bounds__(128, LUMOS_CLUSTER_MINB) cluster_walk_kernel(WalkParams P) {
@@ -1608,29 +1626,61 @@ cudaError_t launch_replay_walk(const WalkParams& p, int n_slots, cudaStream_t st
              : launch_walk_v<int64_t, 2>(p, n_slots, t, stream);
 }
 
-template <int kMode, bool kWS, bool kWF>
-static cudaError_t launch_cluster_t(const WalkParams& p, size_t smem, unsigned blocks,
-                                    cudaStream_t stream) {
-  auto kern = cluster_walk_kernel<kMode, kWS, kWF>;
+// shared-memory carveout of the cluster walk (percent of the unified L1 /
+// shared array; LUMOS_CLUSTER_CARVEOUT, default the driver's choice = -1):
+// the driver sizes it for the register-limited occupancy, which can leave
+// shared memory the binding limit once registers allow more CTAs per SM
+static int cluster_carveout() {
+  static const int v = [] {
+    const char* e = std::getenv("LUMOS_CLUSTER_CARVEOUT");
+    return e ? std::atoi(e) : LUMOS_CLUSTER_CARVEOUT_DEFAULT;
+  }();
+  return v;
+}
+
+template <typename K>
+static cudaError_t cluster_attrs(K kern, size_t smem, int cl_size) {
   cudaError_t e = cudaSuccess;
   if (smem > 48 * 1024)
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-  if (e == cudaSuccess && p.cl_size > 8)
+  if (e == cudaSuccess && cl_size > 8)
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess && cluster_carveout() >= 0)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cluster_carveout());
+  return e;
+}
+
+template <int kMode, bool kWS, bool kWF>
+static cudaError_t launch_cluster_t(const WalkParams& p, size_t smem, unsigned blocks,
+                                    cudaStream_t stream) {
+  auto kern = cluster_walk_kernel<kMode, kWS, kWF>;
+  cudaError_t e = cluster_attrs(kern, smem, p.cl_size);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.cl_size);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // LUMOS_CLUSTER_POLICY=1 spread / 2 load-balancing (default: the driver's)
+  static const int policy = [] {
+    const char* e = std::getenv("LUMOS_CLUSTER_POLICY");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (policy == 1 || policy == 2) {
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference =
+        policy == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
@@ -1648,13 +1698,7 @@ bool cluster_walk_supported(int cl_size, int n_slots) {
   if (cl_size < 1 || cl_size > 16 || walk_width(n_slots, true) != 128) return false;
   auto kern = cluster_walk_kernel<kModeJitter, true, true>;
   const size_t smem = walk_smem(n_slots, 128, 8);
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess)
-    return cudaGetLastError(), false;
-  if (cl_size > 8 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-    return cudaGetLastError(), false;
+  if (cluster_attrs(kern, smem, cl_size) != cudaSuccess) return cudaGetLastError(), false;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(cl_size));
   cfg.blockDim = dim3(128);

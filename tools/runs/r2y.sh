@@ -1,0 +1,4 @@
+P="python tools/walk_probe.py config3 4096 1 ncu"
+$P > gpurun_out/r2y_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"cluster_walk" -s 1 -c 1 \
+    -o gpurun_out/r2y_cluster $P > gpurun_out/r2y_ncu.log 2>&1
