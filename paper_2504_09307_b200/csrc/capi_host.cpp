@@ -1,5 +1,6 @@
 // capi_host.cpp — extern "C" entry points of the host-side graph sources
 // (synthetic generator, trace-event graph builder); see include/lumos_b200.h.
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <fstream>
@@ -101,7 +102,10 @@ const char* ts_host_graph_name(const ts_host_graph* g, int32_t id) {
 
 void ts_host_graph_free(ts_host_graph* g) { delete g; }
 
-static int ingest(const IngestOptions& opts, ts_host_graph** out) {
+static int ingest(IngestOptions opts, ts_host_graph** out) {
+  // LUMOS_INGEST_DOM=1 parses every file on the DOM path (the fast scanner's check)
+  const char* dom = std::getenv("LUMOS_INGEST_DOM");
+  opts.dom_only = dom && dom[0] == '1';
   auto* h = new ts_host_graph;
   std::vector<RtMeta> rt;
   std::string err;

@@ -6,11 +6,19 @@
 // the default CategoryTable :156-172), load_multirank / split_by_rank rank
 // assignment (trace_parse.cpp:260-298, cli.cpp:93-116), build_graph per rank
 // (build.cpp:338-510, restated in ingest.cpp) and merge_ranks (build.cpp:512-542).
-// Files are parsed on a pool of host threads (JSON parsing with nlohmann::json,
-// the reference's own parser, so numbers and strings decode identically), the
-// name table is interned in rank order, and ranks are built in parallel; the
-// result equals the sequential reference path task for task.
+// Files are parsed on a pool of host threads by a single-pass scanner
+// (FastScan: no DOM, only the fields parse_trace reads are decoded); a file it
+// does not model exactly — malformed JSON, unexpected field types, values that
+// need nlohmann's number formatting — is re-parsed on the DOM path
+// (nlohmann::json, the reference's own parser), so errors and exotic values
+// behave identically.  The name table is interned in rank order and ranks are
+// built in parallel; the result equals the sequential reference path task for
+// task.
 #include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cstdlib>
+#include <cerrno>
 #include <atomic>
 #include <fstream>
 #include <map>
@@ -234,6 +242,524 @@ void parse_dom(const json& root, std::vector<RawEvent>& out, const CatOverrides&
     return a.ev.tid < b.ev.tid;
   });
 }
+
+// ------------------------------------------------------------- fast path
+// A single-pass scanner over the trace text that builds RawEvents without a
+// DOM: the hot path of ingest (a DOM parse costs ~20-30 MB/s per thread).  It
+// validates the JSON it walks (strings incl. UTF-8 and \u escapes, the number
+// grammar, nesting) and decodes only the fields parse_trace reads; anything it
+// does not model exactly — malformed JSON, a field of an unexpected type, a
+// float where a prefix-parsed argument or a kept argument needs nlohmann's
+// number formatting — returns false and the caller re-parses the file with
+// parse_dom, so errors and exotic values behave exactly as on the DOM path.
+class FastScan {
+ public:
+  FastScan(const std::string& text, const CatOverrides& cats, bool keep_args)
+      : p_(text.data()), e_(text.data() + text.size()), cats_(cats), keep_(keep_args) {}
+
+  bool run(std::vector<RawEvent>& out) {
+    out.reserve(static_cast<size_t>(e_ - p_) / 160);
+    ws();
+    if (p_ >= e_) return false;
+    if (*p_ == '[') {
+      if (!events(out)) return false;
+    } else if (*p_ == '{') {
+      ++p_;
+      bool found = false;
+      if (!members([&](const std::string& key) {
+            if (key != "traceEvents") return skip(0);
+            ws();
+            if (p_ >= e_ || *p_ != '[') return false;  // non-array traceEvents: DOM path
+            out.clear();
+            found = true;
+            return events(out);
+          }))
+        return false;
+      if (!found) return false;
+    } else {
+      return false;
+    }
+    ws();
+    if (p_ != e_) return false;
+    // parse_trace's stable (pid, ts, tid) order; recorded traces usually are
+    // in it already, otherwise an index permutation moves each event once
+    auto less = [&](const RawEvent& a, const RawEvent& b) {
+      if (a.ev.pid != b.ev.pid) return a.ev.pid < b.ev.pid;
+      if (a.ev.ts != b.ev.ts) return a.ev.ts < b.ev.ts;
+      return a.ev.tid < b.ev.tid;
+    };
+    if (!std::is_sorted(out.begin(), out.end(), less)) {
+      std::vector<uint32_t> idx(out.size());
+      for (uint32_t k = 0; k < idx.size(); ++k) idx[k] = k;
+      std::stable_sort(idx.begin(), idx.end(),
+                       [&](uint32_t a, uint32_t b) { return less(out[a], out[b]); });
+      std::vector<RawEvent> sorted;
+      sorted.reserve(out.size());
+      for (uint32_t k : idx) sorted.push_back(std::move(out[k]));
+      out.swap(sorted);
+    }
+    return true;
+  }
+
+ private:
+  enum Kind : uint8_t { K_NONE, K_STR, K_INT, K_UINT, K_FLT, K_TRUE, K_FALSE, K_NULL, K_ARR, K_OBJ };
+  struct Val {
+    Kind kind = K_NONE;
+    std::string s;
+    int64_t i = 0;
+    uint64_t u = 0;
+    double d = 0.0;
+    bool is_int() const { return kind == K_INT || kind == K_UINT; }
+    int64_t as_i64() const { return kind == K_INT ? i : static_cast<int64_t>(u); }
+  };
+
+  const char* p_;
+  const char* e_;
+  const CatOverrides& cats_;
+  bool keep_;
+
+  void ws() {
+    while (p_ < e_ && (*p_ == ' ' || *p_ == '\n' || *p_ == '\r' || *p_ == '\t')) ++p_;
+  }
+
+  // "..." with escapes decoded and UTF-8 validated (RFC 3629 as nlohmann's lexer)
+  bool str(std::string& out) {
+    if (p_ >= e_ || *p_ != '"') return false;
+    ++p_;
+    out.clear();
+    for (;;) {
+      const char* run = p_;
+      while (p_ < e_ && static_cast<unsigned char>(*p_) >= 0x20 && *p_ != '"' && *p_ != '\\' &&
+             static_cast<unsigned char>(*p_) < 0x80)
+        ++p_;
+      out.append(run, p_);
+      if (p_ >= e_) return false;
+      const unsigned char c = static_cast<unsigned char>(*p_);
+      if (c == '"') {
+        ++p_;
+        return true;
+      }
+      if (c < 0x20) return false;
+      if (c == '\\') {
+        if (++p_ >= e_) return false;
+        switch (*p_++) {
+          case '"': out += '"'; break;
+          case '\\': out += '\\'; break;
+          case '/': out += '/'; break;
+          case 'b': out += '\b'; break;
+          case 'f': out += '\f'; break;
+          case 'n': out += '\n'; break;
+          case 'r': out += '\r'; break;
+          case 't': out += '\t'; break;
+          case 'u': {
+            uint32_t cp = 0;
+            if (!hex4(cp)) return false;
+            if (cp >= 0xD800 && cp <= 0xDBFF) {
+              uint32_t lo = 0;
+              if (e_ - p_ < 2 || p_[0] != '\\' || p_[1] != 'u') return false;
+              p_ += 2;
+              if (!hex4(lo) || lo < 0xDC00 || lo > 0xDFFF) return false;
+              cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+            } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
+              return false;
+            }
+            utf8(cp, out);
+            break;
+          }
+          default: return false;
+        }
+        continue;
+      }
+      // a multi-byte UTF-8 sequence
+      int n = 0;
+      uint32_t lo = 0x80, hi = 0xBF;
+      if (c >= 0xC2 && c <= 0xDF) n = 1;
+      else if (c == 0xE0) { n = 2; lo = 0xA0; }
+      else if ((c >= 0xE1 && c <= 0xEC) || c == 0xEE || c == 0xEF) n = 2;
+      else if (c == 0xED) { n = 2; hi = 0x9F; }
+      else if (c == 0xF0) { n = 3; lo = 0x90; }
+      else if (c >= 0xF1 && c <= 0xF3) n = 3;
+      else if (c == 0xF4) { n = 3; hi = 0x8F; }
+      else return false;
+      if (e_ - p_ < n + 1) return false;
+      const unsigned char c1 = static_cast<unsigned char>(p_[1]);
+      if (c1 < lo || c1 > hi) return false;
+      for (int k = 2; k <= n; ++k) {
+        const unsigned char ck = static_cast<unsigned char>(p_[k]);
+        if (ck < 0x80 || ck > 0xBF) return false;
+      }
+      out.append(p_, p_ + n + 1);
+      p_ += n + 1;
+    }
+  }
+  bool hex4(uint32_t& v) {
+    if (e_ - p_ < 4) return false;
+    v = 0;
+    for (int k = 0; k < 4; ++k) {
+      const char c = *p_++;
+      v <<= 4;
+      if (c >= '0' && c <= '9') v |= static_cast<uint32_t>(c - '0');
+      else if (c >= 'a' && c <= 'f') v |= static_cast<uint32_t>(c - 'a' + 10);
+      else if (c >= 'A' && c <= 'F') v |= static_cast<uint32_t>(c - 'A' + 10);
+      else return false;
+    }
+    return true;
+  }
+  static void utf8(uint32_t cp, std::string& out) {
+    if (cp < 0x80) {
+      out += static_cast<char>(cp);
+    } else if (cp < 0x800) {
+      out += static_cast<char>(0xC0 | (cp >> 6));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    } else if (cp < 0x10000) {
+      out += static_cast<char>(0xE0 | (cp >> 12));
+      out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    } else {
+      out += static_cast<char>(0xF0 | (cp >> 18));
+      out += static_cast<char>(0x80 | ((cp >> 12) & 0x3F));
+      out += static_cast<char>(0x80 | ((cp >> 6) & 0x3F));
+      out += static_cast<char>(0x80 | (cp & 0x3F));
+    }
+  }
+
+  // the JSON number grammar; integers as int64 / uint64 (overflow: double)
+  bool number(Val& v) {
+    const char* b = p_;
+    if (p_ < e_ && *p_ == '-') ++p_;
+    if (p_ >= e_) return false;
+    if (*p_ == '0') {
+      ++p_;
+    } else if (*p_ >= '1' && *p_ <= '9') {
+      while (p_ < e_ && *p_ >= '0' && *p_ <= '9') ++p_;
+    } else {
+      return false;
+    }
+    bool flt = false;
+    if (p_ < e_ && *p_ == '.') {
+      flt = true;
+      ++p_;
+      if (p_ >= e_ || *p_ < '0' || *p_ > '9') return false;
+      while (p_ < e_ && *p_ >= '0' && *p_ <= '9') ++p_;
+    }
+    if (p_ < e_ && (*p_ == 'e' || *p_ == 'E')) {
+      flt = true;
+      ++p_;
+      if (p_ < e_ && (*p_ == '+' || *p_ == '-')) ++p_;
+      if (p_ >= e_ || *p_ < '0' || *p_ > '9') return false;
+      while (p_ < e_ && *p_ >= '0' && *p_ <= '9') ++p_;
+    }
+    if (!flt) {  // accumulate; an overflow becomes a double like nlohmann's
+      const bool neg = *b == '-';
+      uint64_t x = 0;
+      bool over = false;
+      for (const char* q = b + (neg ? 1 : 0); q < p_; ++q) {
+        const uint64_t d = static_cast<uint64_t>(*q - '0');
+        if (x > (UINT64_MAX - d) / 10) {
+          over = true;
+          break;
+        }
+        x = x * 10 + d;
+      }
+      if (!over && !neg) {
+        v.kind = K_UINT;
+        v.u = x;
+        return true;
+      }
+      if (!over && x <= static_cast<uint64_t>(INT64_MAX) + 1) {
+        v.kind = K_INT;
+        v.i = x == static_cast<uint64_t>(INT64_MAX) + 1 ? INT64_MIN : -static_cast<int64_t>(x);
+        return true;
+      }
+    }
+    const std::string t(b, p_);
+    v.kind = K_FLT;
+    v.d = std::strtod(t.c_str(), nullptr);
+    return true;
+  }
+  bool word(const char* w, Kind k, Val* v) {
+    const size_t n = std::strlen(w);
+    if (static_cast<size_t>(e_ - p_) < n || std::memcmp(p_, w, n) != 0) return false;
+    p_ += n;
+    if (v) v->kind = k;
+    return true;
+  }
+  // a value; strings and scalars decoded into v (when given), containers validated
+  bool value(Val* v, int depth) {
+    ws();
+    if (p_ >= e_ || depth > 256) return false;
+    switch (*p_) {
+      case '"': {
+        if (!v) {
+          std::string tmp;
+          return str(tmp);
+        }
+        v->kind = K_STR;
+        return str(v->s);
+      }
+      case '{':
+        ++p_;
+        if (v) v->kind = K_OBJ;
+        return members([&](const std::string&) { return skip(depth + 1); });
+      case '[':
+        ++p_;
+        if (v) v->kind = K_ARR;
+        return elements([&] { return skip(depth + 1); });
+      case 't': return word("true", K_TRUE, v);
+      case 'f': return word("false", K_FALSE, v);
+      case 'n': return word("null", K_NULL, v);
+      default: {
+        Val tmp;
+        return number(v ? *v : tmp);
+      }
+    }
+  }
+  bool skip(int depth) { return value(nullptr, depth); }
+
+  // object members after '{': f(key) consumes the value
+  template <typename F>
+  bool members(F&& f) {
+    ws();
+    if (p_ < e_ && *p_ == '}') {
+      ++p_;
+      return true;
+    }
+    std::string key;
+    for (;;) {
+      ws();
+      if (!str(key)) return false;
+      ws();
+      if (p_ >= e_ || *p_ != ':') return false;
+      ++p_;
+      if (!f(key)) return false;
+      ws();
+      if (p_ >= e_) return false;
+      if (*p_ == ',') {
+        ++p_;
+        continue;
+      }
+      if (*p_ == '}') {
+        ++p_;
+        return true;
+      }
+      return false;
+    }
+  }
+  template <typename F>
+  bool elements(F&& f) {
+    ws();
+    if (p_ < e_ && *p_ == ']') {
+      ++p_;
+      return true;
+    }
+    for (;;) {
+      if (!f()) return false;
+      ws();
+      if (p_ >= e_) return false;
+      if (*p_ == ',') {
+        ++p_;
+        continue;
+      }
+      if (*p_ == ']') {
+        ++p_;
+        return true;
+      }
+      return false;
+    }
+  }
+
+  bool events(std::vector<RawEvent>& out) {
+    ++p_;  // '['
+    return elements([&] {
+      ws();
+      if (p_ >= e_ || *p_ != '{') return false;  // "event is not an object": DOM path
+      ++p_;
+      return event(out);
+    });
+  }
+
+  // one trace event (parse_trace's per-record rules, trace_parse.cpp:79-154)
+  // per-event scratch, reused (capacity kept across events)
+  Val ph_, name_, cat_, ts_, dur_, pid_, tid_;
+  std::vector<std::pair<std::string, Val>> args_;
+  size_t n_args_ = 0;
+  std::string last_cat_;
+  uint8_t last_cat_code_ = 0;
+  bool have_cat_ = false;
+
+  bool event(std::vector<RawEvent>& out) {
+    Val &ph = ph_, &name = name_, &cat = cat_, &ts = ts_, &dur = dur_, &pid = pid_, &tid = tid_;
+    for (Val* v : {&ph, &name, &cat, &ts, &dur, &pid, &tid}) v->kind = K_NONE;
+    bool has_args = false;
+    auto& args = args_;
+    auto slot = [&](const std::string& k) -> Val* {
+      switch (k.size()) {
+        case 2: return k == "ph" ? &ph : k == "ts" ? &ts : nullptr;
+        case 3: return k == "cat" ? &cat : k == "dur" ? &dur : k == "pid" ? &pid
+                     : k == "tid" ? &tid : nullptr;
+        case 4: return k == "name" ? &name : nullptr;
+        default: return nullptr;
+      }
+    };
+    if (!members([&](const std::string& key) {
+          if (key.size() == 4 && key == "args") {
+            ws();
+            if (p_ < e_ && *p_ == '{') {
+              ++p_;
+              has_args = true;
+              n_args_ = 0;  // a repeated key: the last object wins
+              return members([&](const std::string& k) {
+                if (n_args_ == args.size()) args.emplace_back();
+                auto& slot_kv = args[n_args_];
+                slot_kv.first = k;
+                slot_kv.second.kind = K_NONE;
+                if (!value(&slot_kv.second, 2)) return false;
+                ++n_args_;
+                return true;
+              });
+            }
+            has_args = false;  // present but not an object: ignored
+            return skip(1);
+          }
+          if (Val* v = slot(key)) {
+            v->kind = K_NONE;
+            return value(v, 1);
+          }
+          return skip(1);
+        }))
+      return false;
+    size_t na = has_args ? n_args_ : 0;
+    if (na > 1) {  // object keys: key order (stable), the last duplicate wins
+      for (size_t a = 1; a < na; ++a)
+        for (size_t b = a; b > 0 && args[b].first < args[b - 1].first; --b)
+          std::swap(args[b], args[b - 1]);
+      size_t w = 0;
+      for (size_t a = 0; a < na; ++a) {
+        if (w > 0 && args[w - 1].first == args[a].first) std::swap(args[w - 1], args[a]);
+        else if (w != a) std::swap(args[w++], args[a]);
+        else ++w;
+      }
+      na = w;
+    }
+    auto find = [&](const char* k) -> const Val* {
+      for (size_t a = 0; a < na; ++a)
+        if (args[a].first == k) return &args[a].second;
+      return nullptr;
+    };
+    if (ph.kind != K_NONE && ph.kind != K_STR) return false;
+    const std::string phs = ph.kind == K_STR ? ph.s : "X";
+    const bool duration_event = phs == "X";
+    if (!duration_event) {
+      bool keep = name.kind == K_STR && (name.s.find("EventRecord") != std::string::npos ||
+                                         name.s.find("WaitEvent") != std::string::npos);
+      keep = keep || (has_args && (find("correlation") || find("correlation_id")));
+      if (!keep) return true;
+    }
+    if (phs == "M") return true;
+    if ((name.kind != K_NONE && name.kind != K_STR) || (cat.kind != K_NONE && cat.kind != K_STR))
+      return false;
+    auto micros = [](const Val& v, int64_t& o) {
+      if (v.is_int()) o = v.as_i64();
+      else if (v.kind == K_FLT) o = static_cast<int64_t>(std::llround(v.d));
+      else return false;
+      return true;
+    };
+    RawEvent r;
+    Event& e = r.ev;
+    r.name = name.s;
+    if (!have_cat_ || cat.s != last_cat_) {  // categories repeat: one lookup per change
+      last_cat_ = cat.s;
+      last_cat_code_ = lookup_category(cat.s, cats_);
+      have_cat_ = true;
+    }
+    e.cat = last_cat_code_;
+    if (!micros(ts, e.ts) || e.ts < 0) return false;  // missing / bad / negative: DOM path
+    if (duration_event && (!micros(dur, e.dur) || e.dur < 0)) return false;
+    auto small = [](const Val& v, int32_t& o) {
+      if (v.kind == K_NONE) o = 0;
+      else if (v.kind == K_INT) o = static_cast<int32_t>(v.i);
+      else if (v.kind == K_UINT) o = static_cast<int32_t>(v.u);
+      else return false;
+      return true;
+    };
+    if (!small(pid, e.pid) || !small(tid, e.tid)) return false;
+    int64_t stream = 0;
+    bool has_stream = false, has_corr = false;
+    if (has_args) {
+      auto to_int = [&](const char* k, int64_t& o) {  // arg_to_int (trace_parse.cpp:65-77)
+        const Val* v = find(k);
+        if (!v) return false;
+        if (v->is_int()) {
+          o = v->as_i64();
+          return true;
+        }
+        return v->kind == K_STR && prefix_i64(v->s, o);
+      };
+      int64_t corr = 0;
+      if (to_int("correlation", corr) || to_int("correlation_id", corr)) {
+        e.corr = corr;
+        has_corr = true;
+      }
+      has_stream = to_int("stream", stream);
+      for (size_t a = 0; a < na; ++a) {
+        const std::string& k = args[a].first;
+        const Val& v = args[a].second;
+        std::string s;
+        switch (v.kind) {
+          case K_STR: s = v.s; break;
+          case K_INT: s = std::to_string(v.i); break;
+          case K_UINT: s = std::to_string(v.u); break;
+          case K_TRUE: s = "true"; break;
+          case K_FALSE: s = "false"; break;
+          case K_NULL: s = "null"; break;
+          default:  // floats and containers: nlohmann's dump text is needed
+            if (keep_ || (v.kind == K_FLT && (k == "event" || k == "stream"))) return false;
+            continue;  // no interpreted key accepts them
+        }
+        if (keep_) r.args.emplace_back(k, s);
+        int64_t x = 0;
+        switch (k.size()) {
+          case 1:
+            if ((k[0] == 'm' || k[0] == 'n' || k[0] == 'k') && strict_i64(s, x))
+              (k[0] == 'm' ? r.rt.m : k[0] == 'n' ? r.rt.n : r.rt.k) = x;
+            break;
+          case 3:
+            if (k == "dir") r.rt.dir_recv = s == "recv";
+            break;
+          case 5:
+            if (k == "event") {
+              if (prefix_i64(s, x)) e.arg_event = x;
+            } else if (k == "bytes") {
+              if (strict_i64(s, x)) r.rt.bytes = x;
+            }
+            break;
+          case 6:
+            if (k == "stream") {
+              if (prefix_i64(s, x)) e.arg_stream = x;
+            } else if (k == "region") {
+              r.rt.region_opt = s == "opt";
+              r.rt.region_p2p = s == "p2p";
+            }
+            break;
+          case 10:
+            if (k == "group_size") {
+              if (strict_i64(s, x)) r.rt.group = x;
+            } else if (k == "collective") {
+              r.rt.allreduce = s == "allreduce";
+            }
+            break;
+          default: break;
+        }
+      }
+    }
+    const bool gpu = e.cat == CAT_KERNEL || e.cat == CAT_MEMCPY || e.cat == CAT_MEMSET;
+    if (has_stream) e.stream = static_cast<int32_t>(stream);
+    else if (gpu) e.stream = e.tid;
+    if (e.cat == CAT_RUNTIME && is_launch_name(r.name) && !has_corr) return false;
+    out.push_back(std::move(r));
+    return true;
+  }
+};
 
 // the last "rank_?(\\d+)" match of a path (trace_parse.cpp:260-270), scanned
 // by hand: matches of that pattern never overlap, so the last one wins.  Which
@@ -507,7 +1033,11 @@ int ingest_traces(const IngestOptions& opts, Names& names, HostGraph& out,
       return;
     }
     try {
-      parse_dom(json::parse(text), parsed[i], opts.categories, opts.keep_meta);
+      // fast scanner first; anything it does not model re-parses on the DOM
+      if (opts.dom_only || !FastScan(text, opts.categories, opts.keep_meta).run(parsed[i])) {
+        parsed[i].clear();
+        parse_dom(json::parse(text), parsed[i], opts.categories, opts.keep_meta);
+      }
     } catch (const ParseError& e) {
       errs[i] = path + ": " + e.msg;
     } catch (const json::parse_error& e) {

@@ -28,6 +28,7 @@ struct IngestOptions {
   BuildPolicyLite policy;          // --policy (BuildPolicy::from_json)
   int threads = 0;                 // host threads (<= 0: all cores)
   bool keep_meta = false;          // keep Task.meta / correlation ids (what-if rebuild)
+  bool dom_only = false;           // skip the fast scanner (LUMOS_INGEST_DOM=1; tests)
 };
 
 // build_from_inputs (cli.cpp:118-137): parse_trace of every input,

@@ -193,3 +193,86 @@ def test_ingest_manifest_categories_policy(tmp_path):
                          policy_path=str(tmp_path / "badp.json"))
     with pytest.raises(Exception, match="window must be 'full', 'auto' or START:END"):
         ingest_traces_ex([], manifest=str(tmp_path / "manifest.json"), window="last")
+
+
+def _tricky_events():
+    """Records that exercise the fast scanner's JSON handling: escapes and
+    UTF-8 in names, every number form, duplicate keys, args of every type,
+    skipped phases and non-object args."""
+    return [
+        {"ph": "X", "cat": "cuda_runtime", "name": "cudaLaunchKernel", "pid": 0, "tid": 9,
+         "ts": 100, "dur": 4, "args": {"correlation": 1, "Input Dims": [[1, 2], []],
+                                         "flag": True, "none": None, "ratio": 0.25,
+                                         "nested": {"a": [1, {"b": "c"}]}}},
+        {"ph": "X", "cat": "KERNEL", "name": "gemm \"q\\k\"\tv/é\U0001F600 layers.3",
+         "pid": 0, "tid": 7, "ts": 1.04e2, "dur": 20, "args": {"correlation": 1, "stream": 7,
+                                                                "m": "2048", "n": 4096,
+                                                                "k": "1024", "region": "p2p",
+                                                                "bytes": 18446744073709551615}},
+        {"ph": "X", "cat": "cuda_runtime", "name": "cudaLaunchKernel", "pid": 0, "tid": 9,
+         "ts": 104, "dur": 3, "args": {"correlation_id": "2"}},
+        {"ph": "X", "cat": "kernel", "name": "ncclDevKernel_AllReduce", "pid": 0, "tid": 9,
+         "ts": 130, "dur": 5, "args": {"correlation": 2, "stream": "11", "collective": "allreduce",
+                                      "group_size": "4", "bytes": "1048576"}},
+        {"ph": "i", "cat": "cuda_runtime", "name": "cudaEventRecord", "pid": 0, "tid": 9,
+         "ts": 140, "args": {"event": "5x", "stream": 11}},
+        {"ph": "B", "cat": "cpu_op", "name": "begin-only", "pid": 0, "tid": 9, "ts": 141},
+        {"ph": "M", "name": "thread_name", "pid": 0, "tid": 9, "args": {"name": "main"}},
+        {"ph": "X", "cat": "cpu_op", "name": "aten::mm", "pid": 0, "tid": 9, "ts": 150.5,
+         "dur": 2.5, "args": [1, 2]},
+        {"ph": "X", "cat": "cpu_op", "name": "late", "pid": 0, "tid": 9, "ts": 149, "dur": 1},
+        {"ph": "X", "cat": "unknown_cat", "pid": 0, "tid": 9, "ts": 160, "dur": 0},
+    ]
+
+
+def _write_tricky(path, dup_keys):
+    text = json.dumps({"meta": {"x": [1, 2.5, "y"]}, "traceEvents": _tricky_events(),
+                       "tail": None}, ensure_ascii=False, indent=1)
+    if dup_keys:  # a repeated key: the last value wins (nlohmann)
+        text = text.replace('"ts": 149', '"ts": 1, "ts": 149', 1)
+        text = text.replace('"args": {"event": "5x"', '"args": {"stream": 3, "event": "5x"', 1)
+    path.write_text(text, encoding="utf-8")
+
+
+@pytest.mark.parametrize("dup_keys", [False, True])
+def test_fast_scanner_equals_dom_and_reference(tmp_path, monkeypatch, dup_keys):
+    # the single-pass scanner (default) and the DOM path (LUMOS_INGEST_DOM=1)
+    # must both equal the reference's parse_trace + build_graph
+    p = tmp_path / "rank_0.json"
+    _write_tricky(p, dup_keys)
+    ref = R.ingest_traces([str(p)])
+    for dom in ("0", "1"):
+        monkeypatch.setenv("LUMOS_INGEST_DOM", dom)
+        _same(ingest_traces([str(p)], names=True), ref)
+
+
+def test_fast_scanner_on_generated_traces(tmp_path, monkeypatch):
+    R.write_rank_traces(R.synth_spec(pp=2, dp=2, m=4, layers=4, jitter=0.05), str(tmp_path))
+    paths = sorted(glob.glob(str(tmp_path / "rank_*.json")))
+    h = R.ingest_traces(paths)
+    for dom in ("0", "1"):
+        monkeypatch.setenv("LUMOS_INGEST_DOM", dom)
+        _same(ingest_traces(paths, threads=2, names=True), h)
+
+
+@pytest.mark.parametrize("body", [
+    '{"traceEvents": [{"ph": "X", "name": "a", "cat": "cpu_op", "ts": 1, "dur": 2,}]}',
+    '{"traceEvents": [{"ph": "X", "name": "a\\x", "cat": "cpu_op", "ts": 1, "dur": 2}]}',
+    '{"traceEvents": [{"ph": "X", "name": "\\ud800", "cat": "cpu_op", "ts": 1, "dur": 2}]}',
+    '{"traceEvents": [{"ph": "X", "name": "a", "cat": "cpu_op", "ts": 01, "dur": 2}]}',
+    '{"traceEvents": []} trailing',
+    '{"traceEvents": [{"ph": 3, "name": "a", "cat": "cpu_op", "ts": 1, "dur": 2}]}',
+    '{"traceEvents": [{"ph": "X", "name": "a", "cat": "cpu_op", "ts": "1", "dur": 2}]}',
+])
+def test_fast_scanner_defers_errors_to_the_dom_path(tmp_path, monkeypatch, body):
+    # malformed JSON and unexpected field types raise exactly what the DOM
+    # path raises (the scanner hands such files to it)
+    p = tmp_path / "rank_0.json"
+    p.write_text(body)
+    errs = []
+    for dom in ("0", "1"):
+        monkeypatch.setenv("LUMOS_INGEST_DOM", dom)
+        with pytest.raises(Exception) as e:
+            ingest_traces([str(p)])
+        errs.append(str(e.value))
+    assert errs[0] == errs[1]
