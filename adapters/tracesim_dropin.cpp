@@ -9,8 +9,7 @@
 // acceptance gate, the tests — then replays on the GPU.  Exceptions follow the
 // reference taxonomy (types.hpp:109-138): invalid graphs and deadlocks throw
 // SimulationError with the reference's message text ("invalid graph: ...";
-// "deadlock with N tasks blocked" — the witness id list of simulate.cpp:300 is
-// not reproduced).
+// "deadlock with N tasks blocked: <witness ids>" as simulate.cpp:300 builds it).
 //
 // The batched entry point (not in the reference) is declared in
 // tracesim_b200.hpp: N duration scenarios of one graph in one call.

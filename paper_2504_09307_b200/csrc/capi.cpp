@@ -513,6 +513,66 @@ int ts_graph_streams(const ts_graph* g, int32_t* rank, int32_t* lane) {
   return TS_OK;
 }
 
+// report_deadlock (simulate.cpp:258-303) on the final state of one replayed
+// scenario, read back from its DES scratch (des.cu carve layout): the chain of
+// blockers from the lowest unstarted task, the cycle if it closes one.
+static std::string deadlock_witness(const DesTables& T, int32_t n, const std::vector<char>& scr,
+                                    int64_t unstarted) {
+  const int32_t nl = T.n_lanes;
+  const int64_t* sim_start = reinterpret_cast<const int64_t*>(scr.data());
+  const int32_t* p32 = reinterpret_cast<const int32_t*>(
+      sim_start + 3 * static_cast<int64_t>(n) + nl + 2 * static_cast<int64_t>(n));
+  const int32_t* indeg = p32;
+  const int32_t* heap = p32 + n;
+  const int32_t* hsize = p32 + 3 * static_cast<int64_t>(n);
+  auto started = [&](int32_t t) { return sim_start[t] != INT64_MIN; };
+  // ready sets in (original_start, id) order
+  std::vector<std::vector<int32_t>> ready(nl);
+  for (int32_t l = 0; l < nl; ++l) {
+    ready[l].assign(heap + T.lane_off[l], heap + T.lane_off[l] + hsize[l]);
+    std::sort(ready[l].begin(), ready[l].end(), [&](int32_t a, int32_t b) {
+      return std::make_pair(T.ostart[a], a) < std::make_pair(T.ostart[b], b);
+    });
+  }
+  std::vector<int32_t> min_pred(n, -1);  // lowest unstarted fixed-edge predecessor
+  for (int32_t u = 0; u < n; ++u) {
+    if (started(u)) continue;
+    for (int32_t k = T.succ_off[u]; k < T.succ_off[u + 1]; ++k) {
+      const int32_t v = T.succ[k];
+      if (!started(v) && (min_pred[v] < 0 || u < min_pred[v])) min_pred[v] = u;
+    }
+  }
+  auto blocker_of = [&](int32_t t) -> int32_t {
+    if (indeg[t] > 0) return min_pred[t];
+    const auto& own = ready[T.lane_of[t]];
+    if (!own.empty() && std::make_pair(T.ostart[own[0]], own[0]) < std::make_pair(T.ostart[t], t))
+      return own[0];
+    const int32_t r = T.rule_of[t];
+    if (r >= 0) {
+      if (T.rule_kind[r] == TS_RULE_EVENT_SYNC) return T.rule_bound[r];
+      for (int32_t w = T.rule_wl_off[r]; w < T.rule_wl_off[r + 1]; ++w)
+        for (int32_t id : ready[T.rule_wl[w]])
+          if (id != t) return id;
+    }
+    return -1;
+  };
+  int32_t cur = -1;
+  for (int32_t i = 0; i < n && cur < 0; ++i)
+    if (!started(i)) cur = i;
+  std::vector<int32_t> path;
+  std::vector<char> on_path(n, 0);
+  while (cur >= 0 && !on_path[cur]) {
+    on_path[cur] = 1;
+    path.push_back(cur);
+    cur = blocker_of(cur);
+  }
+  std::vector<int32_t> cycle = path;
+  if (cur >= 0) cycle.assign(std::find(path.begin(), path.end(), cur), path.end());
+  std::string msg = "deadlock with " + std::to_string(unstarted) + " tasks blocked: ";
+  for (size_t i = 0; i < cycle.size(); ++i) msg += (i ? " " : "") + std::to_string(cycle[i]);
+  return msg;
+}
+
 static int scenario_params(const ts_graph* g, const ts_scenarios* sc, ScenarioParams& sp) {
   std::memset(&sp, 0, sizeof(sp));
   if (sc->count < 0) return fail(TS_E_INVALID_ARGUMENT, "scenario count must be >= 0");
@@ -1290,13 +1350,23 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
   for (int32_t i = 0; i < static_cast<int32_t>(host_status.size()); ++i)
     if (host_status[i] < 0 && n_dead++ == 0) first_dead = i;
   if (c.des_only && n_dead > 0) {
-    // the reference's message (simulate.cpp:300) without the witness ids
+    // the reference's message (simulate.cpp:300); the witness ids of a single
+    // scenario come from its final event-driven state (still in the scratch)
     int64_t blocked = 0;
     if (cudaMemcpy(&blocked, hi + first_dead, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
       cudaGetLastError();
       blocked = -1;
     }
     std::string msg = "deadlock with " + std::to_string(blocked) + " tasks blocked";
+    if (count == 1 && blocked >= 0 && g->des_scratch.bytes > 0) {
+      std::vector<char> scr(des_scratch_bytes(c.n_tasks, c.des.n_lanes));
+      if (scr.size() <= g->des_scratch.bytes &&
+          cudaMemcpy(scr.data(), g->des_scratch.as<char>(), scr.size(),
+                     cudaMemcpyDeviceToHost) == cudaSuccess)
+        msg = deadlock_witness(c.des, c.n_tasks, scr, blocked);
+      else
+        cudaGetLastError();
+    }
     if (count > 1)
       msg += " (scenario " + std::to_string(sc->first + first_dead) + "; " +
              std::to_string(n_dead) + " of " + std::to_string(count) + " scenarios deadlocked)";

@@ -183,8 +183,12 @@ def test_deadlock_raises_simulation_error():
     # test_simulator.cpp:197-220: two syncs watching each other's lanes
     g = _graph([(0, 1, 0, 5), (0, 2, 0, 5)],
                rules=[(0, 0, -1, [(0, 0, 2)]), (0, 1, -1, [(0, 0, 1)])])
-    with pytest.raises(SimulationError, match="deadlock"):
+    with pytest.raises(SimulationError, match="deadlock") as e:
         simulate(g)
+    # the reference's full message, witness chain included (simulate.cpp:258-303)
+    with pytest.raises(R.RefError) as r:
+        R.from_graph(g).simulate()
+    assert str(e.value) == str(r.value).split("] ", 1)[1]
 
 
 def test_certificate_failure_is_resolved_exactly():
