@@ -509,7 +509,9 @@ def main():
                 sc_bytes += 72  # the ts_scenarios descriptor read from host memory
                 dg.replay_batch(spec, start=start, fin=fin, ld=tile,
                                 span=h_span[t0_:t0_ + tile], rank_breakdown=h_bd[t0_:t0_ + tile],
-                                stream_busy=h_busy[t0_:t0_ + tile], stream=sptr)
+                                stream_busy=h_busy[t0_:t0_ + tile], stream=sptr,
+                                host_async=True)
+            dg.wait()  # every tile's results are in host memory before the step ends
         e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -528,8 +530,9 @@ def main():
                "h2d_bytes_per_step": sc_bytes * world, "d2h_bytes_per_step": d2h * world,
                "ms_per_step": e2e_s * 1e3,
                "note": "host scenario descriptors in, per-scenario span + per-rank breakdown + "
-                       "per-stream busy copied to pinned host memory every step; timestamps "
-                       "stay in device memory"}
+                       "per-stream busy copied to pinned host memory every step (each tile's "
+                       "copy overlaps the next tile's kernels, host_async; the step ends after "
+                       "ts_graph_wait); timestamps stay in device memory"}
 
     # scenarios the exact event-driven path re-ran (failed sync certificates),
     # counted on one extra step outside the timed region

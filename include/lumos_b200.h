@@ -229,7 +229,11 @@ typedef struct {
                               task -1 pads a graph with fewer tasks */
   int32_t delta_worst_n;   /* entries per scenario, 1..64 (0 means 1); the
                               reference's default is 10 (metrics.hpp:82-83) */
-  int32_t pad2;
+  int32_t host_async;      /* 1: host output buffers are filled by copies on the
+                              graph's copy stream that overlap the next call's
+                              kernels; the call returns once they are enqueued and
+                              ts_graph_wait() blocks until they have landed (calls
+                              that must read a status back stay synchronous) */
   int32_t* n_fixups;       /* [1] scenarios of this call re-run by the exact
                               event-driven path (failed sync certificates), or NULL */
 } ts_result;
@@ -238,6 +242,8 @@ typedef struct {
  * default).  Returns after the work is enqueued when every output pointer is
  * device memory; otherwise it synchronises and copies to the host buffers. */
 int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, void* stream);
+/* waits for the host copies of ts_result.host_async calls */
+int ts_graph_wait(ts_graph* g);
 
 /* simulate(const ExecutionGraph&) (simulate.hpp:51): one replay at the
  * graph's own durations; host buffers start/fin [n_tasks], span[3]. */

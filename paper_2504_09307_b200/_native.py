@@ -74,7 +74,7 @@ class TsResult(C.Structure):
                 ("util_bin_width", C.c_int64), ("util_max_bins", C.c_int32),
                 ("util_pad", C.c_int32), ("util_covered", i64p), ("util_n_bins", i32p),
                 ("delta_abs_sum", i64p), ("delta_worst", i64p), ("delta_worst_n", C.c_int32),
-                ("pad2", C.c_int32), ("n_fixups", i32p)]
+                ("host_async", C.c_int32), ("n_fixups", i32p)]
 
 
 ABI_VERSION = 5  # TS_ABI_VERSION in include/lumos_b200.h
@@ -105,6 +105,8 @@ def lib():
         L.ts_replay_batch.restype = C.c_int
         L.ts_replay_batch.argtypes = [C.c_void_p, C.POINTER(TsScenarios), C.POINTER(TsResult),
                                       C.c_void_p]
+        L.ts_graph_wait.restype = C.c_int
+        L.ts_graph_wait.argtypes = [C.c_void_p]
         L.ts_simulate.restype = C.c_int
         L.ts_simulate.argtypes = [C.c_void_p, i64p, i64p, i64p]
         L.ts_scenario_durations.restype = C.c_int
@@ -141,4 +143,4 @@ EXPORTED = ["ts_abi_version", "ts_last_error", "ts_kernel_launches", "ts_graph_c
             "ts_host_graph_op_index", "ts_host_graph_n_ops", "ts_host_graph_name_ids",
             "ts_host_graph_name", "ts_host_graph_free", "ts_build_rank_graph",
             "ts_ingest_traces", "ts_ingest_traces_ex", "ts_pipeline_defaults", "ts_pipeline_graph",
-            "ts_rebuild_pipeline", "ts_pipeline_spec_get", "ts_pipeline_free"]
+            "ts_rebuild_pipeline", "ts_pipeline_spec_get", "ts_pipeline_free", "ts_graph_wait"]

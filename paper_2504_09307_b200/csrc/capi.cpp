@@ -156,6 +156,14 @@ struct ts_graph {
   DevBuf span_lo, span_hi, status, scratch_ts;
   DevBuf stage[12];  // host-pointer staging: start, fin, span, breakdown, busy, num, dur,
                      // util, util bins, delta sum, delta worst, internal bin counts
+  // ts_result.host_async: output staging in two sets, copied to the host on
+  // copy_stream while the next call's kernels run; copy_done[k] guards set k
+  DevBuf astage[2][12];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done[2] = {nullptr, nullptr};
+  cudaEvent_t kernels_done = nullptr;
+  bool copy_pending[2] = {false, false};
+  int async_set = 0;
   DevBuf delta_scratch;
   // device-time accounting
   bool profile = false;
@@ -429,12 +437,25 @@ int ts_graph_create(const ts_graph_desc* desc, int device, ts_graph** out) {
   return TS_OK;
 }
 
+int ts_graph_wait(ts_graph* g) {
+  if (!g) return fail(TS_E_INVALID_ARGUMENT, "null argument");
+  if (g->copy_stream && cudaStreamSynchronize(g->copy_stream) != cudaSuccess)
+    return fail(TS_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+  return TS_OK;
+}
+
 void ts_graph_destroy(ts_graph* g) {
   if (!g) return;
   if (g->has_device) {
     int prev = -1;
     cudaGetDevice(&prev);
     if (g->device >= 0) cudaSetDevice(g->device);
+    if (g->copy_stream) {
+      cudaStreamSynchronize(g->copy_stream);
+      cudaStreamDestroy(g->copy_stream);
+      for (cudaEvent_t e : {g->copy_done[0], g->copy_done[1], g->kernels_done})
+        if (e) cudaEventDestroy(e);
+    }
     for (void* p : {static_cast<void*>(g->d_ops), static_cast<void*>(g->d_progs),
                     static_cast<void*>(g->d_comps), static_cast<void*>(g->d_comp_order),
                     static_cast<void*>(g->d_coop_comps), static_cast<void*>(g->d_coop_prog_off),
@@ -868,12 +889,20 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     void* dev;
   };
   std::vector<OutBuf> copies;
+  const bool host_async = out->host_async != 0;
+  const int aset = g->async_set;
+  if (host_async && g->copy_pending[aset]) {
+    // the set's previous host copy must finish before this call rewrites it
+    CUDA_TRY(cudaStreamWaitEvent(stream, g->copy_done[aset], 0));
+    g->copy_pending[aset] = false;
+  }
   auto out_ptr = [&](int slot, void* user, size_t bytes) -> void* {
     if (!user || bytes == 0) return nullptr;
     if (is_device_ptr(user)) return user;
-    if (g->stage[slot].reserve(bytes) != cudaSuccess) return nullptr;
-    copies.push_back({user, bytes, g->stage[slot].p});
-    return g->stage[slot].p;
+    DevBuf& b = host_async ? g->astage[aset][slot] : g->stage[slot];
+    if (b.reserve(bytes) != cudaSuccess) return nullptr;
+    copies.push_back({user, bytes, b.p});
+    return b.p;
   };
   const size_t ts_bytes = static_cast<size_t>(c.n_tasks) * static_cast<size_t>(out->ld) * 8;
   int64_t* d_start = static_cast<int64_t*>(out_ptr(0, out->start, ts_bytes));
@@ -1305,6 +1334,23 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
     host_nbins.resize(count);
     CUDA_TRY(cudaMemcpyAsync(host_nbins.data(), d_nbins_chk, static_cast<size_t>(count) * 4,
                              cudaMemcpyDeviceToHost, stream));
+  }
+  if (host_async && !copies.empty() && host_status.empty() && host_nbins.empty()) {
+    // copies run on the graph's copy stream behind this call's kernels; the
+    // call returns at once (ts_graph_wait blocks until they have landed)
+    if (!g->copy_stream) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&g->copy_done[0], &g->copy_done[1], &g->kernels_done})
+        CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(g->kernels_done, stream));
+    CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->kernels_done, 0));
+    for (const OutBuf& b : copies)
+      CUDA_TRY(cudaMemcpyAsync(b.user, b.dev, b.bytes, cudaMemcpyDeviceToHost, g->copy_stream));
+    CUDA_TRY(cudaEventRecord(g->copy_done[aset], g->copy_stream));
+    g->copy_pending[aset] = true;
+    g->async_set = aset ^ 1;
+    copies.clear();
   }
   for (const OutBuf& b : copies)
     CUDA_TRY(cudaMemcpyAsync(b.user, b.dev, b.bytes, cudaMemcpyDeviceToHost, stream));

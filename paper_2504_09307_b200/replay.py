@@ -225,9 +225,12 @@ class DeviceGraph:
     def replay_batch(self, spec: ScenarioSpec, start=None, fin=None, ld: int = 0, span=None,
                      rank_breakdown=None, stream_busy=None, status=None, stream=None,
                      util_bin_width: int = 0, util_covered=None, util_n_bins=None,
-                     delta_abs_sum=None, delta_worst=None, n_fixups=None) -> None:
+                     delta_abs_sum=None, delta_worst=None, n_fixups=None,
+                     host_async: bool = False) -> None:
         """Raw ts_replay_batch: outputs are caller-owned numpy (host) or torch
-        (device or host) buffers; see include/lumos_b200.h for shapes."""
+        (device or host) buffers; see include/lumos_b200.h for shapes.  With
+        host_async the host buffers are filled by copies that overlap the next
+        call's kernels; wait() before reading them (pinned buffers, kept alive)."""
         sc = spec.to_c()
         r = N.TsResult()
         r.start = _ptr(start, N.i64p)
@@ -248,8 +251,15 @@ class DeviceGraph:
         r.delta_worst_n = int(delta_worst.shape[1]) if (delta_worst is not None and
                                                           len(delta_worst.shape) == 3) else 1
         r.n_fixups = _ptr(n_fixups, N.i32p)
+        r.host_async = 1 if host_async else 0
         s = C.c_void_p(stream) if isinstance(stream, int) else stream
         rc = N.lib().ts_replay_batch(self.h, C.byref(sc), C.byref(r), s)
+        if rc != N.TS_OK:
+            _raise(rc)
+
+    def wait(self) -> None:
+        """Block until the host copies of host_async replay_batch calls have landed."""
+        rc = N.lib().ts_graph_wait(self.h)
         if rc != N.TS_OK:
             _raise(rc)
 
