@@ -170,3 +170,28 @@ def test_rebuild_needs_task_metadata():
         assert "task metadata" in L.ts_last_error().decode()
     finally:
         L.ts_host_graph_free(h)
+
+
+def test_rebuild_from_traces_with_exotic_args(tmp_path, monkeypatch):
+    # recorded traces whose kernels carry float / array / object args: those
+    # files take the DOM path when Task.meta is kept (nlohmann's dump text is
+    # the meta value), and the args travel into the rebuilt KernelSpecs
+    import json
+    smodel = _model()
+    R.write_rank_traces(R.synth_spec(pp=2, dp=1, m=4), str(tmp_path))
+    paths = sorted(str(tmp_path / f) for f in os.listdir(tmp_path))
+    for p in paths:
+        d = json.load(open(p))
+        for ev in d["traceEvents"]:
+            if ev.get("cat") == "kernel" and ev["name"].startswith("gemm"):
+                ev.setdefault("args", {}).update({"flops": 1.5e12, "dims": [2048, [1, 2]],
+                                                  "misc": {"a": None, "b": True}})
+        json.dump(d, open(p, "w"))
+    w = WhatIfConfig(smodel, smodel, ParallelismConfig(1, 2, 1, 4), ParallelismConfig(1, 4, 1, 4))
+    spec = rebuild_pipeline(paths, w)
+    k = spec.stages[0].layers_fwd[0][0]
+    assert k.name == "gemm_qkv" and k.args["flops"] == "1500000000000.0", k.args
+    assert k.args["dims"] == "[2048,[1,2]]" and k.args["misc"] == '{"a":null,"b":true}'
+    ref, _ = R.ingest_traces(paths).apply_whatif(_tuple(smodel), _tuple(smodel),
+                                                 _par(w.source_par), _par(w.target_par))
+    _assert_graph_equals_reference(spec, ref)
