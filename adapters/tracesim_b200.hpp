@@ -11,6 +11,7 @@
 #include "tracesim/metrics.hpp"
 #include "tracesim/pipeline.hpp"
 #include "tracesim/simulate.hpp"
+#include "tracesim/transform.hpp"
 
 namespace tracesim::b200 {
 
@@ -91,6 +92,22 @@ struct EstimateResult {
 };
 EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scenarios,
                               const BatchOptions& options = {}, int tp = 1);
+
+// estimate() of a structural what-if, batched: the PipelineSpec
+// rebuild_pipeline (transform.cpp:556-701) lays out for `cfg` from the
+// measured source graph (tag_tasks + measure_pipeline over its Task.meta, on
+// the host, ts_rebuild_pipeline), replayed like estimate_batch.  cfg's cost
+// model must be an AnalyticalCostModel; errors throw TransformError with the
+// reference's text.  rebuilt = false (nothing replayed) when the target
+// differs in nothing the rebuild models — apply_whatif then retimes in place
+// (ScenarioSpec's retime fields) or returns the source.
+struct WhatIfEstimate : EstimateResult {
+  bool rebuilt = false;
+  PipelineSpec spec;  // the rebuilt spec
+};
+WhatIfEstimate estimate_whatif(const ExecutionGraph& source, const WhatIfConfig& cfg,
+                               const ScenarioSpec& scenarios, const BatchOptions& options = {},
+                               int tp = 1);
 
 // Scenario s of a batch run with timestamps as a SimulatedTrace (entries in
 // (sim_start, task_id) order, simulate.hpp:12-24) — e.g. for

@@ -594,15 +594,17 @@ struct PipelinePod {
 
 }  // namespace
 
-EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scenarios,
-                              const BatchOptions& options, int tp) {
+namespace {
+
+// the estimate graph of a ts_pipeline_spec replayed for `scenarios`
+EstimateResult estimate_pod(const ts_pipeline_spec& spec, const ScenarioSpec& scenarios,
+                            const BatchOptions& options, int tp) {
   if (!scenarios.alpha_us.empty())
     throw std::invalid_argument(
         "estimate_batch: retime the PipelineSpec itself (rebuild_pipeline) instead of per scenario");
-  PipelinePod pod(spec);
   ts_host_graph* hg = nullptr;
   EstimateResult out;
-  if (int rc = ts_pipeline_graph(&pod.c, 1, tp, &hg, &out.truth_makespan)) {
+  if (int rc = ts_pipeline_graph(&spec, 1, tp, &hg, &out.truth_makespan)) {
     const std::string msg = ts_last_error();
     if (rc == TS_E_INVALID_ARGUMENT) throw std::invalid_argument(msg);
     rethrow(rc);
@@ -629,6 +631,132 @@ EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scen
   o.util_bin_width = 0;  // the reductions of an estimate graph are not defined here
   o.deltas = false;
   out.batch = run_batch(g, n, scenarios, o, 0);
+  return out;
+}
+
+std::vector<KernelSpec> kernels_of(const ts_kernel_list& l) {
+  std::vector<KernelSpec> out;
+  for (int32_t i = 0; i < l.n; ++i) {
+    const ts_kernel_spec& k = l.k[i];
+    KernelSpec ks;
+    ks.name = k.name ? k.name : "";
+    ks.duration = k.duration;
+    ks.op_class = static_cast<OpClass>(k.op_class);
+    for (int32_t a = 0; a < k.n_args; ++a) ks.args[k.arg_keys[a]] = k.arg_values[a];
+    out.push_back(std::move(ks));
+  }
+  return out;
+}
+
+PipelineSpec spec_of(const ts_pipeline_spec& c) {
+  PipelineSpec p;
+  p.pp = c.pp;
+  p.dp = c.dp;
+  p.num_microbatches = c.num_microbatches;
+  p.host = {c.launch_us, c.record_us, c.wait_us, c.sync_us};
+  p.p2p_send = c.p2p_send_us;
+  p.p2p_recv_base = c.p2p_recv_base_us;
+  p.activation_bytes = c.activation_bytes;
+  p.origin = c.origin;
+  p.compute_stream = c.compute_stream;
+  p.reduce_stream = c.reduce_stream;
+  p.p2p_stream = c.p2p_stream;
+  p.main_thread = c.main_thread;
+  p.helper_thread = c.helper_thread;
+  p.first_event = c.first_event;
+  p.first_correlation = c.first_correlation;
+  for (int32_t s = 0; s < c.n_stages; ++s) {
+    const ts_stage_spec& cs = c.stages[s];
+    StageSpec st;
+    for (int32_t l = 0; l < cs.n_layers; ++l) {
+      st.layers_fwd.push_back(kernels_of(cs.layers_fwd[l]));
+      st.layers_bwd.push_back(kernels_of(cs.layers_bwd[l]));
+    }
+    st.pre_fwd = kernels_of(cs.pre_fwd);
+    st.post_fwd = kernels_of(cs.post_fwd);
+    st.pre_bwd = kernels_of(cs.pre_bwd);
+    st.post_bwd = kernels_of(cs.post_bwd);
+    st.reduce = kernels_of(cs.reduce);
+    st.optimizer = kernels_of(cs.optimizer);
+    p.stages.push_back(std::move(st));
+  }
+  return p;
+}
+
+}  // namespace
+
+EstimateResult estimate_batch(const PipelineSpec& spec, const ScenarioSpec& scenarios,
+                              const BatchOptions& options, int tp) {
+  PipelinePod pod(spec);
+  return estimate_pod(pod.c, scenarios, options, tp);
+}
+
+WhatIfEstimate estimate_whatif(const ExecutionGraph& source, const WhatIfConfig& cfg,
+                               const ScenarioSpec& scenarios, const BatchOptions& options,
+                               int tp) {
+  const auto* am = dynamic_cast<const AnalyticalCostModel*>(cfg.cost_model.get());
+  if (!cfg.cost_model) throw TransformError("what-if config has no cost model");
+  if (!am) throw TransformError("estimate_whatif: the device rebuild takes an AnalyticalCostModel");
+  // the source graph with its Task.meta and correlation ids
+  Soa soa(source);
+  const std::size_t n = source.tasks.size();
+  std::vector<const char*> names(n), mk, mv;
+  std::vector<int64_t> corr(n, -1);
+  std::vector<int32_t> moff(n + 1, 0);
+  for (std::size_t i = 0; i < n; ++i) {
+    const Task& t = source.tasks[i];
+    names[i] = t.name.c_str();
+    if (t.correlation_id) corr[i] = *t.correlation_id;
+    for (const auto& [k, v] : t.meta) {
+      mk.push_back(k.c_str());
+      mv.push_back(v.c_str());
+    }
+    moff[i + 1] = static_cast<int32_t>(mk.size());
+  }
+  ts_host_graph* hg = nullptr;
+  if (int rc = ts_host_graph_from_tasks(&soa.desc, names.data(), corr.data(), moff.data(),
+                                        mk.data(), mv.data(), &hg))
+    rethrow(rc);
+  struct Free {
+    ts_host_graph* h;
+    ~Free() { ts_host_graph_free(h); }
+  } free_hg{hg};
+  auto model = [](const ModelConfig& m) {
+    ts_model_config c{};
+    c.n_params = m.n_params;
+    c.n_layers = m.n_layers;
+    c.d_model = m.d_model;
+    c.d_ffn = m.d_ffn;
+    c.n_heads = m.n_heads;
+    c.d_head = m.d_head;
+    return c;
+  };
+  auto par = [](const ParallelismConfig& p) {
+    return ts_par_config{p.tp, p.pp, p.dp, p.num_microbatches};
+  };
+  ts_whatif w{};
+  w.source_model = model(cfg.source_model);
+  w.target_model = model(cfg.target_model);
+  w.source_par = par(cfg.source_par);
+  w.target_par = par(cfg.target_par);
+  w.alpha_us = am->alpha_us();
+  w.bytes_per_us = am->bytes_per_us();
+  w.activation_bytes = cfg.activation_bytes;
+  ts_pipeline* p = nullptr;
+  if (int rc = ts_rebuild_pipeline(hg, &w, &p)) {
+    if (rc == TS_E_INVALID_ARGUMENT) throw TransformError(ts_last_error());
+    rethrow(rc);
+  }
+  WhatIfEstimate out;
+  if (!p) return out;  // nothing the rebuild models changes: replay the source instead
+  struct FreeP {
+    ts_pipeline* p;
+    ~FreeP() { ts_pipeline_free(p); }
+  } free_p{p};
+  const ts_pipeline_spec* c = ts_pipeline_spec_get(p);
+  out.spec = spec_of(*c);
+  static_cast<EstimateResult&>(out) = estimate_pod(*c, scenarios, options, tp);
+  out.rebuilt = true;
   return out;
 }
 

@@ -374,6 +374,14 @@ typedef struct {                 /* WhatIfConfig (transform.hpp:28-41) */
   const char* tag_policy_json;   /* TagPolicy::from_json text, NULL = defaults */
 } ts_whatif;
 typedef struct ts_pipeline ts_pipeline;
+/* A host graph from task arrays and their metadata, for callers that hold a
+ * built ExecutionGraph (the C++ drop-in): desc's tasks, edges, rules and
+ * window; per task its name, correlation id (-1 = none) and Task.meta as
+ * meta_off[n + 1] into meta_keys / meta_values (types.hpp:73-87). */
+int ts_host_graph_from_tasks(const ts_graph_desc* desc, const char* const* names,
+                             const int64_t* corr, const int32_t* meta_off,
+                             const char* const* meta_keys, const char* const* meta_values,
+                             ts_host_graph** out);
 int ts_rebuild_pipeline(const ts_host_graph* source, const ts_whatif* whatif, ts_pipeline** out);
 /* the rebuilt spec; valid while the ts_pipeline lives */
 const ts_pipeline_spec* ts_pipeline_spec_get(const ts_pipeline* p);

@@ -10,6 +10,7 @@
 // the C restatement of the scenario formula (lumos_oracle.c).
 #include <cstdio>
 #include <map>
+#include <memory>
 #include <vector>
 
 #include "json.hpp"
@@ -208,8 +209,59 @@ int main() {
     }
   }
   bad += bad_est;
+  // structural what-if through the C++ API: estimate_whatif(source graph,
+  // WhatIfConfig) rebuilds the spec on the device library's host side; its
+  // nominal makespan equals simulate() of the reference apply_whatif graph
+  // (test_transform.cpp:294-304) and every scenario equals the reference
+  // build_pipeline(rebuilt spec, hook)
+  int bad_wi = 0;
+  {
+    WhatIfConfig cfg;
+    cfg.source_model = SynthSpec::from_json(j.dump()).model;
+    cfg.target_model = cfg.source_model;
+    cfg.target_model.n_layers = 8;
+    cfg.source_par = SynthSpec::from_json(j.dump()).par;
+    cfg.target_par = cfg.source_par;
+    cfg.target_par.pp = 4;
+    cfg.target_par.dp = 4;
+    cfg.target_par.num_microbatches = 8;
+    cfg.cost_model = std::make_shared<AnalyticalCostModel>(10.0, 50000.0);
+    b200::ScenarioSpec es;
+    es.first = 2;
+    es.count = 5;
+    es.seed = 17;
+    es.jitter = 0.2;
+    b200::BatchOptions eo;
+    eo.timestamps = true;
+    const b200::WhatIfEstimate we = b200::estimate_whatif(g, cfg, es, eo);
+    const TransformResult ref = apply_whatif(g, cfg);
+    if (!we.rebuilt || we.truth_makespan != simulate(ref.graph).makespan) {
+      ++bad_wi;
+      std::printf("estimate_whatif: rebuilt %d nominal %lld vs reference %lld\n",
+                  static_cast<int>(we.rebuilt), static_cast<long long>(we.truth_makespan),
+                  static_cast<long long>(simulate(ref.graph).makespan));
+    }
+    orc_scenarios esc{};
+    esc.seed = es.seed;
+    esc.jitter = es.jitter;
+    const std::size_t n = we.base.size();
+    std::vector<uint8_t> ecls(n, 0);
+    std::vector<int64_t> d(n);
+    for (int s = 0; s < es.count && we.rebuilt; ++s) {
+      orc_fill_durations(&esc, es.first + s, static_cast<int32_t>(n), we.base.data(),
+                         ecls.data(), d.data());
+      std::vector<Micros> hook(static_cast<std::size_t>(we.n_ops), 0);
+      for (std::size_t t = 0; t < n; ++t)
+        if (we.op_index[t] >= 0) hook[static_cast<std::size_t>(we.op_index[t])] = d[t];
+      const BuiltPipeline b = build_pipeline(
+          we.spec, [&](std::size_t i, Micros base) { return i < hook.size() ? hook[i] : base; });
+      if (b.end - we.spec.origin != we.batch.span[3 * s + 2]) ++bad_wi;
+    }
+  }
+  bad += bad_wi;
   std::printf("%s: %d scenarios, %zu tasks, %d mismatches (retime: %d scenarios, %d; "
-              "estimate_batch: %d)\n",
-              bad ? "FAIL" : "PASS", spec.count, g.tasks.size(), bad, rs.count, bad_rt, bad_est);
+              "estimate_batch: %d; estimate_whatif: %d)\n",
+              bad ? "FAIL" : "PASS", spec.count, g.tasks.size(), bad, rs.count, bad_rt, bad_est,
+              bad_wi);
   return bad ? 1 : 0;
 }

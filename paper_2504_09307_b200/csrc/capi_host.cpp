@@ -5,6 +5,7 @@
 #include <deque>
 #include <fstream>
 #include <sstream>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -212,6 +213,59 @@ static void build_pod(ts_pipeline& h) {
   h.spec.p2p_recv_base_us = p.p2p_recv_base;
   h.spec.activation_bytes = p.activation_bytes;
   h.spec.origin = p.origin;
+}
+
+int ts_host_graph_from_tasks(const ts_graph_desc* d, const char* const* names,
+                             const int64_t* corr, const int32_t* meta_off,
+                             const char* const* meta_keys, const char* const* meta_values,
+                             ts_host_graph** out) {
+  if (!d || !out || d->n_tasks < 0 || (d->n_tasks > 0 && (!d->duration || !d->original_start ||
+                                                          !d->rank || !d->lane_kind || !d->lane ||
+                                                          !d->op_class || !d->task_kind)))
+    return set_error(TS_E_INVALID_ARGUMENT, "null argument");
+  auto* h = new ts_host_graph;
+  HostGraph& g = h->s.graph;
+  const int32_t n = d->n_tasks;
+  g.duration.assign(d->duration, d->duration + n);
+  g.original_start.assign(d->original_start, d->original_start + n);
+  g.rank.assign(d->rank, d->rank + n);
+  g.lane_kind.assign(d->lane_kind, d->lane_kind + n);
+  g.lane.assign(d->lane, d->lane + n);
+  g.op_class.assign(d->op_class, d->op_class + n);
+  g.task_kind.assign(d->task_kind, d->task_kind + n);
+  if (d->n_edges > 0 && d->edge_from && d->edge_to) {
+    g.edge_from.assign(d->edge_from, d->edge_from + d->n_edges);
+    g.edge_to.assign(d->edge_to, d->edge_to + d->n_edges);
+  }
+  if (d->n_rules > 0 && d->rule_kind && d->rule_task && d->rule_bound && d->rule_watch_off) {
+    g.rule_kind.assign(d->rule_kind, d->rule_kind + d->n_rules);
+    g.rule_task.assign(d->rule_task, d->rule_task + d->n_rules);
+    g.rule_bound.assign(d->rule_bound, d->rule_bound + d->n_rules);
+    g.rule_watch_off.assign(d->rule_watch_off, d->rule_watch_off + d->n_rules + 1);
+    const int32_t nw = d->rule_watch_off[d->n_rules];
+    if (nw > 0 && d->watch_rank && d->watch_kind && d->watch_lane) {
+      g.watch_rank.assign(d->watch_rank, d->watch_rank + nw);
+      g.watch_kind.assign(d->watch_kind, d->watch_kind + nw);
+      g.watch_lane.assign(d->watch_lane, d->watch_lane + nw);
+    }
+  }
+  g.window_start = d->window_start;
+  g.window_end = d->window_end;
+  g.op_index.assign(n, -1);
+  g.name.resize(n);
+  for (int32_t t = 0; t < n; ++t) g.name[t] = h->s.names.get(names && names[t] ? names[t] : "");
+  g.corr.assign(n, -1);
+  if (corr) g.corr.assign(corr, corr + n);
+  g.meta.assign(n, MetaList{});
+  if (meta_off && meta_keys && meta_values)
+    for (int32_t t = 0; t < n; ++t) {
+      std::map<std::string, std::string> m;
+      for (int32_t k = meta_off[t]; k < meta_off[t + 1]; ++k)
+        m[meta_keys[k] ? meta_keys[k] : ""] = meta_values[k] ? meta_values[k] : "";
+      g.meta[t].assign(m.begin(), m.end());
+    }
+  *out = h;
+  return TS_OK;
 }
 
 int ts_rebuild_pipeline(const ts_host_graph* source, const ts_whatif* w, ts_pipeline** out) {
