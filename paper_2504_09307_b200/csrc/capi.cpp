@@ -1238,6 +1238,10 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       const size_t budget = std::max<size_t>(size_t(1) << 30, (free_b + g->des_scratch.bytes) / 4);
       dp.n_slots = static_cast<int32_t>(
           std::max<size_t>(1, std::min<size_t>(static_cast<size_t>(bn), budget / per)));
+      // lane state in shared memory when it fits two CTAs per SM (LUMOS_DES_SMEM=0: global)
+      const char* des_env = std::getenv("LUMOS_DES_SMEM");
+      const bool des_smem = !(des_env && des_env[0] == '0');
+      dp.smem_lanes = des_smem && T.n_lanes > 0 && des_smem_bytes(T.n_lanes) <= 96 * 1024;
       CUDA_TRY(g->des_scratch.reserve(per * dp.n_slots));
       dp.scratch = g->des_scratch.as<char>();
       dp.scratch_bytes = static_cast<int64_t>(per);

@@ -49,6 +49,8 @@ struct DesScratch {
   int32_t* lheap;      // [nl] free lanes with a non-empty ready set, min by head key
   int32_t* lpos;       // [nl] position in lheap; kOut / kParked
   int32_t* parked;     // [nl]
+  int64_t* hkey;       // [nl] key (original_start) of each lane's ready head
+  int32_t* hid;        // [nl] the head task (valid while hsize > 0)
 };
 
 constexpr int32_t kOut = -1, kParked = -2;
@@ -69,6 +71,10 @@ __device__ DesScratch carve(char* base, int32_t n, int32_t nl) {
   s.lheap = s.hsize + nl;
   s.lpos = s.lheap + nl;
   s.parked = s.lpos + nl;
+  // the head cache after the int32 region, 8-byte aligned
+  const uintptr_t end32 = reinterpret_cast<uintptr_t>(s.parked + nl);
+  s.hkey = reinterpret_cast<int64_t*>((end32 + 7) & ~uintptr_t(7));
+  s.hid = reinterpret_cast<int32_t*>(s.hkey + nl);
   return s;
 }
 
@@ -77,12 +83,22 @@ struct Des {
   DesScratch s;
   int64_t now = 0;
   int32_t lsize = 0, nparked = 0;
+  int32_t comp_cap = 0x7FFFFFFF;  // completion heap capacity (shared-memory mode: lanes)
 
   __device__ bool key_less(int32_t a, int32_t b) const {
     const int64_t ka = P.ostart[a], kb = P.ostart[b];
     return ka < kb || (ka == kb && a < b);
   }
-  __device__ int32_t head(int32_t l) const { return s.heap[P.lane_off[l]]; }
+  __device__ int32_t head(int32_t l) const { return s.hid[l]; }
+  // lane order = head order, from the cached (key, id) of each head
+  __device__ bool lane_less(int32_t a, int32_t b) const {
+    const int64_t ka = s.hkey[a], kb = s.hkey[b];
+    return ka < kb || (ka == kb && s.hid[a] < s.hid[b]);
+  }
+  __device__ void set_head(int32_t l, int32_t t) {
+    s.hid[l] = t;
+    s.hkey[l] = P.ostart[t];
+  }
   // lane heap: free lanes (clock <= now) with a non-empty ready set
   __device__ void lh_set(int32_t i, int32_t l) {
     s.lheap[i] = l;
@@ -90,10 +106,9 @@ struct Des {
   }
   __device__ void lh_up(int32_t i) {
     const int32_t l = s.lheap[i];
-    const int32_t hl = head(l);
     while (i > 0) {
       const int32_t p = (i - 1) >> 1;
-      if (!key_less(hl, head(s.lheap[p]))) break;
+      if (!lane_less(l, s.lheap[p])) break;
       lh_set(i, s.lheap[p]);
       i = p;
     }
@@ -109,16 +124,15 @@ struct Des {
     const int32_t n = --lsize;
     if (n > 0) {
       const int32_t l = s.lheap[n];
-      const int32_t hl = head(l);
       int32_t i = 0;
       for (;;) {
         const int32_t a = 2 * i + 1, b = a + 1;
-        int32_t m = -1, hm = hl;
-        if (a < n && key_less(head(s.lheap[a]), hm)) {
+        int32_t m = -1, lm = l;
+        if (a < n && lane_less(s.lheap[a], lm)) {
           m = a;
-          hm = head(s.lheap[a]);
+          lm = s.lheap[a];
         }
-        if (b < n && key_less(head(s.lheap[b]), hm)) m = b;
+        if (b < n && lane_less(s.lheap[b], lm)) m = b;
         if (m < 0) break;
         lh_set(i, s.lheap[m]);
         i = m;
@@ -145,6 +159,7 @@ struct Des {
       h[p] = x;
       i = p;
     }
+    if (i == 0) set_head(l, t);
     const int32_t pos = s.lpos[l];
     if (pos >= 0) {
       if (i == 0) lh_up(pos);
@@ -168,6 +183,7 @@ struct Des {
       h[m] = x;
       i = m;
     }
+    if (n > 0) set_head(l, h[0]);
   }
   __device__ bool comp_less(int32_t i, int32_t j) const {
     return s.comp_t[i] < s.comp_t[j] || (s.comp_t[i] == s.comp_t[j] && s.comp_id[i] < s.comp_id[j]);
@@ -181,6 +197,7 @@ struct Des {
     s.comp_id[j] = d;
   }
   __device__ void comp_push(int32_t& size, int64_t t, int32_t id) {
+    if (!LUMOS_OK(size < comp_cap)) return;
     int32_t i = size++;
     s.comp_t[i] = t;
     s.comp_id[i] = id;
@@ -256,11 +273,31 @@ __device__ void sort_i64(int64_t* a, int32_t n) {
 }
 
 __global__ void des_kernel(DesParams P) {
+  extern __shared__ __align__(16) unsigned char des_smem[];
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= P.n_slots) return;
   const int32_t n = P.n, nl = P.nl;
   Des E{P, carve(P.scratch + static_cast<int64_t>(slot) * P.scratch_bytes, n, nl)};
   DesScratch& s = E.s;
+  int32_t* const g_hsize = s.hsize;
+  if (P.smem_lanes) {
+    // one scenario per CTA: the per-lane state and the completion heap (at
+    // most one positive-duration task in flight per lane) in shared memory,
+    // so the heap walks of every start hit ~30-cycle loads instead of DRAM
+    int64_t* sm64 = reinterpret_cast<int64_t*>(des_smem);
+    s.clock = sm64;
+    s.comp_t = sm64 + nl;
+    int32_t* sm32 = reinterpret_cast<int32_t*>(sm64 + 2 * static_cast<int64_t>(nl));
+    s.hsize = sm32;
+    s.lheap = sm32 + nl;
+    s.lpos = sm32 + 2 * nl;
+    s.parked = sm32 + 3 * nl;
+    s.comp_id = sm32 + 4 * nl;
+    s.hid = sm32 + 5 * nl;
+    s.hkey = reinterpret_cast<int64_t*>(
+        (reinterpret_cast<uintptr_t>(sm32 + 6 * nl) + 7) & ~uintptr_t(7));
+    E.comp_cap = nl;
+  }
   for (int col = slot; col < P.sp.count; col += P.n_slots) {
     if (P.fixup && P.status[col] == 0) continue;
     ThreadScen ts;
@@ -329,6 +366,8 @@ __global__ void des_kernel(DesParams P) {
     if (dead) {  // span_hi carries the blocked-task count for the error message
       P.status[col] = -1;
       P.span_hi[col] = unstarted;
+      if (P.smem_lanes)  // the ready-set sizes, for the host's deadlock witness
+        for (int32_t l = 0; l < nl; ++l) g_hsize[l] = s.hsize[l];
       continue;
     }
     int64_t lo = W, hi = W;
@@ -427,12 +466,25 @@ int debug_bounds_status_des() { return 0; }
 
 size_t des_scratch_bytes(int32_t n, int32_t nl) {
   const size_t b = (static_cast<size_t>(n) * 3 + nl + 2 * static_cast<size_t>(n)) * 8 +
-                   (static_cast<size_t>(n) * 3 + 4 * static_cast<size_t>(nl)) * 4;
+                   (static_cast<size_t>(n) * 3 + 4 * static_cast<size_t>(nl)) * 4 + 8 +
+                   static_cast<size_t>(nl) * 12;  // + the head cache
   return (b + 255) / 256 * 256;
 }
 
+size_t des_smem_bytes(int32_t nl) { return static_cast<size_t>(nl) * 48 + 8; }
+
 cudaError_t launch_des(const DesParams& p, cudaStream_t stream) {
   if (p.n_slots <= 0 || p.sp.count <= 0) return cudaSuccess;
+  if (p.smem_lanes) {
+    const size_t smem = des_smem_bytes(p.nl);
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(des_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    des_kernel<<<p.n_slots, 1, smem, stream>>>(p);
+    return cudaGetLastError();
+  }
   const int threads = 64;
   des_kernel<<<(p.n_slots + threads - 1) / threads, threads, 0, stream>>>(p);
   return cudaGetLastError();

@@ -194,6 +194,7 @@ struct DesParams {
   int32_t util_max_bins;
   int32_t fixup;    // only scenarios whose status is non-zero (certificate failed)
   int32_t n_slots;  // concurrent scenarios (scratch slots)
+  int32_t smem_lanes;  // 1: one scenario per CTA, lane state + completion heap in shared memory
   char* scratch;
   int64_t scratch_bytes;  // per slot
   RetimeParams rt;  // has_rt: retime each duration first (fix-up of a retime walk)
@@ -201,6 +202,7 @@ struct DesParams {
   int32_t pad3;
 };
 size_t des_scratch_bytes(int32_t n, int32_t nl);
+size_t des_smem_bytes(int32_t nl);  // shared memory per CTA of the smem_lanes mode
 cudaError_t launch_des(const DesParams& p, cudaStream_t stream);
 
 int walk_threads();

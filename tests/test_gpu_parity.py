@@ -499,15 +499,18 @@ def test_split_accounting_equals_full_sweep(shape, monkeypatch):
             assert tuple(out["1"].rank_breakdown[s_, i]) == ref[r]
 
 
-def test_event_driven_path_equals_walk(monkeypatch):
+@pytest.mark.parametrize("des_smem", ["1", "0"])
+def test_event_driven_path_equals_walk(monkeypatch, des_smem):
     # two independent device restatements of simulate(): the straight-line
     # walk and the event-driven kernel (LUMOS_FORCE_DES=1 sends every scenario
-    # to it) agree on every timestamp, span, breakdown and stream busy value
+    # to it; lane state in shared or global memory) agree on every timestamp,
+    # span, breakdown and stream busy value
     h, _ = R.generate(R.synth_spec(pp=2, dp=2, m=4, layers=4))
     g = h.export()
     spec = ScenarioSpec(count=40, first=6, seed=31, jitter=0.2)
     walk = simulate_batch(g, spec)
     monkeypatch.setenv("LUMOS_FORCE_DES", "1")
+    monkeypatch.setenv("LUMOS_DES_SMEM", des_smem)
     dg = DeviceGraph(g)
     assert dg.info["des_only"] == 1
     des = simulate_batch(dg, spec)
