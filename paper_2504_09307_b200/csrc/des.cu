@@ -86,7 +86,7 @@ struct Des {
   int32_t comp_cap = 0x7FFFFFFF;  // completion heap capacity (shared-memory mode: lanes)
 
   __device__ bool key_less(int32_t a, int32_t b) const {
-    const int64_t ka = P.ostart[a], kb = P.ostart[b];
+    const int64_t ka = __ldg(&P.ostart[a]), kb = __ldg(&P.ostart[b]);
     return ka < kb || (ka == kb && a < b);
   }
   __device__ int32_t head(int32_t l) const { return s.hid[l]; }
@@ -97,7 +97,7 @@ struct Des {
   }
   __device__ void set_head(int32_t l, int32_t t) {
     s.hid[l] = t;
-    s.hkey[l] = P.ostart[t];
+    s.hkey[l] = __ldg(&P.ostart[t]);
   }
   // lane heap: free lanes (clock <= now) with a non-empty ready set
   __device__ void lh_set(int32_t i, int32_t l) {
@@ -148,7 +148,7 @@ struct Des {
   // ready heap of lane l (min by (original_start, id)); a new head of a lane
   // in the lane heap moves it up, a free idle lane enters it
   __device__ void ready_push(int32_t l, int32_t t) {
-    int32_t* h = s.heap + P.lane_off[l];
+    int32_t* h = s.heap + __ldg(&P.lane_off[l]);
     int32_t i = s.hsize[l]++;
     h[i] = t;
     while (i > 0) {
@@ -168,7 +168,7 @@ struct Des {
     }
   }
   __device__ void ready_pop(int32_t l) {
-    int32_t* h = s.heap + P.lane_off[l];
+    int32_t* h = s.heap + __ldg(&P.lane_off[l]);
     const int32_t n = --s.hsize[l];
     h[0] = h[n];
     int32_t i = 0;
@@ -225,15 +225,15 @@ struct Des {
   }
   // rule_ok (simulate.cpp:202-217)
   __device__ bool rule_ok(int32_t t, int32_t own, int64_t now) const {
-    const int32_t r = P.rule_of[t];
+    const int32_t r = __ldg(&P.rule_of[t]);
     if (r < 0) return true;
-    if (P.rule_kind[r] == TS_RULE_EVENT_SYNC) {
-      const int32_t b = P.rule_bound[r];
+    if (__ldg(&P.rule_kind[r]) == TS_RULE_EVENT_SYNC) {
+      const int32_t b = __ldg(&P.rule_bound[r]);
       if (b < 0) return true;
       return s.sim_start[b] != kMinI64 && s.sim_end[b] <= now;
     }
-    for (int32_t w = P.rule_wl_off[r]; w < P.rule_wl_off[r + 1]; ++w) {
-      const int32_t lw = P.rule_wl[w];
+    for (int32_t w = __ldg(&P.rule_wl_off[r]); w < __ldg(&P.rule_wl_off[r + 1]); ++w) {
+      const int32_t lw = __ldg(&P.rule_wl[w]);
       if (s.clock[lw] > now) return false;
       const int32_t pending = s.hsize[lw] - (lw == own ? 1 : 0);
       if (pending > 0) return false;
@@ -241,10 +241,10 @@ struct Des {
     return true;
   }
   __device__ void complete(int32_t t) {
-    for (int32_t k = P.succ_off[t]; k < P.succ_off[t + 1]; ++k) {
-      int32_t v = P.succ[k];
+    for (int32_t k = __ldg(&P.succ_off[t]); k < __ldg(&P.succ_off[t + 1]); ++k) {
+      int32_t v = __ldg(&P.succ[k]);
       if (!LUMOS_OK(v >= 0 && v < P.n)) v = 0;
-      if (--s.indeg[v] == 0) ready_push(P.lane_of[v], v);
+      if (--s.indeg[v] == 0) ready_push(__ldg(&P.lane_of[v]), v);
     }
   }
 };
@@ -314,11 +314,11 @@ __global__ void des_kernel(DesParams P) {
       s.lpos[l] = kOut;
     }
     for (int32_t t = 0; t < n; ++t) {
-      s.indeg[t] = P.indeg0[t];
+      s.indeg[t] = __ldg(&P.indeg0[t]);
       s.sim_start[t] = kMinI64;
     }
     for (int32_t t = 0; t < n; ++t)
-      if (s.indeg[t] == 0) E.ready_push(P.lane_of[t], t);
+      if (s.indeg[t] == 0) E.ready_push(__ldg(&P.lane_of[t]), t);
     int32_t unstarted = n, comp = 0;
     bool dead = false;
     for (;;) {
@@ -333,8 +333,8 @@ __global__ void des_kernel(DesParams P) {
           continue;
         }
         E.ready_pop(lane);
-        const int64_t b = P.has_rt ? rt_task(P.rt, rc, best) : P.base[best];
-        const int64_t d = scenario_duration<-1>(P.sp, ts, best, b, P.cls[best]);
+        const int64_t b = P.has_rt ? rt_task(P.rt, rc, best) : __ldg(&P.base[best]);
+        const int64_t d = scenario_duration<-1>(P.sp, ts, best, b, __ldg(&P.cls[best]));
         s.sim_start[best] = now;
         s.sim_end[best] = now + d;
         --unstarted;
@@ -358,7 +358,7 @@ __global__ void des_kernel(DesParams P) {
         const int32_t done = s.comp_id[0];
         E.comp_pop(comp);
         E.complete(done);
-        const int32_t l = P.lane_of[done];
+        const int32_t l = __ldg(&P.lane_of[done]);
         if (s.lpos[l] == kOut && s.hsize[l] > 0) E.lh_push(l);
       }
       E.unpark_all();
@@ -392,19 +392,19 @@ __global__ void des_kernel(DesParams P) {
     if (wend < W) wend = W;
     int32_t l = 0;
     while (l < nl) {
-      const int32_t r = P.lane_rank[l];
+      const int32_t r = __ldg(&P.lane_rank[l]);
       int32_t ne = 0;
       int32_t l1 = l;
-      for (; l1 < nl && P.lane_rank[l1] == r; ++l1) {
-        const int32_t st = P.lane_stream[l1];
+      for (; l1 < nl && __ldg(&P.lane_rank[l1]) == r; ++l1) {
+        const int32_t st = __ldg(&P.lane_stream[l1]);
         if (st < 0) continue;
         int64_t busy = 0;
-        for (int32_t k = P.lane_off[l1]; k < P.lane_off[l1 + 1]; ++k) {
-          const int32_t t = P.lane_tasks[k];
+        for (int32_t k = __ldg(&P.lane_off[l1]); k < __ldg(&P.lane_off[l1 + 1]); ++k) {
+          const int32_t t = __ldg(&P.lane_tasks[k]);
           const int64_t a = imax(s.sim_start[t], W), b = imin(s.sim_end[t], wend);
           if (a >= b) continue;
           busy += b - a;
-          const int64_t c = P.is_comm[t] ? 2 : 0;  // 0 compute, 2 comm; +1 = end
+          const int64_t c = __ldg(&P.is_comm[t]) ? 2 : 0;  // 0 compute, 2 comm; +1 = end
           if (!LUMOS_OK(ne + 2 <= 2 * n)) break;
           s.ev[ne++] = ((a - W) << 2) | c;
           s.ev[ne++] = ((b - W) << 2) | (c + 1);
