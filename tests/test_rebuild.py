@@ -195,3 +195,51 @@ def test_rebuild_from_traces_with_exotic_args(tmp_path, monkeypatch):
     ref, _ = R.ingest_traces(paths).apply_whatif(_tuple(smodel), _tuple(smodel),
                                                  _par(w.source_par), _par(w.target_par))
     _assert_graph_equals_reference(spec, ref)
+
+
+def test_rebuild_random_whatifs_equal_reference():
+    # seeded sweep over structural what-ifs (pp, dp, microbatches, layers,
+    # widths): every rebuilt graph equals the reference apply_whatif graph, and
+    # configs the reference rejects are rejected with the same message
+    import random
+    rnd = random.Random(2504)
+    widths = [(1024, 4096, 16), (1536, 6144, 24), (2048, 8192, 32), (1024, 2048, 16)]
+    checked = 0
+    errors = 0
+    for trial in range(40):
+        spp, sdp = rnd.choice([1, 2, 4]), rnd.choice([1, 2])
+        sm = rnd.choice([4, 6, 8])
+        slayers = spp * rnd.choice([1, 2])
+        sw = rnd.choice(widths)
+        tpp, tdp = rnd.choice([1, 2, 4]), rnd.choice([1, 2, 4])
+        tm = rnd.choice([4, 6, 8])
+        tlayers = tpp * rnd.choice([1, 2, 3])
+        tw = rnd.choice(widths)
+        smodel = _model(layers=slayers, d=sw[0], f=sw[1], heads=sw[2])
+        tmodel = _model(layers=tlayers, d=tw[0], f=tw[1], heads=tw[2])
+        if sm < spp:
+            continue
+        w = WhatIfConfig(smodel, tmodel, ParallelismConfig(1, spp, sdp, sm),
+                         ParallelismConfig(1, tpp, tdp, tm))
+        ref_h = _ref_source(spp, sdp, sm, smodel)
+        try:
+            ref, notes = ref_h.apply_whatif(_tuple(smodel), _tuple(tmodel),
+                                            _par(w.source_par), _par(w.target_par))
+            ref_err = None
+        except R.RefError as e:
+            ref, notes, ref_err = None, "", str(e).split("] ", 1)[1]
+        try:
+            spec = rebuild_pipeline(_synth(spp, sdp, sm, smodel), w)
+            err = None
+        except Exception as e:
+            spec, err = None, str(e)
+        if ref_err is not None:
+            assert err == ref_err, (trial, err, ref_err)
+            errors += 1
+            continue
+        if not notes.startswith("rebuilt pipeline"):
+            continue  # in-place retime / no-op: not the rebuild's branch
+        assert err is None, (trial, err)
+        _assert_graph_equals_reference(spec, ref)
+        checked += 1
+    assert checked >= 12 and errors >= 1, (checked, errors)
