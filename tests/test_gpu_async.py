@@ -33,3 +33,19 @@ def test_host_async_outputs_equal_synchronous_outputs():
                         rank_breakdown=want[1], stream_busy=want[2])
         for a, b in zip(got[k], want):
             assert np.array_equal(a.numpy(), b), f"call {k}"
+
+
+def test_host_async_falls_back_to_synchronous_when_status_is_read(monkeypatch):
+    # an event-driven graph reads its scenario status back (deadlock check):
+    # host_async then stays synchronous, results unchanged
+    monkeypatch.setenv("LUMOS_FORCE_DES", "1")
+    g = generate_graph(SynthSpec(pp=2, dp=1, num_microbatches=2, n_layers=2)).graph
+    dg = DeviceGraph(g, device=0)
+    assert dg.info["des_only"] == 1
+    spec = ScenarioSpec(count=16, seed=4, jitter=0.1)
+    a = np.zeros((16, 3), np.int64)
+    b = np.zeros((16, 3), np.int64)
+    dg.replay_batch(spec, span=a, host_async=True)
+    dg.wait()
+    dg.replay_batch(spec, span=b)
+    assert np.array_equal(a, b) and (a[:, 2] > 0).all()
