@@ -10,6 +10,11 @@ dependency graph with its p2p rendezvous / collective-barrier gates, i.e. what
 scenarios on the GPU.  A scenario's durations play the DurationHook: task t
 of the graph is hook slot ``op_index[t]`` (launch = two slots, negative -> 0).
 Everything goes through the C ABI (``ts_pipeline_graph``); there is no CPU path.
+
+``rebuild_pipeline`` / ``estimate_whatif`` add the structural what-if host
+step (``ts_rebuild_pipeline``: tag_tasks + measure_pipeline + rebuild_pipeline,
+transform.cpp:71-701) so a measured trace can be estimated at a new PP / DP /
+microbatch count / depth / width.
 """
 from __future__ import annotations
 
