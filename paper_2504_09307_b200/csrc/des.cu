@@ -141,9 +141,18 @@ struct Des {
     }
     return top;
   }
+  // parked lanes whose rule now holds go back to the lane heap; the others
+  // stay parked (re-pushing them would only pop and park them again: between
+  // here and their pop only positive-duration starts can happen, and those
+  // cannot unblock a rule)
   __device__ void unpark_all() {
-    for (int32_t k = 0; k < nparked; ++k) lh_push(s.parked[k]);
-    nparked = 0;
+    int32_t keep = 0;
+    for (int32_t k = 0; k < nparked; ++k) {
+      const int32_t l = s.parked[k];
+      if (rule_ok(head(l), l, now)) lh_push(l);
+      else s.parked[keep++] = l;
+    }
+    nparked = keep;
   }
   // ready heap of lane l (min by (original_start, id)); a new head of a lane
   // in the lane heap moves it up, a free idle lane enters it
