@@ -399,15 +399,26 @@ __global__ void des_kernel(DesParams P) {
     int64_t wend = P.window_end;
     if (W + (hi - lo) > wend) wend = W + (hi - lo);
     if (wend < W) wend = W;
+    // Each stream's events are appended in its task order; a stream runs one
+    // task at a time, so when that order is also the execution order (always
+    // for chained lanes) every run is sorted by time and the sweep merges the
+    // runs instead of sorting.  Events at equal times may be taken in any
+    // order: spans between them are empty.
+    constexpr int kMaxRuns = 8;
     int32_t l = 0;
     while (l < nl) {
       const int32_t r = __ldg(&P.lane_rank[l]);
       int32_t ne = 0;
       int32_t l1 = l;
+      int32_t run_b[kMaxRuns + 1];
+      int nrun = 0;
+      bool merge = true;
       for (; l1 < nl && __ldg(&P.lane_rank[l1]) == r; ++l1) {
         const int32_t st = __ldg(&P.lane_stream[l1]);
         if (st < 0) continue;
-        int64_t busy = 0;
+        if (nrun < kMaxRuns) run_b[nrun++] = ne;
+        else merge = false;
+        int64_t busy = 0, last = INT64_MIN;
         for (int32_t k = __ldg(&P.lane_off[l1]); k < __ldg(&P.lane_off[l1 + 1]); ++k) {
           const int32_t t = __ldg(&P.lane_tasks[k]);
           const int64_t a = imax(s.sim_start[t], W), b = imin(s.sim_end[t], wend);
@@ -415,12 +426,15 @@ __global__ void des_kernel(DesParams P) {
           busy += b - a;
           const int64_t c = __ldg(&P.is_comm[t]) ? 2 : 0;  // 0 compute, 2 comm; +1 = end
           if (!LUMOS_OK(ne + 2 <= 2 * n)) break;
+          merge = merge && a >= last;
+          last = b;
           s.ev[ne++] = ((a - W) << 2) | c;
           s.ev[ne++] = ((b - W) << 2) | (c + 1);
         }
         if (P.stream_busy) P.stream_busy[static_cast<int64_t>(col) * P.n_streams + st] = busy;
       }
-      sort_i64(s.ev, ne);
+      run_b[nrun] = ne;
+      if (!merge) sort_i64(s.ev, ne);
       int compute = 0, commc = 0;
       int64_t prev = W, ec = 0, em = 0, ov = 0, ot = 0;
       BinAcc ua;
@@ -436,14 +450,34 @@ __global__ void des_kernel(DesParams P) {
         if (P.util && (compute > 0 || commc > 0)) ua.add(prev - W, upto - W, 1);
         prev = upto;
       };
-      for (int32_t k = 0; k < ne; ++k) {
-        account(W + (s.ev[k] >> 2));
-        switch (s.ev[k] & 3) {
+      auto event = [&](int64_t e) {
+        account(W + (e >> 2));
+        switch (e & 3) {
           case 0: ++compute; break;
           case 1: --compute; break;
           case 2: ++commc; break;
           default: --commc; break;
         }
+      };
+      if (merge) {
+        int32_t pos[kMaxRuns];
+        for (int j = 0; j < nrun; ++j) pos[j] = run_b[j];
+        for (;;) {
+          int best = -1;
+          int64_t bt = 0;
+          for (int j = 0; j < nrun; ++j) {
+            if (pos[j] >= run_b[j + 1]) continue;
+            const int64_t tj = s.ev[pos[j]] >> 2;
+            if (best < 0 || tj < bt) {
+              best = j;
+              bt = tj;
+            }
+          }
+          if (best < 0) break;
+          event(s.ev[pos[best]++]);
+        }
+      } else {
+        for (int32_t k = 0; k < ne; ++k) event(s.ev[k]);
       }
       account(wend);
       if (P.util) ua.flush();
