@@ -99,6 +99,7 @@ struct WalkParams {
   uint64_t* cl_mail;
   int32_t cl_size;             // CTAs per cluster (ranks of the widest component)
   int32_t cl_n_mail;           // mailboxes per cluster
+  int32_t cl_check;            // 1: check every finish for a uint32 wrap (window not proven)
 };
 // debug builds: the source line of the first failed bounds check since the
 // last call (0 = none), cleared by the read; always 0 in release builds

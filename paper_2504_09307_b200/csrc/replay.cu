@@ -107,7 +107,7 @@ __device__ __forceinline__ void mail_store(uint64_t* p, uint64_t v) {
 }
 
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS,
-          bool kCl = false>
+          bool kCl = false, bool kClCheck = true>
 __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
   using VP = VPack<V, kS>;
   constexpr bool kRel = sizeof(V) == 4;
@@ -334,10 +334,10 @@ __device__ __forceinline__ void replay_walk_body(const WalkParams& P) {
         if (kS == 2) __stcs(fin_c0 + at + dcol, absv(fin.v[kS - 1]));
       }
     }
-    if constexpr (kCl) {
+    if constexpr (kCl && kClCheck) {
       // the cluster walk's uint32 window is sized by the nominal path (like
       // the cooperative walk): a wrapped addition sends the scenario to the
-      // int64 re-run
+      // int64 re-run (elided when the host proves the window: cl_check = 0)
 #pragma unroll
       for (int s = 0; s < kS; ++s)
         fail[s] = fail[s] || fin.v[s] < fb.v[s] || fin.v[s] == static_cast<V>(0xFFFFFFFFu);
@@ -592,9 +592,9 @@ __global__ void __launch_bounds__(kT, sizeof(V) == 4 && LUMOS_WALK_MINB > 0 ? LU
 #ifndef LUMOS_CLUSTER_CARVEOUT_DEFAULT
 #define LUMOS_CLUSTER_CARVEOUT_DEFAULT -1
 #endif
-template <int kMode, bool kWriteStart, bool kWriteFin>
+template <int kMode, bool kWriteStart, bool kWriteFin, bool kCheck>
 __global__ void __launch_bounds__(128, LUMOS_CLUSTER_MINB) cluster_walk_kernel(WalkParams P) {
-  replay_walk_body<128, kMode, kWriteStart, kWriteFin, uint32_t, 2, true>(P);
+  replay_walk_body<128, kMode, kWriteStart, kWriteFin, uint32_t, 2, true, kCheck>(P);
 }
 // retime walks: at least 6 CTAs of 128 threads per SM (<= 80 registers)
 template <int kT, int kMode, bool kWriteStart, bool kWriteFin, typename V, int kS>
@@ -1655,7 +1655,8 @@ static cudaError_t cluster_attrs(K kern, size_t smem, int cl_size) {
 template <int kMode, bool kWS, bool kWF>
 static cudaError_t launch_cluster_t(const WalkParams& p, size_t smem, unsigned blocks,
                                     cudaStream_t stream) {
-  auto kern = cluster_walk_kernel<kMode, kWS, kWF>;
+  auto kern = p.cl_check ? cluster_walk_kernel<kMode, kWS, kWF, true>
+                         : cluster_walk_kernel<kMode, kWS, kWF, false>;
   cudaError_t e = cluster_attrs(kern, smem, p.cl_size);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1696,7 +1697,7 @@ static cudaError_t launch_cluster_mode(const WalkParams& p, size_t smem, unsigne
 
 bool cluster_walk_supported(int cl_size, int n_slots) {
   if (cl_size < 1 || cl_size > 16 || walk_width(n_slots, true) != 128) return false;
-  auto kern = cluster_walk_kernel<kModeJitter, true, true>;
+  auto kern = cluster_walk_kernel<kModeJitter, true, true, true>;
   const size_t smem = walk_smem(n_slots, 128, 8);
   if (cluster_attrs(kern, smem, cl_size) != cudaSuccess) return cudaGetLastError(), false;
   cudaLaunchConfig_t cfg = {};
