@@ -1021,8 +1021,12 @@ int ts_replay_batch(ts_graph* g, const ts_scenarios* sc, const ts_result* out, v
       f *= static_cast<double>(sp.scale_lo + static_cast<int64_t>(sp.scale_span) - 1) /
            static_cast<double>(sp.scale_den);
     if (sp.mode & kModeJitter) f *= 1.0 + 0.5 * sp.two_j;
-    const double bound = static_cast<double>(c.max_comp_dur_sum) * f +
-                         3.0 * static_cast<double>(c.max_comp_tasks) + 16.0;
+    // a value is a max-plus path from W: at most f x the component's nominal
+    // longest path plus 1 us of rounding per task (or the looser sum bound)
+    const double bound =
+        std::min(static_cast<double>(c.max_comp_dur_sum) * f,
+                 static_cast<double>(c.max_comp_path) * f) +
+        3.0 * static_cast<double>(c.max_comp_tasks) + 16.0;
     // offsets from O = W rounded down to a multiple of 2^32 (replay.cu):
     // W - O + every time must stay below 2^32 - 1
     const double w_lo = static_cast<double>(static_cast<uint32_t>(c.window_start));

@@ -552,6 +552,7 @@ int compile_programs(const ts_graph_desc& d, CompiledGraph& out, std::string& er
     comp_path.assign(n_comp, 0);
     for (int32_t t = 0; t < n; ++t)
       comp_path[comp_of[t]] = std::max(comp_path[comp_of[t]], nfin[t] - d.window_start);
+    for (int64_t v : comp_path) out.max_comp_path = std::max(out.max_comp_path, v);
 
     for (int64_t k = na - 1; k >= 0; --k) {
       const int32_t a = by_topo[k];

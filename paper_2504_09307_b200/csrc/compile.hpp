@@ -54,6 +54,7 @@ struct CompiledGraph {
   // (W + any path <= W + sum of the component's durations), which decides
   // whether the walk may keep uint32 offsets from W
   int64_t max_comp_dur_sum = 0;
+  int64_t max_comp_path = 0;  // nominal longest path (W-relative) over all components
   int32_t max_comp_tasks = 0;
   int32_t n_syncs = 0;
   int32_t n_gpu_tasks = 0;
